@@ -1,0 +1,288 @@
+"""Generate golden vectors by running the REFERENCE implementation.
+
+Run in the build container (where /root/reference exists):
+
+    python tests/golden/make_golden.py
+
+The reference package is copied to a temporary directory first (so nothing is
+written under /root/reference: Numba's cache and __pycache__ land in the
+copy) and imported from there.  The inputs are produced by this repo's seeded
+scene generator and handed to the reference as plain arrays, so the goldens
+pin the reference's arithmetic only.  The resulting .npz files are committed;
+tests and the oracle read them on machines without /root/reference.
+"""
+
+from __future__ import annotations
+
+import os
+import shutil
+import sys
+import tempfile
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(HERE))
+REF_SRC = "/root/reference/pkg/src/raysplat"
+
+
+def import_reference():
+    tmp = tempfile.mkdtemp(prefix="raysplat_ref_")
+    shutil.copytree(REF_SRC, os.path.join(tmp, "raysplat"))
+    os.environ["NUMBA_CACHE_DIR"] = os.path.join(tmp, "numba_cache")
+    sys.dont_write_bytecode = True
+    sys.path.insert(0, tmp)
+    import raysplat.gaussians as G  # noqa: E402
+    import raysplat.geometry as GEO
+    import raysplat.mapper as M
+    import raysplat.rasterizer as R
+    import raysplat.tracker as T
+    from raysplat.datasets import RgbdFrame
+    return tmp, G, GEO, M, R, T, RgbdFrame
+
+
+def ref_map(G, GEO, params, intr_ref, pose, frame_index):
+    return G.PixelGaussianMap(
+        frame_index=frame_index, pose=GEO.Pose(pose.rotation, pose.translation),
+        intrinsics=intr_ref, base_depth=params.base_depth.copy(), delta=params.delta.copy(),
+        color=params.color.copy(), log_radius=params.log_radius.copy(),
+        opacity_logit=params.opacity_logit.copy(), active_mask=params.active_mask.copy())
+
+
+def ref_intr(GEO, intr):
+    return GEO.Intrinsics(fx=intr.fx, fy=intr.fy, cx=intr.cx, cy=intr.cy, width=intr.width,
+                          height=intr.height)
+
+
+def params_dict(prefix, p):
+    return {f"{prefix}base_depth": p.base_depth, f"{prefix}delta": p.delta,
+            f"{prefix}log_radius": p.log_radius, f"{prefix}opacity_logit": p.opacity_logit,
+            f"{prefix}color": p.color, f"{prefix}active_mask": p.active_mask}
+
+
+def golden_c1(G, GEO, M, R, RgbdFrame):
+    from paper_2603_21055_b200 import scenes
+    intr, frame, learn, target = scenes.config_c1()
+    ri = ref_intr(GEO, intr)
+    ident = GEO.Pose.identity()
+    m_learn = ref_map(G, GEO, learn, ri, ident, 0)
+    m_tgt = ref_map(G, GEO, target, ri, ident, 0)
+    t_out = R.splat([m_tgt], ident, ri)
+    t_color = np.clip(t_out.color, 0.0, 1.0).astype(np.float32)
+    t_depth = t_out.depth.astype(np.float32)
+    t_mask = frame.valid_mask.copy()
+    tf = RgbdFrame(color=t_color, depth=t_depth, valid_mask=t_mask, intrinsics=ri, timestamp=0.0,
+                   index=0)
+    cfg = M.MapperConfig(tau=0.0)
+    loss, grads, out = M.mapping_loss([m_learn], tf, ident, cfg)
+    batch = R._prepare([m_learn], ident, ri, learnable_map=0)
+    offsets, lists = R._build_tile_lists(batch.u0, batch.v0, batch.sigma, intr.height,
+                                         intr.width, R._TILE)
+    opt = M.MapOptimizer(m_learn, cfg)
+    opt.step(grads)
+    d = params_dict("in_", learn)
+    d.update(t_color=t_color, t_depth=t_depth, t_mask=t_mask,
+             intr=np.array([intr.fx, intr.fy, intr.cx, intr.cy, intr.width, intr.height]),
+             loss=np.array([loss.total, loss.color_l1, loss.ssim_term, loss.depth_l1]),
+             out_color=out.color, out_depth=out.depth, out_alpha=out.alpha,
+             out_count=out.contributors, g_color=grads.color, g_radius=grads.radius,
+             g_logit=grads.opacity_logit, g_delta=grads.delta,
+             b_u0=batch.u0, b_v0=batch.v0, b_z=batch.z, b_sigma=batch.sigma,
+             b_opacity=batch.opacity, b_pixel=batch.pixel_index, offsets=offsets,
+             lists=lists.astype(np.int32),
+             adam_color=m_learn.color, adam_log_radius=m_learn.log_radius,
+             adam_logit=m_learn.opacity_logit, adam_delta=m_learn.delta)
+    return d
+
+
+def golden_window(G, GEO, R):
+    """Delta D1 window: 3 frames of 64x48, all learnable, 2 target views."""
+    from paper_2603_21055_b200 import scenes
+    intr_kw = dict(fx=60.0, fy=60.0, cx=31.5, cy=23.5, width=64, height=48)
+    wc = scenes.config_window("golden", 3, intr_kw)
+    rng = np.random.default_rng(7)
+    params = []
+    for p in wc.params:  # perturb so every attribute carries gradient
+        h, w = p.base_depth.shape
+        p.delta = scenes._f32(rng.normal(0.0, 0.01, (h, w)))
+        p.opacity_logit = scenes._f32(rng.normal(1.0, 1.0, (h, w)))
+        p.log_radius = scenes._f32(p.log_radius + rng.normal(0.0, 0.3, (h, w)))
+        params.append(p)
+    ri = ref_intr(GEO, wc.intr)
+    maps = [ref_map(G, GEO, p, ri, wc.poses[i], i) for i, p in enumerate(params)]
+    d = {}
+    for i, p in enumerate(params):
+        d.update(params_dict(f"m{i}_", p))
+        d[f"m{i}_pose"] = np.concatenate([wc.poses[i].rotation.reshape(9),
+                                          wc.poses[i].translation])
+    d["intr"] = np.array([ri.fx, ri.fy, ri.cx, ri.cy, ri.width, ri.height])
+    views = [0, 2]
+    grng = np.random.default_rng(8)
+    for v in views:
+        pose = GEO.Pose(wc.poses[v].rotation, wc.poses[v].translation)
+        batch = R._prepare(maps, pose, ri, learnable_map=0)
+        offsets, lists = R._build_tile_lists(batch.u0, batch.v0, batch.sigma, ri.height, ri.width,
+                                             R._TILE)
+        out = R.splat(maps, pose, ri)
+        gc = grng.normal(size=(ri.height, ri.width, 3))
+        gd = grng.normal(size=(ri.height, ri.width))
+        ga = grng.normal(size=(ri.height, ri.width))
+        frame_of = np.concatenate([np.full(int(m.active_mask.sum()), m.frame_index) for m in maps])
+        del frame_of
+        d[f"v{v}_offsets"] = offsets
+        d[f"v{v}_lists"] = lists.astype(np.int32)
+        d[f"v{v}_b_pixel"] = batch.pixel_index
+        d[f"v{v}_b_u0"], d[f"v{v}_b_v0"] = batch.u0, batch.v0
+        d[f"v{v}_b_z"], d[f"v{v}_b_sigma"] = batch.z, batch.sigma
+        d[f"v{v}_color"], d[f"v{v}_depth"] = out.color, out.depth
+        d[f"v{v}_alpha"], d[f"v{v}_count"] = out.alpha, out.contributors
+        d[f"v{v}_gc"], d[f"v{v}_gd"], d[f"v{v}_ga"] = gc, gd, ga
+        for i in range(len(maps)):
+            g = R.splat_backward(maps, pose, ri, gc, gd, ga, learnable_map=i)
+            d[f"v{v}_m{i}_g_color"] = g.color
+            d[f"v{v}_m{i}_g_radius"] = g.radius
+            d[f"v{v}_m{i}_g_logit"] = g.opacity_logit
+            d[f"v{v}_m{i}_g_delta"] = g.delta
+        gn = R.splat_backward(maps, pose, ri, gc, gd, ga, learnable_map=1, normalize_depth=True)
+        d[f"v{v}_norm_m1_g_delta"] = gn.delta
+        d[f"v{v}_norm_m1_g_radius"] = gn.radius
+        outn = R.splat(maps, pose, ri, normalize_depth=True)
+        d[f"v{v}_norm_depth"] = outn.depth
+    d["views"] = np.array(views)
+    return d
+
+
+def golden_eig(GEO):
+    rng = np.random.default_rng(31)
+    mats = []
+    for _ in range(300):
+        a = rng.normal(size=(3, 3))
+        mats.append(a @ a.T + 1e-6 * np.eye(3))
+    mats.append(np.diag([4.0, 1.0, 0.25]))
+    mats.append(np.eye(3))
+    mats.append(np.diag([2.0, 1.0, 0.0]))
+    mats.append(np.diag([1.0, 1.0 + 1e-13, 2.0]))
+    mats.append(np.diag([1.0, 0.5, -1e-12]))
+    pts = rng.normal(size=(200, 24, 3)) * np.array([1.0, 0.3, 1e-4])
+    for k in range(200):
+        dd = pts[k] - pts[k].mean(0)
+        mats.append(dd.T @ dd / 24.0)
+    mats = np.array(mats)
+    rot, vals = GEO.sym_eigh3_batch(mats)
+    return dict(mats=mats, rot=rot, vals=vals)
+
+
+def window_fit_ref(T, GEO, depth, mask, intr, win=5, k_min=4, scale_mode="ellipse"):
+    """Delta D2 restated ONLY in the neighbour selection; the covariance line,
+    eigensolver, floor, normalisation and orientation are the reference's own
+    (tracker.py:158-169, geometry.py:275)."""
+    h, w = depth.shape
+    valid = mask & (depth > 0)
+    vs, us = np.nonzero(valid)
+    z_all = depth[vs, us].astype(np.float64)
+    pts = np.zeros((h, w, 3))
+    pts[vs, us] = np.stack([(us - intr.cx) / intr.fx * z_all, (vs - intr.cy) / intr.fy * z_all,
+                            z_all], axis=1)
+    r = win // 2
+    centers, covs, idx = [], [], []
+    for v, u in zip(vs, us):
+        nb = []
+        for dv in range(-r, r + 1):
+            for du in range(-r, r + 1):
+                if dv == 0 and du == 0:
+                    continue
+                y, x = v + dv, u + du
+                if 0 <= y < h and 0 <= x < w and valid[y, x]:
+                    nb.append(pts[y, x])
+        if len(nb) < k_min:
+            continue
+        nbr = np.array(nb)[None]
+        diff = nbr - nbr.mean(axis=1, keepdims=True)
+        cov = np.einsum("nki,nkj->nij", diff, diff) / nbr.shape[1]
+        covs.append(cov[0])
+        centers.append(pts[v, u])
+        idx.append(v * w + u)
+    centers = np.array(centers)
+    cov = np.array(covs)
+    rot, vals = GEO.sym_eigh3_batch(cov)
+    vals = np.maximum(vals, T.EIGVAL_FLOOR_REL * vals[:, :1])
+    scales = T._normalize_scales(np.sqrt(vals), scale_mode)
+    normals = rot[:, :, 2].copy()
+    flip = np.einsum("ni,ni->n", normals, -centers) < 0.0
+    normals[flip] *= -1.0
+    rot[flip, :, 2] *= -1.0
+    rot[flip, :, 1] *= -1.0
+    return np.array(idx), centers, rot, scales, normals
+
+
+def golden_track(T, GEO):
+    from paper_2603_21055_b200 import scenes
+    intr_kw = dict(fx=60.0, fy=60.0, cx=39.5, cy=29.5, width=80, height=60)
+    intr = scenes.Intrinsics(**intr_kw)
+    prims = scenes.plane_spheres_scene(0)
+    rng = np.random.default_rng(3)
+    axis = rng.normal(size=3)
+    axis /= np.linalg.norm(axis)
+    angle = rng.uniform(0.0, np.deg2rad(2.0))
+    shift = rng.normal(size=3)
+    shift = shift / np.linalg.norm(shift) * rng.uniform(0.0, 0.05)
+    truth = scenes.Pose(scenes.se3_exp(np.concatenate([axis * angle, np.zeros(3)])).rotation, shift)
+    ref = scenes.render_frame(prims, scenes.Pose.identity(), intr, 0, depth_noise_rel=0.01)
+    qry = scenes.render_frame(prims, truth, intr, 1, depth_noise_rel=0.01)
+    d = dict(ref_depth=ref.depth, ref_mask=ref.valid_mask, qry_depth=qry.depth,
+             qry_mask=qry.valid_mask, intr=np.array([intr.fx, intr.fy, intr.cx, intr.cy,
+                                                     intr.width, intr.height]),
+             truth=np.concatenate([truth.rotation.reshape(9), truth.translation]))
+    fits = {}
+    for name, fr in (("ref", ref), ("qry", qry)):
+        idx, c, rot, s, n = window_fit_ref(T, GEO, fr.depth, fr.valid_mask, intr)
+        fits[name] = (c, rot, s, n)
+        d.update({f"{name}_idx": idx, f"{name}_centers": c, f"{name}_rot": rot,
+                  f"{name}_scales": s, f"{name}_normals": n})
+    c, rot, s, n = fits["ref"]
+    g = T.GlobalGeomSet(voxel_size=1e-4)
+    added = g.insert(c, rot, s, n)
+    assert added == len(c)
+    c, rot, s, n = fits["qry"]
+    local = T.LocalGeomSet(centers=c, rotations=rot, scales=s, normals=n)
+    cfg = T.TrackerConfig(max_gicp_iters=20, convergence_eps=0.0)
+    pose, diag = T.gicp_align(local, g, GEO.Pose.identity(), cfg)
+    d.update(gicp_pose=np.concatenate([pose.rotation.reshape(9), pose.translation]),
+             gicp_iters=np.array(diag.iterations), gicp_inliers=np.array(diag.inlier_count),
+             gicp_cost_pairs=np.array(diag.cost_pairs), gicp_final_cost=np.array(diag.final_cost),
+             gicp_accepted_first=diag.accepted_first)
+    # the first iteration's normal equations, restated from tracker.py:286-321
+    pts = local.centers.copy()
+    dist, j = g.query_nearest(pts)
+    b = g.centers[j]
+    dd = b - pts
+    metric = np.abs(np.einsum("ni,ni->n", g.normals[j], dd))
+    acc = metric < cfg.correspondence_dist_max
+    c_comb = g.covariances(j[acc]) + local.covariances()[acc]
+    wts = np.linalg.inv(c_comb)
+    p_acc = pts[acc]
+    jac = np.concatenate([T._skew(p_acc), -np.broadcast_to(np.eye(3), (int(acc.sum()), 3, 3))], 2)
+    d["first_H"] = np.einsum("nij,nik,nkl->jl", jac, wts, jac)
+    d["first_g"] = np.einsum("nij,nik,nk->j", jac, wts, dd[acc])
+    d["first_nn"] = j
+    d["first_cost"] = np.array(float(np.einsum("ni,nij,nj->", dd[acc], wts, dd[acc])))
+    return d
+
+
+def main():
+    sys.path.insert(0, ROOT)
+    tmp, G, GEO, M, R, T, RgbdFrame = import_reference()
+    try:
+        np.savez_compressed(os.path.join(HERE, "c1.npz"), **golden_c1(G, GEO, M, R, RgbdFrame))
+        np.savez_compressed(os.path.join(HERE, "window.npz"), **golden_window(G, GEO, R))
+        np.savez_compressed(os.path.join(HERE, "eig.npz"), **golden_eig(GEO))
+        np.savez_compressed(os.path.join(HERE, "track.npz"), **golden_track(T, GEO))
+    finally:
+        shutil.rmtree(tmp, ignore_errors=True)
+    for f in sorted(os.listdir(HERE)):
+        if f.endswith(".npz"):
+            print(f, os.path.getsize(os.path.join(HERE, f)))
+
+
+if __name__ == "__main__":
+    main()
