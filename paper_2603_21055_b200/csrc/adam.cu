@@ -1,0 +1,83 @@
+// K6: Adam over the six learnable planes of a keyframe window
+// (restates /root/reference/pkg/src/raysplat/mapper.py:73-95).
+//
+// params [F, 7, HW] fp32 (base, delta, log_radius, logit, R, G, B)
+// grads  [F*HW, 8]  (delta, radius, logit, R, G, B, -, -), consumed and zeroed
+// m, v   [F, 6, HW] fp32 (delta, log_radius, logit, R, G, B)
+// Arithmetic in fp64 per element, mirroring the reference's in-place numpy
+// sequence; storage fp32 (BASELINE: parameters in fp32).
+#include "common.cuh"
+
+namespace sgad {
+
+struct AdamArgs {
+  double lr[6];
+  double b1, b2, eps, bc1, bc2;
+  int update_delta;
+};
+
+template <typename P>
+__global__ void __launch_bounds__(256)
+k_adam(P* __restrict__ params, P* __restrict__ grads, P* __restrict__ m,
+       P* __restrict__ v, int64_t n_frames, int64_t hw, AdamArgs a) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_frames * hw) return;
+  const int64_t f = i / hw, p = i - f * hw;
+  P* gp = grads + 8 * i;
+  double gr[6];
+#pragma unroll
+  for (int c = 0; c < 6; ++c) {
+    gr[c] = (double)gp[c];
+    gp[c] = (P)0;
+  }
+  P* pf = params + f * 7 * hw + p;
+  P* mf = m + f * 6 * hw + p;
+  P* vf = v + f * 6 * hw + p;
+  // mapper.py:77: the radius gradient is chained onto log-radius
+  const double radius = exp((double)pf[2 * hw]);
+  const double g[6] = {gr[0], SG_MUL(gr[1], radius), gr[2], gr[3], gr[4], gr[5]};
+#pragma unroll
+  for (int c = 0; c < 6; ++c) {
+    if (c == 0 && !a.update_delta) continue;
+    // m *= b1; m += (1 - b1) g; v *= b2; v += (1 - b2) g g (in-place numpy order)
+    const double mm = SG_ADD(SG_MUL((double)mf[c * hw], a.b1), SG_MUL(SG_SUB(1.0, a.b1), g[c]));
+    const double vv = SG_ADD(SG_MUL((double)vf[c * hw], a.b2),
+                             SG_MUL(SG_MUL(SG_SUB(1.0, a.b2), g[c]), g[c]));
+    const double mhat = SG_DIV(mm, a.bc1), vhat = SG_DIV(vv, a.bc2);
+    double prm = (double)pf[(c + 1) * hw];
+    prm = SG_SUB(prm, SG_DIV(SG_MUL(a.lr[c], mhat), SG_ADD(sqrt(vhat), a.eps)));
+    if (c >= 3) prm = fmin(fmax(prm, 0.0), 1.0);  // colour clip, mapper.py:95
+    pf[(c + 1) * hw] = (P)prm;
+    mf[c * hw] = (P)mm;
+    vf[c * hw] = (P)vv;
+  }
+}
+
+}  // namespace sgad
+
+extern "C" int sgad_adam_step(void* params, void* grads, void* m, void* v, int64_t n_frames,
+                              int64_t hw, const double* lr, double beta1, double beta2, double eps,
+                              double bc1, double bc2, int32_t update_delta, int32_t f64,
+                              void* stream) {
+  SGAD_REQUIRE(params && grads && m && v && lr && n_frames >= 0 && hw >= 0,
+               "sgad_adam_step: bad arguments");
+  const int64_t n = n_frames * hw;
+  if (n == 0) return SGAD_OK;
+  sgad::AdamArgs a;
+  for (int c = 0; c < 6; ++c) a.lr[c] = lr[c];
+  a.b1 = beta1;
+  a.b2 = beta2;
+  a.eps = eps;
+  a.bc1 = bc1;
+  a.bc2 = bc2;
+  a.update_delta = update_delta;
+  const unsigned nb = (unsigned)((n + 255) / 256);
+  if (f64)
+    sgad::k_adam<double><<<nb, 256, 0, (cudaStream_t)stream>>>(
+        (double*)params, (double*)grads, (double*)m, (double*)v, n_frames, hw, a);
+  else
+    sgad::k_adam<float><<<nb, 256, 0, (cudaStream_t)stream>>>(
+        (float*)params, (float*)grads, (float*)m, (float*)v, n_frames, hw, a);
+  SGAD_LAUNCH_CHECK();
+  return SGAD_OK;
+}

@@ -1,0 +1,1016 @@
+// Mapping hot path: projection (K1), depth sort (K2), tile binning (K3),
+// front-to-back compositing with optional fused L1 loss (K4) and the
+// backward sweep with chain rule (K5).
+//
+// Restates /root/reference/pkg/src/raysplat/rasterizer.py:
+//   K1 <- _prepare :86-135      K2 <- lexsort :157-158
+//   K3 <- _build_tile_lists :178-218
+//   K4 <- _forward_kernel :221-269 (+ mapper.py:118-152 loss, tau = 0)
+//   K5 <- _backward_kernel :272-363 + chain rule :462-483
+//
+// Layout (HBM): survivors live in EMISSION order (frame, pixel) as 64-byte
+// records; the depth sort produces a permutation, tile lists hold emission
+// indices in depth order.  Per-view scratch is owned by the sgad_raster handle.
+#include <cub/cub.cuh>
+#include <stdarg.h>
+#include <algorithm>
+#include <vector>
+
+#include "common.cuh"
+
+namespace sgad {
+
+struct __align__(16) Record {
+  double u0, v0, sigma, opacity, z;
+  float r, g, b;
+  uint32_t gid;          // bit 31: learnable
+  uint16_t tx0, tx1, ty0, ty1;
+};
+static_assert(sizeof(Record) == 64, "record must be one 64-byte line");
+
+struct ChainCoef {  // fused backward: d(param)/d(image-space quantity), fp32
+  float k_r;        // d sigma -> radius: fx / z
+  float a_u, a_v, a_z, a_s;  // delta <- (u0, v0, z, sigma)
+  float k_op;       // opacity -> logit: op (1 - op)
+};
+
+constexpr uint32_t GID_LEARN = 0x80000000u;
+constexpr int PROJ_THREADS = 256;
+constexpr int BATCH = 256;  // records staged per compositing batch
+constexpr int RASTER_THREADS = 256;
+
+}  // namespace sgad
+
+struct sgad_raster {
+  sgad::DevBuf frames, status, counters, records, coef, keys0, keys1, vals0, vals1;
+  sgad::DevBuf pcount, poffset, pkeys0, pkeys1, pvals0, pvals1, ranges, cub_tmp;
+  sgad::DevBuf trans_final, last_idx, signs, raw_grads, rank_of, scratch, col64;
+  int any_f64 = 0;
+  std::vector<sgad_frame> host_frames;
+  sgad_camera cam{};
+  int64_t n_total = 0, n_surv = 0, n_pairs = 0;
+  int32_t n_tiles = 0, ntx = 0, nty = 0;
+  int prepared = 0, forwarded = 0, have_coef = 0, fused_ready = 0;
+  double rho = 0, sigma_d = 0;
+  int64_t n_depth = 0;
+  uint32_t* pinned = nullptr;  // host-pinned counters
+};
+
+namespace sgad {
+
+static thread_local char g_err[1024] = "";
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof g_err, fmt, ap);
+  va_end(ap);
+}
+
+// ------------------------------------------------------------------ K1
+__device__ __forceinline__ int find_frame(const sgad_frame* frames, int n, uint32_t gid) {
+  int lo = 0, hi = n - 1;
+  while (lo < hi) {
+    int mid = (lo + hi + 1) >> 1;
+    if ((uint64_t)frames[mid].gauss_offset <= gid) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+__device__ __forceinline__ double plane_ld(const sgad_frame& f, int64_t i) {
+  return f.planes_f64 ? reinterpret_cast<const double*>(f.planes)[i]
+                      : (double)reinterpret_cast<const float*>(f.planes)[i];
+}
+
+struct Proj {
+  double u0, v0, z, sig, op, bd;
+  double dir[3], y[3];
+};
+
+// rasterizer.py:86-116 for one active pixel p of frame f; true if it survives
+// the near-plane and on-screen culls.  Operation order matches the reference.
+__device__ __forceinline__ bool project_point(const sgad_frame& f, int64_t p, int64_t hw,
+                                              const sgad_camera& cam, Proj& o) {
+  const double xx = (double)(p % f.width), yy = (double)(p / f.width);
+  const double base = plane_ld(f, p), delta = plane_ld(f, hw + p), logr = plane_ld(f, 2 * hw + p);
+  const double r0 = SG_DIV(SG_SUB(xx, f.cx), f.fx);
+  const double r1 = SG_DIV(SG_SUB(yy, f.cy), f.fy);
+  o.bd = SG_ADD(base, delta);
+  const double dadj = fabs(o.bd);
+#pragma unroll
+  for (int j = 0; j < 3; ++j) {
+    // rays @ R.T as OpenBLAS evaluates it: fma(r1, R[j,1], r0 * R[j,0]) + R[j,2]
+    o.dir[j] = SG_ADD(SG_FMA(r1, f.rot[3 * j + 1], SG_MUL(r0, f.rot[3 * j])), f.rot[3 * j + 2]);
+    o.y[j] = SG_ADD(SG_MUL(o.dir[j], dadj), f.trans[j]);
+  }
+  o.z = o.y[2];
+  if (!(o.z > SGAD_Z_NEAR)) return false;
+  const double radius = sgad_exp(logr);
+  o.u0 = SG_ADD(SG_DIV(SG_MUL(cam.fx, o.y[0]), o.z), cam.cx);
+  o.v0 = SG_ADD(SG_DIV(SG_MUL(cam.fy, o.y[1]), o.z), cam.cy);
+  o.sig = SG_DIV(SG_MUL(radius, cam.fx), o.z);
+  const double margin = SG_MUL(3.0, o.sig);
+  const double wlim = SG_SUB((double)cam.width, 1.0), hlim = SG_SUB((double)cam.height, 1.0);
+  if (!(SG_ADD(o.u0, margin) >= 0.0 && SG_SUB(o.u0, margin) <= wlim &&
+        SG_ADD(o.v0, margin) >= 0.0 && SG_SUB(o.v0, margin) <= hlim))
+    return false;
+  o.op = sgad_sigmoid(plane_ld(f, 3 * hw + p));
+  return true;
+}
+
+__global__ void __launch_bounds__(PROJ_THREADS)
+k_project(const sgad_frame* __restrict__ frames, int n_frames, sgad_camera cam, uint32_t n_total,
+          int ntx, int nty, int want_coef, Record* __restrict__ rec, ChainCoef* __restrict__ coef,
+          double* __restrict__ col64,
+          unsigned long long* __restrict__ keys, uint32_t* __restrict__ vals,
+          uint32_t* __restrict__ status, uint32_t* __restrict__ counters) {
+  typedef cub::BlockScan<uint32_t, PROJ_THREADS> Scan;
+  __shared__ typename Scan::TempStorage scan_tmp;
+  __shared__ uint32_t s_tile, s_prefix;
+  if (threadIdx.x == 0) s_tile = atomicAdd(&counters[0], 1u);
+  __syncthreads();
+  const int tile = (int)s_tile;
+  const uint32_t gid = (uint32_t)tile * PROJ_THREADS + threadIdx.x;
+
+  bool keep = false;
+  Record r;
+  ChainCoef c;
+  double c64[3];
+  if (gid < n_total) {
+    const sgad_frame& f = frames[find_frame(frames, n_frames, gid)];
+    const int64_t hw = (int64_t)f.height * f.width;
+    const int64_t p = (int64_t)gid - f.gauss_offset;
+    Proj o;
+    if (p < hw && f.mask[p] && project_point(f, p, hw, cam, o)) {
+      keep = true;
+      r.u0 = o.u0;
+      r.v0 = o.v0;
+      r.sigma = o.sig;
+      r.opacity = o.op;
+      r.z = o.z;
+      r.r = (float)plane_ld(f, 4 * hw + p);
+      r.g = (float)plane_ld(f, 5 * hw + p);
+      r.b = (float)plane_ld(f, 6 * hw + p);
+      c64[0] = plane_ld(f, 4 * hw + p);
+      c64[1] = plane_ld(f, 5 * hw + p);
+      c64[2] = plane_ld(f, 6 * hw + p);
+      r.gid = gid | (f.learnable ? GID_LEARN : 0u);
+      // tile bbox (rasterizer.py:187-199)
+      const double rr = SG_MUL(3.0, o.sig), t16 = (double)SGAD_TILE;
+      long long x0 = (long long)floor(SG_DIV(SG_SUB(o.u0, rr), t16));
+      long long x1 = (long long)floor(SG_DIV(SG_ADD(o.u0, rr), t16));
+      long long y0 = (long long)floor(SG_DIV(SG_SUB(o.v0, rr), t16));
+      long long y1 = (long long)floor(SG_DIV(SG_ADD(o.v0, rr), t16));
+      x0 = x0 < 0 ? 0 : x0;
+      y0 = y0 < 0 ? 0 : y0;
+      x1 = x1 > ntx - 1 ? ntx - 1 : x1;
+      y1 = y1 > nty - 1 ? nty - 1 : y1;
+      r.tx0 = (uint16_t)x0;
+      r.tx1 = (uint16_t)x1;
+      r.ty0 = (uint16_t)y0;
+      r.ty1 = (uint16_t)y1;
+      if (want_coef) {
+        const double sgn = o.bd >= 0.0 ? 1.0 : -1.0;
+        const double iz = 1.0 / o.z;
+        c.k_r = (float)(cam.fx * iz);
+        c.a_u = (float)(sgn * cam.fx * iz * (o.dir[0] - o.dir[2] * o.y[0] * iz));
+        c.a_v = (float)(sgn * cam.fy * iz * (o.dir[1] - o.dir[2] * o.y[1] * iz));
+        c.a_z = (float)(sgn * o.dir[2]);
+        c.a_s = (float)(-sgn * o.dir[2] * o.sig * iz);
+        c.k_op = (float)(o.op * (1.0 - o.op));
+      }
+    }
+  }
+
+  uint32_t rank, agg;
+  Scan(scan_tmp).ExclusiveSum(keep ? 1u : 0u, rank, agg);
+  if (threadIdx.x == 0) {
+    if (tile == 0) {
+      st_volatile_u32(status, LB_FLAG_P | agg);
+      s_prefix = 0;
+    } else {
+      st_volatile_u32(status + tile, LB_FLAG_A | agg);
+    }
+  }
+  if (tile > 0 && threadIdx.x < 32) {
+    const uint32_t excl = lookback_exclusive(status, tile);
+    if (threadIdx.x == 0) {
+      st_volatile_u32(status + tile, LB_FLAG_P | (excl + agg));
+      s_prefix = excl;
+    }
+  }
+  __syncthreads();
+  const uint32_t slot = s_prefix + rank;
+  if (keep) {
+    rec[slot] = r;
+    if (want_coef) coef[slot] = c;
+    if (col64) {
+      col64[3 * slot] = c64[0];
+      col64[3 * slot + 1] = c64[1];
+      col64[3 * slot + 2] = c64[2];
+    }
+    keys[slot] = (unsigned long long)__double_as_longlong(r.z);
+    vals[slot] = slot;
+  }
+  if (threadIdx.x == 0 && (uint32_t)(tile + 1) * PROJ_THREADS >= n_total) counters[1] = s_prefix + agg;
+}
+
+// ------------------------------------------------------------------ K3
+__global__ void k_tile_count(const uint32_t* __restrict__ perm, const Record* __restrict__ rec,
+                             uint32_t n, uint32_t* __restrict__ cnt) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const Record& r = rec[perm[i]];
+  cnt[i] = (uint32_t)(r.tx1 - r.tx0 + 1) * (uint32_t)(r.ty1 - r.ty0 + 1);
+}
+
+__global__ void k_tile_emit(const uint32_t* __restrict__ perm, const Record* __restrict__ rec,
+                            const uint32_t* __restrict__ off, uint32_t n, int ntx,
+                            uint32_t* __restrict__ pkeys, uint32_t* __restrict__ pvals) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint32_t e = perm[i];
+  const Record& r = rec[e];
+  uint32_t o = off[i];
+  for (int ty = r.ty0; ty <= r.ty1; ++ty)
+    for (int tx = r.tx0; tx <= r.tx1; ++tx) {
+      pkeys[o] = (uint32_t)(ty * ntx + tx);
+      pvals[o] = e;
+      ++o;
+    }
+}
+
+__global__ void k_tile_ranges(const uint32_t* __restrict__ pkeys, uint32_t n,
+                              uint2* __restrict__ ranges) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint32_t t = pkeys[i];
+  if (i == 0 || pkeys[i - 1] != t) ranges[t].x = i;
+  if (i == n - 1 || pkeys[i + 1] != t) ranges[t].y = i + 1;
+}
+
+// ------------------------------------------------------------------ K4 / K5 shared
+struct TileGeom {
+  int tile, tx, ty, warp, lane, px, py;
+  bool valid;
+};
+
+__device__ __forceinline__ TileGeom tile_geom(int ntx, int width, int height) {
+  TileGeom g;
+  g.tile = blockIdx.x;
+  g.ty = g.tile / ntx;
+  g.tx = g.tile - g.ty * ntx;
+  g.warp = threadIdx.x >> 5;
+  g.lane = threadIdx.x & 31;
+  // warp w covers an 8x4 sub-tile: columns (w&1)*8.., rows (w>>1)*4..
+  g.px = g.tx * SGAD_TILE + (g.warp & 1) * 8 + (g.lane & 7);
+  g.py = g.ty * SGAD_TILE + (g.warp >> 1) * 4 + (g.lane >> 3);
+  g.valid = g.px < width && g.py < height;
+  return g;
+}
+
+struct StageSmem {
+  double u0[BATCH], v0[BATCH], thr[BATCH], s2[BATCH], op[BATCH], z[BATCH], sig[BATCH];
+  double rgb[3][BATCH];
+  uint32_t gid[BATCH];
+  uint8_t wmask[BATCH];
+};
+
+// Conservative: bit w set unless every pixel centre of warp w's 8x4 sub-tile
+// fails the reference test d2 > 9 s2 (computed with the same rounded ops, so
+// the rectangle's closest pixel gives the minimum; K4).
+__device__ __forceinline__ uint8_t warp_cull_mask(double u0, double v0, double thr, int tx, int ty,
+                                                  uint8_t active_warps) {
+  uint8_t m = 0;
+#pragma unroll
+  for (int w = 0; w < 8; ++w) {
+    if (!((active_warps >> w) & 1)) continue;
+    const double xlo = (double)(tx * SGAD_TILE + (w & 1) * 8), xhi = xlo + 7.0;
+    const double ylo = (double)(ty * SGAD_TILE + (w >> 1) * 4), yhi = ylo + 3.0;
+    double dx = 0.0, dy = 0.0;
+    if (u0 < xlo) dx = SG_SUB(u0, xlo); else if (u0 > xhi) dx = SG_SUB(u0, xhi);
+    if (v0 < ylo) dy = SG_SUB(v0, ylo); else if (v0 > yhi) dy = SG_SUB(v0, yhi);
+    const double d2 = SG_ADD(SG_MUL(dx, dx), SG_MUL(dy, dy));
+    if (!(d2 > thr)) m |= (uint8_t)(1u << w);
+  }
+  return m;
+}
+
+__device__ __forceinline__ void stage_record(StageSmem& s, int j, const Record& r,
+                                             const double* col64, uint32_t e) {
+  s.u0[j] = r.u0;
+  s.v0[j] = r.v0;
+  s.sig[j] = r.sigma;
+  const double s2 = SG_MUL(r.sigma, r.sigma);
+  s.s2[j] = s2;
+  s.thr[j] = SG_MUL(9.0, s2);
+  s.op[j] = r.opacity;
+  s.z[j] = r.z;
+  if (col64) {  // fp64 drop-in maps keep exact fp64 colours
+    s.rgb[0][j] = col64[3 * (size_t)e];
+    s.rgb[1][j] = col64[3 * (size_t)e + 1];
+    s.rgb[2][j] = col64[3 * (size_t)e + 2];
+  } else {
+    s.rgb[0][j] = r.r;
+    s.rgb[1][j] = r.g;
+    s.rgb[2][j] = r.b;
+  }
+  s.gid[j] = r.gid;
+}
+
+__device__ __forceinline__ Record load_record(const Record* rec, uint32_t e) {
+  const float4* src = reinterpret_cast<const float4*>(rec + e);
+  Record r;
+  float4* dst = reinterpret_cast<float4*>(&r);
+  dst[0] = __ldg(src);
+  dst[1] = __ldg(src + 1);
+  dst[2] = __ldg(src + 2);
+  dst[3] = __ldg(src + 3);
+  return r;
+}
+
+
+// Per-warp activity bytes are double-buffered by batch parity so one
+// __syncthreads() separates "warps publish activity" from "stage next batch".
+__device__ __forceinline__ uint32_t block_active_warps(volatile uint8_t (*flags)[8], int parity,
+                                                       bool warp_active, int warp, int lane) {
+  if (lane == 0) flags[parity][warp] = warp_active ? 1 : 0;
+  __syncthreads();
+  uint32_t act = 0;
+#pragma unroll
+  for (int w = 0; w < 8; ++w) act |= (uint32_t)flags[parity][w] << w;
+  return act;
+}
+
+// ------------------------------------------------------------------ K4
+template <bool IMAGES, bool STATE, bool LOSS>
+__global__ void __launch_bounds__(RASTER_THREADS)
+k_forward(const uint2* __restrict__ ranges, const uint32_t* __restrict__ lists,
+          const Record* __restrict__ rec, const double* __restrict__ col64, int ntx, int width,
+          int height, double* __restrict__ out_color, double* __restrict__ out_depth,
+          double* __restrict__ out_alpha, int32_t* __restrict__ out_count,
+          double* __restrict__ t_final, int32_t* __restrict__ last_out,
+          uint8_t* __restrict__ signs, sgad_loss_target tgt) {
+  __shared__ StageSmem s;
+  __shared__ volatile uint8_t s_flags[2][8];
+  __shared__ double s_red[2][8];
+  const TileGeom g = tile_geom(ntx, width, height);
+  const uint2 rg = ranges[g.tile];
+  const double pxd = (double)g.px, pyd = (double)g.py;
+  double T = 1.0, C0 = 0.0, C1 = 0.0, C2 = 0.0, D = 0.0, A = 0.0;
+  int cnt = 0, last = -1;
+  bool done = !g.valid;
+  int parity = 0;
+
+  for (uint32_t base = rg.x; base < rg.y; base += BATCH, parity ^= 1) {
+    const bool wact = __any_sync(0xffffffffu, !done);
+    const uint32_t act = block_active_warps(s_flags, parity, wact, g.warp, g.lane);
+    if (act == 0) break;
+    const uint32_t k = base + threadIdx.x;
+    uint8_t wm = 0;
+    if (k < rg.y) {
+      const uint32_t e = lists[k];
+      const Record r = load_record(rec, e);
+      stage_record(s, threadIdx.x, r, col64, e);
+      wm = warp_cull_mask(r.u0, r.v0, s.thr[threadIdx.x], g.tx, g.ty, (uint8_t)act);
+    }
+    s.wmask[threadIdx.x] = wm;
+    __syncthreads();
+    if (wact) {
+#pragma unroll 1
+      for (int c = 0; c < BATCH / 32; ++c) {
+        uint32_t m = __ballot_sync(0xffffffffu, (s.wmask[c * 32 + g.lane] >> g.warp) & 1);
+        while (m) {
+          const int j = c * 32 + __ffs(m) - 1;
+          m &= m - 1;
+          if (!done) {
+            const double dx = SG_SUB(s.u0[j], pxd), dy = SG_SUB(s.v0[j], pyd);
+            const double d2 = SG_ADD(SG_MUL(dx, dx), SG_MUL(dy, dy));
+            if (!(d2 > s.thr[j])) {
+              const double w = sgad_exp(SG_DIV(SG_MUL(-0.5, d2), s.s2[j]));
+              double a = SG_MUL(s.op[j], w);
+              if (a > SGAD_ALPHA_MAX) a = SGAD_ALPHA_MAX;
+              const double at = SG_MUL(a, T);
+              C0 = SG_ADD(C0, SG_MUL(s.rgb[0][j], at));
+              C1 = SG_ADD(C1, SG_MUL(s.rgb[1][j], at));
+              C2 = SG_ADD(C2, SG_MUL(s.rgb[2][j], at));
+              D = SG_ADD(D, SG_MUL(s.z[j], at));
+              A = SG_ADD(A, at);
+              ++cnt;
+              last = (int)(base + j);
+              T = SG_MUL(T, SG_SUB(1.0, a));
+              if (T < SGAD_TRANSMITTANCE_MIN) done = true;
+            }
+          }
+        }
+      }
+    }
+  }
+
+  const int64_t p = (int64_t)g.py * width + g.px;
+  if (g.valid) {
+    if (IMAGES) {
+      if (out_color) {
+        out_color[3 * p] = C0;
+        out_color[3 * p + 1] = C1;
+        out_color[3 * p + 2] = C2;
+      }
+      if (out_depth) out_depth[p] = D;
+      if (out_alpha) out_alpha[p] = A;
+      if (out_count) out_count[p] = cnt;
+    }
+    if (STATE) {
+      t_final[p] = T;
+      last_out[p] = last;
+    }
+  }
+  if (LOSS) {
+    double lc = 0.0, ld = 0.0;
+    uint8_t code = 0;
+    if (g.valid) {
+      const double rc[3] = {SG_SUB(C0, (double)tgt.color[3 * p]),
+                            SG_SUB(C1, (double)tgt.color[3 * p + 1]),
+                            SG_SUB(C2, (double)tgt.color[3 * p + 2])};
+#pragma unroll
+      for (int ch = 0; ch < 3; ++ch) {
+        lc += fabs(rc[ch]);
+        code |= (uint8_t)((rc[ch] > 0.0 ? 1u : (rc[ch] < 0.0 ? 2u : 0u)) << (2 * ch));
+      }
+      if (tgt.mask[p]) {
+        const double rd = SG_SUB(D, (double)tgt.depth[p]);
+        ld = fabs(rd);
+        code |= (uint8_t)((rd > 0.0 ? 1u : (rd < 0.0 ? 2u : 0u)) << 6);
+      }
+      signs[p] = code;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      lc += __shfl_xor_sync(0xffffffffu, lc, o);
+      ld += __shfl_xor_sync(0xffffffffu, ld, o);
+    }
+    if (g.lane == 0) {
+      s_red[0][g.warp] = lc;
+      s_red[1][g.warp] = ld;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double a = 0.0, b = 0.0;
+      for (int w = 0; w < 8; ++w) {
+        a += s_red[0][w];
+        b += s_red[1][w];
+      }
+      atomicAdd(tgt.loss_accum, a);
+      atomicAdd(tgt.loss_accum + 1, b);
+    }
+  }
+}
+
+// ------------------------------------------------------------------ K5
+struct BwdSmem {
+  StageSmem st;
+  uint32_t eidx[BATCH];
+  float coef[6][BATCH];
+};
+
+struct Upstream {  // fused-loss upstream scales: rho / (3HW), sigma / |U|
+  double kc, kd;
+};
+
+__device__ __forceinline__ double sign_of(uint32_t code) {
+  return code == 1u ? 1.0 : (code == 2u ? -1.0 : 0.0);
+}
+
+template <bool FUSED>
+__global__ void __launch_bounds__(RASTER_THREADS)
+k_backward(const uint2* __restrict__ ranges, const uint32_t* __restrict__ lists,
+           const Record* __restrict__ rec, const ChainCoef* __restrict__ coef,
+           const double* __restrict__ col64, int ntx, int width,
+           int height, const double* __restrict__ t_final, const int32_t* __restrict__ last_idx,
+           const uint8_t* __restrict__ signs, Upstream up, const double* __restrict__ g_color,
+           const double* __restrict__ g_depth, const double* __restrict__ g_alpha,
+           double* __restrict__ raw, float* __restrict__ grad_accum) {
+  __shared__ BwdSmem s;
+  __shared__ volatile uint8_t s_flags[2][8];
+  __shared__ int s_end;
+  const TileGeom g = tile_geom(ntx, width, height);
+  const uint2 rg = ranges[g.tile];
+  const double pxd = (double)g.px, pyd = (double)g.py;
+  const int64_t p = (int64_t)g.py * width + g.px;
+
+  double gc0 = 0.0, gc1 = 0.0, gc2 = 0.0, gd = 0.0, ga = 0.0, T = 0.0;
+  int mylast = -1;
+  if (g.valid) {
+    if (FUSED) {
+      const uint32_t code = signs[p];
+      // mapper.py:145-152: rho * sign / n_color; sigma * sign * mask / n_depth
+      gc0 = SG_MUL(up.kc, sign_of(code & 3u));
+      gc1 = SG_MUL(up.kc, sign_of((code >> 2) & 3u));
+      gc2 = SG_MUL(up.kc, sign_of((code >> 4) & 3u));
+      gd = SG_MUL(up.kd, sign_of((code >> 6) & 3u));
+    } else {
+      gc0 = g_color[3 * p];
+      gc1 = g_color[3 * p + 1];
+      gc2 = g_color[3 * p + 2];
+      gd = g_depth[p];
+      ga = g_alpha[p];
+    }
+    const bool any = !(gc0 == 0.0 && gc1 == 0.0 && gc2 == 0.0 && gd == 0.0 && ga == 0.0);
+    if (any) {
+      mylast = last_idx[p];
+      T = t_final[p];
+    }
+  }
+  if (threadIdx.x == 0) s_end = (int)rg.x;
+  __syncthreads();
+  if (mylast >= 0) atomicMax(&s_end, mylast + 1);
+  __syncthreads();
+  const int end = s_end;
+
+  double sc0 = 0.0, sc1 = 0.0, sc2 = 0.0, sd = 0.0, sa = 0.0;
+  int parity = 0;
+  for (int bend = end; bend > (int)rg.x; bend -= BATCH, parity ^= 1) {
+    const int bstart = max((int)rg.x, bend - BATCH);
+    const bool wact = __any_sync(0xffffffffu, mylast >= bstart);
+    const uint32_t act = block_active_warps(s_flags, parity, wact, g.warp, g.lane);
+    if (act == 0) continue;  // uniform across the block
+    const int k = bstart + (int)threadIdx.x;
+    uint8_t wm = 0;
+    if (k < bend) {
+      const uint32_t e = lists[k];
+      const Record r = load_record(rec, e);
+      stage_record(s.st, threadIdx.x, r, col64, e);
+      s.eidx[threadIdx.x] = e;
+      if (FUSED) {
+        const ChainCoef cc = coef[e];
+        s.coef[0][threadIdx.x] = cc.k_r;
+        s.coef[1][threadIdx.x] = cc.a_u;
+        s.coef[2][threadIdx.x] = cc.a_v;
+        s.coef[3][threadIdx.x] = cc.a_z;
+        s.coef[4][threadIdx.x] = cc.a_s;
+        s.coef[5][threadIdx.x] = cc.k_op;
+      }
+      wm = warp_cull_mask(r.u0, r.v0, s.st.thr[threadIdx.x], g.tx, g.ty, (uint8_t)act);
+    }
+    s.st.wmask[threadIdx.x] = wm;
+    __syncthreads();
+    if (wact) {
+#pragma unroll 1
+      for (int c = BATCH / 32 - 1; c >= 0; --c) {
+        uint32_t m = __ballot_sync(0xffffffffu, (s.st.wmask[c * 32 + g.lane] >> g.warp) & 1);
+        while (m) {
+          const int hb = 31 - __clz(m);
+          m &= ~(1u << hb);
+          const int j = c * 32 + hb;
+          const int kk = bstart + j;
+          bool contrib = false;
+          float q[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+          if (kk <= mylast) {
+            const double dx = SG_SUB(s.st.u0[j], pxd), dy = SG_SUB(s.st.v0[j], pyd);
+            const double d2 = SG_ADD(SG_MUL(dx, dx), SG_MUL(dy, dy));
+            if (!(d2 > s.st.thr[j])) {
+              const double s2 = s.st.s2[j], op = s.st.op[j], z = s.st.z[j];
+              const double w = sgad_exp(SG_DIV(SG_MUL(-0.5, d2), s2));
+              const double aw = SG_MUL(op, w);
+              const bool clamped = aw > SGAD_ALPHA_MAX;
+              const double a = clamped ? SGAD_ALPHA_MAX : aw;
+              const double om = SG_SUB(1.0, a);
+              const double tb = SG_DIV(T, om);
+              const double at = SG_MUL(a, tb);
+              const double c0 = s.st.rgb[0][j], c1 = s.st.rgb[1][j], c2 = s.st.rgb[2][j];
+              const uint32_t gidw = s.st.gid[j];
+              if (gidw & GID_LEARN) {
+                double d_alpha = SG_MUL(gc0, SG_SUB(SG_MUL(c0, tb), SG_DIV(sc0, om)));
+                d_alpha = SG_ADD(d_alpha, SG_MUL(gc1, SG_SUB(SG_MUL(c1, tb), SG_DIV(sc1, om))));
+                d_alpha = SG_ADD(d_alpha, SG_MUL(gc2, SG_SUB(SG_MUL(c2, tb), SG_DIV(sc2, om))));
+                d_alpha = SG_ADD(d_alpha, SG_MUL(gd, SG_SUB(SG_MUL(z, tb), SG_DIV(sd, om))));
+                d_alpha = SG_ADD(d_alpha, SG_MUL(ga, SG_SUB(tb, SG_DIV(sa, om))));
+                const double gcol0 = SG_MUL(gc0, at), gcol1 = SG_MUL(gc1, at),
+                             gcol2 = SG_MUL(gc2, at), gz = SG_MUL(gd, at);
+                double gop = 0.0, gsig = 0.0, gu = 0.0, gv = 0.0;
+                if (!clamped) {
+                  const double gw = SG_MUL(d_alpha, op);
+                  gop = SG_MUL(d_alpha, w);
+                  gsig = SG_DIV(SG_MUL(SG_MUL(gw, w), d2), SG_MUL(s2, s.st.sig[j]));
+                  const double gd2 = SG_MUL(gw, SG_DIV(SG_MUL(-0.5, w), s2));
+                  gu = SG_MUL(SG_MUL(gd2, 2.0), dx);
+                  gv = SG_MUL(SG_MUL(gd2, 2.0), dy);
+                }
+                if (FUSED) {
+                  q[0] = (float)(s.coef[1][j] * gu + s.coef[2][j] * gv + s.coef[3][j] * gz +
+                                 s.coef[4][j] * gsig);
+                  q[1] = (float)(s.coef[0][j] * gsig);
+                  q[2] = (float)(s.coef[5][j] * gop);
+                  q[3] = (float)gcol0;
+                  q[4] = (float)gcol1;
+                  q[5] = (float)gcol2;
+                  contrib = true;
+                } else {
+                  double* dst = raw + (size_t)s.eidx[j] * 8;
+                  atomicAdd(dst + 0, gcol0);
+                  atomicAdd(dst + 1, gcol1);
+                  atomicAdd(dst + 2, gcol2);
+                  atomicAdd(dst + 3, gop);
+                  atomicAdd(dst + 4, gu);
+                  atomicAdd(dst + 5, gv);
+                  atomicAdd(dst + 6, gsig);
+                  atomicAdd(dst + 7, gz);
+                }
+              }
+              sc0 = SG_ADD(sc0, SG_MUL(c0, at));
+              sc1 = SG_ADD(sc1, SG_MUL(c1, at));
+              sc2 = SG_ADD(sc2, SG_MUL(c2, at));
+              sd = SG_ADD(sd, SG_MUL(z, at));
+              sa = SG_ADD(sa, at);
+              T = tb;
+            }
+          }
+          if (FUSED) {
+            if (__any_sync(0xffffffffu, contrib)) {
+#pragma unroll
+              for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+                for (int i = 0; i < 6; ++i) q[i] += __shfl_xor_sync(0xffffffffu, q[i], o);
+              }
+              if (g.lane == 0) {
+                float4* dst = reinterpret_cast<float4*>(grad_accum + (size_t)(s.st.gid[j] & ~GID_LEARN) * 8);
+                atomicAdd(dst, make_float4(q[0], q[1], q[2], q[3]));
+                atomicAdd(reinterpret_cast<float2*>(dst + 1), make_float2(q[4], q[5]));
+              }
+            }
+          }
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// Exact-mode chain rule (rasterizer.py:462-483) from per-survivor fp64 sums.
+__global__ void k_chain_exact(const Record* __restrict__ rec, const double* __restrict__ raw,
+                              uint32_t n_surv, const sgad_frame* __restrict__ frames, int n_frames,
+                              sgad_camera cam, double* const* __restrict__ map_grads) {
+  const uint32_t e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n_surv) return;
+  const uint32_t gidw = rec[e].gid;
+  if (!(gidw & GID_LEARN)) return;
+  const uint32_t gid = gidw & ~GID_LEARN;
+  const int fi = find_frame(frames, n_frames, gid);
+  double* out = map_grads[fi];
+  if (!out) return;
+  const sgad_frame& f = frames[fi];
+  const int64_t hw = (int64_t)f.height * f.width;
+  const int64_t p = (int64_t)gid - f.gauss_offset;
+  Proj o;
+  project_point(f, p, hw, cam, o);
+  const double* rg = raw + (size_t)e * 8;
+  const double g_op = rg[3], g_u0 = rg[4], g_v0 = rg[5], g_sig = rg[6], g_z = rg[7];
+  const double z = o.z, z2 = SG_MUL(z, z);
+  const double g_radius = SG_DIV(SG_MUL(g_sig, cam.fx), z);
+  double g_zt = SG_SUB(g_z, SG_DIV(SG_MUL(g_sig, o.sig), z));
+  g_zt = SG_SUB(g_zt, SG_DIV(SG_MUL(SG_MUL(g_u0, cam.fx), o.y[0]), z2));
+  g_zt = SG_SUB(g_zt, SG_DIV(SG_MUL(SG_MUL(g_v0, cam.fy), o.y[1]), z2));
+  const double g_y0 = SG_DIV(SG_MUL(g_u0, cam.fx), z);
+  const double g_y1 = SG_DIV(SG_MUL(g_v0, cam.fy), z);
+  const double g_dadj =
+      SG_ADD(SG_ADD(SG_MUL(g_y0, o.dir[0]), SG_MUL(g_y1, o.dir[1])), SG_MUL(g_zt, o.dir[2]));
+  const double sgn = o.bd >= 0.0 ? 1.0 : -1.0;
+  out[p] += SG_MUL(g_dadj, sgn);
+  out[hw + p] += g_radius;
+  out[2 * hw + p] += SG_MUL(SG_MUL(g_op, o.op), SG_SUB(1.0, o.op));
+  out[3 * hw + p] += rg[0];
+  out[4 * hw + p] += rg[1];
+  out[5 * hw + p] += rg[2];
+}
+
+__global__ void k_rank_of(const uint32_t* __restrict__ perm, uint32_t n, uint32_t* __restrict__ rank) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) rank[perm[i]] = i;
+}
+
+__global__ void k_export_lists(const uint32_t* __restrict__ pvals, const uint32_t* __restrict__ rank,
+                               uint32_t n, int64_t* __restrict__ out) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = rank[pvals[i]];
+}
+
+__global__ void k_export_ranges(const uint2* __restrict__ r, int n, int64_t* __restrict__ out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) {
+    out[2 * i] = r[i].x;
+    out[2 * i + 1] = r[i].y;
+  }
+}
+
+__global__ void k_export_surv(const uint32_t* __restrict__ perm, const Record* __restrict__ rec,
+                              uint32_t n, int64_t* gid, double* u0, double* v0, double* z,
+                              double* sigma, double* opacity) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const Record& r = rec[perm[i]];
+  if (gid) gid[i] = r.gid & ~GID_LEARN;
+  if (u0) u0[i] = r.u0;
+  if (v0) v0[i] = r.v0;
+  if (z) z[i] = r.z;
+  if (sigma) sigma[i] = r.sigma;
+  if (opacity) opacity[i] = r.opacity;
+}
+
+static inline unsigned blocks_for(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
+
+static int bits_for(uint32_t maxval) {
+  int b = 1;
+  while (b < 32 && (maxval >> b) != 0) ++b;
+  return b;
+}
+
+}  // namespace sgad
+
+using namespace sgad;
+
+extern "C" {
+
+const char* sgad_last_error(void) { return g_err; }
+int sgad_version(void) { return 1; }
+
+int sgad_raster_create(sgad_raster** out) {
+  SGAD_REQUIRE(out != nullptr, "sgad_raster_create: null out");
+  sgad_raster* h = new sgad_raster();
+  cudaError_t e = cudaMallocHost(&h->pinned, 16 * sizeof(uint32_t));
+  if (e != cudaSuccess) {
+    delete h;
+    set_error("cudaMallocHost: %s", cudaGetErrorString(e));
+    return SGAD_E_CUDA;
+  }
+  *out = h;
+  return SGAD_OK;
+}
+
+int sgad_raster_destroy(sgad_raster* h) {
+  if (!h) return SGAD_OK;
+  DevBuf* bufs[] = {&h->frames, &h->status, &h->counters, &h->records, &h->coef, &h->keys0,
+                    &h->keys1, &h->vals0, &h->vals1, &h->pcount, &h->poffset, &h->pkeys0,
+                    &h->pkeys1, &h->pvals0, &h->pvals1, &h->ranges, &h->cub_tmp,
+                    &h->trans_final, &h->last_idx, &h->signs, &h->raw_grads, &h->rank_of,
+                    &h->scratch, &h->col64};
+  for (DevBuf* b : bufs) b->release();
+  if (h->pinned) cudaFreeHost(h->pinned);
+  delete h;
+  return SGAD_OK;
+}
+
+int sgad_raster_tile_count(sgad_raster* h, int64_t* n_tiles) {
+  SGAD_REQUIRE(h && n_tiles, "sgad_raster_tile_count: null argument");
+  *n_tiles = h->n_tiles;
+  return SGAD_OK;
+}
+
+int sgad_raster_prepare(sgad_raster* h, const sgad_frame* frames, int32_t n_frames,
+                        const sgad_camera* cam, int32_t want_coef, void* stream_,
+                        int64_t* n_survivors, int64_t* n_pairs) {
+  SGAD_REQUIRE(h && cam && n_frames >= 0 && (n_frames == 0 || frames), "sgad_raster_prepare: bad args");
+  SGAD_REQUIRE(cam->width > 0 && cam->height > 0, "sgad_raster_prepare: empty camera");
+  cudaStream_t st = (cudaStream_t)stream_;
+  h->prepared = h->forwarded = h->fused_ready = 0;
+  h->cam = *cam;
+  h->ntx = (cam->width + SGAD_TILE - 1) / SGAD_TILE;
+  h->nty = (cam->height + SGAD_TILE - 1) / SGAD_TILE;
+  h->n_tiles = h->ntx * h->nty;
+  SGAD_REQUIRE(h->ntx <= 65535 && h->nty <= 65535, "image too large");
+  h->host_frames.assign(frames, frames + n_frames);
+  int64_t n_total = 0;
+  for (int i = 0; i < n_frames; ++i) {
+    SGAD_REQUIRE(frames[i].gauss_offset == n_total, "frames must be packed: gauss_offset[%d]", i);
+    n_total += (int64_t)frames[i].height * frames[i].width;
+  }
+  SGAD_REQUIRE(n_total < (1ll << 30), "too many Gaussians (%lld)", (long long)n_total);
+  h->n_total = n_total;
+  h->have_coef = want_coef != 0;
+  h->any_f64 = 0;
+  for (int i = 0; i < n_frames; ++i) h->any_f64 |= frames[i].planes_f64 ? 1 : 0;
+  const int64_t nt = h->n_tiles;
+  SGAD_CHECK_CUDA(h->ranges.ensure(sizeof(uint2) * nt));
+  SGAD_CHECK_CUDA(cudaMemsetAsync(h->ranges.p, 0, sizeof(uint2) * nt, st));
+  if (n_total == 0) {
+    h->n_surv = h->n_pairs = 0;
+    *n_survivors = *n_pairs = 0;
+    h->prepared = 1;
+    return SGAD_OK;
+  }
+  const int64_t n_tiles_proj = (n_total + PROJ_THREADS - 1) / PROJ_THREADS;
+  SGAD_CHECK_CUDA(h->frames.ensure(sizeof(sgad_frame) * n_frames));
+  SGAD_CHECK_CUDA(h->status.ensure(sizeof(uint32_t) * n_tiles_proj));
+  SGAD_CHECK_CUDA(h->counters.ensure(sizeof(uint32_t) * 8));
+  SGAD_CHECK_CUDA(h->records.ensure(sizeof(Record) * n_total));
+  if (want_coef) SGAD_CHECK_CUDA(h->coef.ensure(sizeof(ChainCoef) * n_total));
+  if (h->any_f64) SGAD_CHECK_CUDA(h->col64.ensure(sizeof(double) * 3 * n_total));
+  SGAD_CHECK_CUDA(h->keys0.ensure(sizeof(unsigned long long) * n_total));
+  SGAD_CHECK_CUDA(h->keys1.ensure(sizeof(unsigned long long) * n_total));
+  SGAD_CHECK_CUDA(h->vals0.ensure(sizeof(uint32_t) * n_total));
+  SGAD_CHECK_CUDA(h->vals1.ensure(sizeof(uint32_t) * n_total));
+  SGAD_CHECK_CUDA(cudaMemcpyAsync(h->frames.p, frames, sizeof(sgad_frame) * n_frames,
+                                  cudaMemcpyHostToDevice, st));
+  SGAD_CHECK_CUDA(cudaMemsetAsync(h->status.p, 0, sizeof(uint32_t) * n_tiles_proj, st));
+  SGAD_CHECK_CUDA(cudaMemsetAsync(h->counters.p, 0, sizeof(uint32_t) * 8, st));
+  k_project<<<(unsigned)n_tiles_proj, PROJ_THREADS, 0, st>>>(
+      h->frames.as<sgad_frame>(), n_frames, *cam, (uint32_t)n_total, h->ntx, h->nty, want_coef,
+      h->records.as<Record>(), h->coef.as<ChainCoef>(), h->any_f64 ? h->col64.as<double>() : nullptr,
+      h->keys0.as<unsigned long long>(),
+      h->vals0.as<uint32_t>(), h->status.as<uint32_t>(), h->counters.as<uint32_t>());
+  SGAD_LAUNCH_CHECK();
+  SGAD_CHECK_CUDA(cudaMemcpyAsync(h->pinned, h->counters.as<uint32_t>() + 1, sizeof(uint32_t),
+                                  cudaMemcpyDeviceToHost, st));
+  SGAD_CHECK_CUDA(cudaStreamSynchronize(st));
+  const uint32_t ns = h->pinned[0];
+  h->n_surv = ns;
+  *n_survivors = ns;
+  if (ns == 0) {
+    h->n_pairs = 0;
+    *n_pairs = 0;
+    h->prepared = 1;
+    return SGAD_OK;
+  }
+  // K2: stable LSD radix sort of the fp64 depth bits (z > 0, so bit 63 is 0);
+  // ties keep emission = (frame, pixel) order, matching np.lexsort.
+  cub::DoubleBuffer<unsigned long long> dk(h->keys0.as<unsigned long long>(),
+                                           h->keys1.as<unsigned long long>());
+  cub::DoubleBuffer<uint32_t> dv(h->vals0.as<uint32_t>(), h->vals1.as<uint32_t>());
+  size_t tmp = 0;
+  SGAD_CHECK_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, dk, dv, (int)ns, 0, 63, st));
+  SGAD_CHECK_CUDA(h->cub_tmp.ensure(tmp));
+  SGAD_CHECK_CUDA(cub::DeviceRadixSort::SortPairs(h->cub_tmp.p, tmp, dk, dv, (int)ns, 0, 63, st));
+  uint32_t* perm = dv.Current();
+  // keep the permutation in vals0 for later kernels
+  if (perm != h->vals0.as<uint32_t>()) {
+    SGAD_CHECK_CUDA(cudaMemcpyAsync(h->vals0.p, perm, sizeof(uint32_t) * ns,
+                                    cudaMemcpyDeviceToDevice, st));
+    perm = h->vals0.as<uint32_t>();
+  }
+  // K3: per-survivor tile counts in depth order, exclusive scan, emit, stable tile sort
+  SGAD_CHECK_CUDA(h->pcount.ensure(sizeof(uint32_t) * (ns + 1)));
+  SGAD_CHECK_CUDA(h->poffset.ensure(sizeof(uint32_t) * (ns + 1)));
+  k_tile_count<<<blocks_for(ns, 256), 256, 0, st>>>(perm, h->records.as<Record>(), ns,
+                                                    h->pcount.as<uint32_t>());
+  SGAD_LAUNCH_CHECK();
+  SGAD_CHECK_CUDA(cudaMemsetAsync(h->pcount.as<uint32_t>() + ns, 0, sizeof(uint32_t), st));
+  tmp = 0;
+  SGAD_CHECK_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, h->pcount.as<uint32_t>(),
+                                                h->poffset.as<uint32_t>(), (int)ns + 1, st));
+  SGAD_CHECK_CUDA(h->cub_tmp.ensure(tmp));
+  SGAD_CHECK_CUDA(cub::DeviceScan::ExclusiveSum(h->cub_tmp.p, tmp, h->pcount.as<uint32_t>(),
+                                                h->poffset.as<uint32_t>(), (int)ns + 1, st));
+  SGAD_CHECK_CUDA(cudaMemcpyAsync(h->pinned + 1, h->poffset.as<uint32_t>() + ns, sizeof(uint32_t),
+                                  cudaMemcpyDeviceToHost, st));
+  SGAD_CHECK_CUDA(cudaStreamSynchronize(st));
+  const uint32_t np_ = h->pinned[1];
+  h->n_pairs = np_;
+  *n_pairs = np_;
+  SGAD_CHECK_CUDA(h->pkeys0.ensure(sizeof(uint32_t) * (np_ + 1)));
+  SGAD_CHECK_CUDA(h->pkeys1.ensure(sizeof(uint32_t) * (np_ + 1)));
+  SGAD_CHECK_CUDA(h->pvals0.ensure(sizeof(uint32_t) * (np_ + 1)));
+  SGAD_CHECK_CUDA(h->pvals1.ensure(sizeof(uint32_t) * (np_ + 1)));
+  k_tile_emit<<<blocks_for(ns, 256), 256, 0, st>>>(perm, h->records.as<Record>(),
+                                                   h->poffset.as<uint32_t>(), ns, h->ntx,
+                                                   h->pkeys0.as<uint32_t>(), h->pvals0.as<uint32_t>());
+  SGAD_LAUNCH_CHECK();
+  cub::DoubleBuffer<uint32_t> pk(h->pkeys0.as<uint32_t>(), h->pkeys1.as<uint32_t>());
+  cub::DoubleBuffer<uint32_t> pv(h->pvals0.as<uint32_t>(), h->pvals1.as<uint32_t>());
+  const int tbits = bits_for((uint32_t)(h->n_tiles - 1));
+  tmp = 0;
+  SGAD_CHECK_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, pk, pv, (int)np_, 0, tbits, st));
+  SGAD_CHECK_CUDA(h->cub_tmp.ensure(tmp));
+  SGAD_CHECK_CUDA(cub::DeviceRadixSort::SortPairs(h->cub_tmp.p, tmp, pk, pv, (int)np_, 0, tbits, st));
+  if (pk.Current() != h->pkeys0.as<uint32_t>()) {
+    SGAD_CHECK_CUDA(cudaMemcpyAsync(h->pkeys0.p, pk.Current(), sizeof(uint32_t) * np_,
+                                    cudaMemcpyDeviceToDevice, st));
+    SGAD_CHECK_CUDA(cudaMemcpyAsync(h->pvals0.p, pv.Current(), sizeof(uint32_t) * np_,
+                                    cudaMemcpyDeviceToDevice, st));
+  }
+  k_tile_ranges<<<blocks_for(np_, 256), 256, 0, st>>>(h->pkeys0.as<uint32_t>(), np_,
+                                                      h->ranges.as<uint2>());
+  SGAD_LAUNCH_CHECK();
+  h->prepared = 1;
+  return SGAD_OK;
+}
+
+int sgad_raster_forward(sgad_raster* h, double* out_color, double* out_depth, double* out_alpha,
+                        int32_t* out_count, int32_t save_state, const sgad_loss_target* target,
+                        void* stream_) {
+  SGAD_REQUIRE(h && h->prepared, "sgad_raster_forward: view not prepared");
+  cudaStream_t st = (cudaStream_t)stream_;
+  const int64_t npx = (int64_t)h->cam.width * h->cam.height;
+  const bool images = out_color || out_depth || out_alpha || out_count;
+  const bool loss = target != nullptr;
+  const bool state = save_state || loss;
+  if (state) {
+    SGAD_CHECK_CUDA(h->trans_final.ensure(sizeof(double) * npx));
+    SGAD_CHECK_CUDA(h->last_idx.ensure(sizeof(int32_t) * npx));
+  }
+  sgad_loss_target tg{};
+  if (loss) {
+    SGAD_REQUIRE(target->color && target->depth && target->mask && target->loss_accum,
+                 "sgad_raster_forward: incomplete loss target");
+    SGAD_CHECK_CUDA(h->signs.ensure(npx));
+    tg = *target;
+    h->rho = target->rho;
+    h->sigma_d = target->sigma;
+    h->n_depth = target->n_depth;
+  }
+  const dim3 grid((unsigned)h->n_tiles), block(RASTER_THREADS);
+  const double* col64 = h->any_f64 ? h->col64.as<double>() : nullptr;
+#define SGAD_FWD(I, S, L)                                                                      \
+  k_forward<I, S, L><<<grid, block, 0, st>>>(                                                \
+      h->ranges.as<uint2>(), h->pvals0.as<uint32_t>(), h->records.as<Record>(), col64, h->ntx, \
+      h->cam.width, h->cam.height, out_color, out_depth, out_alpha, out_count,               \
+      h->trans_final.as<double>(), h->last_idx.as<int32_t>(), h->signs.as<uint8_t>(), tg)
+  if (images && state && loss) SGAD_FWD(true, true, true);
+  else if (images && state) SGAD_FWD(true, true, false);
+  else if (images) SGAD_FWD(true, false, false);
+  else if (loss) SGAD_FWD(false, true, true);
+  else if (state) SGAD_FWD(false, true, false);
+  else SGAD_FWD(true, false, false);
+#undef SGAD_FWD
+  SGAD_LAUNCH_CHECK();
+  h->forwarded = state ? 1 : 0;
+  h->fused_ready = loss ? 1 : 0;
+  return SGAD_OK;
+}
+
+int sgad_raster_backward(sgad_raster* h, int32_t mode, const double* g_color,
+                         const double* g_depth, const double* g_alpha, double* const* map_grads,
+                         float* grad_accum, void* stream_) {
+  SGAD_REQUIRE(h && h->prepared && h->forwarded, "sgad_raster_backward: run forward with state first");
+  cudaStream_t st = (cudaStream_t)stream_;
+  if (h->n_surv == 0) return SGAD_OK;
+  const dim3 grid((unsigned)h->n_tiles), block(RASTER_THREADS);
+  const int64_t npx = (int64_t)h->cam.width * h->cam.height;
+  if (mode == 1) {
+    SGAD_REQUIRE(h->fused_ready && h->have_coef && grad_accum,
+                 "fused backward needs a loss forward, chain coefficients and grad_accum");
+    Upstream up;
+    up.kc = h->rho / (double)(3 * npx);
+    up.kd = h->n_depth > 0 ? h->sigma_d / (double)h->n_depth : 0.0;
+    k_backward<true><<<grid, block, 0, st>>>(
+        h->ranges.as<uint2>(), h->pvals0.as<uint32_t>(), h->records.as<Record>(),
+        h->coef.as<ChainCoef>(), h->any_f64 ? h->col64.as<double>() : nullptr, h->ntx,
+        h->cam.width, h->cam.height,
+        h->trans_final.as<double>(), h->last_idx.as<int32_t>(), h->signs.as<uint8_t>(), up,
+        nullptr, nullptr, nullptr, nullptr, grad_accum);
+    SGAD_LAUNCH_CHECK();
+    return SGAD_OK;
+  }
+  SGAD_REQUIRE(mode == 0 && g_color && g_depth && g_alpha && map_grads,
+               "exact backward needs upstream images and map_grads");
+  const int n_frames = (int)h->host_frames.size();
+  SGAD_CHECK_CUDA(h->raw_grads.ensure(sizeof(double) * 8 * h->n_surv));
+  SGAD_CHECK_CUDA(cudaMemsetAsync(h->raw_grads.p, 0, sizeof(double) * 8 * h->n_surv, st));
+  SGAD_CHECK_CUDA(h->scratch.ensure(sizeof(double*) * n_frames));
+  SGAD_CHECK_CUDA(cudaMemcpyAsync(h->scratch.p, map_grads, sizeof(double*) * n_frames,
+                                  cudaMemcpyHostToDevice, st));
+  Upstream up{0.0, 0.0};
+  k_backward<false><<<grid, block, 0, st>>>(
+      h->ranges.as<uint2>(), h->pvals0.as<uint32_t>(), h->records.as<Record>(), nullptr,
+      h->any_f64 ? h->col64.as<double>() : nullptr, h->ntx, h->cam.width, h->cam.height, h->trans_final.as<double>(), h->last_idx.as<int32_t>(),
+      nullptr, up, g_color, g_depth, g_alpha, h->raw_grads.as<double>(), nullptr);
+  SGAD_LAUNCH_CHECK();
+  k_chain_exact<<<blocks_for(h->n_surv, 256), 256, 0, st>>>(
+      h->records.as<Record>(), h->raw_grads.as<double>(), (uint32_t)h->n_surv,
+      h->frames.as<sgad_frame>(), n_frames, h->cam, h->scratch.as<double*>());
+  SGAD_LAUNCH_CHECK();
+  // the pointer table is read by the kernel; keep the host copy alive until done
+  SGAD_CHECK_CUDA(cudaStreamSynchronize(st));
+  return SGAD_OK;
+}
+
+int sgad_raster_get_survivors(sgad_raster* h, int64_t* gid, double* u0, double* v0, double* z,
+                              double* sigma, double* opacity, void* stream_) {
+  SGAD_REQUIRE(h && h->prepared, "sgad_raster_get_survivors: view not prepared");
+  if (h->n_surv == 0) return SGAD_OK;
+  k_export_surv<<<blocks_for(h->n_surv, 256), 256, 0, (cudaStream_t)stream_>>>(
+      h->vals0.as<uint32_t>(), h->records.as<Record>(), (uint32_t)h->n_surv, gid, u0, v0, z,
+      sigma, opacity);
+  SGAD_LAUNCH_CHECK();
+  return SGAD_OK;
+}
+
+int sgad_raster_get_tiles(sgad_raster* h, int64_t* ranges, int64_t* lists, void* stream_) {
+  SGAD_REQUIRE(h && h->prepared, "sgad_raster_get_tiles: view not prepared");
+  cudaStream_t st = (cudaStream_t)stream_;
+  if (ranges) {
+    k_export_ranges<<<blocks_for(h->n_tiles, 256), 256, 0, st>>>(h->ranges.as<uint2>(),
+                                                                 h->n_tiles, ranges);
+    SGAD_LAUNCH_CHECK();
+  }
+  if (lists && h->n_pairs > 0) {
+    SGAD_CHECK_CUDA(h->rank_of.ensure(sizeof(uint32_t) * h->n_surv));
+    k_rank_of<<<blocks_for(h->n_surv, 256), 256, 0, st>>>(h->vals0.as<uint32_t>(),
+                                                          (uint32_t)h->n_surv,
+                                                          h->rank_of.as<uint32_t>());
+    SGAD_LAUNCH_CHECK();
+    k_export_lists<<<blocks_for(h->n_pairs, 256), 256, 0, st>>>(
+        h->pvals0.as<uint32_t>(), h->rank_of.as<uint32_t>(), (uint32_t)h->n_pairs, lists);
+    SGAD_LAUNCH_CHECK();
+  }
+  return SGAD_OK;
+}
+
+}  // extern "C"

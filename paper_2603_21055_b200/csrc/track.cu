@@ -1,0 +1,849 @@
+// Tracking hot path: local geometry Gaussian fit (K7), exact 1-NN grid
+// (K10), fused GICP normal equations (K8) and frozen-weight cost (K9).
+//
+// Restates /root/reference/pkg/src/raysplat/tracker.py and geometry.py:
+//   K7  <- build_local_set :193-230 / _fit_oriented_gaussians :144-170 with the
+//          5x5 window neighbourhood of north_star (delta D2), sym_eigh3_batch
+//          geometry.py:275-353
+//   K10 <- GlobalGeomSet.query_nearest :125-128 (scipy cKDTree exact 1-NN)
+//   K8  <- gicp_align :286-321 (gate, C_b + R C_a R^T, W = C^-1, H, g, cost)
+//   K9  <- gicp_align :312-314,329-333 (cost_at for step halving)
+// Everything is fp64: the sizes are small (M ~ 1e5) and the passes are
+// latency-bound, so fp64 costs nothing measurable and keeps H within the
+// 1e-3 parity bar with margin.  Reductions are two-stage and deterministic.
+#include <cub/cub.cuh>
+
+#include "common.cuh"
+
+namespace sgad {
+
+constexpr int TRK_THREADS = 256;
+constexpr double EIG_GAP_FALLBACK = 1e-8;
+constexpr double EIGVAL_FLOOR_REL = 1e-6;
+
+// ---------------------------------------------------------------- 3x3 eig
+__device__ __forceinline__ double det3(const double* a) {
+  return a[0] * (a[4] * a[8] - a[5] * a[7]) - a[1] * (a[3] * a[8] - a[5] * a[6]) +
+         a[2] * (a[3] * a[7] - a[4] * a[6]);
+}
+
+__device__ __forceinline__ void matmul3(const double* a, const double* b, double* c) {
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j)
+      c[3 * i + j] = a[3 * i] * b[j] + a[3 * i + 1] * b[3 + j] + a[3 * i + 2] * b[6 + j];
+}
+
+// column of `a` with the largest norm, normalised (geometry.py:339-343)
+__device__ __forceinline__ void principal_column(const double* a, double* v) {
+  double best = -1.0;
+  int idx = 0;
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    const double n = sqrt(a[c] * a[c] + a[3 + c] * a[3 + c] + a[6 + c] * a[6 + c]);
+    if (n > best) {
+      best = n;
+      idx = c;
+    }
+  }
+  const double n = sqrt(a[idx] * a[idx] + a[3 + idx] * a[3 + idx] + a[6 + idx] * a[6 + idx]);
+  v[0] = a[idx] / n;
+  v[1] = a[3 + idx] / n;
+  v[2] = a[6 + idx] / n;
+}
+
+// Cyclic Jacobi for the near-degenerate cases the reference hands to LAPACK
+// (geometry.py:320-324); eigenvalues descending, vectors in columns.
+__device__ void jacobi_eig3(const double* m, double* rot, double* vals) {
+  double a[9], v[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1};
+#pragma unroll
+  for (int i = 0; i < 9; ++i) a[i] = m[i];
+  for (int sweep = 0; sweep < 32; ++sweep) {
+    const double off = a[1] * a[1] + a[2] * a[2] + a[5] * a[5];
+    if (off == 0.0) break;
+    for (int pq = 0; pq < 3; ++pq) {
+      const int p = pq == 2 ? 1 : 0, q = pq == 0 ? 1 : 2;
+      const double apq = a[3 * p + q];
+      if (apq == 0.0) continue;
+      const double theta = (a[3 * q + q] - a[3 * p + p]) / (2.0 * apq);
+      const double t = (theta >= 0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
+      const double c = 1.0 / sqrt(t * t + 1.0), s = t * c;
+      for (int k = 0; k < 3; ++k) {  // A <- A J
+        const double akp = a[3 * k + p], akq = a[3 * k + q];
+        a[3 * k + p] = c * akp - s * akq;
+        a[3 * k + q] = s * akp + c * akq;
+      }
+      for (int k = 0; k < 3; ++k) {  // A <- J^T A
+        const double apk = a[3 * p + k], aqk = a[3 * q + k];
+        a[3 * p + k] = c * apk - s * aqk;
+        a[3 * q + k] = s * apk + c * aqk;
+      }
+      for (int k = 0; k < 3; ++k) {
+        const double vkp = v[3 * k + p], vkq = v[3 * k + q];
+        v[3 * k + p] = c * vkp - s * vkq;
+        v[3 * k + q] = s * vkp + c * vkq;
+      }
+    }
+  }
+  int order[3] = {0, 1, 2};
+  double d[3] = {a[0], a[4], a[8]};
+  for (int i = 0; i < 2; ++i)
+    for (int j = 0; j < 2 - i; ++j)
+      if (d[order[j]] < d[order[j + 1]]) {
+        int t = order[j];
+        order[j] = order[j + 1];
+        order[j + 1] = t;
+      }
+  for (int c = 0; c < 3; ++c) {
+    vals[c] = d[order[c]];
+    for (int r = 0; r < 3; ++r) rot[3 * r + c] = v[3 * r + order[c]];
+  }
+}
+
+// geometry.py:275-332 for one matrix; rot row-major with eigenvectors as columns.
+__device__ void sym_eigh3(const double* m, double* rot, double* vals) {
+  const double q = (m[0] + m[4] + m[8]) / 3.0;
+  const double off = m[1] * m[1] + m[2] * m[2] + m[5] * m[5];
+  const double d0 = m[0] - q, d1 = m[4] - q, d2 = m[8] - q;
+  const double p2 = (d0 * d0 + d1 * d1 + d2 * d2) + 2.0 * off;
+  double scale = 0.0;
+#pragma unroll
+  for (int i = 0; i < 9; ++i) scale = fmax(scale, fabs(m[i]));
+  scale = fmax(scale, 1e-300);
+  if (p2 <= (1e-14 * scale) * (1e-14 * scale)) {
+    vals[0] = vals[1] = vals[2] = q;
+#pragma unroll
+    for (int i = 0; i < 9; ++i) rot[i] = (i % 4 == 0) ? 1.0 : 0.0;
+  } else {
+    const double p = sqrt(p2 / 6.0);
+    double b[9];
+#pragma unroll
+    for (int i = 0; i < 9; ++i) b[i] = (m[i] - ((i % 4 == 0) ? q : 0.0)) / p;
+    const double detb = det3(b);
+    const double phi = acos(fmin(fmax(detb / 2.0, -1.0), 1.0)) / 3.0;
+    const double e1 = q + 2.0 * p * cos(phi);
+    const double e3 = q + 2.0 * p * cos(phi + 2.0 * 3.141592653589793 / 3.0);
+    const double e2 = 3.0 * q - e1 - e3;
+    const double gap = fmin(e1 - e2, e2 - e3) / scale;
+    if (gap > EIG_GAP_FALLBACK) {
+      double m1[9], m2[9], m3[9], t[9], v1[3], v3[3];
+#pragma unroll
+      for (int i = 0; i < 9; ++i) {
+        const double dg = (i % 4 == 0) ? 1.0 : 0.0;
+        m1[i] = m[i] - e1 * dg;
+        m2[i] = m[i] - e2 * dg;
+        m3[i] = m[i] - e3 * dg;
+      }
+      matmul3(m2, m3, t);
+      principal_column(t, v1);
+      matmul3(m1, m2, t);
+      principal_column(t, v3);
+      const double dt = v3[0] * v1[0] + v3[1] * v1[1] + v3[2] * v1[2];
+      v3[0] -= dt * v1[0];
+      v3[1] -= dt * v1[1];
+      v3[2] -= dt * v1[2];
+      const double n3 = sqrt(v3[0] * v3[0] + v3[1] * v3[1] + v3[2] * v3[2]);
+      v3[0] /= n3;
+      v3[1] /= n3;
+      v3[2] /= n3;
+      const double v2[3] = {v3[1] * v1[2] - v3[2] * v1[1], v3[2] * v1[0] - v3[0] * v1[2],
+                            v3[0] * v1[1] - v3[1] * v1[0]};
+      for (int r = 0; r < 3; ++r) {
+        rot[3 * r] = v1[r];
+        rot[3 * r + 1] = v2[r];
+        rot[3 * r + 2] = v3[r];
+      }
+      vals[0] = e1;
+      vals[1] = e2;
+      vals[2] = e3;
+    } else {
+      jacobi_eig3(m, rot, vals);
+    }
+  }
+  if (det3(rot) < 0.0) {
+    rot[2] = -rot[2];
+    rot[5] = -rot[5];
+    rot[8] = -rot[8];
+  }
+}
+
+__global__ void k_sym_eigh3(const double* __restrict__ mats, int64_t n, double* __restrict__ rot,
+                            double* __restrict__ vals) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double m[9], r[9], v[3];
+#pragma unroll
+  for (int k = 0; k < 9; ++k) m[k] = mats[9 * i + k];
+  sym_eigh3(m, r, v);
+#pragma unroll
+  for (int k = 0; k < 9; ++k) rot[9 * i + k] = r[k];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) vals[3 * i + k] = v[k];
+}
+
+// ---------------------------------------------------------------- K7 fit
+struct FitArgs {
+  const float* depth;
+  const uint8_t* mask;
+  int height, width, stride, win, k_min, scale_mode;
+  double fx, fy, cx, cy;
+};
+
+__device__ __forceinline__ void backproject(const FitArgs& a, int u, int v, double z, double* p) {
+  // tracker.py:210-212: ((u - cx) / fx) * z, ((v - cy) / fy) * z, z
+  p[0] = SG_MUL(SG_DIV(SG_SUB((double)u, a.cx), a.fx), z);
+  p[1] = SG_MUL(SG_DIV(SG_SUB((double)v, a.cy), a.fy), z);
+  p[2] = z;
+}
+
+__global__ void __launch_bounds__(TRK_THREADS)
+k_track_fit(FitArgs a, double* __restrict__ centers, double* __restrict__ cov,
+            double* __restrict__ normals, double* __restrict__ rot_out,
+            double* __restrict__ scales_out, int64_t* __restrict__ pixel_out,
+            uint32_t* __restrict__ status, uint32_t* __restrict__ counters,
+            int64_t* __restrict__ count_out) {
+  typedef cub::BlockScan<uint32_t, TRK_THREADS> Scan;
+  __shared__ typename Scan::TempStorage scan_tmp;
+  __shared__ uint32_t s_tile, s_prefix;
+  if (threadIdx.x == 0) s_tile = atomicAdd(&counters[0], 1u);
+  __syncthreads();
+  const int tile = (int)s_tile;
+  const int64_t npx = (int64_t)a.height * a.width;
+  const int64_t pix = (int64_t)tile * TRK_THREADS + threadIdx.x;
+  bool keep = false;
+  double c[3], rot[9], s[3], nrm[3];
+  if (pix < npx) {
+    const int v = (int)(pix / a.width), u = (int)(pix % a.width);
+    if (v % a.stride == 0 && u % a.stride == 0 && a.mask[pix]) {
+      backproject(a, u, v, (double)a.depth[pix], c);
+      const int r = a.win / 2;
+      double sum[3] = {0, 0, 0};
+      int k = 0;
+      for (int dv = -r; dv <= r; ++dv)
+        for (int du = -r; du <= r; ++du) {
+          if (dv == 0 && du == 0) continue;
+          const int y = v + dv, x = u + du;
+          if (y < 0 || y >= a.height || x < 0 || x >= a.width) continue;
+          const int64_t q = (int64_t)y * a.width + x;
+          if (!a.mask[q]) continue;
+          double pt[3];
+          backproject(a, x, y, (double)a.depth[q], pt);
+          sum[0] += pt[0];
+          sum[1] += pt[1];
+          sum[2] += pt[2];
+          ++k;
+        }
+      if (k >= a.k_min) {
+        const double mean[3] = {sum[0] / k, sum[1] / k, sum[2] / k};
+        double cv[6] = {0, 0, 0, 0, 0, 0};
+        for (int dv = -r; dv <= r; ++dv)
+          for (int du = -r; du <= r; ++du) {
+            if (dv == 0 && du == 0) continue;
+            const int y = v + dv, x = u + du;
+            if (y < 0 || y >= a.height || x < 0 || x >= a.width) continue;
+            const int64_t q = (int64_t)y * a.width + x;
+            if (!a.mask[q]) continue;
+            double pt[3];
+            backproject(a, x, y, (double)a.depth[q], pt);
+            const double d0 = pt[0] - mean[0], d1 = pt[1] - mean[1], d2 = pt[2] - mean[2];
+            cv[0] += d0 * d0;
+            cv[1] += d0 * d1;
+            cv[2] += d0 * d2;
+            cv[3] += d1 * d1;
+            cv[4] += d1 * d2;
+            cv[5] += d2 * d2;
+          }
+        double m[9] = {cv[0] / k, cv[1] / k, cv[2] / k, cv[1] / k, cv[3] / k,
+                       cv[4] / k, cv[2] / k, cv[4] / k, cv[5] / k};
+        double vals[3];
+        sym_eigh3(m, rot, vals);
+        // tracker.py:162-169
+        const double fl = EIGVAL_FLOOR_REL * vals[0];
+        for (int i = 0; i < 3; ++i) s[i] = sqrt(fmax(vals[i], fl));
+        if (a.scale_mode == 0) {
+          const double nn = sqrt(s[0] * s[0] + s[1] * s[1] + s[2] * s[2]);
+          s[0] /= nn;
+          s[1] /= nn;
+          s[2] /= nn;
+        } else if (a.scale_mode == 1) {
+          s[0] = 1.0;
+          s[1] = 1.0;
+          s[2] = 1e-3;
+        }
+        nrm[0] = rot[2];
+        nrm[1] = rot[5];
+        nrm[2] = rot[8];
+        if (nrm[0] * -c[0] + nrm[1] * -c[1] + nrm[2] * -c[2] < 0.0) {
+          for (int i = 0; i < 3; ++i) {
+            nrm[i] = -nrm[i];
+            rot[3 * i + 2] = -rot[3 * i + 2];
+            rot[3 * i + 1] = -rot[3 * i + 1];
+          }
+        }
+        keep = true;
+      }
+    }
+  }
+  uint32_t rank, agg;
+  Scan(scan_tmp).ExclusiveSum(keep ? 1u : 0u, rank, agg);
+  if (threadIdx.x == 0) {
+    if (tile == 0) {
+      st_volatile_u32(status, LB_FLAG_P | agg);
+      s_prefix = 0;
+    } else {
+      st_volatile_u32(status + tile, LB_FLAG_A | agg);
+    }
+  }
+  if (tile > 0 && threadIdx.x < 32) {
+    const uint32_t excl = lookback_exclusive(status, tile);
+    if (threadIdx.x == 0) {
+      st_volatile_u32(status + tile, LB_FLAG_P | (excl + agg));
+      s_prefix = excl;
+    }
+  }
+  __syncthreads();
+  if (keep) {
+    const int64_t o = s_prefix + rank;
+    for (int i = 0; i < 3; ++i) {
+      centers[3 * o + i] = c[i];
+      normals[3 * o + i] = nrm[i];
+      if (scales_out) scales_out[3 * o + i] = s[i];
+    }
+    if (rot_out)
+      for (int i = 0; i < 9; ++i) rot_out[9 * o + i] = rot[i];
+    if (pixel_out) pixel_out[o] = pix;
+    // covariance R diag(s^2) R^T (tracker.py:76-78), upper triangle
+    const double s2[3] = {s[0] * s[0], s[1] * s[1], s[2] * s[2]};
+    double cc[6];
+    int t = 0;
+    for (int i = 0; i < 3; ++i)
+      for (int j = i; j < 3; ++j) {
+        cc[t++] = rot[3 * i] * s2[0] * rot[3 * j] + rot[3 * i + 1] * s2[1] * rot[3 * j + 1] +
+                  rot[3 * i + 2] * s2[2] * rot[3 * j + 2];
+      }
+    for (int i = 0; i < 6; ++i) cov[6 * o + i] = cc[i];
+  }
+  if (threadIdx.x == 0 && (int64_t)(tile + 1) * TRK_THREADS >= npx) *count_out = s_prefix + agg;
+}
+
+// ---------------------------------------------------------------- K10 grid NN
+__device__ __forceinline__ unsigned long long dkey(double x) {
+  unsigned long long b = (unsigned long long)__double_as_longlong(x);
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double dkey_inv(unsigned long long k) {
+  return __longlong_as_double((long long)((k >> 63) ? (k & 0x7fffffffffffffffull) : ~k));
+}
+
+__global__ void k_bbox(const double* __restrict__ pts, int64_t n, unsigned long long* __restrict__ bb) {
+  unsigned long long lo[3] = {~0ull, ~0ull, ~0ull}, hi[3] = {0, 0, 0};
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    for (int k = 0; k < 3; ++k) {
+      const unsigned long long key = dkey(pts[3 * i + k]);
+      lo[k] = key < lo[k] ? key : lo[k];
+      hi[k] = key > hi[k] ? key : hi[k];
+    }
+  for (int k = 0; k < 3; ++k) {
+    atomicMin(bb + k, lo[k]);
+    atomicMax(bb + 3 + k, hi[k]);
+  }
+}
+
+struct Grid {
+  double lo[3];
+  double h;
+  int dim[3];
+};
+
+__device__ __forceinline__ int cell_coord(double x, double lo, double h, int dim) {
+  double c = floor((x - lo) / h);
+  c = fmin(fmax(c, 0.0), (double)(dim - 1));
+  return (int)c;
+}
+
+__global__ void k_grid_count(const double* __restrict__ pts, int64_t n, Grid g,
+                             uint32_t* __restrict__ cnt, uint32_t* __restrict__ cell_of) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int cx = cell_coord(pts[3 * i], g.lo[0], g.h, g.dim[0]);
+  const int cy = cell_coord(pts[3 * i + 1], g.lo[1], g.h, g.dim[1]);
+  const int cz = cell_coord(pts[3 * i + 2], g.lo[2], g.h, g.dim[2]);
+  const uint32_t c = ((uint32_t)cx * g.dim[1] + cy) * g.dim[2] + cz;
+  cell_of[i] = c;
+  atomicAdd(cnt + c, 1u);
+}
+
+__global__ void k_grid_fill(const uint32_t* __restrict__ cell_of, int64_t n,
+                            uint32_t* __restrict__ cursor, uint32_t* __restrict__ items) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  items[atomicAdd(cursor + cell_of[i], 1u)] = (uint32_t)i;
+}
+
+struct GridView {
+  Grid g;
+  const uint32_t* start;  // [ncells + 1]
+  const uint32_t* items;
+  const double* pts;
+};
+
+// Exact Euclidean nearest neighbour: expanding Chebyshev rings around the
+// query's (clamped) cell, stopping once the best squared distance is no
+// larger than the squared distance to any cell not yet visited.
+__device__ void grid_nearest(const GridView& v, const double* q, int64_t& best_j, double& best_d2) {
+  const Grid& g = v.g;
+  int c0[3];
+  for (int k = 0; k < 3; ++k) c0[k] = cell_coord(q[k], g.lo[k], g.h, g.dim[k]);
+  best_j = -1;
+  best_d2 = INFINITY;
+  const int rmax = max(g.dim[0], max(g.dim[1], g.dim[2]));
+  for (int r = 0; r <= rmax; ++r) {
+    const int x0 = max(c0[0] - r, 0), x1 = min(c0[0] + r, g.dim[0] - 1);
+    const int y0 = max(c0[1] - r, 0), y1 = min(c0[1] + r, g.dim[1] - 1);
+    const int z0 = max(c0[2] - r, 0), z1 = min(c0[2] + r, g.dim[2] - 1);
+    for (int x = x0; x <= x1; ++x)
+      for (int y = y0; y <= y1; ++y) {
+        const bool edge_xy = abs(x - c0[0]) == r || abs(y - c0[1]) == r;
+        for (int z = z0; z <= z1; ++z) {
+          if (!edge_xy && abs(z - c0[2]) != r) {
+            // interior of the ring cube: jump to the far face
+            if (z < c0[2] + r) z = c0[2] + r - 1;
+            continue;
+          }
+          const uint32_t cell = ((uint32_t)x * g.dim[1] + y) * g.dim[2] + z;
+          for (uint32_t t = v.start[cell]; t < v.start[cell + 1]; ++t) {
+            const uint32_t j = v.items[t];
+            const double dx = q[0] - v.pts[3 * j], dy = q[1] - v.pts[3 * j + 1],
+                         dz = q[2] - v.pts[3 * j + 2];
+            const double d2 = dx * dx + dy * dy + dz * dz;
+            if (d2 < best_d2 || (d2 == best_d2 && (int64_t)j < best_j)) {
+              best_d2 = d2;
+              best_j = j;
+            }
+          }
+        }
+      }
+    // lower bound on the distance to any cell outside the visited box
+    double lb = INFINITY;
+    bool all_sat = true;
+    const int lo_c[3] = {x0, y0, z0}, hi_c[3] = {x1, y1, z1};
+    for (int k = 0; k < 3; ++k) {
+      if (lo_c[k] > 0) {
+        all_sat = false;
+        lb = fmin(lb, fmax(q[k] - (g.lo[k] + lo_c[k] * g.h), 0.0));
+      }
+      if (hi_c[k] < g.dim[k] - 1) {
+        all_sat = false;
+        lb = fmin(lb, fmax((g.lo[k] + (hi_c[k] + 1) * g.h) - q[k], 0.0));
+      }
+    }
+    if (all_sat) break;
+    if (best_j >= 0 && best_d2 <= lb * lb * (1.0 - 1e-12)) break;
+  }
+}
+
+__global__ void k_nearest(GridView v, const double* __restrict__ queries, int64_t m,
+                          int64_t* __restrict__ idx, double* __restrict__ dist) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  const double q[3] = {queries[3 * i], queries[3 * i + 1], queries[3 * i + 2]};
+  int64_t j;
+  double d2;
+  grid_nearest(v, q, j, d2);
+  idx[i] = j;
+  if (dist) dist[i] = sqrt(d2);
+}
+
+// ---------------------------------------------------------------- K8 / K9
+struct PoseArg {
+  double r[9], t[3];
+};
+
+__device__ __forceinline__ void apply_pose(const PoseArg& P, const double* a, double* p) {
+  // pts @ R.T + t, in the order OpenBLAS dgemm evaluates it:
+  // fma(a2, R[j,2], fma(a1, R[j,1], a0 * R[j,0])) + t[j]
+#pragma unroll
+  for (int j = 0; j < 3; ++j)
+    p[j] = SG_ADD(SG_FMA(a[2], P.r[3 * j + 2], SG_FMA(a[1], P.r[3 * j + 1], SG_MUL(a[0], P.r[3 * j]))),
+                  P.t[j]);
+}
+
+constexpr int NE_VALS = 29;  // 21 (H upper) + 6 (g) + cost + inliers
+
+__global__ void __launch_bounds__(TRK_THREADS)
+k_normal_eqs(GridView v, const double* __restrict__ cov_b, const double* __restrict__ nrm_b,
+             const double* __restrict__ a_c, const double* __restrict__ a_cov, int64_t m,
+             PoseArg P, int metric_mode, double dist_max, double* __restrict__ w_out,
+             double* __restrict__ b_out, uint8_t* __restrict__ acc_out,
+             double* __restrict__ partial) {
+  __shared__ double s_part[TRK_THREADS / 32][NE_VALS];
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  double acc[NE_VALS];
+#pragma unroll
+  for (int k = 0; k < NE_VALS; ++k) acc[k] = 0.0;
+  if (i < m) {
+    const double a[3] = {a_c[3 * i], a_c[3 * i + 1], a_c[3 * i + 2]};
+    double p[3];
+    apply_pose(P, a, p);
+    int64_t j;
+    double d2;
+    grid_nearest(v, p, j, d2);
+    const double b[3] = {v.pts[3 * j], v.pts[3 * j + 1], v.pts[3 * j + 2]};
+    const double d[3] = {b[0] - p[0], b[1] - p[1], b[2] - p[2]};
+    double metric;
+    if (metric_mode == 0)
+      metric = fabs(nrm_b[3 * j] * d[0] + nrm_b[3 * j + 1] * d[1] + nrm_b[3 * j + 2] * d[2]);
+    else
+      metric = sqrt(d2);
+    const bool ok = metric < dist_max;
+    acc_out[i] = ok ? 1 : 0;
+    if (ok) {
+      // C = C_b + R C_a R^T (tracker.py:305-307)
+      const double* cb = cov_b + 6 * j;
+      const double* ca = a_cov + 6 * i;
+      const double A[9] = {ca[0], ca[1], ca[2], ca[1], ca[3], ca[4], ca[2], ca[4], ca[5]};
+      double RA[9], C[9];
+      matmul3(P.r, A, RA);
+      for (int r = 0; r < 3; ++r)
+        for (int c = 0; c < 3; ++c)
+          C[3 * r + c] = RA[3 * r] * P.r[3 * c] + RA[3 * r + 1] * P.r[3 * c + 1] +
+                         RA[3 * r + 2] * P.r[3 * c + 2];
+      const double B[9] = {cb[0], cb[1], cb[2], cb[1], cb[3], cb[4], cb[2], cb[4], cb[5]};
+      for (int k = 0; k < 9; ++k) C[k] += B[k];
+      // W = C^-1 (symmetric adjugate)
+      const double c00 = C[4] * C[8] - C[5] * C[7], c01 = C[2] * C[7] - C[1] * C[8],
+                   c02 = C[1] * C[5] - C[2] * C[4];
+      const double c11 = C[0] * C[8] - C[2] * C[6], c12 = C[2] * C[3] - C[0] * C[5];
+      const double c22 = C[0] * C[4] - C[1] * C[3];
+      const double det = C[0] * c00 + C[1] * (C[5] * C[6] - C[3] * C[8]) + C[2] * (C[3] * C[7] - C[4] * C[6]);
+      const double id = 1.0 / det;
+      const double W[9] = {c00 * id, c01 * id, c02 * id, c01 * id, c11 * id,
+                           c12 * id, c02 * id, c12 * id, c22 * id};
+      // J = [skew(p) | -I]; S^T = -S
+      const double S[9] = {0.0, -p[2], p[1], p[2], 0.0, -p[0], -p[1], p[0], 0.0};
+      double WS[9], StWS[9];
+      matmul3(W, S, WS);
+      for (int r = 0; r < 3; ++r)
+        for (int c = 0; c < 3; ++c)
+          StWS[3 * r + c] = -(S[3 * r] * WS[c] + S[3 * r + 1] * WS[3 + c] + S[3 * r + 2] * WS[6 + c]);
+      // H blocks: [StWS, -S^T W; -W S, W] = [StWS, (WS)^T ; -WS, W]
+      double H[36];
+      for (int r = 0; r < 3; ++r)
+        for (int c = 0; c < 3; ++c) {
+          H[6 * r + c] = StWS[3 * r + c];
+          H[6 * r + 3 + c] = -WS[3 * c + r];  // -S^T W = S W = -(W S)^T
+          H[6 * (3 + r) + c] = -WS[3 * r + c];
+          H[6 * (3 + r) + 3 + c] = W[3 * r + c];
+        }
+      const double Wd[3] = {W[0] * d[0] + W[1] * d[1] + W[2] * d[2],
+                            W[3] * d[0] + W[4] * d[1] + W[5] * d[2],
+                            W[6] * d[0] + W[7] * d[1] + W[8] * d[2]};
+      // g = J^T W d = [S^T W d; -W d]
+      const double gr[3] = {S[0] * Wd[0] + S[3] * Wd[1] + S[6] * Wd[2],
+                            S[1] * Wd[0] + S[4] * Wd[1] + S[7] * Wd[2],
+                            S[2] * Wd[0] + S[5] * Wd[1] + S[8] * Wd[2]};
+      int t = 0;
+      for (int r = 0; r < 6; ++r)
+        for (int c = r; c < 6; ++c) acc[t++] = H[6 * r + c];
+      acc[21] = gr[0];
+      acc[22] = gr[1];
+      acc[23] = gr[2];
+      acc[24] = -Wd[0];
+      acc[25] = -Wd[1];
+      acc[26] = -Wd[2];
+      acc[27] = d[0] * Wd[0] + d[1] * Wd[1] + d[2] * Wd[2];
+      acc[28] = 1.0;
+      w_out[6 * i + 0] = W[0];
+      w_out[6 * i + 1] = W[1];
+      w_out[6 * i + 2] = W[2];
+      w_out[6 * i + 3] = W[4];
+      w_out[6 * i + 4] = W[5];
+      w_out[6 * i + 5] = W[8];
+      b_out[3 * i] = b[0];
+      b_out[3 * i + 1] = b[1];
+      b_out[3 * i + 2] = b[2];
+    } else {
+      for (int k = 0; k < 6; ++k) w_out[6 * i + k] = 0.0;
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < NE_VALS; ++k) {
+    double x = acc[k];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
+    if ((threadIdx.x & 31) == 0) s_part[threadIdx.x >> 5][k] = x;
+  }
+  __syncthreads();
+  if (threadIdx.x < NE_VALS) {
+    double x = 0.0;
+    for (int w = 0; w < TRK_THREADS / 32; ++w) x += s_part[w][threadIdx.x];
+    partial[(size_t)blockIdx.x * NE_VALS + threadIdx.x] = x;
+  }
+}
+
+// fixed-order sum of per-block partials: deterministic results
+__global__ void k_reduce_partials(const double* __restrict__ partial, int nblocks, int nvals,
+                                  double* __restrict__ out) {
+  const int k = threadIdx.x;
+  if (k >= nvals) return;
+  double x = 0.0;
+  for (int b = 0; b < nblocks; ++b) x += partial[(size_t)b * nvals + k];
+  out[k] = x;
+}
+
+constexpr int MAX_CAND = 8;
+
+__global__ void __launch_bounds__(TRK_THREADS)
+k_cost(const double* __restrict__ a_c, const double* __restrict__ w, const double* __restrict__ bb,
+       const uint8_t* __restrict__ acc_in, int64_t m, int n_cand, const PoseArg* __restrict__ poses,
+       double* __restrict__ partial) {
+  __shared__ PoseArg s_pose[MAX_CAND];
+  __shared__ double s_part[TRK_THREADS / 32][MAX_CAND];
+  if (threadIdx.x < n_cand) s_pose[threadIdx.x] = poses[threadIdx.x];
+  __syncthreads();
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  double cst[MAX_CAND];
+#pragma unroll
+  for (int c = 0; c < MAX_CAND; ++c) cst[c] = 0.0;
+  if (i < m && acc_in[i]) {
+    const double a[3] = {a_c[3 * i], a_c[3 * i + 1], a_c[3 * i + 2]};
+    const double* W = w + 6 * i;
+    for (int c = 0; c < n_cand; ++c) {
+      double p[3];
+      apply_pose(s_pose[c], a, p);
+      const double r0 = bb[3 * i] - p[0], r1 = bb[3 * i + 1] - p[1], r2 = bb[3 * i + 2] - p[2];
+      cst[c] = r0 * (W[0] * r0 + W[1] * r1 + W[2] * r2) + r1 * (W[1] * r0 + W[3] * r1 + W[4] * r2) +
+               r2 * (W[2] * r0 + W[4] * r1 + W[5] * r2);
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < MAX_CAND; ++c) {
+    double x = cst[c];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
+    if ((threadIdx.x & 31) == 0) s_part[threadIdx.x >> 5][c] = x;
+  }
+  __syncthreads();
+  if (threadIdx.x < MAX_CAND) {
+    double x = 0.0;
+    for (int wi = 0; wi < TRK_THREADS / 32; ++wi) x += s_part[wi][threadIdx.x];
+    partial[(size_t)blockIdx.x * MAX_CAND + threadIdx.x] = x;
+  }
+}
+
+}  // namespace sgad
+
+struct sgad_geomset {
+  sgad::DevBuf pts, cov, nrm, bbox, cnt, start, cursor, cell_of, items, cub_tmp;
+  sgad::DevBuf w, b, acc, partial, poses;
+  sgad::Grid grid{};
+  int64_t n = 0;
+  unsigned long long* pinned = nullptr;
+};
+
+using namespace sgad;
+
+static inline unsigned nblk(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
+
+extern "C" {
+
+int sgad_sym_eigh3(const double* mats, int64_t n, double* rot, double* vals, void* stream) {
+  SGAD_REQUIRE(n >= 0 && (n == 0 || (mats && rot && vals)), "sgad_sym_eigh3: bad arguments");
+  if (n == 0) return SGAD_OK;
+  k_sym_eigh3<<<nblk(n, 128), 128, 0, (cudaStream_t)stream>>>(mats, n, rot, vals);
+  SGAD_LAUNCH_CHECK();
+  return SGAD_OK;
+}
+
+int sgad_track_fit(const float* depth, const uint8_t* mask, int32_t height, int32_t width,
+                   double fx, double fy, double cx, double cy, int32_t stride, int32_t win,
+                   int32_t k_min, int32_t scale_mode, double* centers, double* cov,
+                   double* normals, double* rot, double* scales, int64_t* pixel,
+                   int64_t* count, void* stream_) {
+  SGAD_REQUIRE(depth && mask && centers && cov && normals && count, "sgad_track_fit: null buffer");
+  SGAD_REQUIRE(height > 0 && width > 0 && stride >= 1 && win >= 3 && (win & 1) && k_min >= 1 &&
+                   scale_mode >= 0 && scale_mode <= 2,
+               "sgad_track_fit: bad parameters");
+  cudaStream_t st = (cudaStream_t)stream_;
+  const int64_t npx = (int64_t)height * width;
+  const int64_t tiles = (npx + TRK_THREADS - 1) / TRK_THREADS;
+  static thread_local DevBuf status, counters;
+  SGAD_CHECK_CUDA(status.ensure(sizeof(uint32_t) * tiles));
+  SGAD_CHECK_CUDA(counters.ensure(sizeof(uint32_t) * 4));
+  SGAD_CHECK_CUDA(cudaMemsetAsync(status.p, 0, sizeof(uint32_t) * tiles, st));
+  SGAD_CHECK_CUDA(cudaMemsetAsync(counters.p, 0, sizeof(uint32_t) * 4, st));
+  FitArgs a{depth, mask, height, width, stride, win, k_min, scale_mode, fx, fy, cx, cy};
+  k_track_fit<<<(unsigned)tiles, TRK_THREADS, 0, st>>>(a, centers, cov, normals, rot, scales, pixel,
+                                                      status.as<uint32_t>(), counters.as<uint32_t>(),
+                                                      count);
+  SGAD_LAUNCH_CHECK();
+  return SGAD_OK;
+}
+
+int sgad_geomset_create(sgad_geomset** out) {
+  SGAD_REQUIRE(out, "sgad_geomset_create: null out");
+  sgad_geomset* g = new sgad_geomset();
+  if (cudaMallocHost(&g->pinned, 8 * sizeof(unsigned long long)) != cudaSuccess) {
+    delete g;
+    set_error("cudaMallocHost failed");
+    return SGAD_E_CUDA;
+  }
+  *out = g;
+  return SGAD_OK;
+}
+
+int sgad_geomset_destroy(sgad_geomset* g) {
+  if (!g) return SGAD_OK;
+  DevBuf* bufs[] = {&g->pts, &g->cov, &g->nrm, &g->bbox, &g->cnt, &g->start, &g->cursor,
+                    &g->cell_of, &g->items, &g->cub_tmp, &g->w, &g->b, &g->acc, &g->partial,
+                    &g->poses};
+  for (DevBuf* b : bufs) b->release();
+  if (g->pinned) cudaFreeHost(g->pinned);
+  delete g;
+  return SGAD_OK;
+}
+
+int sgad_geomset_set(sgad_geomset* g, const double* centers, const double* cov,
+                     const double* normals, int64_t n, void* stream_) {
+  SGAD_REQUIRE(g && centers && cov && normals && n > 0, "sgad_geomset_set: bad arguments");
+  SGAD_REQUIRE(n < (1ll << 31), "sgad_geomset_set: too many points");
+  cudaStream_t st = (cudaStream_t)stream_;
+  g->n = n;
+  SGAD_CHECK_CUDA(g->pts.ensure(sizeof(double) * 3 * n));
+  SGAD_CHECK_CUDA(g->cov.ensure(sizeof(double) * 6 * n));
+  SGAD_CHECK_CUDA(g->nrm.ensure(sizeof(double) * 3 * n));
+  SGAD_CHECK_CUDA(cudaMemcpyAsync(g->pts.p, centers, sizeof(double) * 3 * n, cudaMemcpyDefault, st));
+  SGAD_CHECK_CUDA(cudaMemcpyAsync(g->cov.p, cov, sizeof(double) * 6 * n, cudaMemcpyDefault, st));
+  SGAD_CHECK_CUDA(cudaMemcpyAsync(g->nrm.p, normals, sizeof(double) * 3 * n, cudaMemcpyDefault, st));
+  // bounding box -> grid geometry
+  SGAD_CHECK_CUDA(g->bbox.ensure(sizeof(unsigned long long) * 6));
+  unsigned long long init[6] = {~0ull, ~0ull, ~0ull, 0, 0, 0};
+  memcpy(g->pinned, init, sizeof init);
+  SGAD_CHECK_CUDA(cudaMemcpyAsync(g->bbox.p, g->pinned, sizeof init, cudaMemcpyHostToDevice, st));
+  k_bbox<<<min(nblk(n, 256), 1024u), 256, 0, st>>>(g->pts.as<double>(), n,
+                                                   g->bbox.as<unsigned long long>());
+  SGAD_LAUNCH_CHECK();
+  SGAD_CHECK_CUDA(cudaMemcpyAsync(g->pinned, g->bbox.p, sizeof init, cudaMemcpyDeviceToHost, st));
+  SGAD_CHECK_CUDA(cudaStreamSynchronize(st));
+  double lo[3], hi[3];
+  for (int k = 0; k < 3; ++k) {
+    unsigned long long kl = g->pinned[k], kh = g->pinned[3 + k];
+    uint64_t bl = (kl >> 63) ? (kl & 0x7fffffffffffffffull) : ~kl;
+    uint64_t bh = (kh >> 63) ? (kh & 0x7fffffffffffffffull) : ~kh;
+    memcpy(&lo[k], &bl, 8);
+    memcpy(&hi[k], &bh, 8);
+  }
+  double ext[3], vol = 1.0;
+  for (int k = 0; k < 3; ++k) {
+    ext[k] = fmax(hi[k] - lo[k], 1e-9);
+    vol *= ext[k];
+  }
+  // ~n/2 cells over the box; points on surfaces land a few per occupied cell
+  double h = cbrt(vol / fmax(0.5 * (double)n, 1.0));
+  const double hmin = fmax(fmax(ext[0], ext[1]), ext[2]) / 1024.0;
+  h = fmax(h, hmin);
+  Grid gr;
+  int64_t ncells = 1;
+  for (int k = 0; k < 3; ++k) {
+    gr.lo[k] = lo[k];
+    gr.dim[k] = (int)fmin(ceil(ext[k] / h) + 1.0, 1024.0);
+    ncells *= gr.dim[k];
+  }
+  gr.h = h;
+  g->grid = gr;
+  SGAD_CHECK_CUDA(g->cnt.ensure(sizeof(uint32_t) * (ncells + 1)));
+  SGAD_CHECK_CUDA(g->start.ensure(sizeof(uint32_t) * (ncells + 1)));
+  SGAD_CHECK_CUDA(g->cursor.ensure(sizeof(uint32_t) * (ncells + 1)));
+  SGAD_CHECK_CUDA(g->cell_of.ensure(sizeof(uint32_t) * n));
+  SGAD_CHECK_CUDA(g->items.ensure(sizeof(uint32_t) * n));
+  SGAD_CHECK_CUDA(cudaMemsetAsync(g->cnt.p, 0, sizeof(uint32_t) * (ncells + 1), st));
+  k_grid_count<<<nblk(n, 256), 256, 0, st>>>(g->pts.as<double>(), n, gr, g->cnt.as<uint32_t>(),
+                                             g->cell_of.as<uint32_t>());
+  SGAD_LAUNCH_CHECK();
+  size_t tmp = 0;
+  SGAD_CHECK_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, g->cnt.as<uint32_t>(),
+                                                g->start.as<uint32_t>(), (int)ncells + 1, st));
+  SGAD_CHECK_CUDA(g->cub_tmp.ensure(tmp));
+  SGAD_CHECK_CUDA(cub::DeviceScan::ExclusiveSum(g->cub_tmp.p, tmp, g->cnt.as<uint32_t>(),
+                                                g->start.as<uint32_t>(), (int)ncells + 1, st));
+  SGAD_CHECK_CUDA(cudaMemcpyAsync(g->cursor.p, g->start.p, sizeof(uint32_t) * (ncells + 1),
+                                  cudaMemcpyDeviceToDevice, st));
+  k_grid_fill<<<nblk(n, 256), 256, 0, st>>>(g->cell_of.as<uint32_t>(), n, g->cursor.as<uint32_t>(),
+                                            g->items.as<uint32_t>());
+  SGAD_LAUNCH_CHECK();
+  return SGAD_OK;
+}
+
+static GridView view_of(sgad_geomset* g) {
+  GridView v;
+  v.g = g->grid;
+  v.start = g->start.as<uint32_t>();
+  v.items = g->items.as<uint32_t>();
+  v.pts = g->pts.as<double>();
+  return v;
+}
+
+int sgad_geomset_nearest(sgad_geomset* g, const double* queries, int64_t m, int64_t* idx,
+                         double* dist, void* stream_) {
+  SGAD_REQUIRE(g && g->n > 0, "global set is empty");
+  SGAD_REQUIRE(m >= 0 && (m == 0 || (queries && idx)), "sgad_geomset_nearest: bad arguments");
+  if (m == 0) return SGAD_OK;
+  k_nearest<<<nblk(m, 128), 128, 0, (cudaStream_t)stream_>>>(view_of(g), queries, m, idx, dist);
+  SGAD_LAUNCH_CHECK();
+  return SGAD_OK;
+}
+
+int sgad_track_normal_eqs(sgad_geomset* g, const double* local_centers, const double* local_cov,
+                          int64_t m, const double* rot, const double* trans, int32_t metric_mode,
+                          double dist_max, double* out, void* stream_) {
+  SGAD_REQUIRE(g && g->n > 0, "global set is empty");
+  SGAD_REQUIRE(local_centers && local_cov && rot && trans && out && m > 0,
+               "sgad_track_normal_eqs: bad arguments");
+  cudaStream_t st = (cudaStream_t)stream_;
+  const unsigned nb = nblk(m, TRK_THREADS);
+  SGAD_CHECK_CUDA(g->w.ensure(sizeof(double) * 6 * m));
+  SGAD_CHECK_CUDA(g->b.ensure(sizeof(double) * 3 * m));
+  SGAD_CHECK_CUDA(g->acc.ensure(m));
+  SGAD_CHECK_CUDA(g->partial.ensure(sizeof(double) * NE_VALS * nb));
+  PoseArg P;
+  for (int k = 0; k < 9; ++k) P.r[k] = rot[k];
+  for (int k = 0; k < 3; ++k) P.t[k] = trans[k];
+  k_normal_eqs<<<nb, TRK_THREADS, 0, st>>>(view_of(g), g->cov.as<double>(), g->nrm.as<double>(),
+                                           local_centers, local_cov, m, P, metric_mode, dist_max,
+                                           g->w.as<double>(), g->b.as<double>(),
+                                           g->acc.as<uint8_t>(), g->partial.as<double>());
+  SGAD_LAUNCH_CHECK();
+  k_reduce_partials<<<1, 32, 0, st>>>(g->partial.as<double>(), (int)nb, NE_VALS, out);
+  SGAD_LAUNCH_CHECK();
+  return SGAD_OK;
+}
+
+int sgad_track_cost(sgad_geomset* g, const double* local_centers, int64_t m, const double* poses,
+                    int32_t n_cand, double* out, void* stream_) {
+  SGAD_REQUIRE(g && local_centers && poses && out && m > 0 && n_cand > 0 && n_cand <= MAX_CAND,
+               "sgad_track_cost: bad arguments");
+  SGAD_REQUIRE(g->w.cap >= sizeof(double) * 6 * m, "sgad_track_cost: run normal_eqs first");
+  cudaStream_t st = (cudaStream_t)stream_;
+  const unsigned nb = nblk(m, TRK_THREADS);
+  SGAD_CHECK_CUDA(g->partial.ensure(sizeof(double) * MAX_CAND * nb));
+  SGAD_CHECK_CUDA(g->poses.ensure(sizeof(PoseArg) * MAX_CAND));
+  PoseArg hp[MAX_CAND];
+  for (int c = 0; c < n_cand; ++c) {
+    for (int k = 0; k < 9; ++k) hp[c].r[k] = poses[12 * c + k];
+    for (int k = 0; k < 3; ++k) hp[c].t[k] = poses[12 * c + 9 + k];
+  }
+  SGAD_CHECK_CUDA(cudaMemcpyAsync(g->poses.p, hp, sizeof(PoseArg) * n_cand, cudaMemcpyHostToDevice, st));
+  k_cost<<<nb, TRK_THREADS, 0, st>>>(local_centers, g->w.as<double>(), g->b.as<double>(),
+                                     g->acc.as<uint8_t>(), m, n_cand, g->poses.as<PoseArg>(),
+                                     g->partial.as<double>());
+  SGAD_LAUNCH_CHECK();
+  k_reduce_partials<<<1, 32, 0, st>>>(g->partial.as<double>(), (int)nb, MAX_CAND, out);
+  SGAD_LAUNCH_CHECK();
+  // hp lives on this stack frame: make sure the copy has been consumed
+  SGAD_CHECK_CUDA(cudaStreamSynchronize(st));
+  return SGAD_OK;
+}
+
+}  // extern "C"
