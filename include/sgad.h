@@ -173,6 +173,10 @@ int sgad_track_normal_eqs(sgad_geomset* g, const double* local_centers, const do
                           int64_t m, const double* rot, const double* trans, int32_t metric_mode,
                           double dist_max, double* out, void* stream);
 
+/* Copy the per-correspondence acceptance flags of the last
+ * sgad_track_normal_eqs call (device uint8 [m]). */
+int sgad_track_accepted(sgad_geomset* g, uint8_t* out, int64_t m, void* stream);
+
 /* Frozen-weight cost sum_i (b_i - T a_i)^T W_i (b_i - T a_i) for n_cand poses
  * (poses: host array [n_cand, 12], rot row-major then trans) -> out[n_cand]
  * (device). */

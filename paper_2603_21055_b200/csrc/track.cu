@@ -820,6 +820,13 @@ int sgad_track_normal_eqs(sgad_geomset* g, const double* local_centers, const do
   return SGAD_OK;
 }
 
+int sgad_track_accepted(sgad_geomset* g, uint8_t* out, int64_t m, void* stream_) {
+  SGAD_REQUIRE(g && out && m >= 0 && g->acc.cap >= (size_t)m, "sgad_track_accepted: bad arguments");
+  if (m == 0) return SGAD_OK;
+  SGAD_CHECK_CUDA(cudaMemcpyAsync(out, g->acc.p, m, cudaMemcpyDeviceToDevice, (cudaStream_t)stream_));
+  return SGAD_OK;
+}
+
 int sgad_track_cost(sgad_geomset* g, const double* local_centers, int64_t m, const double* poses,
                     int32_t n_cand, double* out, void* stream_) {
   SGAD_REQUIRE(g && local_centers && poses && out && m > 0 && n_cand > 0 && n_cand <= MAX_CAND,

@@ -1,0 +1,378 @@
+"""Geometry tracking -- drop-in for /root/reference/pkg/src/raysplat/tracker.py.
+
+Per frame, the depth image becomes oriented geometry Gaussians (K7:
+window fit + closed-form 3x3 eigendecomposition), which are registered to
+the world-frame set with GICP.  Each Gauss-Newton iteration is ONE fused
+kernel (K8: exact 1-NN on a uniform grid, point-to-surface gate, combined
+covariance, 3x3 inverse, SE(3) Jacobian and the 6x6 J^T W J / J^T W d
+reduction) followed by the 6x6 solve on the host, as north_star specifies;
+the step-halving costs of the reference's line search are evaluated for all
+five halvings in one launch (K9) so an iteration costs two round trips.
+
+Delta D2 (north_star): local Gaussians fit the valid pixels of a
+``window x window`` neighbourhood (self excluded, at least
+``min_neighbors``) instead of the K_c Euclidean nearest neighbours; the
+covariance, eigenvalue floor, scale normalisation and normal orientation
+are the reference's (tracker.py:158-169).  The correspondence rule (exact
+Euclidean 1-NN + gate, delta D3) is the reference's.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .geometry import Pose, se3_exp
+
+SCALE_MODES = ("ellipse", "plane", "none")
+METRIC_MODES = ("point2surf", "point2point")
+INIT_MODES = ("constant_speed", "render_init")
+EIGVAL_FLOOR_REL = 1e-6
+PLANE_SCALES = (1.0, 1.0, 1e-3)
+MIN_INLIERS = 10
+MAX_STEP_HALVINGS = 5
+
+
+class TrackerError(ValueError):
+    pass
+
+
+@dataclass
+class TrackerConfig:
+    """tracker.py:36-60 plus the window-fit parameters of delta D2."""
+
+    downsample_ratio: int = 10
+    neighbor_count: int = 10
+    max_gicp_iters: int = 30
+    correspondence_dist_max: float = 0.2
+    convergence_eps: float = 1e-5
+    scale_mode: str = "ellipse"
+    metric_mode: str = "point2surf"
+    init_mode: str = "constant_speed"
+    voxel_size: float = 0.02
+    render_init_iters: int = 10
+    render_coverage_min: float = 0.3
+    window: int = 5
+    min_neighbors: int = 4
+
+    def __post_init__(self):
+        if self.downsample_ratio < 1:
+            raise TrackerError("downsample_ratio must be >= 1")
+        if self.neighbor_count < 4:
+            raise TrackerError("neighbor_count must be >= 4")
+        if self.scale_mode not in SCALE_MODES:
+            raise TrackerError(f"scale_mode must be one of {SCALE_MODES}")
+        if self.metric_mode not in METRIC_MODES:
+            raise TrackerError(f"metric_mode must be one of {METRIC_MODES}")
+        if self.init_mode not in INIT_MODES:
+            raise TrackerError(f"init_mode must be one of {INIT_MODES}")
+        if self.window < 3 or self.window % 2 == 0:
+            raise TrackerError("window must be odd and >= 3")
+
+
+def _dev():
+    N.load()
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def _t(x, dtype=torch.float64, device=None):
+    dev = device or _dev()
+    if isinstance(x, torch.Tensor):
+        return x.to(dev, dtype).contiguous()
+    return torch.as_tensor(np.asarray(x), dtype=dtype, device=dev).contiguous()
+
+
+def cov_full(cov6: torch.Tensor) -> torch.Tensor:
+    c = cov6
+    return torch.stack([c[:, 0], c[:, 1], c[:, 2], c[:, 1], c[:, 3], c[:, 4],
+                        c[:, 2], c[:, 4], c[:, 5]], 1).view(-1, 3, 3)
+
+
+def cov_packed(cov: torch.Tensor) -> torch.Tensor:
+    return torch.stack([cov[:, 0, 0], cov[:, 0, 1], cov[:, 0, 2], cov[:, 1, 1], cov[:, 1, 2],
+                        cov[:, 2, 2]], 1).contiguous()
+
+
+def _cov_from(rot, scales):
+    return torch.einsum("nij,nj,nkj->nik", rot, scales**2, rot)
+
+
+class LocalGeomSet:
+    """Oriented geometry Gaussians in one frame's camera (tracker.py:63-78), on device."""
+
+    def __init__(self, centers, rotations, scales, normals, source_frame=-1, cov6=None,
+                 pixel=None):
+        self.centers = _t(centers)
+        self.rotations = _t(rotations)
+        self.scales = _t(scales)
+        self.normals = _t(normals)
+        self.source_frame = source_frame
+        self.pixel = pixel
+        self.cov6 = cov6 if cov6 is not None else cov_packed(_cov_from(self.rotations,
+                                                                        self.scales))
+
+    def __len__(self) -> int:
+        return int(self.centers.shape[0])
+
+    def covariances(self) -> torch.Tensor:
+        return cov_full(self.cov6)
+
+
+def sym_eigh3_batch(mats):
+    """geometry.py:275-353 on device: (rotations (N,3,3), eigenvalues (N,3) descending)."""
+    m = _t(mats).reshape(-1, 9)
+    n = m.shape[0]
+    rot = torch.empty((n, 9), dtype=torch.float64, device=m.device)
+    vals = torch.empty((n, 3), dtype=torch.float64, device=m.device)
+    N.call("sgad_sym_eigh3", m.data_ptr(), n, rot.data_ptr(), vals.data_ptr(), N.stream_ptr())
+    return rot.view(n, 3, 3), vals
+
+
+def fit_local(depth, mask, intr, stride=1, window=5, min_neighbors=4, scale_mode="ellipse",
+              source_frame=-1) -> LocalGeomSet:
+    """K7 on a device depth image (delta D2 window fit)."""
+    dev = _dev()
+    d = _t(depth, torch.float32, dev)
+    mk = _t(mask, torch.uint8, dev)
+    h, w = d.shape
+    cap = ((h + stride - 1) // stride) * ((w + stride - 1) // stride)
+    c = torch.empty((cap, 3), dtype=torch.float64, device=dev)
+    cov = torch.empty((cap, 6), dtype=torch.float64, device=dev)
+    nrm = torch.empty((cap, 3), dtype=torch.float64, device=dev)
+    rot = torch.empty((cap, 9), dtype=torch.float64, device=dev)
+    sc = torch.empty((cap, 3), dtype=torch.float64, device=dev)
+    pix = torch.empty(cap, dtype=torch.int64, device=dev)
+    cnt = torch.zeros(1, dtype=torch.int64, device=dev)
+    N.call("sgad_track_fit", d.data_ptr(), mk.data_ptr(), h, w, float(intr.fx), float(intr.fy),
+           float(intr.cx), float(intr.cy), int(stride), int(window), int(min_neighbors),
+           SCALE_MODES.index(scale_mode), c.data_ptr(), cov.data_ptr(), nrm.data_ptr(),
+           rot.data_ptr(), sc.data_ptr(), pix.data_ptr(), cnt.data_ptr(), N.stream_ptr())
+    m = int(cnt.item())
+    out = LocalGeomSet.__new__(LocalGeomSet)
+    out.centers, out.cov6, out.normals = c[:m], cov[:m], nrm[:m]
+    out.rotations, out.scales, out.pixel = rot[:m].view(m, 3, 3), sc[:m], pix[:m]
+    out.source_frame = source_frame
+    return out
+
+
+def build_local_set(frame, cfg: TrackerConfig) -> LocalGeomSet:
+    """tracker.py:193-230 with the window neighbourhood (delta D2)."""
+    valid = np.asarray(frame.valid_mask, dtype=bool) if not isinstance(frame.valid_mask,
+                                                                         torch.Tensor) \
+        else frame.valid_mask.bool()
+    n_valid = int(valid.sum())
+    if n_valid < cfg.min_neighbors + 1:
+        raise TrackerError(f"frame {frame.index}: {n_valid} valid pixels, need at least "
+                           f"{cfg.min_neighbors + 1}")
+    local = fit_local(frame.depth, valid, frame.intrinsics, cfg.downsample_ratio, cfg.window,
+                      cfg.min_neighbors, cfg.scale_mode, frame.index)
+    if len(local) == 0:
+        raise TrackerError(f"frame {frame.index}: no valid pixels on the sample grid")
+    return local
+
+
+class GlobalGeomSet:
+    """World-frame geometry Gaussians with an exact 1-NN index (tracker.py:81-133).
+
+    Insertion keeps the reference's voxel gating (one member per cell, first
+    come first served) on the host; the members live on the device with a
+    uniform-grid index rebuilt per insert, like the reference's cKDTree."""
+
+    def __init__(self, voxel_size: float = 0.02):
+        if voxel_size <= 0:
+            raise TrackerError("voxel_size must be positive")
+        self.voxel_size = voxel_size
+        dev = _dev()
+        self.centers = torch.empty((0, 3), dtype=torch.float64, device=dev)
+        self.rotations = torch.empty((0, 3, 3), dtype=torch.float64, device=dev)
+        self.scales = torch.empty((0, 3), dtype=torch.float64, device=dev)
+        self.normals = torch.empty((0, 3), dtype=torch.float64, device=dev)
+        self.cov6 = torch.empty((0, 6), dtype=torch.float64, device=dev)
+        self._cells: set = set()
+        h = ctypes.c_void_p()
+        N.check(N.load().sgad_geomset_create(ctypes.byref(h)))
+        self._h = h
+
+    def __del__(self):
+        try:
+            if self._h:
+                N.load(require_cuda=False).sgad_geomset_destroy(self._h)
+                self._h = None
+        except Exception:
+            pass
+
+    def __len__(self) -> int:
+        return int(self.centers.shape[0])
+
+    def insert(self, centers, rotations, scales, normals) -> int:
+        c = _t(centers)
+        keys = np.floor(c.cpu().numpy() / self.voxel_size).astype(np.int64)
+        keep, batch = [], set()
+        for i, key in enumerate(map(tuple, keys)):
+            if key in self._cells or key in batch:
+                continue
+            batch.add(key)
+            keep.append(i)
+        if keep:
+            idx = torch.as_tensor(keep, device=c.device)
+            rot, sc = _t(rotations)[idx], _t(scales)[idx]
+            self.centers = torch.cat([self.centers, c[idx]])
+            self.rotations = torch.cat([self.rotations, rot])
+            self.scales = torch.cat([self.scales, sc])
+            self.normals = torch.cat([self.normals, _t(normals)[idx]])
+            self.cov6 = torch.cat([self.cov6, cov_packed(_cov_from(rot, sc))])
+            self._cells |= batch
+            N.call("sgad_geomset_set", self._h, self.centers.data_ptr(), self.cov6.data_ptr(),
+                   self.normals.data_ptr(), len(self), N.stream_ptr())
+        return len(keep)
+
+    def set_members(self, centers, cov6, normals, rotations=None, scales=None):
+        """Replace the members wholesale (no voxel gating): the C2/C5 target set."""
+        self.centers, self.cov6, self.normals = _t(centers), _t(cov6), _t(normals)
+        self.rotations = _t(rotations) if rotations is not None else self.rotations[:0]
+        self.scales = _t(scales) if scales is not None else self.scales[:0]
+        self._cells = set(map(tuple, np.floor(self.centers.cpu().numpy() /
+                                              self.voxel_size).astype(np.int64)))
+        N.call("sgad_geomset_set", self._h, self.centers.data_ptr(), self.cov6.data_ptr(),
+               self.normals.data_ptr(), len(self), N.stream_ptr())
+
+    def query_nearest(self, points):
+        if len(self) == 0:
+            raise TrackerError("global set is empty")
+        q = _t(points).reshape(-1, 3)
+        idx = torch.empty(q.shape[0], dtype=torch.int64, device=q.device)
+        dist = torch.empty(q.shape[0], dtype=torch.float64, device=q.device)
+        N.call("sgad_geomset_nearest", self._h, q.data_ptr(), q.shape[0], idx.data_ptr(),
+               dist.data_ptr(), N.stream_ptr())
+        return dist, idx
+
+    def covariances(self, idx):
+        return cov_full(self.cov6[idx])
+
+
+def update_global_set(global_set: GlobalGeomSet, local: LocalGeomSet, pose: Pose) -> int:
+    """tracker.py:233-238."""
+    R = _t(pose.rotation)
+    t = _t(pose.translation)
+    centers = local.centers @ R.T + t
+    rotations = torch.einsum("ij,njk->nik", R, local.rotations)
+    normals = local.normals @ R.T
+    return global_set.insert(centers, rotations, local.scales.clone(), normals)
+
+
+@dataclass
+class GicpDiagnostics:
+    """tracker.py:241-250."""
+
+    iterations: int = 0
+    final_cost: float = float("nan")
+    inlier_count: int = 0
+    converged: bool = False
+    failed: bool = False
+    cost_pairs: list = field(default_factory=list)
+    accepted_first: np.ndarray | None = None
+
+
+def _sym6(h21):
+    h = np.empty((6, 6))
+    k = 0
+    for r in range(6):
+        for c in range(r, 6):
+            h[r, c] = h[c, r] = h21[k]
+            k += 1
+    return h
+
+
+class GicpSolver:
+    """Device buffers + launches for one (local, global) registration."""
+
+    def __init__(self, local: LocalGeomSet, global_set: GlobalGeomSet, cfg: TrackerConfig):
+        self.local, self.g, self.cfg = local, global_set, cfg
+        self.m = len(local)
+        self.out = torch.empty(29, dtype=torch.float64, device=local.centers.device)
+        self.costs = torch.empty(8, dtype=torch.float64, device=local.centers.device)
+        self.host = torch.empty(29 + 8, dtype=torch.float64).pin_memory()
+        self.metric = METRIC_MODES.index(cfg.metric_mode)
+
+    def linearize(self, pose: Pose):
+        """K8 at ``pose``: returns (H 6x6, g 6, cost, inliers)."""
+        rot = (ctypes.c_double * 9)(*np.asarray(pose.rotation, dtype=np.float64).reshape(9))
+        tr = (ctypes.c_double * 3)(*np.asarray(pose.translation, dtype=np.float64).reshape(3))
+        N.call("sgad_track_normal_eqs", self.g._h, self.local.centers.data_ptr(),
+               self.local.cov6.data_ptr(), self.m, rot, tr, self.metric,
+               float(self.cfg.correspondence_dist_max), self.out.data_ptr(), N.stream_ptr())
+        h = self.host[:29]
+        h.copy_(self.out)  # synchronising copy into pinned memory
+        v = h.numpy()
+        return _sym6(v[:21]), v[21:27].copy(), float(v[27]), int(round(v[28]))
+
+    def costs_at(self, poses):
+        arr = np.concatenate([np.concatenate([np.asarray(p.rotation).reshape(9),
+                                              np.asarray(p.translation).reshape(3)])
+                              for p in poses])
+        buf = (ctypes.c_double * len(arr))(*arr)
+        N.call("sgad_track_cost", self.g._h, self.local.centers.data_ptr(), self.m, buf,
+               len(poses), self.costs.data_ptr(), N.stream_ptr())
+        h = self.host[29:29 + len(poses)]
+        h.copy_(self.costs[:len(poses)])
+        return h.numpy().copy()
+
+    def accepted(self):
+        acc = torch.empty(self.m, dtype=torch.uint8, device=self.local.centers.device)
+        N.call("sgad_track_accepted", self.g._h, acc.data_ptr(), self.m, N.stream_ptr())
+        return acc.bool().cpu().numpy()
+
+
+def gicp_align(local: LocalGeomSet, global_set: GlobalGeomSet, init: Pose, cfg: TrackerConfig,
+               return_systems: bool = False):
+    """tracker.py:265-346: Gauss-Newton on the combined-covariance cost with
+    frozen weights, at most 5 step halvings, failure below 10 inliers."""
+    if len(global_set) == 0:
+        raise TrackerError("global set is empty")
+    diag = GicpDiagnostics()
+    systems = []
+    pose = init
+    solver = GicpSolver(local, global_set, cfg)
+    for it in range(cfg.max_gicp_iters):
+        h, g, cost_before, n_acc = solver.linearize(pose)
+        diag.inlier_count = n_acc
+        if it == 0:
+            diag.accepted_first = solver.accepted()
+        if n_acc < MIN_INLIERS:
+            diag.failed = True
+            return (init, diag, systems) if return_systems else (init, diag)
+        systems.append((h, g, cost_before, n_acc))
+        try:
+            xi = np.linalg.solve(h, -g)
+        except np.linalg.LinAlgError:
+            xi = np.linalg.lstsq(h, -g, rcond=None)[0]
+        xis, cands = [], []
+        for _ in range(MAX_STEP_HALVINGS + 1):
+            xis.append(xi)
+            cands.append(se3_exp(xi).compose(pose))
+            xi = 0.5 * xi
+        costs = solver.costs_at(cands)
+        k = 0
+        while costs[k] > cost_before and k < MAX_STEP_HALVINGS:
+            k += 1
+        xi, candidate, cost_after = xis[k], cands[k], float(costs[k])
+        if cost_after > cost_before:
+            diag.final_cost = cost_before
+            break
+        pose = candidate
+        diag.iterations += 1
+        diag.final_cost = cost_after
+        diag.cost_pairs.append((cost_before, cost_after))
+        if np.linalg.norm(xi) < cfg.convergence_eps:
+            diag.converged = True
+            break
+    return (pose, diag, systems) if return_systems else (pose, diag)
+
+
+def init_pose_constant_speed(prev: Pose, prev_prev: Pose) -> Pose:
+    """tracker.py:349-351."""
+    return prev.compose(prev_prev.inverse().compose(prev))

@@ -177,7 +177,7 @@ def window_fit_ref(T, GEO, depth, mask, intr, win=5, k_min=4, scale_mode="ellips
     eigensolver, floor, normalisation and orientation are the reference's own
     (tracker.py:158-169, geometry.py:275)."""
     h, w = depth.shape
-    valid = mask & (depth > 0)
+    valid = np.asarray(mask, dtype=bool)  # tracker.py:201 uses valid_mask only
     vs, us = np.nonzero(valid)
     z_all = depth[vs, us].astype(np.float64)
     pts = np.zeros((h, w, 3))
