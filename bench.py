@@ -40,6 +40,7 @@ def parse():
     ap.add_argument("--config", default="c4", choices=["c3", "c4", "c5"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-track", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-views", type=int, default=0, help="views in the CPU sample (0: auto)")
     return ap.parse_args()
 
@@ -277,7 +278,7 @@ def run_ours(args):
 
     # e2e through the public API with host buffers (params + targets up, params down)
     e2e = None
-    if rank == 0 or world > 1:
+    if not args.no_e2e:
         e2e = measure_e2e(wm, args, dev, world)
 
     track = None

@@ -170,6 +170,28 @@ def mapping_step(gmap, optimizer: MapOptimizer, target_frame, target_pose, neigh
 # ---------------------------------------------------------------- window engine
 
 
+def shard_views(n_views: int, rank: int, world: int):
+    """Views rendered by ``rank``: round-robin, so every rank gets n/world of
+    them when world divides the window (8 keyframes over 1/2/4/8 GPUs)."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("bad rank/world")
+    return list(range(rank, n_views, world))
+
+
+def allreduce_window(grad: torch.Tensor, loss_acc: torch.Tensor, group=None) -> bool:
+    """The one exchange step of a window iteration: SUM of the per-Gaussian
+    gradient buffer [N, 8] and of the per-view loss sums over ranks (the
+    objective is a sum over views).  No-op without an initialised group."""
+    dist = torch.distributed
+    if not (dist.is_available() and dist.is_initialized()):
+        return False
+    if dist.get_world_size(group) == 1:
+        return False
+    dist.all_reduce(grad, group=group)
+    dist.all_reduce(loss_acc, group=group)
+    return True
+
+
 class WindowMapper:
     """All-learnable keyframe window, fp32 parameters, fused loss + backward.
 
@@ -256,10 +278,7 @@ class WindowMapper:
         with torch.cuda.device(self.dev):
             for v in self.views:
                 self.render_view_grads(v)
-            if self.pg is not None or (torch.distributed.is_available() and
-                                       torch.distributed.is_initialized()):
-                torch.distributed.all_reduce(self.grad, group=self.pg)
-                torch.distributed.all_reduce(self.loss_acc, group=self.pg)
+            allreduce_window(self.grad, self.loss_acc, self.pg)
             self.t += 1
             _adam(self.planes, self.grad, self.m, self.v, self.F, self.HW, self.cfg, self.t, False)
         n_color = 3.0 * self.HW

@@ -107,7 +107,7 @@ def test_gicp_failure_and_empty():
     pts = rng.uniform(-1, 1, (500, 3))
     rot = np.broadcast_to(np.eye(3), (500, 3, 3)).copy()
     sc = np.full((500, 3), 1 / np.sqrt(3))
-    nrm = np.tile([0.0, 0.0, -1.0], (500, 1))
+    nrm = np.tile([1.0, 0.0, 0.0], (500, 1))  # offsets along x fail the surface gate
     local = LocalGeomSet(pts, rot, sc, nrm)
     with pytest.raises(TrackerError, match="empty"):
         gicp_align(local, GlobalGeomSet(), Pose.identity(), TrackerConfig())
