@@ -269,53 +269,27 @@ __device__ __forceinline__ TileGeom tile_geom(int ntx, int width, int height) {
   return g;
 }
 
-struct StageSmem {
-  double u0[BATCH], v0[BATCH], thr[BATCH], s2[BATCH], op[BATCH], z[BATCH], sig[BATCH];
-  double rgb[3][BATCH];
-  uint32_t gid[BATCH];
-  uint8_t wmask[BATCH];
+// Each warp owns one 8x4 sub-tile and walks the tile's depth-ordered list on
+// its own (no block barriers: sub-tiles finish at different list positions).
+// Per chunk of 32 list entries the warp culls against its rectangle, stages
+// the survivors in its private shared-memory slots, then every lane builds a
+// bitmask of the staged entries its pixel passes (the reference's exact
+// d2 > 9 s2 test) and pops its own bits in list order -- lanes work on
+// different Gaussians at the same time, so divergence only costs the tail.
+struct WarpStage {
+  double u0[32], v0[32], thr[32], s2[32], sig[32], op[32], z[32], rgb[3][32];
+  uint32_t k[32], gid[32];
 };
 
-// Conservative: bit w set unless every pixel centre of warp w's 8x4 sub-tile
-// fails the reference test d2 > 9 s2 (computed with the same rounded ops, so
-// the rectangle's closest pixel gives the minimum; K4).
-__device__ __forceinline__ uint8_t warp_cull_mask(double u0, double v0, double thr, int tx, int ty,
-                                                  uint8_t active_warps) {
-  uint8_t m = 0;
-#pragma unroll
-  for (int w = 0; w < 8; ++w) {
-    if (!((active_warps >> w) & 1)) continue;
-    const double xlo = (double)(tx * SGAD_TILE + (w & 1) * 8), xhi = xlo + 7.0;
-    const double ylo = (double)(ty * SGAD_TILE + (w >> 1) * 4), yhi = ylo + 3.0;
-    double dx = 0.0, dy = 0.0;
-    if (u0 < xlo) dx = SG_SUB(u0, xlo); else if (u0 > xhi) dx = SG_SUB(u0, xhi);
-    if (v0 < ylo) dy = SG_SUB(v0, ylo); else if (v0 > yhi) dy = SG_SUB(v0, yhi);
-    const double d2 = SG_ADD(SG_MUL(dx, dx), SG_MUL(dy, dy));
-    if (!(d2 > thr)) m |= (uint8_t)(1u << w);
-  }
-  return m;
-}
-
-__device__ __forceinline__ void stage_record(StageSmem& s, int j, const Record& r,
-                                             const double* col64, uint32_t e) {
-  s.u0[j] = r.u0;
-  s.v0[j] = r.v0;
-  s.sig[j] = r.sigma;
-  const double s2 = SG_MUL(r.sigma, r.sigma);
-  s.s2[j] = s2;
-  s.thr[j] = SG_MUL(9.0, s2);
-  s.op[j] = r.opacity;
-  s.z[j] = r.z;
-  if (col64) {  // fp64 drop-in maps keep exact fp64 colours
-    s.rgb[0][j] = col64[3 * (size_t)e];
-    s.rgb[1][j] = col64[3 * (size_t)e + 1];
-    s.rgb[2][j] = col64[3 * (size_t)e + 2];
-  } else {
-    s.rgb[0][j] = r.r;
-    s.rgb[1][j] = r.g;
-    s.rgb[2][j] = r.b;
-  }
-  s.gid[j] = r.gid;
+// Conservative sub-tile cull: false only if every pixel centre of the 8x4
+// rectangle fails the reference test (the closest pixel's d2 is computed with
+// the same rounded ops, and rounding is monotone; K4).
+__device__ __forceinline__ bool rect_hit(double u0, double v0, double thr, double xlo, double ylo) {
+  const double xhi = xlo + 7.0, yhi = ylo + 3.0;
+  double dx = 0.0, dy = 0.0;
+  if (u0 < xlo) dx = SG_SUB(u0, xlo); else if (u0 > xhi) dx = SG_SUB(u0, xhi);
+  if (v0 < ylo) dy = SG_SUB(v0, ylo); else if (v0 > yhi) dy = SG_SUB(v0, yhi);
+  return !(SG_ADD(SG_MUL(dx, dx), SG_MUL(dy, dy)) > thr);
 }
 
 __device__ __forceinline__ Record load_record(const Record* rec, uint32_t e) {
@@ -329,17 +303,49 @@ __device__ __forceinline__ Record load_record(const Record* rec, uint32_t e) {
   return r;
 }
 
-
-// Per-warp activity bytes are double-buffered by batch parity so one
-// __syncthreads() separates "warps publish activity" from "stage next batch".
-__device__ __forceinline__ uint32_t block_active_warps(volatile uint8_t (*flags)[8], int parity,
-                                                       bool warp_active, int warp, int lane) {
-  if (lane == 0) flags[parity][warp] = warp_active ? 1 : 0;
-  __syncthreads();
-  uint32_t act = 0;
-#pragma unroll
-  for (int w = 0; w < 8; ++w) act |= (uint32_t)flags[parity][w] << w;
-  return act;
+// Stage list entries [base, base+32) that hit this warp's rectangle, in list
+// order; returns their count (uniform across the warp).
+__device__ __forceinline__ int stage_chunk(WarpStage& s, const uint32_t* __restrict__ lists,
+                                           const Record* __restrict__ rec,
+                                           const double* __restrict__ col64, uint32_t base,
+                                           uint32_t end, double xlo, double ylo, int lane,
+                                           uint32_t* eidx_out) {
+  const uint32_t k = base + lane;
+  bool keep = false;
+  Record r;
+  uint32_t e = 0;
+  double thr = 0.0;
+  if (k < end) {
+    e = lists[k];
+    r = load_record(rec, e);
+    thr = SG_MUL(9.0, SG_MUL(r.sigma, r.sigma));
+    keep = rect_hit(r.u0, r.v0, thr, xlo, ylo);
+  }
+  const uint32_t km = __ballot_sync(0xffffffffu, keep);
+  if (keep) {
+    const int j = __popc(km & ((1u << lane) - 1u));
+    s.u0[j] = r.u0;
+    s.v0[j] = r.v0;
+    s.thr[j] = thr;
+    s.s2[j] = SG_MUL(r.sigma, r.sigma);
+    s.sig[j] = r.sigma;
+    s.op[j] = r.opacity;
+    s.z[j] = r.z;
+    if (col64) {  // fp64 drop-in maps keep exact fp64 colours
+      s.rgb[0][j] = col64[3 * (size_t)e];
+      s.rgb[1][j] = col64[3 * (size_t)e + 1];
+      s.rgb[2][j] = col64[3 * (size_t)e + 2];
+    } else {
+      s.rgb[0][j] = r.r;
+      s.rgb[1][j] = r.g;
+      s.rgb[2][j] = r.b;
+    }
+    s.k[j] = k;
+    s.gid[j] = r.gid;
+    if (eidx_out) eidx_out[j] = e;
+  }
+  __syncwarp();
+  return __popc(km);
 }
 
 // ------------------------------------------------------------------ K4
@@ -351,60 +357,51 @@ k_forward(const uint2* __restrict__ ranges, const uint32_t* __restrict__ lists,
           double* __restrict__ out_alpha, int32_t* __restrict__ out_count,
           double* __restrict__ t_final, int32_t* __restrict__ last_out,
           uint8_t* __restrict__ signs, sgad_loss_target tgt) {
-  __shared__ StageSmem s;
-  __shared__ volatile uint8_t s_flags[2][8];
-  __shared__ double s_red[2][8];
+  __shared__ WarpStage stage[RASTER_THREADS / 32];
+  __shared__ double s_red[2][RASTER_THREADS / 32];
   const TileGeom g = tile_geom(ntx, width, height);
+  WarpStage& s = stage[g.warp];
   const uint2 rg = ranges[g.tile];
   const double pxd = (double)g.px, pyd = (double)g.py;
+  const double xlo = (double)(g.tx * SGAD_TILE + (g.warp & 1) * 8);
+  const double ylo = (double)(g.ty * SGAD_TILE + (g.warp >> 1) * 4);
   double T = 1.0, C0 = 0.0, C1 = 0.0, C2 = 0.0, D = 0.0, A = 0.0;
   int cnt = 0, last = -1;
   bool done = !g.valid;
-  int parity = 0;
 
-  for (uint32_t base = rg.x; base < rg.y; base += BATCH, parity ^= 1) {
-    const bool wact = __any_sync(0xffffffffu, !done);
-    const uint32_t act = block_active_warps(s_flags, parity, wact, g.warp, g.lane);
-    if (act == 0) break;
-    const uint32_t k = base + threadIdx.x;
-    uint8_t wm = 0;
-    if (k < rg.y) {
-      const uint32_t e = lists[k];
-      const Record r = load_record(rec, e);
-      stage_record(s, threadIdx.x, r, col64, e);
-      wm = warp_cull_mask(r.u0, r.v0, s.thr[threadIdx.x], g.tx, g.ty, (uint8_t)act);
-    }
-    s.wmask[threadIdx.x] = wm;
-    __syncthreads();
-    if (wact) {
-#pragma unroll 1
-      for (int c = 0; c < BATCH / 32; ++c) {
-        uint32_t m = __ballot_sync(0xffffffffu, (s.wmask[c * 32 + g.lane] >> g.warp) & 1);
-        while (m) {
-          const int j = c * 32 + __ffs(m) - 1;
-          m &= m - 1;
-          if (!done) {
-            const double dx = SG_SUB(s.u0[j], pxd), dy = SG_SUB(s.v0[j], pyd);
-            const double d2 = SG_ADD(SG_MUL(dx, dx), SG_MUL(dy, dy));
-            if (!(d2 > s.thr[j])) {
-              const double w = sgad_exp(SG_DIV(SG_MUL(-0.5, d2), s.s2[j]));
-              double a = SG_MUL(s.op[j], w);
-              if (a > SGAD_ALPHA_MAX) a = SGAD_ALPHA_MAX;
-              const double at = SG_MUL(a, T);
-              C0 = SG_ADD(C0, SG_MUL(s.rgb[0][j], at));
-              C1 = SG_ADD(C1, SG_MUL(s.rgb[1][j], at));
-              C2 = SG_ADD(C2, SG_MUL(s.rgb[2][j], at));
-              D = SG_ADD(D, SG_MUL(s.z[j], at));
-              A = SG_ADD(A, at);
-              ++cnt;
-              last = (int)(base + j);
-              T = SG_MUL(T, SG_SUB(1.0, a));
-              if (T < SGAD_TRANSMITTANCE_MIN) done = true;
-            }
-          }
-        }
+  for (uint32_t base = rg.x; base < rg.y; base += 32) {
+    if (__all_sync(0xffffffffu, done)) break;
+    const int c = stage_chunk(s, lists, rec, col64, base, rg.y, xlo, ylo, g.lane, nullptr);
+    uint32_t mine = 0;
+    if (!done) {
+      for (int j = 0; j < c; ++j) {
+        const double dx = SG_SUB(s.u0[j], pxd), dy = SG_SUB(s.v0[j], pyd);
+        if (!(SG_ADD(SG_MUL(dx, dx), SG_MUL(dy, dy)) > s.thr[j])) mine |= 1u << j;
       }
     }
+    while (mine) {
+      const int j = __ffs(mine) - 1;
+      mine &= mine - 1;
+      const double dx = SG_SUB(s.u0[j], pxd), dy = SG_SUB(s.v0[j], pyd);
+      const double d2 = SG_ADD(SG_MUL(dx, dx), SG_MUL(dy, dy));
+      const double w = sgad_exp(SG_DIV(SG_MUL(-0.5, d2), s.s2[j]));
+      double a = SG_MUL(s.op[j], w);
+      if (a > SGAD_ALPHA_MAX) a = SGAD_ALPHA_MAX;
+      const double at = SG_MUL(a, T);
+      C0 = SG_ADD(C0, SG_MUL(s.rgb[0][j], at));
+      C1 = SG_ADD(C1, SG_MUL(s.rgb[1][j], at));
+      C2 = SG_ADD(C2, SG_MUL(s.rgb[2][j], at));
+      D = SG_ADD(D, SG_MUL(s.z[j], at));
+      A = SG_ADD(A, at);
+      ++cnt;
+      last = (int)s.k[j];
+      T = SG_MUL(T, SG_SUB(1.0, a));
+      if (T < SGAD_TRANSMITTANCE_MIN) {
+        done = true;
+        mine = 0;
+      }
+    }
+    __syncwarp();
   }
 
   const int64_t p = (int64_t)g.py * width + g.px;
@@ -455,7 +452,7 @@ k_forward(const uint2* __restrict__ ranges, const uint32_t* __restrict__ lists,
     __syncthreads();
     if (threadIdx.x == 0) {
       double a = 0.0, b = 0.0;
-      for (int w = 0; w < 8; ++w) {
+      for (int w = 0; w < RASTER_THREADS / 32; ++w) {
         a += s_red[0][w];
         b += s_red[1][w];
       }
@@ -466,12 +463,6 @@ k_forward(const uint2* __restrict__ ranges, const uint32_t* __restrict__ lists,
 }
 
 // ------------------------------------------------------------------ K5
-struct BwdSmem {
-  StageSmem st;
-  uint32_t eidx[BATCH];
-  float coef[6][BATCH];
-};
-
 struct Upstream {  // fused-loss upstream scales: rho / (3HW), sigma / |U|
   double kc, kd;
 };
@@ -480,21 +471,30 @@ __device__ __forceinline__ double sign_of(uint32_t code) {
   return code == 1u ? 1.0 : (code == 2u ? -1.0 : 0.0);
 }
 
+struct BwdExtra {
+  uint32_t eidx[32];
+  float coef[6][32];
+  float acc[6][32];
+};
+
 template <bool FUSED>
 __global__ void __launch_bounds__(RASTER_THREADS)
 k_backward(const uint2* __restrict__ ranges, const uint32_t* __restrict__ lists,
            const Record* __restrict__ rec, const ChainCoef* __restrict__ coef,
-           const double* __restrict__ col64, int ntx, int width,
-           int height, const double* __restrict__ t_final, const int32_t* __restrict__ last_idx,
+           const double* __restrict__ col64, int ntx, int width, int height,
+           const double* __restrict__ t_final, const int32_t* __restrict__ last_idx,
            const uint8_t* __restrict__ signs, Upstream up, const double* __restrict__ g_color,
            const double* __restrict__ g_depth, const double* __restrict__ g_alpha,
            double* __restrict__ raw, float* __restrict__ grad_accum) {
-  __shared__ BwdSmem s;
-  __shared__ volatile uint8_t s_flags[2][8];
-  __shared__ int s_end;
+  __shared__ WarpStage stage[RASTER_THREADS / 32];
+  __shared__ BwdExtra extra[RASTER_THREADS / 32];
   const TileGeom g = tile_geom(ntx, width, height);
+  WarpStage& s = stage[g.warp];
+  BwdExtra& x = extra[g.warp];
   const uint2 rg = ranges[g.tile];
   const double pxd = (double)g.px, pyd = (double)g.py;
+  const double xlo = (double)(g.tx * SGAD_TILE + (g.warp & 1) * 8);
+  const double ylo = (double)(g.ty * SGAD_TILE + (g.warp >> 1) * 4);
   const int64_t p = (int64_t)g.py * width + g.px;
 
   double gc0 = 0.0, gc1 = 0.0, gc2 = 0.0, gd = 0.0, ga = 0.0, T = 0.0;
@@ -520,128 +520,112 @@ k_backward(const uint2* __restrict__ ranges, const uint32_t* __restrict__ lists,
       T = t_final[p];
     }
   }
-  if (threadIdx.x == 0) s_end = (int)rg.x;
-  __syncthreads();
-  if (mylast >= 0) atomicMax(&s_end, mylast + 1);
-  __syncthreads();
-  const int end = s_end;
-
+  int wend = mylast + 1;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) wend = max(wend, __shfl_xor_sync(0xffffffffu, wend, o));
+  if (FUSED) {
+#pragma unroll
+    for (int i = 0; i < 6; ++i) x.acc[i][g.lane] = 0.f;
+  }
   double sc0 = 0.0, sc1 = 0.0, sc2 = 0.0, sd = 0.0, sa = 0.0;
-  int parity = 0;
-  for (int bend = end; bend > (int)rg.x; bend -= BATCH, parity ^= 1) {
-    const int bstart = max((int)rg.x, bend - BATCH);
-    const bool wact = __any_sync(0xffffffffu, mylast >= bstart);
-    const uint32_t act = block_active_warps(s_flags, parity, wact, g.warp, g.lane);
-    if (act == 0) continue;  // uniform across the block
-    const int k = bstart + (int)threadIdx.x;
-    uint8_t wm = 0;
-    if (k < bend) {
-      const uint32_t e = lists[k];
-      const Record r = load_record(rec, e);
-      stage_record(s.st, threadIdx.x, r, col64, e);
-      s.eidx[threadIdx.x] = e;
-      if (FUSED) {
-        const ChainCoef cc = coef[e];
-        s.coef[0][threadIdx.x] = cc.k_r;
-        s.coef[1][threadIdx.x] = cc.a_u;
-        s.coef[2][threadIdx.x] = cc.a_v;
-        s.coef[3][threadIdx.x] = cc.a_z;
-        s.coef[4][threadIdx.x] = cc.a_s;
-        s.coef[5][threadIdx.x] = cc.k_op;
-      }
-      wm = warp_cull_mask(r.u0, r.v0, s.st.thr[threadIdx.x], g.tx, g.ty, (uint8_t)act);
+  for (int top = wend; top > (int)rg.x; top -= 32) {
+    const uint32_t base = (uint32_t)max((int)rg.x, top - 32);
+    const int c = stage_chunk(s, lists, rec, col64, base, (uint32_t)top, xlo, ylo, g.lane, x.eidx);
+    if (FUSED && g.lane < c) {
+      const ChainCoef cc = coef[x.eidx[g.lane]];
+      x.coef[0][g.lane] = cc.k_r;
+      x.coef[1][g.lane] = cc.a_u;
+      x.coef[2][g.lane] = cc.a_v;
+      x.coef[3][g.lane] = cc.a_z;
+      x.coef[4][g.lane] = cc.a_s;
+      x.coef[5][g.lane] = cc.k_op;
     }
-    s.st.wmask[threadIdx.x] = wm;
-    __syncthreads();
-    if (wact) {
-#pragma unroll 1
-      for (int c = BATCH / 32 - 1; c >= 0; --c) {
-        uint32_t m = __ballot_sync(0xffffffffu, (s.st.wmask[c * 32 + g.lane] >> g.warp) & 1);
-        while (m) {
-          const int hb = 31 - __clz(m);
-          m &= ~(1u << hb);
-          const int j = c * 32 + hb;
-          const int kk = bstart + j;
-          bool contrib = false;
-          float q[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-          if (kk <= mylast) {
-            const double dx = SG_SUB(s.st.u0[j], pxd), dy = SG_SUB(s.st.v0[j], pyd);
-            const double d2 = SG_ADD(SG_MUL(dx, dx), SG_MUL(dy, dy));
-            if (!(d2 > s.st.thr[j])) {
-              const double s2 = s.st.s2[j], op = s.st.op[j], z = s.st.z[j];
-              const double w = sgad_exp(SG_DIV(SG_MUL(-0.5, d2), s2));
-              const double aw = SG_MUL(op, w);
-              const bool clamped = aw > SGAD_ALPHA_MAX;
-              const double a = clamped ? SGAD_ALPHA_MAX : aw;
-              const double om = SG_SUB(1.0, a);
-              const double tb = SG_DIV(T, om);
-              const double at = SG_MUL(a, tb);
-              const double c0 = s.st.rgb[0][j], c1 = s.st.rgb[1][j], c2 = s.st.rgb[2][j];
-              const uint32_t gidw = s.st.gid[j];
-              if (gidw & GID_LEARN) {
-                double d_alpha = SG_MUL(gc0, SG_SUB(SG_MUL(c0, tb), SG_DIV(sc0, om)));
-                d_alpha = SG_ADD(d_alpha, SG_MUL(gc1, SG_SUB(SG_MUL(c1, tb), SG_DIV(sc1, om))));
-                d_alpha = SG_ADD(d_alpha, SG_MUL(gc2, SG_SUB(SG_MUL(c2, tb), SG_DIV(sc2, om))));
-                d_alpha = SG_ADD(d_alpha, SG_MUL(gd, SG_SUB(SG_MUL(z, tb), SG_DIV(sd, om))));
-                d_alpha = SG_ADD(d_alpha, SG_MUL(ga, SG_SUB(tb, SG_DIV(sa, om))));
-                const double gcol0 = SG_MUL(gc0, at), gcol1 = SG_MUL(gc1, at),
-                             gcol2 = SG_MUL(gc2, at), gz = SG_MUL(gd, at);
-                double gop = 0.0, gsig = 0.0, gu = 0.0, gv = 0.0;
-                if (!clamped) {
-                  const double gw = SG_MUL(d_alpha, op);
-                  gop = SG_MUL(d_alpha, w);
-                  gsig = SG_DIV(SG_MUL(SG_MUL(gw, w), d2), SG_MUL(s2, s.st.sig[j]));
-                  const double gd2 = SG_MUL(gw, SG_DIV(SG_MUL(-0.5, w), s2));
-                  gu = SG_MUL(SG_MUL(gd2, 2.0), dx);
-                  gv = SG_MUL(SG_MUL(gd2, 2.0), dy);
-                }
-                if (FUSED) {
-                  q[0] = (float)(s.coef[1][j] * gu + s.coef[2][j] * gv + s.coef[3][j] * gz +
-                                 s.coef[4][j] * gsig);
-                  q[1] = (float)(s.coef[0][j] * gsig);
-                  q[2] = (float)(s.coef[5][j] * gop);
-                  q[3] = (float)gcol0;
-                  q[4] = (float)gcol1;
-                  q[5] = (float)gcol2;
-                  contrib = true;
-                } else {
-                  double* dst = raw + (size_t)s.eidx[j] * 8;
-                  atomicAdd(dst + 0, gcol0);
-                  atomicAdd(dst + 1, gcol1);
-                  atomicAdd(dst + 2, gcol2);
-                  atomicAdd(dst + 3, gop);
-                  atomicAdd(dst + 4, gu);
-                  atomicAdd(dst + 5, gv);
-                  atomicAdd(dst + 6, gsig);
-                  atomicAdd(dst + 7, gz);
-                }
-              }
-              sc0 = SG_ADD(sc0, SG_MUL(c0, at));
-              sc1 = SG_ADD(sc1, SG_MUL(c1, at));
-              sc2 = SG_ADD(sc2, SG_MUL(c2, at));
-              sd = SG_ADD(sd, SG_MUL(z, at));
-              sa = SG_ADD(sa, at);
-              T = tb;
-            }
-          }
-          if (FUSED) {
-            if (__any_sync(0xffffffffu, contrib)) {
-#pragma unroll
-              for (int o = 16; o > 0; o >>= 1) {
-#pragma unroll
-                for (int i = 0; i < 6; ++i) q[i] += __shfl_xor_sync(0xffffffffu, q[i], o);
-              }
-              if (g.lane == 0) {
-                float4* dst = reinterpret_cast<float4*>(grad_accum + (size_t)(s.st.gid[j] & ~GID_LEARN) * 8);
-                atomicAdd(dst, make_float4(q[0], q[1], q[2], q[3]));
-                atomicAdd(reinterpret_cast<float2*>(dst + 1), make_float2(q[4], q[5]));
-              }
-            }
-          }
+    __syncwarp();
+    uint32_t mine = 0;
+    for (int j = 0; j < c; ++j) {
+      if ((int)s.k[j] > mylast) continue;
+      const double dx = SG_SUB(s.u0[j], pxd), dy = SG_SUB(s.v0[j], pyd);
+      if (!(SG_ADD(SG_MUL(dx, dx), SG_MUL(dy, dy)) > s.thr[j])) mine |= 1u << j;
+    }
+    while (mine) {
+      const int j = 31 - __clz(mine);
+      mine &= ~(1u << j);
+      const double dx = SG_SUB(s.u0[j], pxd), dy = SG_SUB(s.v0[j], pyd);
+      const double d2 = SG_ADD(SG_MUL(dx, dx), SG_MUL(dy, dy));
+      const double s2 = s.s2[j], op = s.op[j], z = s.z[j];
+      const double w = sgad_exp(SG_DIV(SG_MUL(-0.5, d2), s2));
+      const double aw = SG_MUL(op, w);
+      const bool clamped = aw > SGAD_ALPHA_MAX;
+      const double a = clamped ? SGAD_ALPHA_MAX : aw;
+      const double om = SG_SUB(1.0, a);
+      const double tb = SG_DIV(T, om);
+      const double at = SG_MUL(a, tb);
+      const double c0 = s.rgb[0][j], c1 = s.rgb[1][j], c2 = s.rgb[2][j];
+      if (s.gid[j] & GID_LEARN) {
+        const double iom = FUSED ? 1.0 / om : 0.0;
+        double d_alpha;
+        if (FUSED) {  // gradients carry a 1e-3 bar: one reciprocal instead of five divisions
+          d_alpha = gc0 * (c0 * tb - sc0 * iom) + gc1 * (c1 * tb - sc1 * iom) +
+                    gc2 * (c2 * tb - sc2 * iom) + gd * (z * tb - sd * iom) + ga * (tb - sa * iom);
+        } else {
+          d_alpha = SG_MUL(gc0, SG_SUB(SG_MUL(c0, tb), SG_DIV(sc0, om)));
+          d_alpha = SG_ADD(d_alpha, SG_MUL(gc1, SG_SUB(SG_MUL(c1, tb), SG_DIV(sc1, om))));
+          d_alpha = SG_ADD(d_alpha, SG_MUL(gc2, SG_SUB(SG_MUL(c2, tb), SG_DIV(sc2, om))));
+          d_alpha = SG_ADD(d_alpha, SG_MUL(gd, SG_SUB(SG_MUL(z, tb), SG_DIV(sd, om))));
+          d_alpha = SG_ADD(d_alpha, SG_MUL(ga, SG_SUB(tb, SG_DIV(sa, om))));
+        }
+        const double gcol0 = SG_MUL(gc0, at), gcol1 = SG_MUL(gc1, at), gcol2 = SG_MUL(gc2, at),
+                     gz = SG_MUL(gd, at);
+        double gop = 0.0, gsig = 0.0, gu = 0.0, gv = 0.0;
+        if (!clamped) {
+          const double gw = SG_MUL(d_alpha, op);
+          gop = SG_MUL(d_alpha, w);
+          gsig = SG_DIV(SG_MUL(SG_MUL(gw, w), d2), SG_MUL(s2, s.sig[j]));
+          const double gd2 = SG_MUL(gw, SG_DIV(SG_MUL(-0.5, w), s2));
+          gu = SG_MUL(SG_MUL(gd2, 2.0), dx);
+          gv = SG_MUL(SG_MUL(gd2, 2.0), dy);
+        }
+        if (FUSED) {
+          atomicAdd(&x.acc[0][j], (float)(x.coef[1][j] * gu + x.coef[2][j] * gv +
+                                          x.coef[3][j] * gz + x.coef[4][j] * gsig));
+          atomicAdd(&x.acc[1][j], (float)(x.coef[0][j] * gsig));
+          atomicAdd(&x.acc[2][j], (float)(x.coef[5][j] * gop));
+          atomicAdd(&x.acc[3][j], (float)gcol0);
+          atomicAdd(&x.acc[4][j], (float)gcol1);
+          atomicAdd(&x.acc[5][j], (float)gcol2);
+        } else {
+          double* dst = raw + (size_t)x.eidx[j] * 8;
+          atomicAdd(dst + 0, gcol0);
+          atomicAdd(dst + 1, gcol1);
+          atomicAdd(dst + 2, gcol2);
+          atomicAdd(dst + 3, gop);
+          atomicAdd(dst + 4, gu);
+          atomicAdd(dst + 5, gv);
+          atomicAdd(dst + 6, gsig);
+          atomicAdd(dst + 7, gz);
         }
       }
+      sc0 = SG_ADD(sc0, SG_MUL(c0, at));
+      sc1 = SG_ADD(sc1, SG_MUL(c1, at));
+      sc2 = SG_ADD(sc2, SG_MUL(c2, at));
+      sd = SG_ADD(sd, SG_MUL(z, at));
+      sa = SG_ADD(sa, at);
+      T = tb;
     }
-    __syncthreads();
+    __syncwarp();
+    if (FUSED && g.lane < c) {
+      const int j = g.lane;
+      const float q0 = x.acc[0][j], q1 = x.acc[1][j], q2 = x.acc[2][j], q3 = x.acc[3][j],
+                  q4 = x.acc[4][j], q5 = x.acc[5][j];
+      if (q0 != 0.f || q1 != 0.f || q2 != 0.f || q3 != 0.f || q4 != 0.f || q5 != 0.f) {
+        float4* dst = reinterpret_cast<float4*>(grad_accum + (size_t)(s.gid[j] & ~GID_LEARN) * 8);
+        atomicAdd(dst, make_float4(q0, q1, q2, q3));
+        atomicAdd(reinterpret_cast<float2*>(dst + 1), make_float2(q4, q5));
+      }
+#pragma unroll
+      for (int i = 0; i < 6; ++i) x.acc[i][j] = 0.f;
+    }
+    __syncwarp();
   }
 }
 

@@ -233,6 +233,21 @@ def plane_spheres_scene(seed: int = 0):
     return prims
 
 
+def corner_spheres_scene(seed: int = 0):
+    """C2: floor, back wall and side wall (a well-posed registration target)
+    plus 3 spheres of radius 0.3-0.6 m; depth spans ~1-3 m."""
+    rng = np.random.default_rng(seed)
+    grey = Checker((0.5, 0.5, 0.5), (0.7, 0.7, 0.7), cell=0.3)
+    prims = [Rect((-3.0, 0.8, -1.0), (6.0, 0.0, 0.0), (0.0, 0.0, 6.0), grey),
+             Rect((-3.0, -2.0, 3.0), (6.0, 0.0, 0.0), (0.0, 2.8, 0.0), grey),
+             Rect((-1.4, -2.0, -1.0), (0.0, 2.8, 0.0), (0.0, 0.0, 4.0), grey)]
+    for _ in range(3):
+        r = float(rng.uniform(0.3, 0.6))
+        prims.append(Sphere((float(rng.uniform(-0.6, 0.8)), float(rng.uniform(-0.3, 0.8 - r)),
+                             float(rng.uniform(1.5, 2.6))), r, tuple(rng.uniform(0.2, 0.9, 3))))
+    return prims
+
+
 def room_scene(seed: int = 0, n_spheres: int = 20):
     """Five box walls (floor, ceiling, back, left, right) plus random spheres."""
     rng = np.random.default_rng(seed)
@@ -346,7 +361,7 @@ def config_c2(device="cpu"):
     """C2: reference frame (identity) and a query under a seeded <=2 deg / <=5 cm
     perturbation; both with 1 % multiplicative depth noise."""
     intr = Intrinsics(**C2_INTR)
-    prims = plane_spheres_scene(0)
+    prims = corner_spheres_scene(0)
     rng = np.random.default_rng(3)
     axis = rng.normal(size=3)
     axis /= np.linalg.norm(axis)
