@@ -327,13 +327,21 @@ k_track_fit(FitArgs a, double* __restrict__ centers, double* __restrict__ cov,
   if (threadIdx.x == 0 && (int64_t)(tile + 1) * TRK_THREADS >= npx) *count_out = s_prefix + agg;
 }
 
-// ---------------------------------------------------------------- K10 grid NN
+// ---------------------------------------------------------------- K10 exact 1-NN
+// Uniform hash grid over the target centres.  The cell size adapts to the
+// point density (surfaces: ~3 points per occupied cell).  A query searches
+// Chebyshev rings of cells around its (clamped) cell, pruning cells whose box
+// is farther than the best distance so far, and stops when no unvisited cell
+// can hold a closer point.  Queries still unresolved after MAX_RINGS rings
+// (far from every surface) fall back to an exact block-parallel scan, so the
+// result is always the exact Euclidean nearest neighbour (ties -> lower index),
+// as scipy cKDTree gives the reference (tracker.py:125-128).
+constexpr int MAX_RINGS = 4;
+constexpr unsigned long long HASH_EMPTY = ~0ull;
+
 __device__ __forceinline__ unsigned long long dkey(double x) {
   unsigned long long b = (unsigned long long)__double_as_longlong(x);
   return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
-}
-__device__ __forceinline__ double dkey_inv(unsigned long long k) {
-  return __longlong_as_double((long long)((k >> 63) ? (k & 0x7fffffffffffffffull) : ~k));
 }
 
 __global__ void k_bbox(const double* __restrict__ pts, int64_t n, unsigned long long* __restrict__ bb) {
@@ -355,6 +363,7 @@ struct Grid {
   double lo[3];
   double h;
   int dim[3];
+  unsigned long long hmask;  // hash table size - 1
 };
 
 __device__ __forceinline__ int cell_coord(double x, double lo, double h, int dim) {
@@ -363,57 +372,106 @@ __device__ __forceinline__ int cell_coord(double x, double lo, double h, int dim
   return (int)c;
 }
 
-__global__ void k_grid_count(const double* __restrict__ pts, int64_t n, Grid g,
-                             uint32_t* __restrict__ cnt, uint32_t* __restrict__ cell_of) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const int cx = cell_coord(pts[3 * i], g.lo[0], g.h, g.dim[0]);
-  const int cy = cell_coord(pts[3 * i + 1], g.lo[1], g.h, g.dim[1]);
-  const int cz = cell_coord(pts[3 * i + 2], g.lo[2], g.h, g.dim[2]);
-  const uint32_t c = ((uint32_t)cx * g.dim[1] + cy) * g.dim[2] + cz;
-  cell_of[i] = c;
-  atomicAdd(cnt + c, 1u);
+__device__ __forceinline__ unsigned long long cell_key(int x, int y, int z) {
+  return ((unsigned long long)x << 42) | ((unsigned long long)y << 21) | (unsigned long long)z;
 }
 
-__global__ void k_grid_fill(const uint32_t* __restrict__ cell_of, int64_t n,
-                            uint32_t* __restrict__ cursor, uint32_t* __restrict__ items) {
+__device__ __forceinline__ unsigned long long hash64(unsigned long long k) {
+  k ^= k >> 33;
+  k *= 0xff51afd7ed558ccdull;
+  k ^= k >> 33;
+  k *= 0xc4ceb9fe1a85ec53ull;
+  k ^= k >> 33;
+  return k;
+}
+
+__global__ void k_cell_keys(const double* __restrict__ pts, int64_t n, Grid g,
+                            unsigned long long* __restrict__ keys, uint32_t* __restrict__ idx) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  items[atomicAdd(cursor + cell_of[i], 1u)] = (uint32_t)i;
+  keys[i] = cell_key(cell_coord(pts[3 * i], g.lo[0], g.h, g.dim[0]),
+                     cell_coord(pts[3 * i + 1], g.lo[1], g.h, g.dim[1]),
+                     cell_coord(pts[3 * i + 2], g.lo[2], g.h, g.dim[2]));
+  idx[i] = (uint32_t)i;
+}
+
+__global__ void k_cell_heads(const unsigned long long* __restrict__ keys, int64_t n,
+                             uint32_t* __restrict__ head) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  head[i] = (i == 0 || keys[i] != keys[i - 1]) ? 1u : 0u;
+}
+
+// head_scan = inclusive scan of head: cell id of point i is head_scan[i] - 1
+__global__ void k_cell_table(const unsigned long long* __restrict__ keys, int64_t n,
+                             const uint32_t* __restrict__ head_scan, uint32_t* __restrict__ start,
+                             unsigned long long* __restrict__ hkeys, uint32_t* __restrict__ hvals,
+                             unsigned long long hmask) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  if (i == 0 || keys[i] != keys[i - 1]) {
+    const uint32_t c = head_scan[i] - 1;
+    start[c] = (uint32_t)i;
+    const unsigned long long k = keys[i];
+    unsigned long long s = hash64(k) & hmask;
+    while (true) {
+      const unsigned long long prev = atomicCAS(hkeys + s, HASH_EMPTY, k);
+      if (prev == HASH_EMPTY) {
+        hvals[s] = c;
+        break;
+      }
+      s = (s + 1) & hmask;
+    }
+  }
+  if (i == n - 1) start[head_scan[i]] = (uint32_t)n;
 }
 
 struct GridView {
   Grid g;
-  const uint32_t* start;  // [ncells + 1]
+  const unsigned long long* hkeys;
+  const uint32_t* hvals;
+  const uint32_t* start;
   const uint32_t* items;
   const double* pts;
+  int64_t n;
 };
 
-// Exact Euclidean nearest neighbour: expanding Chebyshev rings around the
-// query's (clamped) cell, stopping once the best squared distance is no
-// larger than the squared distance to any cell not yet visited.
-__device__ void grid_nearest(const GridView& v, const double* q, int64_t& best_j, double& best_d2) {
+__device__ __forceinline__ int hash_find(const GridView& v, unsigned long long k) {
+  unsigned long long s = hash64(k) & v.g.hmask;
+  while (true) {
+    const unsigned long long hk = v.hkeys[s];
+    if (hk == k) return (int)v.hvals[s];
+    if (hk == HASH_EMPTY) return -1;
+    s = (s + 1) & v.g.hmask;
+  }
+}
+
+// Bounded ring search; returns false if MAX_RINGS rings did not settle it.
+__device__ bool grid_nearest(const GridView& v, const double* q, int64_t& best_j, double& best_d2) {
   const Grid& g = v.g;
   int c0[3];
   for (int k = 0; k < 3; ++k) c0[k] = cell_coord(q[k], g.lo[k], g.h, g.dim[k]);
   best_j = -1;
   best_d2 = INFINITY;
-  const int rmax = max(g.dim[0], max(g.dim[1], g.dim[2]));
-  for (int r = 0; r <= rmax; ++r) {
+  for (int r = 0; r <= MAX_RINGS; ++r) {
     const int x0 = max(c0[0] - r, 0), x1 = min(c0[0] + r, g.dim[0] - 1);
     const int y0 = max(c0[1] - r, 0), y1 = min(c0[1] + r, g.dim[1] - 1);
     const int z0 = max(c0[2] - r, 0), z1 = min(c0[2] + r, g.dim[2] - 1);
-    for (int x = x0; x <= x1; ++x)
+    for (int x = x0; x <= x1; ++x) {
+      const double bx0 = g.lo[0] + x * g.h, bx = fmax(fmax(bx0 - q[0], q[0] - (bx0 + g.h)), 0.0);
       for (int y = y0; y <= y1; ++y) {
+        const double by0 = g.lo[1] + y * g.h, by = fmax(fmax(by0 - q[1], q[1] - (by0 + g.h)), 0.0);
         const bool edge_xy = abs(x - c0[0]) == r || abs(y - c0[1]) == r;
         for (int z = z0; z <= z1; ++z) {
           if (!edge_xy && abs(z - c0[2]) != r) {
-            // interior of the ring cube: jump to the far face
-            if (z < c0[2] + r) z = c0[2] + r - 1;
+            if (z < c0[2] + r) z = c0[2] + r - 1;  // skip the interior of the ring cube
             continue;
           }
-          const uint32_t cell = ((uint32_t)x * g.dim[1] + y) * g.dim[2] + z;
-          for (uint32_t t = v.start[cell]; t < v.start[cell + 1]; ++t) {
+          const double bz0 = g.lo[2] + z * g.h, bz = fmax(fmax(bz0 - q[2], q[2] - (bz0 + g.h)), 0.0);
+          if (bx * bx + by * by + bz * bz > best_d2) continue;
+          const int c = hash_find(v, cell_key(x, y, z));
+          if (c < 0) continue;
+          for (uint32_t t = v.start[c]; t < v.start[c + 1]; ++t) {
             const uint32_t j = v.items[t];
             const double dx = q[0] - v.pts[3 * j], dy = q[1] - v.pts[3 * j + 1],
                          dz = q[2] - v.pts[3 * j + 2];
@@ -425,7 +483,9 @@ __device__ void grid_nearest(const GridView& v, const double* q, int64_t& best_j
           }
         }
       }
-    // lower bound on the distance to any cell outside the visited box
+    }
+    // distance to any cell outside the visited box (faces at the grid border
+    // are saturated: nothing lies beyond them)
     double lb = INFINITY;
     bool all_sat = true;
     const int lo_c[3] = {x0, y0, z0}, hi_c[3] = {x1, y1, z1};
@@ -439,21 +499,96 @@ __device__ void grid_nearest(const GridView& v, const double* q, int64_t& best_j
         lb = fmin(lb, fmax((g.lo[k] + (hi_c[k] + 1) * g.h) - q[k], 0.0));
       }
     }
-    if (all_sat) break;
-    if (best_j >= 0 && best_d2 <= lb * lb * (1.0 - 1e-12)) break;
+    if (all_sat) return true;
+    if (best_j >= 0 && best_d2 < lb * lb) return true;
+  }
+  return false;
+}
+
+struct NNArgs {
+  const double* queries;  // [m, 3]
+  int64_t m;
+  int transform;          // apply pose P to the queries first
+  double r[9], t[3];
+  int64_t* idx;
+  double* d2;
+  uint32_t* unresolved;   // [m] list, count in *n_unres
+  uint32_t* n_unres;
+};
+
+__device__ __forceinline__ void query_point(const NNArgs& a, int64_t i, double* p) {
+  const double* s = a.queries + 3 * i;
+  if (a.transform) {
+    // pts @ R.T + t in OpenBLAS dgemm order: fma(a2, R[j,2], fma(a1, R[j,1], a0 * R[j,0])) + t[j]
+#pragma unroll
+    for (int j = 0; j < 3; ++j)
+      p[j] = SG_ADD(SG_FMA(s[2], a.r[3 * j + 2], SG_FMA(s[1], a.r[3 * j + 1], SG_MUL(s[0], a.r[3 * j]))),
+                    a.t[j]);
+  } else {
+    p[0] = s[0];
+    p[1] = s[1];
+    p[2] = s[2];
   }
 }
 
-__global__ void k_nearest(GridView v, const double* __restrict__ queries, int64_t m,
-                          int64_t* __restrict__ idx, double* __restrict__ dist) {
+__global__ void k_nearest(GridView v, NNArgs a) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= m) return;
-  const double q[3] = {queries[3 * i], queries[3 * i + 1], queries[3 * i + 2]};
+  if (i >= a.m) return;
+  double q[3];
+  query_point(a, i, q);
   int64_t j;
   double d2;
-  grid_nearest(v, q, j, d2);
-  idx[i] = j;
-  if (dist) dist[i] = sqrt(d2);
+  if (grid_nearest(v, q, j, d2)) {
+    a.idx[i] = j;
+    a.d2[i] = d2;
+  } else {
+    a.unresolved[atomicAdd(a.n_unres, 1u)] = (uint32_t)i;
+  }
+}
+
+// Exact fallback: one block per unresolved query scans every centre.
+__global__ void __launch_bounds__(256) k_nearest_brute(GridView v, NNArgs a) {
+  __shared__ double s_d[8];
+  __shared__ int64_t s_j[8];
+  const uint32_t nu = *a.n_unres;
+  for (uint32_t u = blockIdx.x; u < nu; u += gridDim.x) {
+    const int64_t i = a.unresolved[u];
+    double q[3];
+    query_point(a, i, q);
+    double best = INFINITY;
+    int64_t bj = -1;
+    for (int64_t j = threadIdx.x; j < v.n; j += blockDim.x) {
+      const double dx = q[0] - v.pts[3 * j], dy = q[1] - v.pts[3 * j + 1], dz = q[2] - v.pts[3 * j + 2];
+      const double d2 = dx * dx + dy * dy + dz * dz;
+      if (d2 < best) {
+        best = d2;
+        bj = j;
+      }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const int64_t oj = __shfl_xor_sync(0xffffffffu, bj, o);
+      if (ob < best || (ob == best && oj >= 0 && (bj < 0 || oj < bj))) {
+        best = ob;
+        bj = oj;
+      }
+    }
+    if ((threadIdx.x & 31) == 0) {
+      s_d[threadIdx.x >> 5] = best;
+      s_j[threadIdx.x >> 5] = bj;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int w = 1; w < (int)(blockDim.x >> 5); ++w)
+        if (s_d[w] < best || (s_d[w] == best && s_j[w] >= 0 && (bj < 0 || s_j[w] < bj))) {
+          best = s_d[w];
+          bj = s_j[w];
+        }
+      a.idx[i] = bj;
+      a.d2[i] = best;
+    }
+    __syncthreads();
+  }
 }
 
 // ---------------------------------------------------------------- K8 / K9
@@ -473,7 +608,8 @@ __device__ __forceinline__ void apply_pose(const PoseArg& P, const double* a, do
 constexpr int NE_VALS = 29;  // 21 (H upper) + 6 (g) + cost + inliers
 
 __global__ void __launch_bounds__(TRK_THREADS)
-k_normal_eqs(GridView v, const double* __restrict__ cov_b, const double* __restrict__ nrm_b,
+k_normal_eqs(GridView v, const int64_t* __restrict__ nn_j, const double* __restrict__ nn_d2,
+             const double* __restrict__ cov_b, const double* __restrict__ nrm_b,
              const double* __restrict__ a_c, const double* __restrict__ a_cov, int64_t m,
              PoseArg P, int metric_mode, double dist_max, double* __restrict__ w_out,
              double* __restrict__ b_out, uint8_t* __restrict__ acc_out,
@@ -487,9 +623,8 @@ k_normal_eqs(GridView v, const double* __restrict__ cov_b, const double* __restr
     const double a[3] = {a_c[3 * i], a_c[3 * i + 1], a_c[3 * i + 2]};
     double p[3];
     apply_pose(P, a, p);
-    int64_t j;
-    double d2;
-    grid_nearest(v, p, j, d2);
+    const int64_t j = nn_j[i];
+    const double d2 = nn_d2[i];
     const double b[3] = {v.pts[3 * j], v.pts[3 * j + 1], v.pts[3 * j + 2]};
     const double d[3] = {b[0] - p[0], b[1] - p[1], b[2] - p[2]};
     double metric;
@@ -633,11 +768,17 @@ k_cost(const double* __restrict__ a_c, const double* __restrict__ w, const doubl
   }
 }
 
+__global__ void k_sqrt(const double* __restrict__ x, int64_t n, double* __restrict__ y) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) y[i] = sqrt(x[i]);
+}
+
 }  // namespace sgad
 
 struct sgad_geomset {
-  sgad::DevBuf pts, cov, nrm, bbox, cnt, start, cursor, cell_of, items, cub_tmp;
-  sgad::DevBuf w, b, acc, partial, poses;
+  sgad::DevBuf pts, cov, nrm, bbox, keys0, keys1, idx0, idx1, head, headscan, start, hkeys, hvals,
+      cub_tmp;
+  sgad::DevBuf w, b, acc, partial, poses, nn_j, nn_d2, unres, counter;
   sgad::Grid grid{};
   int64_t n = 0;
   unsigned long long* pinned = nullptr;
@@ -696,13 +837,57 @@ int sgad_geomset_create(sgad_geomset** out) {
 
 int sgad_geomset_destroy(sgad_geomset* g) {
   if (!g) return SGAD_OK;
-  DevBuf* bufs[] = {&g->pts, &g->cov, &g->nrm, &g->bbox, &g->cnt, &g->start, &g->cursor,
-                    &g->cell_of, &g->items, &g->cub_tmp, &g->w, &g->b, &g->acc, &g->partial,
-                    &g->poses};
+  DevBuf* bufs[] = {&g->pts, &g->cov, &g->nrm, &g->bbox, &g->keys0, &g->keys1, &g->idx0,
+                    &g->idx1, &g->head, &g->headscan, &g->start, &g->hkeys, &g->hvals,
+                    &g->cub_tmp, &g->w, &g->b, &g->acc, &g->partial, &g->poses, &g->nn_j,
+                    &g->nn_d2, &g->unres, &g->counter};
   for (DevBuf* b : bufs) b->release();
   if (g->pinned) cudaFreeHost(g->pinned);
   delete g;
   return SGAD_OK;
+}
+
+// sort the cell keys of all centres for cell size h; returns the number of
+// occupied cells (synchronises)
+static int grid_sort(sgad_geomset* g, Grid& gr, cudaStream_t st, int64_t* n_cells,
+                     unsigned long long** keys_sorted, uint32_t** idx_sorted) {
+  const int64_t n = g->n;
+  k_cell_keys<<<nblk(n, 256), 256, 0, st>>>(g->pts.as<double>(), n, gr,
+                                            g->keys0.as<unsigned long long>(), g->idx0.as<uint32_t>());
+  SGAD_LAUNCH_CHECK();
+  int bits = 1;
+  const unsigned long long maxkey = ((unsigned long long)(gr.dim[0] - 1) << 42) |
+                                    ((unsigned long long)(gr.dim[1] - 1) << 21) |
+                                    (unsigned long long)(gr.dim[2] - 1);
+  while (bits < 64 && (maxkey >> bits)) ++bits;
+  cub::DoubleBuffer<unsigned long long> dk(g->keys0.as<unsigned long long>(),
+                                           g->keys1.as<unsigned long long>());
+  cub::DoubleBuffer<uint32_t> dv(g->idx0.as<uint32_t>(), g->idx1.as<uint32_t>());
+  size_t tmp = 0;
+  SGAD_CHECK_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, dk, dv, (int)n, 0, bits, st));
+  SGAD_CHECK_CUDA(g->cub_tmp.ensure(tmp));
+  SGAD_CHECK_CUDA(cub::DeviceRadixSort::SortPairs(g->cub_tmp.p, tmp, dk, dv, (int)n, 0, bits, st));
+  k_cell_heads<<<nblk(n, 256), 256, 0, st>>>(dk.Current(), n, g->head.as<uint32_t>());
+  SGAD_LAUNCH_CHECK();
+  tmp = 0;
+  SGAD_CHECK_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tmp, g->head.as<uint32_t>(),
+                                                g->headscan.as<uint32_t>(), (int)n, st));
+  SGAD_CHECK_CUDA(g->cub_tmp.ensure(tmp));
+  SGAD_CHECK_CUDA(cub::DeviceScan::InclusiveSum(g->cub_tmp.p, tmp, g->head.as<uint32_t>(),
+                                                g->headscan.as<uint32_t>(), (int)n, st));
+  uint32_t* hp = reinterpret_cast<uint32_t*>(g->pinned);
+  SGAD_CHECK_CUDA(cudaMemcpyAsync(hp, g->headscan.as<uint32_t>() + n - 1, sizeof(uint32_t),
+                                  cudaMemcpyDeviceToHost, st));
+  SGAD_CHECK_CUDA(cudaStreamSynchronize(st));
+  *n_cells = hp[0];
+  *keys_sorted = dk.Current();
+  *idx_sorted = dv.Current();
+  return SGAD_OK;
+}
+
+static void grid_dims(Grid& gr, const double* ext, double h) {
+  gr.h = h;
+  for (int k = 0; k < 3; ++k) gr.dim[k] = (int)fmin(floor(ext[k] / h) + 1.0, (double)(1 << 21) - 1.0);
 }
 
 int sgad_geomset_set(sgad_geomset* g, const double* centers, const double* cov,
@@ -717,7 +902,6 @@ int sgad_geomset_set(sgad_geomset* g, const double* centers, const double* cov,
   SGAD_CHECK_CUDA(cudaMemcpyAsync(g->pts.p, centers, sizeof(double) * 3 * n, cudaMemcpyDefault, st));
   SGAD_CHECK_CUDA(cudaMemcpyAsync(g->cov.p, cov, sizeof(double) * 6 * n, cudaMemcpyDefault, st));
   SGAD_CHECK_CUDA(cudaMemcpyAsync(g->nrm.p, normals, sizeof(double) * 3 * n, cudaMemcpyDefault, st));
-  // bounding box -> grid geometry
   SGAD_CHECK_CUDA(g->bbox.ensure(sizeof(unsigned long long) * 6));
   unsigned long long init[6] = {~0ull, ~0ull, ~0ull, 0, 0, 0};
   memcpy(g->pinned, init, sizeof init);
@@ -735,54 +919,88 @@ int sgad_geomset_set(sgad_geomset* g, const double* centers, const double* cov,
     memcpy(&lo[k], &bl, 8);
     memcpy(&hi[k], &bh, 8);
   }
-  double ext[3], vol = 1.0;
+  double ext[3], vol = 1.0, emax = 0.0;
   for (int k = 0; k < 3; ++k) {
     ext[k] = fmax(hi[k] - lo[k], 1e-9);
     vol *= ext[k];
+    emax = fmax(emax, ext[k]);
   }
-  // ~n/2 cells over the box; points on surfaces land a few per occupied cell
-  double h = cbrt(vol / fmax(0.5 * (double)n, 1.0));
-  const double hmin = fmax(fmax(ext[0], ext[1]), ext[2]) / 1024.0;
-  h = fmax(h, hmin);
+  SGAD_CHECK_CUDA(g->keys0.ensure(sizeof(unsigned long long) * n));
+  SGAD_CHECK_CUDA(g->keys1.ensure(sizeof(unsigned long long) * n));
+  SGAD_CHECK_CUDA(g->idx0.ensure(sizeof(uint32_t) * n));
+  SGAD_CHECK_CUDA(g->idx1.ensure(sizeof(uint32_t) * n));
+  SGAD_CHECK_CUDA(g->head.ensure(sizeof(uint32_t) * n));
+  SGAD_CHECK_CUDA(g->headscan.ensure(sizeof(uint32_t) * n));
   Grid gr;
-  int64_t ncells = 1;
-  for (int k = 0; k < 3; ++k) {
-    gr.lo[k] = lo[k];
-    gr.dim[k] = (int)fmin(ceil(ext[k] / h) + 1.0, 1024.0);
-    ncells *= gr.dim[k];
+  for (int k = 0; k < 3; ++k) gr.lo[k] = lo[k];
+  const double hmin = emax / (double)((1 << 21) - 2);
+  double h = fmax(cbrt(vol / fmax(0.5 * (double)n, 1.0)), hmin);
+  grid_dims(gr, ext, h);
+  int64_t n_cells = 0;
+  unsigned long long* ks;
+  uint32_t* is;
+  int rc = grid_sort(g, gr, st, &n_cells, &ks, &is);
+  if (rc) return rc;
+  // density refinement: points on surfaces -> occupancy scales with h^2
+  const double occ = (double)n / (double)n_cells;
+  if (occ > 6.0) {
+    h = fmax(h * sqrt(3.0 / occ), hmin);
+    grid_dims(gr, ext, h);
+    rc = grid_sort(g, gr, st, &n_cells, &ks, &is);
+    if (rc) return rc;
   }
-  gr.h = h;
+  unsigned long long hsize = 1024;
+  while (hsize < 2ull * (unsigned long long)n_cells) hsize <<= 1;
+  gr.hmask = hsize - 1;
   g->grid = gr;
-  SGAD_CHECK_CUDA(g->cnt.ensure(sizeof(uint32_t) * (ncells + 1)));
-  SGAD_CHECK_CUDA(g->start.ensure(sizeof(uint32_t) * (ncells + 1)));
-  SGAD_CHECK_CUDA(g->cursor.ensure(sizeof(uint32_t) * (ncells + 1)));
-  SGAD_CHECK_CUDA(g->cell_of.ensure(sizeof(uint32_t) * n));
-  SGAD_CHECK_CUDA(g->items.ensure(sizeof(uint32_t) * n));
-  SGAD_CHECK_CUDA(cudaMemsetAsync(g->cnt.p, 0, sizeof(uint32_t) * (ncells + 1), st));
-  k_grid_count<<<nblk(n, 256), 256, 0, st>>>(g->pts.as<double>(), n, gr, g->cnt.as<uint32_t>(),
-                                             g->cell_of.as<uint32_t>());
+  SGAD_CHECK_CUDA(g->start.ensure(sizeof(uint32_t) * (n_cells + 1)));
+  SGAD_CHECK_CUDA(g->hkeys.ensure(sizeof(unsigned long long) * hsize));
+  SGAD_CHECK_CUDA(g->hvals.ensure(sizeof(uint32_t) * hsize));
+  SGAD_CHECK_CUDA(cudaMemsetAsync(g->hkeys.p, 0xff, sizeof(unsigned long long) * hsize, st));
+  k_cell_table<<<nblk(n, 256), 256, 0, st>>>(ks, n, g->headscan.as<uint32_t>(), g->start.as<uint32_t>(),
+                                             g->hkeys.as<unsigned long long>(), g->hvals.as<uint32_t>(),
+                                             gr.hmask);
   SGAD_LAUNCH_CHECK();
-  size_t tmp = 0;
-  SGAD_CHECK_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, g->cnt.as<uint32_t>(),
-                                                g->start.as<uint32_t>(), (int)ncells + 1, st));
-  SGAD_CHECK_CUDA(g->cub_tmp.ensure(tmp));
-  SGAD_CHECK_CUDA(cub::DeviceScan::ExclusiveSum(g->cub_tmp.p, tmp, g->cnt.as<uint32_t>(),
-                                                g->start.as<uint32_t>(), (int)ncells + 1, st));
-  SGAD_CHECK_CUDA(cudaMemcpyAsync(g->cursor.p, g->start.p, sizeof(uint32_t) * (ncells + 1),
-                                  cudaMemcpyDeviceToDevice, st));
-  k_grid_fill<<<nblk(n, 256), 256, 0, st>>>(g->cell_of.as<uint32_t>(), n, g->cursor.as<uint32_t>(),
-                                            g->items.as<uint32_t>());
-  SGAD_LAUNCH_CHECK();
+  // keep the sorted point order (items) in idx0
+  if (is != g->idx0.as<uint32_t>())
+    SGAD_CHECK_CUDA(cudaMemcpyAsync(g->idx0.p, is, sizeof(uint32_t) * n, cudaMemcpyDeviceToDevice, st));
   return SGAD_OK;
 }
 
 static GridView view_of(sgad_geomset* g) {
   GridView v;
   v.g = g->grid;
+  v.hkeys = g->hkeys.as<unsigned long long>();
+  v.hvals = g->hvals.as<uint32_t>();
   v.start = g->start.as<uint32_t>();
-  v.items = g->items.as<uint32_t>();
+  v.items = g->idx0.as<uint32_t>();
   v.pts = g->pts.as<double>();
+  v.n = g->n;
   return v;
+}
+
+// exact 1-NN for m queries (optionally transformed by rot/trans) into idx/d2
+static int run_nearest(sgad_geomset* g, const double* queries, int64_t m, const double* rot,
+                       const double* trans, int64_t* idx, double* d2, cudaStream_t st) {
+  SGAD_CHECK_CUDA(g->unres.ensure(sizeof(uint32_t) * m));
+  SGAD_CHECK_CUDA(g->counter.ensure(sizeof(uint32_t) * 4));
+  SGAD_CHECK_CUDA(cudaMemsetAsync(g->counter.p, 0, sizeof(uint32_t), st));
+  NNArgs a;
+  a.queries = queries;
+  a.m = m;
+  a.transform = rot != nullptr;
+  for (int k = 0; k < 9; ++k) a.r[k] = rot ? rot[k] : 0.0;
+  for (int k = 0; k < 3; ++k) a.t[k] = trans ? trans[k] : 0.0;
+  a.idx = idx;
+  a.d2 = d2;
+  a.unresolved = g->unres.as<uint32_t>();
+  a.n_unres = g->counter.as<uint32_t>();
+  const GridView v = view_of(g);
+  k_nearest<<<nblk(m, 128), 128, 0, st>>>(v, a);
+  SGAD_LAUNCH_CHECK();
+  k_nearest_brute<<<256, 256, 0, st>>>(v, a);
+  SGAD_LAUNCH_CHECK();
+  return SGAD_OK;
 }
 
 int sgad_geomset_nearest(sgad_geomset* g, const double* queries, int64_t m, int64_t* idx,
@@ -790,8 +1008,14 @@ int sgad_geomset_nearest(sgad_geomset* g, const double* queries, int64_t m, int6
   SGAD_REQUIRE(g && g->n > 0, "global set is empty");
   SGAD_REQUIRE(m >= 0 && (m == 0 || (queries && idx)), "sgad_geomset_nearest: bad arguments");
   if (m == 0) return SGAD_OK;
-  k_nearest<<<nblk(m, 128), 128, 0, (cudaStream_t)stream_>>>(view_of(g), queries, m, idx, dist);
-  SGAD_LAUNCH_CHECK();
+  cudaStream_t st = (cudaStream_t)stream_;
+  SGAD_CHECK_CUDA(g->nn_d2.ensure(sizeof(double) * m));
+  int rc = run_nearest(g, queries, m, nullptr, nullptr, idx, g->nn_d2.as<double>(), st);
+  if (rc) return rc;
+  if (dist) {
+    k_sqrt<<<nblk(m, 256), 256, 0, st>>>(g->nn_d2.as<double>(), m, dist);
+    SGAD_LAUNCH_CHECK();
+  }
   return SGAD_OK;
 }
 
@@ -807,10 +1031,15 @@ int sgad_track_normal_eqs(sgad_geomset* g, const double* local_centers, const do
   SGAD_CHECK_CUDA(g->b.ensure(sizeof(double) * 3 * m));
   SGAD_CHECK_CUDA(g->acc.ensure(m));
   SGAD_CHECK_CUDA(g->partial.ensure(sizeof(double) * NE_VALS * nb));
+  SGAD_CHECK_CUDA(g->nn_j.ensure(sizeof(int64_t) * m));
+  SGAD_CHECK_CUDA(g->nn_d2.ensure(sizeof(double) * m));
+  int rc = run_nearest(g, local_centers, m, rot, trans, g->nn_j.as<int64_t>(), g->nn_d2.as<double>(), st);
+  if (rc) return rc;
   PoseArg P;
   for (int k = 0; k < 9; ++k) P.r[k] = rot[k];
   for (int k = 0; k < 3; ++k) P.t[k] = trans[k];
-  k_normal_eqs<<<nb, TRK_THREADS, 0, st>>>(view_of(g), g->cov.as<double>(), g->nrm.as<double>(),
+  k_normal_eqs<<<nb, TRK_THREADS, 0, st>>>(view_of(g), g->nn_j.as<int64_t>(), g->nn_d2.as<double>(),
+                                           g->cov.as<double>(), g->nrm.as<double>(),
                                            local_centers, local_cov, m, P, metric_mode, dist_max,
                                            g->w.as<double>(), g->b.as<double>(),
                                            g->acc.as<uint8_t>(), g->partial.as<double>());
