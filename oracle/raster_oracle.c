@@ -22,6 +22,13 @@
 #include <math.h>
 #include "../include/sgad_numerics.h"
 
+static const double TAB[32] = {SGAD_EXP2_TABLE};
+
+/* Contributor weight, shared convention with the kernels: exp(d2 * (-0.5/s2))
+ * through sgad_exp_neg (the reference evaluates exp(-0.5 * d2 / s2); the two
+ * differ by an ulp or two, far inside the 1e-4 image bar). */
+static inline double weight(double d2, double s2) { return sgad_exp_neg(d2 * (-0.5 / s2), TAB); }
+
 /* rasterizer.py:86-135 for one source map.  Survivors are written in pixel
  * order (np.nonzero order).  Returns the survivor count. */
 int64_t orc_project_map(int64_t h, int64_t w, const double* base, const double* delta,
@@ -166,14 +173,14 @@ void orc_forward(const double* u0, const double* v0, const double* z, const doub
           const double d2 = dx * dx + dy * dy;
           const double s2 = sigma[g] * sigma[g];
           if (d2 > 9.0 * s2) continue;
-          const double wgt = sgad_exp(-0.5 * d2 / s2);
+          const double wgt = weight(d2, s2);
           double a = opacity[g] * wgt;
           if (a > SGAD_ALPHA_MAX) a = SGAD_ALPHA_MAX;
           const double at = a * trans;
-          c0 += color[3 * g + 0] * at;
-          c1 += color[3 * g + 1] * at;
-          c2 += color[3 * g + 2] * at;
-          dep += z[g] * at;
+          c0 = fma(color[3 * g + 0], at, c0);
+          c1 = fma(color[3 * g + 1], at, c1);
+          c2 = fma(color[3 * g + 2], at, c2);
+          dep = fma(z[g], at, dep);
           acc += at;
           cnt += 1;
           trans *= 1.0 - a;
@@ -217,7 +224,7 @@ void orc_backward(const double* u0, const double* v0, const double* z, const dou
           const double d2 = dx * dx + dy * dy;
           const double s2 = sigma[g] * sigma[g];
           if (d2 > 9.0 * s2) continue;
-          double a = opacity[g] * sgad_exp(-0.5 * d2 / s2);
+          double a = opacity[g] * weight(d2, s2);
           if (a > SGAD_ALPHA_MAX) a = SGAD_ALPHA_MAX;
           last = k;
           trans *= 1.0 - a;
@@ -232,7 +239,7 @@ void orc_backward(const double* u0, const double* v0, const double* z, const dou
           const double d2 = dx * dx + dy * dy;
           const double s2 = sigma[g] * sigma[g];
           if (d2 > 9.0 * s2) continue;
-          const double wgt = sgad_exp(-0.5 * d2 / s2);
+          const double wgt = weight(d2, s2);
           const double aw = opacity[g] * wgt;
           const int clamped = aw > SGAD_ALPHA_MAX;
           const double a = clamped ? SGAD_ALPHA_MAX : aw;

@@ -36,7 +36,6 @@ struct ChainCoef {  // fused backward: d(param)/d(image-space quantity), fp32
 
 constexpr uint32_t GID_LEARN = 0x80000000u;
 constexpr int PROJ_THREADS = 256;
-constexpr int BATCH = 256;  // records staged per compositing batch
 constexpr int RASTER_THREADS = 256;
 
 }  // namespace sgad
@@ -271,81 +270,131 @@ __device__ __forceinline__ TileGeom tile_geom(int ntx, int width, int height) {
 
 // Each warp owns one 8x4 sub-tile and walks the tile's depth-ordered list on
 // its own (no block barriers: sub-tiles finish at different list positions).
-// Per chunk of 32 list entries the warp culls against its rectangle, stages
-// the survivors in its private shared-memory slots, then every lane builds a
-// bitmask of the staged entries its pixel passes (the reference's exact
-// d2 > 9 s2 test) and pops its own bits in list order -- lanes work on
-// different Gaussians at the same time, so divergence only costs the tail.
-struct WarpStage {
-  double u0[32], v0[32], thr[32], s2[32], sig[32], op[32], z[32], rgb[3][32];
-  uint32_t k[32], gid[32];
+// It stages the list entries that can touch its rectangle into a private
+// shared-memory window of WIN slots, every lane builds a 64-bit mask of the
+// staged entries its pixel passes (the reference's d2 > 9 s2 test, decided in
+// fp32 with an fp64 fallback inside a guard band), and then pops its own bits
+// in list order: lanes composite different Gaussians at the same time, so
+// divergence only costs the per-window tail.
+constexpr int WIN = 64;
+constexpr int NWARP = RASTER_THREADS / 32;
+
+struct WinStage {
+  double u0[WIN], v0[WIN], thr[WIN], nh[WIN], op[WIN], z[WIN], rgb[3][WIN];
+  float ru[WIN], rv[WIN], thrf[WIN];
+  uint32_t k[WIN], gid[WIN];
 };
 
-// Conservative sub-tile cull: false only if every pixel centre of the 8x4
-// rectangle fails the reference test (the closest pixel's d2 is computed with
-// the same rounded ops, and rounding is monotone; K4).
-__device__ __forceinline__ bool rect_hit(double u0, double v0, double thr, double xlo, double ylo) {
-  const double xhi = xlo + 7.0, yhi = ylo + 3.0;
-  double dx = 0.0, dy = 0.0;
-  if (u0 < xlo) dx = SG_SUB(u0, xlo); else if (u0 > xhi) dx = SG_SUB(u0, xhi);
-  if (v0 < ylo) dy = SG_SUB(v0, ylo); else if (v0 > yhi) dy = SG_SUB(v0, yhi);
-  return !(SG_ADD(SG_MUL(dx, dx), SG_MUL(dy, dy)) > thr);
+struct BwdStage {  // backward-only per-warp slots
+  double is3[WIN];  // 1 / (s2 sigma)
+  uint32_t eidx[WIN];
+  float coef[6][WIN];
+  float acc[6][WIN];
+};
+
+__device__ __forceinline__ void load_head(const Record* rec, uint32_t e, double& u0, double& v0,
+                                          double& sig, double& op) {
+  const double4 h = *reinterpret_cast<const double4*>(rec + e);  // u0, v0, sigma, opacity
+  u0 = h.x;
+  v0 = h.y;
+  sig = h.z;
+  op = h.w;
 }
 
-__device__ __forceinline__ Record load_record(const Record* rec, uint32_t e) {
-  const float4* src = reinterpret_cast<const float4*>(rec + e);
-  Record r;
-  float4* dst = reinterpret_cast<float4*>(&r);
-  dst[0] = __ldg(src);
-  dst[1] = __ldg(src + 1);
-  dst[2] = __ldg(src + 2);
-  dst[3] = __ldg(src + 3);
-  return r;
+// Conservative fp32 cull of a Gaussian against the warp's 8x4 rectangle
+// (pixel centres [xlo, xlo+7] x [ylo, ylo+3]); the exact per-pixel test
+// follows, so a generous margin only costs work, never correctness.
+__device__ __forceinline__ bool rect_maybe(double u0, double v0, double sig, float xlo, float ylo) {
+  const float uf = (float)u0, vf = (float)v0;
+  const float rr = (float)(3.0 * sig) * 1.0001f + 0.01f;
+  const float dx = fmaxf(fmaxf(xlo - uf, uf - (xlo + 7.0f)), 0.0f);
+  const float dy = fmaxf(fmaxf(ylo - vf, vf - (ylo + 3.0f)), 0.0f);
+  return dx * dx + dy * dy <= rr * rr;
 }
 
-// Stage list entries [base, base+32) that hit this warp's rectangle, in list
-// order; returns their count (uniform across the warp).
-__device__ __forceinline__ int stage_chunk(WarpStage& s, const uint32_t* __restrict__ lists,
+// Load list entries [base, base+32) (clipped to [lo, hi)), keep those that may
+// touch the rectangle and append them at slots [slot0, slot0 + kept).
+template <bool BWD>
+__device__ __forceinline__ int stage_chunk(WinStage& s, BwdStage* b, const uint32_t* __restrict__ lists,
                                            const Record* __restrict__ rec,
-                                           const double* __restrict__ col64, uint32_t base,
-                                           uint32_t end, double xlo, double ylo, int lane,
-                                           uint32_t* eidx_out) {
-  const uint32_t k = base + lane;
+                                           const ChainCoef* __restrict__ coef,
+                                           const double* __restrict__ col64, int64_t base,
+                                           int64_t lo, int64_t hi, float xlo, float ylo, int lane,
+                                           int slot0, bool below = false) {
+  const int64_t k = base + lane;
   bool keep = false;
-  Record r;
   uint32_t e = 0;
-  double thr = 0.0;
-  if (k < end) {
+  double u0 = 0.0, v0 = 0.0, sig = 0.0, op = 0.0;
+  if (k >= lo && k < hi) {
     e = lists[k];
-    r = load_record(rec, e);
-    thr = SG_MUL(9.0, SG_MUL(r.sigma, r.sigma));
-    keep = rect_hit(r.u0, r.v0, thr, xlo, ylo);
+    load_head(rec, e, u0, v0, sig, op);
+    keep = rect_maybe(u0, v0, sig, xlo, ylo);
   }
   const uint32_t km = __ballot_sync(0xffffffffu, keep);
   if (keep) {
-    const int j = __popc(km & ((1u << lane) - 1u));
-    s.u0[j] = r.u0;
-    s.v0[j] = r.v0;
+    // ascending list order; `below`: the chunk ends right under slot0
+    const int j = (below ? slot0 - __popc(km) : slot0) + __popc(km & ((1u << lane) - 1u));
+    const Record& r = rec[e];
+    const float4 tail = *reinterpret_cast<const float4*>(&r.r);  // r, g, b, gid
+    const double z = r.z;
+    const double s2 = SG_MUL(sig, sig);
+    const double thr = SG_MUL(9.0, s2);
+    s.u0[j] = u0;
+    s.v0[j] = v0;
     s.thr[j] = thr;
-    s.s2[j] = SG_MUL(r.sigma, r.sigma);
-    s.sig[j] = r.sigma;
-    s.op[j] = r.opacity;
-    s.z[j] = r.z;
+    s.nh[j] = SG_DIV(-0.5, s2);
+    s.op[j] = op;
+    s.z[j] = z;
     if (col64) {  // fp64 drop-in maps keep exact fp64 colours
       s.rgb[0][j] = col64[3 * (size_t)e];
       s.rgb[1][j] = col64[3 * (size_t)e + 1];
       s.rgb[2][j] = col64[3 * (size_t)e + 2];
     } else {
-      s.rgb[0][j] = r.r;
-      s.rgb[1][j] = r.g;
-      s.rgb[2][j] = r.b;
+      s.rgb[0][j] = tail.x;
+      s.rgb[1][j] = tail.y;
+      s.rgb[2][j] = tail.z;
     }
-    s.k[j] = k;
-    s.gid[j] = r.gid;
-    if (eidx_out) eidx_out[j] = e;
+    s.ru[j] = (float)(u0 - (double)xlo);
+    s.rv[j] = (float)(v0 - (double)ylo);
+    s.thrf[j] = (float)thr;
+    s.k[j] = (uint32_t)k;
+    s.gid[j] = __float_as_uint(tail.w);
+    if (BWD) {
+      b->is3[j] = 1.0 / (s2 * sig);
+      b->eidx[j] = e;
+      if (coef) {
+        const ChainCoef cc = coef[e];
+        b->coef[0][j] = cc.k_r;
+        b->coef[1][j] = cc.a_u;
+        b->coef[2][j] = cc.a_v;
+        b->coef[3][j] = cc.a_z;
+        b->coef[4][j] = cc.a_s;
+        b->coef[5][j] = cc.k_op;
+      }
+    }
   }
-  __syncwarp();
   return __popc(km);
+}
+
+// Exact reference test d2 > 9 s2 for staged entry j at this lane's pixel:
+// fp32 decides outside a guard band (|error| < 2e-4 (thr + 1), K4),
+// fp64 decides inside it.
+__device__ __forceinline__ bool passes(const WinStage& s, int j, float lx, float ly, double pxd,
+                                       double pyd) {
+  const float dxf = s.ru[j] - lx, dyf = s.rv[j] - ly;
+  const float d2f = fmaf(dxf, dxf, dyf * dyf);
+  const float thrf = s.thrf[j];
+  const float band = 2e-4f * (thrf + 1.0f);
+  if (d2f > thrf + band) return false;
+  if (d2f < thrf - band) return true;
+  const double dx = SG_SUB(s.u0[j], pxd), dy = SG_SUB(s.v0[j], pyd);
+  return !(SG_ADD(SG_MUL(dx, dx), SG_MUL(dy, dy)) > s.thr[j]);
+}
+
+__device__ __forceinline__ void load_exp_table(double* tab) {
+  const double t[32] = {SGAD_EXP2_TABLE};
+  if (threadIdx.x < 32) tab[threadIdx.x] = t[threadIdx.x];
+  __syncthreads();
 }
 
 // ------------------------------------------------------------------ K4
@@ -357,41 +406,47 @@ k_forward(const uint2* __restrict__ ranges, const uint32_t* __restrict__ lists,
           double* __restrict__ out_alpha, int32_t* __restrict__ out_count,
           double* __restrict__ t_final, int32_t* __restrict__ last_out,
           uint8_t* __restrict__ signs, sgad_loss_target tgt) {
-  __shared__ WarpStage stage[RASTER_THREADS / 32];
-  __shared__ double s_red[2][RASTER_THREADS / 32];
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  WinStage* stage = reinterpret_cast<WinStage*>(smem_raw);
+  __shared__ double tab[32];
+  load_exp_table(tab);
   const TileGeom g = tile_geom(ntx, width, height);
-  WarpStage& s = stage[g.warp];
+  WinStage& s = stage[g.warp];
   const uint2 rg = ranges[g.tile];
   const double pxd = (double)g.px, pyd = (double)g.py;
-  const double xlo = (double)(g.tx * SGAD_TILE + (g.warp & 1) * 8);
-  const double ylo = (double)(g.ty * SGAD_TILE + (g.warp >> 1) * 4);
+  const float xlo = (float)(g.tx * SGAD_TILE + (g.warp & 1) * 8);
+  const float ylo = (float)(g.ty * SGAD_TILE + (g.warp >> 1) * 4);
+  const float lx = (float)(g.lane & 7), ly = (float)(g.lane >> 3);
   double T = 1.0, C0 = 0.0, C1 = 0.0, C2 = 0.0, D = 0.0, A = 0.0;
   int cnt = 0, last = -1;
   bool done = !g.valid;
 
-  for (uint32_t base = rg.x; base < rg.y; base += 32) {
-    if (__all_sync(0xffffffffu, done)) break;
-    const int c = stage_chunk(s, lists, rec, col64, base, rg.y, xlo, ylo, g.lane, nullptr);
-    uint32_t mine = 0;
-    if (!done) {
-      for (int j = 0; j < c; ++j) {
-        const double dx = SG_SUB(s.u0[j], pxd), dy = SG_SUB(s.v0[j], pyd);
-        if (!(SG_ADD(SG_MUL(dx, dx), SG_MUL(dy, dy)) > s.thr[j])) mine |= 1u << j;
-      }
+  int64_t pos = rg.x;
+  while (pos < (int64_t)rg.y && !__all_sync(0xffffffffu, done)) {
+    int n = 0;
+    while (n <= WIN - 32 && pos < (int64_t)rg.y) {
+      n += stage_chunk<false>(s, nullptr, lists, rec, nullptr, col64, pos, rg.x, rg.y, xlo, ylo,
+                              g.lane, n);
+      pos += 32;
     }
+    __syncwarp();
+    unsigned long long mine = 0;
+    if (!done)
+      for (int j = 0; j < n; ++j)
+        if (passes(s, j, lx, ly, pxd, pyd)) mine |= 1ull << j;
     while (mine) {
-      const int j = __ffs(mine) - 1;
+      const int j = __ffsll((long long)mine) - 1;
       mine &= mine - 1;
       const double dx = SG_SUB(s.u0[j], pxd), dy = SG_SUB(s.v0[j], pyd);
       const double d2 = SG_ADD(SG_MUL(dx, dx), SG_MUL(dy, dy));
-      const double w = sgad_exp(SG_DIV(SG_MUL(-0.5, d2), s.s2[j]));
+      const double w = sgad_exp_neg(SG_MUL(d2, s.nh[j]), tab);
       double a = SG_MUL(s.op[j], w);
       if (a > SGAD_ALPHA_MAX) a = SGAD_ALPHA_MAX;
       const double at = SG_MUL(a, T);
-      C0 = SG_ADD(C0, SG_MUL(s.rgb[0][j], at));
-      C1 = SG_ADD(C1, SG_MUL(s.rgb[1][j], at));
-      C2 = SG_ADD(C2, SG_MUL(s.rgb[2][j], at));
-      D = SG_ADD(D, SG_MUL(s.z[j], at));
+      C0 = SG_FMA(s.rgb[0][j], at, C0);
+      C1 = SG_FMA(s.rgb[1][j], at, C1);
+      C2 = SG_FMA(s.rgb[2][j], at, C2);
+      D = SG_FMA(s.z[j], at, D);
       A = SG_ADD(A, at);
       ++cnt;
       last = (int)s.k[j];
@@ -446,18 +501,8 @@ k_forward(const uint2* __restrict__ ranges, const uint32_t* __restrict__ lists,
       ld += __shfl_xor_sync(0xffffffffu, ld, o);
     }
     if (g.lane == 0) {
-      s_red[0][g.warp] = lc;
-      s_red[1][g.warp] = ld;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      double a = 0.0, b = 0.0;
-      for (int w = 0; w < RASTER_THREADS / 32; ++w) {
-        a += s_red[0][w];
-        b += s_red[1][w];
-      }
-      atomicAdd(tgt.loss_accum, a);
-      atomicAdd(tgt.loss_accum + 1, b);
+      atomicAdd(tgt.loss_accum, lc);
+      atomicAdd(tgt.loss_accum + 1, ld);
     }
   }
 }
@@ -471,12 +516,6 @@ __device__ __forceinline__ double sign_of(uint32_t code) {
   return code == 1u ? 1.0 : (code == 2u ? -1.0 : 0.0);
 }
 
-struct BwdExtra {
-  uint32_t eidx[32];
-  float coef[6][32];
-  float acc[6][32];
-};
-
 template <bool FUSED>
 __global__ void __launch_bounds__(RASTER_THREADS)
 k_backward(const uint2* __restrict__ ranges, const uint32_t* __restrict__ lists,
@@ -486,15 +525,19 @@ k_backward(const uint2* __restrict__ ranges, const uint32_t* __restrict__ lists,
            const uint8_t* __restrict__ signs, Upstream up, const double* __restrict__ g_color,
            const double* __restrict__ g_depth, const double* __restrict__ g_alpha,
            double* __restrict__ raw, float* __restrict__ grad_accum) {
-  __shared__ WarpStage stage[RASTER_THREADS / 32];
-  __shared__ BwdExtra extra[RASTER_THREADS / 32];
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  WinStage* stage = reinterpret_cast<WinStage*>(smem_raw);
+  BwdStage* bstage = reinterpret_cast<BwdStage*>(smem_raw + sizeof(WinStage) * NWARP);
+  __shared__ double tab[32];
+  load_exp_table(tab);
   const TileGeom g = tile_geom(ntx, width, height);
-  WarpStage& s = stage[g.warp];
-  BwdExtra& x = extra[g.warp];
+  WinStage& s = stage[g.warp];
+  BwdStage& x = bstage[g.warp];
   const uint2 rg = ranges[g.tile];
   const double pxd = (double)g.px, pyd = (double)g.py;
-  const double xlo = (double)(g.tx * SGAD_TILE + (g.warp & 1) * 8);
-  const double ylo = (double)(g.ty * SGAD_TILE + (g.warp >> 1) * 4);
+  const float xlo = (float)(g.tx * SGAD_TILE + (g.warp & 1) * 8);
+  const float ylo = (float)(g.ty * SGAD_TILE + (g.warp >> 1) * 4);
+  const float lx = (float)(g.lane & 7), ly = (float)(g.lane >> 3);
   const int64_t p = (int64_t)g.py * width + g.px;
 
   double gc0 = 0.0, gc1 = 0.0, gc2 = 0.0, gd = 0.0, ga = 0.0, T = 0.0;
@@ -524,66 +567,51 @@ k_backward(const uint2* __restrict__ ranges, const uint32_t* __restrict__ lists,
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) wend = max(wend, __shfl_xor_sync(0xffffffffu, wend, o));
   if (FUSED) {
+    for (int j = g.lane; j < WIN; j += 32)
 #pragma unroll
-    for (int i = 0; i < 6; ++i) x.acc[i][g.lane] = 0.f;
+      for (int i = 0; i < 6; ++i) x.acc[i][j] = 0.f;
   }
   double sc0 = 0.0, sc1 = 0.0, sc2 = 0.0, sd = 0.0, sa = 0.0;
-  for (int top = wend; top > (int)rg.x; top -= 32) {
-    const uint32_t base = (uint32_t)max((int)rg.x, top - 32);
-    const int c = stage_chunk(s, lists, rec, col64, base, (uint32_t)top, xlo, ylo, g.lane, x.eidx);
-    if (FUSED && g.lane < c) {
-      const ChainCoef cc = coef[x.eidx[g.lane]];
-      x.coef[0][g.lane] = cc.k_r;
-      x.coef[1][g.lane] = cc.a_u;
-      x.coef[2][g.lane] = cc.a_v;
-      x.coef[3][g.lane] = cc.a_z;
-      x.coef[4][g.lane] = cc.a_s;
-      x.coef[5][g.lane] = cc.k_op;
+  int64_t pos = wend;  // exclusive upper end of the unstaged part
+  while (pos > (int64_t)rg.x) {
+    int lo = WIN;  // staged slots are [lo, WIN), ascending in list order
+    while (lo >= 32 && pos > (int64_t)rg.x) {
+      const int64_t base = pos - 32;
+      lo -= stage_chunk<true>(s, &x, lists, rec, FUSED ? coef : nullptr, col64, base, rg.x, pos,
+                              xlo, ylo, g.lane, lo, true);
+      pos = base;
     }
     __syncwarp();
-    uint32_t mine = 0;
-    for (int j = 0; j < c; ++j) {
-      if ((int)s.k[j] > mylast) continue;
-      const double dx = SG_SUB(s.u0[j], pxd), dy = SG_SUB(s.v0[j], pyd);
-      if (!(SG_ADD(SG_MUL(dx, dx), SG_MUL(dy, dy)) > s.thr[j])) mine |= 1u << j;
-    }
+    unsigned long long mine = 0;
+    for (int j = lo; j < WIN; ++j)
+      if ((int)s.k[j] <= mylast && passes(s, j, lx, ly, pxd, pyd)) mine |= 1ull << j;
     while (mine) {
-      const int j = 31 - __clz(mine);
-      mine &= ~(1u << j);
+      const int j = 63 - __clzll((long long)mine);
+      mine &= ~(1ull << j);
       const double dx = SG_SUB(s.u0[j], pxd), dy = SG_SUB(s.v0[j], pyd);
       const double d2 = SG_ADD(SG_MUL(dx, dx), SG_MUL(dy, dy));
-      const double s2 = s.s2[j], op = s.op[j], z = s.z[j];
-      const double w = sgad_exp(SG_DIV(SG_MUL(-0.5, d2), s2));
+      const double nh = s.nh[j], op = s.op[j], z = s.z[j];
+      const double w = sgad_exp_neg(SG_MUL(d2, nh), tab);
       const double aw = SG_MUL(op, w);
       const bool clamped = aw > SGAD_ALPHA_MAX;
       const double a = clamped ? SGAD_ALPHA_MAX : aw;
-      const double om = SG_SUB(1.0, a);
-      const double tb = SG_DIV(T, om);
-      const double at = SG_MUL(a, tb);
+      const double iom = 1.0 / (1.0 - a);
+      const double tb = T * iom;
+      const double at = a * tb;
       const double c0 = s.rgb[0][j], c1 = s.rgb[1][j], c2 = s.rgb[2][j];
       if (s.gid[j] & GID_LEARN) {
-        const double iom = FUSED ? 1.0 / om : 0.0;
-        double d_alpha;
-        if (FUSED) {  // gradients carry a 1e-3 bar: one reciprocal instead of five divisions
-          d_alpha = gc0 * (c0 * tb - sc0 * iom) + gc1 * (c1 * tb - sc1 * iom) +
-                    gc2 * (c2 * tb - sc2 * iom) + gd * (z * tb - sd * iom) + ga * (tb - sa * iom);
-        } else {
-          d_alpha = SG_MUL(gc0, SG_SUB(SG_MUL(c0, tb), SG_DIV(sc0, om)));
-          d_alpha = SG_ADD(d_alpha, SG_MUL(gc1, SG_SUB(SG_MUL(c1, tb), SG_DIV(sc1, om))));
-          d_alpha = SG_ADD(d_alpha, SG_MUL(gc2, SG_SUB(SG_MUL(c2, tb), SG_DIV(sc2, om))));
-          d_alpha = SG_ADD(d_alpha, SG_MUL(gd, SG_SUB(SG_MUL(z, tb), SG_DIV(sd, om))));
-          d_alpha = SG_ADD(d_alpha, SG_MUL(ga, SG_SUB(tb, SG_DIV(sa, om))));
-        }
-        const double gcol0 = SG_MUL(gc0, at), gcol1 = SG_MUL(gc1, at), gcol2 = SG_MUL(gc2, at),
-                     gz = SG_MUL(gd, at);
+        const double d_alpha = gc0 * (c0 * tb - sc0 * iom) + gc1 * (c1 * tb - sc1 * iom) +
+                               gc2 * (c2 * tb - sc2 * iom) + gd * (z * tb - sd * iom) +
+                               ga * (tb - sa * iom);
+        const double gcol0 = gc0 * at, gcol1 = gc1 * at, gcol2 = gc2 * at, gz = gd * at;
         double gop = 0.0, gsig = 0.0, gu = 0.0, gv = 0.0;
         if (!clamped) {
-          const double gw = SG_MUL(d_alpha, op);
-          gop = SG_MUL(d_alpha, w);
-          gsig = SG_DIV(SG_MUL(SG_MUL(gw, w), d2), SG_MUL(s2, s.sig[j]));
-          const double gd2 = SG_MUL(gw, SG_DIV(SG_MUL(-0.5, w), s2));
-          gu = SG_MUL(SG_MUL(gd2, 2.0), dx);
-          gv = SG_MUL(SG_MUL(gd2, 2.0), dy);
+          const double gw = d_alpha * op;
+          gop = d_alpha * w;
+          gsig = gw * w * d2 * x.is3[j];  // gw w d2 / (s2 sigma)
+          const double gd2 = gw * w * nh;  // gw (-0.5 w / s2)
+          gu = 2.0 * gd2 * dx;
+          gv = 2.0 * gd2 * dy;
         }
         if (FUSED) {
           atomicAdd(&x.acc[0][j], (float)(x.coef[1][j] * gu + x.coef[2][j] * gv +
@@ -605,27 +633,28 @@ k_backward(const uint2* __restrict__ ranges, const uint32_t* __restrict__ lists,
           atomicAdd(dst + 7, gz);
         }
       }
-      sc0 = SG_ADD(sc0, SG_MUL(c0, at));
-      sc1 = SG_ADD(sc1, SG_MUL(c1, at));
-      sc2 = SG_ADD(sc2, SG_MUL(c2, at));
-      sd = SG_ADD(sd, SG_MUL(z, at));
-      sa = SG_ADD(sa, at);
+      sc0 = fma(c0, at, sc0);
+      sc1 = fma(c1, at, sc1);
+      sc2 = fma(c2, at, sc2);
+      sd = fma(z, at, sd);
+      sa += at;
       T = tb;
     }
     __syncwarp();
-    if (FUSED && g.lane < c) {
-      const int j = g.lane;
-      const float q0 = x.acc[0][j], q1 = x.acc[1][j], q2 = x.acc[2][j], q3 = x.acc[3][j],
-                  q4 = x.acc[4][j], q5 = x.acc[5][j];
-      if (q0 != 0.f || q1 != 0.f || q2 != 0.f || q3 != 0.f || q4 != 0.f || q5 != 0.f) {
-        float4* dst = reinterpret_cast<float4*>(grad_accum + (size_t)(s.gid[j] & ~GID_LEARN) * 8);
-        atomicAdd(dst, make_float4(q0, q1, q2, q3));
-        atomicAdd(reinterpret_cast<float2*>(dst + 1), make_float2(q4, q5));
-      }
+    if (FUSED) {
+      for (int j = lo + g.lane; j < WIN; j += 32) {
+        const float q0 = x.acc[0][j], q1 = x.acc[1][j], q2 = x.acc[2][j], q3 = x.acc[3][j],
+                    q4 = x.acc[4][j], q5 = x.acc[5][j];
+        if (q0 != 0.f || q1 != 0.f || q2 != 0.f || q3 != 0.f || q4 != 0.f || q5 != 0.f) {
+          float4* dst = reinterpret_cast<float4*>(grad_accum + (size_t)(s.gid[j] & ~GID_LEARN) * 8);
+          atomicAdd(dst, make_float4(q0, q1, q2, q3));
+          atomicAdd(reinterpret_cast<float2*>(dst + 1), make_float2(q4, q5));
 #pragma unroll
-      for (int i = 0; i < 6; ++i) x.acc[i][j] = 0.f;
+          for (int i = 0; i < 6; ++i) x.acc[i][j] = 0.f;
+        }
+      }
+      __syncwarp();
     }
-    __syncwarp();
   }
 }
 
@@ -697,6 +726,24 @@ __global__ void k_export_surv(const uint32_t* __restrict__ perm, const Record* _
   if (z) z[i] = r.z;
   if (sigma) sigma[i] = r.sigma;
   if (opacity) opacity[i] = r.opacity;
+}
+
+constexpr size_t FWD_SMEM = sizeof(WinStage) * NWARP;
+constexpr size_t BWD_SMEM = (sizeof(WinStage) + sizeof(BwdStage)) * NWARP;
+
+// opt in to >48 KB dynamic shared memory once per process
+static int smem_attrs() {
+  static int done = 0;
+  if (done) return SGAD_OK;
+  SGAD_CHECK_CUDA(cudaFuncSetAttribute(k_forward<true, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FWD_SMEM));
+  SGAD_CHECK_CUDA(cudaFuncSetAttribute(k_forward<true, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FWD_SMEM));
+  SGAD_CHECK_CUDA(cudaFuncSetAttribute(k_forward<true, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FWD_SMEM));
+  SGAD_CHECK_CUDA(cudaFuncSetAttribute(k_forward<false, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FWD_SMEM));
+  SGAD_CHECK_CUDA(cudaFuncSetAttribute(k_forward<false, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FWD_SMEM));
+  SGAD_CHECK_CUDA(cudaFuncSetAttribute(k_backward<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)BWD_SMEM));
+  SGAD_CHECK_CUDA(cudaFuncSetAttribute(k_backward<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)BWD_SMEM));
+  done = 1;
+  return SGAD_OK;
 }
 
 static inline unsigned blocks_for(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
@@ -901,8 +948,9 @@ int sgad_raster_forward(sgad_raster* h, double* out_color, double* out_depth, do
   }
   const dim3 grid((unsigned)h->n_tiles), block(RASTER_THREADS);
   const double* col64 = h->any_f64 ? h->col64.as<double>() : nullptr;
+  if (int rc = smem_attrs()) return rc;
 #define SGAD_FWD(I, S, L)                                                                      \
-  k_forward<I, S, L><<<grid, block, 0, st>>>(                                                \
+  k_forward<I, S, L><<<grid, block, FWD_SMEM, st>>>(                                                \
       h->ranges.as<uint2>(), h->pvals0.as<uint32_t>(), h->records.as<Record>(), col64, h->ntx, \
       h->cam.width, h->cam.height, out_color, out_depth, out_alpha, out_count,               \
       h->trans_final.as<double>(), h->last_idx.as<int32_t>(), h->signs.as<uint8_t>(), tg)
@@ -925,6 +973,7 @@ int sgad_raster_backward(sgad_raster* h, int32_t mode, const double* g_color,
   SGAD_REQUIRE(h && h->prepared && h->forwarded, "sgad_raster_backward: run forward with state first");
   cudaStream_t st = (cudaStream_t)stream_;
   if (h->n_surv == 0) return SGAD_OK;
+  if (int rc = smem_attrs()) return rc;
   const dim3 grid((unsigned)h->n_tiles), block(RASTER_THREADS);
   const int64_t npx = (int64_t)h->cam.width * h->cam.height;
   if (mode == 1) {
@@ -933,7 +982,7 @@ int sgad_raster_backward(sgad_raster* h, int32_t mode, const double* g_color,
     Upstream up;
     up.kc = h->rho / (double)(3 * npx);
     up.kd = h->n_depth > 0 ? h->sigma_d / (double)h->n_depth : 0.0;
-    k_backward<true><<<grid, block, 0, st>>>(
+    k_backward<true><<<grid, block, BWD_SMEM, st>>>(
         h->ranges.as<uint2>(), h->pvals0.as<uint32_t>(), h->records.as<Record>(),
         h->coef.as<ChainCoef>(), h->any_f64 ? h->col64.as<double>() : nullptr, h->ntx,
         h->cam.width, h->cam.height,
@@ -951,7 +1000,7 @@ int sgad_raster_backward(sgad_raster* h, int32_t mode, const double* g_color,
   SGAD_CHECK_CUDA(cudaMemcpyAsync(h->scratch.p, map_grads, sizeof(double*) * n_frames,
                                   cudaMemcpyHostToDevice, st));
   Upstream up{0.0, 0.0};
-  k_backward<false><<<grid, block, 0, st>>>(
+  k_backward<false><<<grid, block, BWD_SMEM, st>>>(
       h->ranges.as<uint2>(), h->pvals0.as<uint32_t>(), h->records.as<Record>(), nullptr,
       h->any_f64 ? h->col64.as<double>() : nullptr, h->ntx, h->cam.width, h->cam.height, h->trans_final.as<double>(), h->last_idx.as<int32_t>(),
       nullptr, up, g_color, g_depth, g_alpha, h->raw_grads.as<double>(), nullptr);
