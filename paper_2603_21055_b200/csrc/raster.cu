@@ -294,11 +294,12 @@ struct BwdStage {  // backward-only per-warp slots
 
 __device__ __forceinline__ void load_head(const Record* rec, uint32_t e, double& u0, double& v0,
                                           double& sig, double& op) {
-  const double4 h = *reinterpret_cast<const double4*>(rec + e);  // u0, v0, sigma, opacity
-  u0 = h.x;
-  v0 = h.y;
-  sig = h.z;
-  op = h.w;
+  const double2* hp = reinterpret_cast<const double2*>(rec + e);  // u0, v0 | sigma, opacity
+  const double2 a = __ldg(hp), b = __ldg(hp + 1);
+  u0 = a.x;
+  v0 = a.y;
+  sig = b.x;
+  op = b.y;
 }
 
 // Conservative fp32 cull of a Gaussian against the warp's 8x4 rectangle
@@ -334,9 +335,13 @@ __device__ __forceinline__ int stage_chunk(WinStage& s, BwdStage* b, const uint3
   if (keep) {
     // ascending list order; `below`: the chunk ends right under slot0
     const int j = (below ? slot0 - __popc(km) : slot0) + __popc(km & ((1u << lane) - 1u));
-    const Record& r = rec[e];
-    const float4 tail = *reinterpret_cast<const float4*>(&r.r);  // r, g, b, gid
-    const double z = r.z;
+    // second half of the record: z | r, g | b, gid  (16-byte aligned loads)
+    const double2* tp = reinterpret_cast<const double2*>(rec + e) + 2;
+    const double2 t0 = __ldg(tp), t1 = __ldg(tp + 1);
+    const double z = t0.x;
+    const float2 rg2 = *reinterpret_cast<const float2*>(&t0.y);
+    const float2 bg2 = *reinterpret_cast<const float2*>(&t1.x);
+    const float4 tail = make_float4(rg2.x, rg2.y, bg2.x, bg2.y);
     const double s2 = SG_MUL(sig, sig);
     const double thr = SG_MUL(9.0, s2);
     s.u0[j] = u0;
