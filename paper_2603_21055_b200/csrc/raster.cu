@@ -271,25 +271,32 @@ __device__ __forceinline__ TileGeom tile_geom(int ntx, int width, int height) {
 // Each warp owns one 8x4 sub-tile and walks the tile's depth-ordered list on
 // its own (no block barriers: sub-tiles finish at different list positions).
 // It stages the list entries that can touch its rectangle into a private
-// shared-memory window of WIN slots, every lane builds a 64-bit mask of the
-// staged entries its pixel passes (the reference's d2 > 9 s2 test, decided in
-// fp32 with an fp64 fallback inside a guard band), and then pops its own bits
-// in list order: lanes composite different Gaussians at the same time, so
-// divergence only costs the per-window tail.
-constexpr int WIN = 64;
+// shared-memory window, every lane builds a 64-bit mask of the staged entries
+// its pixel passes (the reference's d2 > 9 s2 test, decided in fp32 with an
+// fp64 fallback inside a guard band), and then pops its own bits in list
+// order: lanes composite different Gaussians at the same time.  The Gaussian
+// weight factorises over the rectangle's 8 columns and 4 rows,
+// w = exp(-dx^2/2s^2) exp(-dy^2/2s^2), so staging evaluates 12 exponentials
+// per entry (one lane per entry, fully converged) and the divergent
+// per-contribution loop only multiplies two staged factors.
 constexpr int NWARP = RASTER_THREADS / 32;
+constexpr int FWD_WIN = 64;
+constexpr int BWD_WIN = 32;
 
+template <int W>
 struct WinStage {
-  double u0[WIN], v0[WIN], thr[WIN], nh[WIN], op[WIN], z[WIN], rgb[3][WIN];
-  float ru[WIN], rv[WIN], thrf[WIN];
-  uint32_t k[WIN], gid[WIN];
+  double u0[W], v0[W], thr[W], op[W], z[W], rgb[3][W];
+  double ex[8][W], ey[4][W];
+  float ru[W], rv[W], thrf[W];
+  uint32_t k[W], gid[W];
 };
 
+template <int W>
 struct BwdStage {  // backward-only per-warp slots
-  double is3[WIN];  // 1 / (s2 sigma)
-  uint32_t eidx[WIN];
-  float coef[6][WIN];
-  float acc[6][WIN];
+  double nh[W];   // -0.5 / s2
+  double is3[W];  // 1 / (s2 sigma)
+  uint32_t eidx[W];
+  float coef[6][W];
 };
 
 __device__ __forceinline__ void load_head(const Record* rec, uint32_t e, double& u0, double& v0,
@@ -313,15 +320,17 @@ __device__ __forceinline__ bool rect_maybe(double u0, double v0, double sig, flo
   return dx * dx + dy * dy <= rr * rr;
 }
 
-// Load list entries [base, base+32) (clipped to [lo, hi)), keep those that may
-// touch the rectangle and append them at slots [slot0, slot0 + kept).
-template <bool BWD>
-__device__ __forceinline__ int stage_chunk(WinStage& s, BwdStage* b, const uint32_t* __restrict__ lists,
+// Load list entries [base, base+32) clipped to [lo, hi), keep those that may
+// touch the rectangle and place them in ascending list order at slots
+// [slot0, slot0 + kept) (or, with `below`, ending right under slot0).
+template <int W, bool BWD>
+__device__ __forceinline__ int stage_chunk(WinStage<W>& s, BwdStage<W>* b,
+                                           const uint32_t* __restrict__ lists,
                                            const Record* __restrict__ rec,
                                            const ChainCoef* __restrict__ coef,
-                                           const double* __restrict__ col64, int64_t base,
-                                           int64_t lo, int64_t hi, float xlo, float ylo, int lane,
-                                           int slot0, bool below = false) {
+                                           const double* __restrict__ col64, const double* tab,
+                                           int64_t base, int64_t lo, int64_t hi, float xlo, float ylo,
+                                           int lane, int slot0, bool below) {
   const int64_t k = base + lane;
   bool keep = false;
   uint32_t e = 0;
@@ -333,38 +342,50 @@ __device__ __forceinline__ int stage_chunk(WinStage& s, BwdStage* b, const uint3
   }
   const uint32_t km = __ballot_sync(0xffffffffu, keep);
   if (keep) {
-    // ascending list order; `below`: the chunk ends right under slot0
     const int j = (below ? slot0 - __popc(km) : slot0) + __popc(km & ((1u << lane) - 1u));
     // second half of the record: z | r, g | b, gid  (16-byte aligned loads)
     const double2* tp = reinterpret_cast<const double2*>(rec + e) + 2;
     const double2 t0 = __ldg(tp), t1 = __ldg(tp + 1);
-    const double z = t0.x;
     const float2 rg2 = *reinterpret_cast<const float2*>(&t0.y);
     const float2 bg2 = *reinterpret_cast<const float2*>(&t1.x);
-    const float4 tail = make_float4(rg2.x, rg2.y, bg2.x, bg2.y);
     const double s2 = SG_MUL(sig, sig);
     const double thr = SG_MUL(9.0, s2);
+    const double nh = SG_DIV(-0.5, s2);
     s.u0[j] = u0;
     s.v0[j] = v0;
     s.thr[j] = thr;
-    s.nh[j] = SG_DIV(-0.5, s2);
     s.op[j] = op;
-    s.z[j] = z;
+    s.z[j] = t0.x;
     if (col64) {  // fp64 drop-in maps keep exact fp64 colours
       s.rgb[0][j] = col64[3 * (size_t)e];
       s.rgb[1][j] = col64[3 * (size_t)e + 1];
       s.rgb[2][j] = col64[3 * (size_t)e + 2];
     } else {
-      s.rgb[0][j] = tail.x;
-      s.rgb[1][j] = tail.y;
-      s.rgb[2][j] = tail.z;
+      s.rgb[0][j] = rg2.x;
+      s.rgb[1][j] = rg2.y;
+      s.rgb[2][j] = bg2.x;
+    }
+    // separable weight factors (columns xlo..xlo+7, rows ylo..ylo+3); a
+    // column/row whose 1-D distance alone fails the test is never used
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const double dx = SG_SUB(u0, (double)xlo + c);
+      const double dx2 = SG_MUL(dx, dx);
+      s.ex[c][j] = dx2 > thr ? 0.0 : sgad_exp_neg(SG_MUL(dx2, nh), tab);
+    }
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const double dy = SG_SUB(v0, (double)ylo + r);
+      const double dy2 = SG_MUL(dy, dy);
+      s.ey[r][j] = dy2 > thr ? 0.0 : sgad_exp_neg(SG_MUL(dy2, nh), tab);
     }
     s.ru[j] = (float)(u0 - (double)xlo);
     s.rv[j] = (float)(v0 - (double)ylo);
     s.thrf[j] = (float)thr;
     s.k[j] = (uint32_t)k;
-    s.gid[j] = __float_as_uint(tail.w);
+    s.gid[j] = __float_as_uint(bg2.y);
     if (BWD) {
+      b->nh[j] = nh;
       b->is3[j] = 1.0 / (s2 * sig);
       b->eidx[j] = e;
       if (coef) {
@@ -384,8 +405,9 @@ __device__ __forceinline__ int stage_chunk(WinStage& s, BwdStage* b, const uint3
 // Exact reference test d2 > 9 s2 for staged entry j at this lane's pixel:
 // fp32 decides outside a guard band (|error| < 2e-4 (thr + 1), K4),
 // fp64 decides inside it.
-__device__ __forceinline__ bool passes(const WinStage& s, int j, float lx, float ly, double pxd,
-                                       double pyd) {
+template <int W>
+__device__ __forceinline__ bool passes(const WinStage<W>& s, int j, float lx, float ly,
+                                       double pxd, double pyd) {
   const float dxf = s.ru[j] - lx, dyf = s.rv[j] - ly;
   const float d2f = fmaf(dxf, dxf, dyf * dyf);
   const float thrf = s.thrf[j];
@@ -411,17 +433,19 @@ k_forward(const uint2* __restrict__ ranges, const uint32_t* __restrict__ lists,
           double* __restrict__ out_alpha, int32_t* __restrict__ out_count,
           double* __restrict__ t_final, int32_t* __restrict__ last_out,
           uint8_t* __restrict__ signs, sgad_loss_target tgt) {
+  constexpr int W = FWD_WIN;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  WinStage* stage = reinterpret_cast<WinStage*>(smem_raw);
+  WinStage<W>* stage = reinterpret_cast<WinStage<W>*>(smem_raw);
   __shared__ double tab[32];
   load_exp_table(tab);
   const TileGeom g = tile_geom(ntx, width, height);
-  WinStage& s = stage[g.warp];
+  WinStage<W>& s = stage[g.warp];
   const uint2 rg = ranges[g.tile];
   const double pxd = (double)g.px, pyd = (double)g.py;
   const float xlo = (float)(g.tx * SGAD_TILE + (g.warp & 1) * 8);
   const float ylo = (float)(g.ty * SGAD_TILE + (g.warp >> 1) * 4);
-  const float lx = (float)(g.lane & 7), ly = (float)(g.lane >> 3);
+  const int lxi = g.lane & 7, lyi = g.lane >> 3;
+  const float lx = (float)lxi, ly = (float)lyi;
   double T = 1.0, C0 = 0.0, C1 = 0.0, C2 = 0.0, D = 0.0, A = 0.0;
   int cnt = 0, last = -1;
   bool done = !g.valid;
@@ -429,9 +453,9 @@ k_forward(const uint2* __restrict__ ranges, const uint32_t* __restrict__ lists,
   int64_t pos = rg.x;
   while (pos < (int64_t)rg.y && !__all_sync(0xffffffffu, done)) {
     int n = 0;
-    while (n <= WIN - 32 && pos < (int64_t)rg.y) {
-      n += stage_chunk<false>(s, nullptr, lists, rec, nullptr, col64, pos, rg.x, rg.y, xlo, ylo,
-                              g.lane, n);
+    while (n <= W - 32 && pos < (int64_t)rg.y) {
+      n += stage_chunk<W, false>(s, nullptr, lists, rec, nullptr, col64, tab, pos, rg.x, rg.y,
+                                 xlo, ylo, g.lane, n, false);
       pos += 32;
     }
     __syncwarp();
@@ -442,9 +466,7 @@ k_forward(const uint2* __restrict__ ranges, const uint32_t* __restrict__ lists,
     while (mine) {
       const int j = __ffsll((long long)mine) - 1;
       mine &= mine - 1;
-      const double dx = SG_SUB(s.u0[j], pxd), dy = SG_SUB(s.v0[j], pyd);
-      const double d2 = SG_ADD(SG_MUL(dx, dx), SG_MUL(dy, dy));
-      const double w = sgad_exp_neg(SG_MUL(d2, s.nh[j]), tab);
+      const double w = SG_MUL(s.ex[lxi][j], s.ey[lyi][j]);
       double a = SG_MUL(s.op[j], w);
       if (a > SGAD_ALPHA_MAX) a = SGAD_ALPHA_MAX;
       const double at = SG_MUL(a, T);
@@ -521,6 +543,15 @@ __device__ __forceinline__ double sign_of(uint32_t code) {
   return code == 1u ? 1.0 : (code == 2u ? -1.0 : 0.0);
 }
 
+__device__ __forceinline__ void red_add_v4(float* addr, float a, float b, float c, float d) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(addr), "f"(a), "f"(b),
+               "f"(c), "f"(d)
+               : "memory");
+}
+__device__ __forceinline__ void red_add_v2(float* addr, float a, float b) {
+  asm volatile("red.global.add.v2.f32 [%0], {%1, %2};" ::"l"(addr), "f"(a), "f"(b) : "memory");
+}
+
 template <bool FUSED>
 __global__ void __launch_bounds__(RASTER_THREADS)
 k_backward(const uint2* __restrict__ ranges, const uint32_t* __restrict__ lists,
@@ -530,19 +561,21 @@ k_backward(const uint2* __restrict__ ranges, const uint32_t* __restrict__ lists,
            const uint8_t* __restrict__ signs, Upstream up, const double* __restrict__ g_color,
            const double* __restrict__ g_depth, const double* __restrict__ g_alpha,
            double* __restrict__ raw, float* __restrict__ grad_accum) {
+  constexpr int W = BWD_WIN;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  WinStage* stage = reinterpret_cast<WinStage*>(smem_raw);
-  BwdStage* bstage = reinterpret_cast<BwdStage*>(smem_raw + sizeof(WinStage) * NWARP);
+  WinStage<W>* stage = reinterpret_cast<WinStage<W>*>(smem_raw);
+  BwdStage<W>* bstage = reinterpret_cast<BwdStage<W>*>(smem_raw + sizeof(WinStage<W>) * NWARP);
   __shared__ double tab[32];
   load_exp_table(tab);
   const TileGeom g = tile_geom(ntx, width, height);
-  WinStage& s = stage[g.warp];
-  BwdStage& x = bstage[g.warp];
+  WinStage<W>& s = stage[g.warp];
+  BwdStage<W>& x = bstage[g.warp];
   const uint2 rg = ranges[g.tile];
   const double pxd = (double)g.px, pyd = (double)g.py;
   const float xlo = (float)(g.tx * SGAD_TILE + (g.warp & 1) * 8);
   const float ylo = (float)(g.ty * SGAD_TILE + (g.warp >> 1) * 4);
-  const float lx = (float)(g.lane & 7), ly = (float)(g.lane >> 3);
+  const int lxi = g.lane & 7, lyi = g.lane >> 3;
+  const float lx = (float)lxi, ly = (float)lyi;
   const int64_t p = (int64_t)g.py * width + g.px;
 
   double gc0 = 0.0, gc1 = 0.0, gc2 = 0.0, gd = 0.0, ga = 0.0, T = 0.0;
@@ -571,32 +604,25 @@ k_backward(const uint2* __restrict__ ranges, const uint32_t* __restrict__ lists,
   int wend = mylast + 1;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) wend = max(wend, __shfl_xor_sync(0xffffffffu, wend, o));
-  if (FUSED) {
-    for (int j = g.lane; j < WIN; j += 32)
-#pragma unroll
-      for (int i = 0; i < 6; ++i) x.acc[i][j] = 0.f;
-  }
   double sc0 = 0.0, sc1 = 0.0, sc2 = 0.0, sd = 0.0, sa = 0.0;
   int64_t pos = wend;  // exclusive upper end of the unstaged part
   while (pos > (int64_t)rg.x) {
-    int lo = WIN;  // staged slots are [lo, WIN), ascending in list order
+    int lo = W;  // staged slots are [lo, W), ascending in list order
     while (lo >= 32 && pos > (int64_t)rg.x) {
       const int64_t base = pos - 32;
-      lo -= stage_chunk<true>(s, &x, lists, rec, FUSED ? coef : nullptr, col64, base, rg.x, pos,
-                              xlo, ylo, g.lane, lo, true);
+      lo -= stage_chunk<W, true>(s, &x, lists, rec, FUSED ? coef : nullptr, col64, tab, base, rg.x,
+                                 pos, xlo, ylo, g.lane, lo, true);
       pos = base;
     }
     __syncwarp();
     unsigned long long mine = 0;
-    for (int j = lo; j < WIN; ++j)
+    for (int j = lo; j < W; ++j)
       if ((int)s.k[j] <= mylast && passes(s, j, lx, ly, pxd, pyd)) mine |= 1ull << j;
     while (mine) {
       const int j = 63 - __clzll((long long)mine);
       mine &= ~(1ull << j);
-      const double dx = SG_SUB(s.u0[j], pxd), dy = SG_SUB(s.v0[j], pyd);
-      const double d2 = SG_ADD(SG_MUL(dx, dx), SG_MUL(dy, dy));
-      const double nh = s.nh[j], op = s.op[j], z = s.z[j];
-      const double w = sgad_exp_neg(SG_MUL(d2, nh), tab);
+      const double op = s.op[j], z = s.z[j];
+      const double w = SG_MUL(s.ex[lxi][j], s.ey[lyi][j]);
       const double aw = SG_MUL(op, w);
       const bool clamped = aw > SGAD_ALPHA_MAX;
       const double a = clamped ? SGAD_ALPHA_MAX : aw;
@@ -611,21 +637,21 @@ k_backward(const uint2* __restrict__ ranges, const uint32_t* __restrict__ lists,
         const double gcol0 = gc0 * at, gcol1 = gc1 * at, gcol2 = gc2 * at, gz = gd * at;
         double gop = 0.0, gsig = 0.0, gu = 0.0, gv = 0.0;
         if (!clamped) {
+          const double dx = SG_SUB(s.u0[j], pxd), dy = SG_SUB(s.v0[j], pyd);
+          const double d2 = SG_ADD(SG_MUL(dx, dx), SG_MUL(dy, dy));
           const double gw = d_alpha * op;
           gop = d_alpha * w;
-          gsig = gw * w * d2 * x.is3[j];  // gw w d2 / (s2 sigma)
-          const double gd2 = gw * w * nh;  // gw (-0.5 w / s2)
+          gsig = gw * w * d2 * x.is3[j];   // gw w d2 / (s2 sigma)
+          const double gd2 = gw * w * x.nh[j];  // gw (-0.5 w / s2)
           gu = 2.0 * gd2 * dx;
           gv = 2.0 * gd2 * dy;
         }
         if (FUSED) {
-          atomicAdd(&x.acc[0][j], (float)(x.coef[1][j] * gu + x.coef[2][j] * gv +
-                                          x.coef[3][j] * gz + x.coef[4][j] * gsig));
-          atomicAdd(&x.acc[1][j], (float)(x.coef[0][j] * gsig));
-          atomicAdd(&x.acc[2][j], (float)(x.coef[5][j] * gop));
-          atomicAdd(&x.acc[3][j], (float)gcol0);
-          atomicAdd(&x.acc[4][j], (float)gcol1);
-          atomicAdd(&x.acc[5][j], (float)gcol2);
+          float* dst = grad_accum + (size_t)(s.gid[j] & ~GID_LEARN) * 8;
+          red_add_v4(dst, (float)(x.coef[1][j] * gu + x.coef[2][j] * gv + x.coef[3][j] * gz +
+                                  x.coef[4][j] * gsig),
+                     (float)(x.coef[0][j] * gsig), (float)(x.coef[5][j] * gop), (float)gcol0);
+          red_add_v2(dst + 4, (float)gcol1, (float)gcol2);
         } else {
           double* dst = raw + (size_t)x.eidx[j] * 8;
           atomicAdd(dst + 0, gcol0);
@@ -646,20 +672,6 @@ k_backward(const uint2* __restrict__ ranges, const uint32_t* __restrict__ lists,
       T = tb;
     }
     __syncwarp();
-    if (FUSED) {
-      for (int j = lo + g.lane; j < WIN; j += 32) {
-        const float q0 = x.acc[0][j], q1 = x.acc[1][j], q2 = x.acc[2][j], q3 = x.acc[3][j],
-                    q4 = x.acc[4][j], q5 = x.acc[5][j];
-        if (q0 != 0.f || q1 != 0.f || q2 != 0.f || q3 != 0.f || q4 != 0.f || q5 != 0.f) {
-          float4* dst = reinterpret_cast<float4*>(grad_accum + (size_t)(s.gid[j] & ~GID_LEARN) * 8);
-          atomicAdd(dst, make_float4(q0, q1, q2, q3));
-          atomicAdd(reinterpret_cast<float2*>(dst + 1), make_float2(q4, q5));
-#pragma unroll
-          for (int i = 0; i < 6; ++i) x.acc[i][j] = 0.f;
-        }
-      }
-      __syncwarp();
-    }
   }
 }
 
@@ -733,8 +745,8 @@ __global__ void k_export_surv(const uint32_t* __restrict__ perm, const Record* _
   if (opacity) opacity[i] = r.opacity;
 }
 
-constexpr size_t FWD_SMEM = sizeof(WinStage) * NWARP;
-constexpr size_t BWD_SMEM = (sizeof(WinStage) + sizeof(BwdStage)) * NWARP;
+constexpr size_t FWD_SMEM = sizeof(WinStage<FWD_WIN>) * NWARP;
+constexpr size_t BWD_SMEM = (sizeof(WinStage<BWD_WIN>) + sizeof(BwdStage<BWD_WIN>)) * NWARP;
 
 // opt in to >48 KB dynamic shared memory once per process
 static int smem_attrs() {
