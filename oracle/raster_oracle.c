@@ -24,14 +24,11 @@
 
 static const double TAB[32] = {SGAD_EXP2_TABLE};
 
-/* Contributor weight, shared convention with the kernels: the separable
- * product exp(dx^2 * nh) * exp(dy^2 * nh), nh = -0.5 / s2, through
- * sgad_exp_neg (the reference evaluates exp(-0.5 * d2 / s2); the two differ
- * by a few ulps, far inside the 1e-4 image bar). */
-static inline double weight(double dx, double dy, double s2) {
-  const double nh = -0.5 / s2;
-  return sgad_exp_neg((dx * dx) * nh, TAB) * sgad_exp_neg((dy * dy) * nh, TAB);
-}
+/* Contributor weight, shared convention with the kernels: exp(d2 * nh),
+ * nh = -0.5 / s2, through sgad_exp_neg (the reference evaluates
+ * exp(-0.5 * d2 / s2); the two differ by an ulp or two, far inside the 1e-4
+ * image bar). */
+static inline double weight(double d2, double s2) { return sgad_exp_neg(d2 * (-0.5 / s2), TAB); }
 
 /* rasterizer.py:86-135 for one source map.  Survivors are written in pixel
  * order (np.nonzero order).  Returns the survivor count. */
@@ -177,7 +174,7 @@ void orc_forward(const double* u0, const double* v0, const double* z, const doub
           const double d2 = dx * dx + dy * dy;
           const double s2 = sigma[g] * sigma[g];
           if (d2 > 9.0 * s2) continue;
-          const double wgt = weight(dx, dy, s2);
+          const double wgt = weight(d2, s2);
           double a = opacity[g] * wgt;
           if (a > SGAD_ALPHA_MAX) a = SGAD_ALPHA_MAX;
           const double at = a * trans;
@@ -228,7 +225,7 @@ void orc_backward(const double* u0, const double* v0, const double* z, const dou
           const double d2 = dx * dx + dy * dy;
           const double s2 = sigma[g] * sigma[g];
           if (d2 > 9.0 * s2) continue;
-          double a = opacity[g] * weight(dx, dy, s2);
+          double a = opacity[g] * weight(d2, s2);
           if (a > SGAD_ALPHA_MAX) a = SGAD_ALPHA_MAX;
           last = k;
           trans *= 1.0 - a;
@@ -243,7 +240,7 @@ void orc_backward(const double* u0, const double* v0, const double* z, const dou
           const double d2 = dx * dx + dy * dy;
           const double s2 = sigma[g] * sigma[g];
           if (d2 > 9.0 * s2) continue;
-          const double wgt = weight(dx, dy, s2);
+          const double wgt = weight(d2, s2);
           const double aw = opacity[g] * wgt;
           const int clamped = aw > SGAD_ALPHA_MAX;
           const double a = clamped ? SGAD_ALPHA_MAX : aw;

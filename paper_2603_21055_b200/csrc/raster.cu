@@ -269,34 +269,29 @@ __device__ __forceinline__ TileGeom tile_geom(int ntx, int width, int height) {
 }
 
 // Each warp owns one 8x4 sub-tile and walks the tile's depth-ordered list on
-// its own (no block barriers: sub-tiles finish at different list positions).
-// It stages the list entries that can touch its rectangle into a private
-// shared-memory window, every lane builds a 64-bit mask of the staged entries
-// its pixel passes (the reference's d2 > 9 s2 test, decided in fp32 with an
-// fp64 fallback inside a guard band), and then pops its own bits in list
-// order: lanes composite different Gaussians at the same time.  The Gaussian
-// weight factorises over the rectangle's 8 columns and 4 rows,
-// w = exp(-dx^2/2s^2) exp(-dy^2/2s^2), so staging evaluates 12 exponentials
-// per entry (one lane per entry, fully converged) and the divergent
-// per-contribution loop only multiplies two staged factors.
+// its own (no block barriers: sub-tiles finish at different list positions),
+// 64 list entries (two chunks) per window:
+//   1. entry-major masks: lane j loads list entry j of a 32-entry chunk, culls
+//      it against the rectangle in fp32, and for survivors evaluates the
+//      reference test d2 > 9 s2 at all 32 pixels (fp32 outside a guard band,
+//      fp64 inside it) -> a 32-bit pixel mask M_j; entries with M_j != 0 are
+//      staged in the warp's shared-memory slots;
+//   2. a 5-round shuffle transpose turns the 32 entry masks into one bitmask
+//      per lane (= per pixel) over the window's entries;
+//   3. every lane pops its own bits in list order and composites in fp64, so
+//      lanes work on different Gaussians at the same time.
 constexpr int NWARP = RASTER_THREADS / 32;
-constexpr int FWD_WIN = 64;
-constexpr int BWD_WIN = 32;
+constexpr int WIN = 64;
 
-template <int W>
 struct WinStage {
-  double u0[W], v0[W], thr[W], op[W], z[W], rgb[3][W];
-  double ex[8][W], ey[4][W];
-  float ru[W], rv[W], thrf[W];
-  uint32_t k[W], gid[W];
+  double u0[WIN], v0[WIN], nh[WIN], op[WIN], z[WIN], rgb[3][WIN];
+  uint32_t gid[WIN];
 };
 
-template <int W>
 struct BwdStage {  // backward-only per-warp slots
-  double nh[W];   // -0.5 / s2
-  double is3[W];  // 1 / (s2 sigma)
-  uint32_t eidx[W];
-  float coef[6][W];
+  double is3[WIN];  // 1 / (s2 sigma)
+  uint32_t eidx[WIN];
+  float coef[6][WIN];
 };
 
 __device__ __forceinline__ void load_head(const Record* rec, uint32_t e, double& u0, double& v0,
@@ -309,51 +304,94 @@ __device__ __forceinline__ void load_head(const Record* rec, uint32_t e, double&
   op = b.y;
 }
 
-// Conservative fp32 cull of a Gaussian against the warp's 8x4 rectangle
-// (pixel centres [xlo, xlo+7] x [ylo, ylo+3]); the exact per-pixel test
-// follows, so a generous margin only costs work, never correctness.
-__device__ __forceinline__ bool rect_maybe(double u0, double v0, double sig, float xlo, float ylo) {
-  const float uf = (float)u0, vf = (float)v0;
-  const float rr = (float)(3.0 * sig) * 1.0001f + 0.01f;
-  const float dx = fmaxf(fmaxf(xlo - uf, uf - (xlo + 7.0f)), 0.0f);
-  const float dy = fmaxf(fmaxf(ylo - vf, vf - (ylo + 3.0f)), 0.0f);
-  return dx * dx + dy * dy <= rr * rr;
+// 32x32 bit transpose across the warp: lane i holds row i on entry, column i
+// on exit.
+__device__ __forceinline__ uint32_t transpose32(uint32_t x, int lane) {
+  const uint32_t masks[5] = {0x0000FFFFu, 0x00FF00FFu, 0x0F0F0F0Fu, 0x33333333u, 0x55555555u};
+#pragma unroll
+  for (int r = 0; r < 5; ++r) {
+    const int s = 16 >> r;
+    const uint32_t m = masks[r];
+    const uint32_t y = __shfl_xor_sync(0xffffffffu, x, s);
+    x = (lane & s) ? ((x & ~m) | ((y >> s) & m)) : ((x & m) | ((y << s) & ~m));
+  }
+  return x;
 }
 
-// Load list entries [base, base+32) clipped to [lo, hi), keep those that may
-// touch the rectangle and place them in ascending list order at slots
-// [slot0, slot0 + kept) (or, with `below`, ending right under slot0).
-template <int W, bool BWD>
-__device__ __forceinline__ int stage_chunk(WinStage<W>& s, BwdStage<W>* b,
-                                           const uint32_t* __restrict__ lists,
-                                           const Record* __restrict__ rec,
-                                           const ChainCoef* __restrict__ coef,
-                                           const double* __restrict__ col64, const double* tab,
-                                           int64_t base, int64_t lo, int64_t hi, float xlo, float ylo,
-                                           int lane, int slot0, bool below) {
+// Exact pixel mask of one Gaussian over the warp's 8x4 rectangle: bit
+// (ly*8 + lx) set iff the reference test d2 > 9 s2 fails at pixel
+// (xlo+lx, ylo+ly).  fp32 decides outside a guard band of 2e-4 (thr + 1)
+// (its error is < 1e-6 (thr + 400) for any Gaussian that reaches the
+// rectangle; K4), fp64 decides inside it.
+__device__ __forceinline__ uint32_t pixel_mask(double u0, double v0, double thr, double xlo,
+                                               double ylo) {
+  const float ru = (float)(u0 - xlo), rv = (float)(v0 - ylo), thrf = (float)thr;
+  const float band = 2e-4f * (thrf + 1.0f);
+  const float hi = thrf + band, lo = thrf - band;
+  uint32_t m = 0;
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const float dyf = rv - (float)r;
+    const float dy2f = dyf * dyf;
+    if (dy2f > hi) continue;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const float dxf = ru - (float)c;
+      const float d2f = fmaf(dxf, dxf, dy2f);
+      bool pass;
+      if (d2f > hi) {
+        pass = false;
+      } else if (d2f < lo) {
+        pass = true;
+      } else {
+        const double dx = SG_SUB(u0, xlo + c), dy = SG_SUB(v0, ylo + r);
+        pass = !(SG_ADD(SG_MUL(dx, dx), SG_MUL(dy, dy)) > thr);
+      }
+      m |= (pass ? 1u : 0u) << (r * 8 + c);
+    }
+  }
+  return m;
+}
+
+// One 32-entry chunk [base, base+32) clipped to [lo, hi): stage entries that
+// touch at least one pixel at slots slot0 + lane; returns this lane's bits.
+template <bool BWD>
+__device__ __forceinline__ uint32_t stage_chunk(WinStage& s, BwdStage* b,
+                                                const uint32_t* __restrict__ lists,
+                                                const Record* __restrict__ rec,
+                                                const ChainCoef* __restrict__ coef,
+                                                const double* __restrict__ col64, int64_t base,
+                                                int64_t lo, int64_t hi, double xlo, double ylo,
+                                                int lane, int slot0) {
   const int64_t k = base + lane;
-  bool keep = false;
+  uint32_t m = 0;
   uint32_t e = 0;
-  double u0 = 0.0, v0 = 0.0, sig = 0.0, op = 0.0;
+  double u0 = 0.0, v0 = 0.0, sig = 0.0, op = 0.0, thr = 0.0;
   if (k >= lo && k < hi) {
     e = lists[k];
     load_head(rec, e, u0, v0, sig, op);
-    keep = rect_maybe(u0, v0, sig, xlo, ylo);
+    // cheap conservative cull of the whole rectangle first
+    const float uf = (float)u0, vf = (float)v0;
+    const float rr = (float)(3.0 * sig) * 1.0001f + 0.01f;
+    const float xl = (float)xlo, yl = (float)ylo;
+    const float dx = fmaxf(fmaxf(xl - uf, uf - (xl + 7.0f)), 0.0f);
+    const float dy = fmaxf(fmaxf(yl - vf, vf - (yl + 3.0f)), 0.0f);
+    if (dx * dx + dy * dy <= rr * rr) {
+      thr = SG_MUL(9.0, SG_MUL(sig, sig));
+      m = pixel_mask(u0, v0, thr, xlo, ylo);
+    }
   }
-  const uint32_t km = __ballot_sync(0xffffffffu, keep);
-  if (keep) {
-    const int j = (below ? slot0 - __popc(km) : slot0) + __popc(km & ((1u << lane) - 1u));
+  if (m) {
+    const int j = slot0 + lane;
     // second half of the record: z | r, g | b, gid  (16-byte aligned loads)
     const double2* tp = reinterpret_cast<const double2*>(rec + e) + 2;
     const double2 t0 = __ldg(tp), t1 = __ldg(tp + 1);
     const float2 rg2 = *reinterpret_cast<const float2*>(&t0.y);
     const float2 bg2 = *reinterpret_cast<const float2*>(&t1.x);
     const double s2 = SG_MUL(sig, sig);
-    const double thr = SG_MUL(9.0, s2);
-    const double nh = SG_DIV(-0.5, s2);
     s.u0[j] = u0;
     s.v0[j] = v0;
-    s.thr[j] = thr;
+    s.nh[j] = SG_DIV(-0.5, s2);
     s.op[j] = op;
     s.z[j] = t0.x;
     if (col64) {  // fp64 drop-in maps keep exact fp64 colours
@@ -365,27 +403,8 @@ __device__ __forceinline__ int stage_chunk(WinStage<W>& s, BwdStage<W>* b,
       s.rgb[1][j] = rg2.y;
       s.rgb[2][j] = bg2.x;
     }
-    // separable weight factors (columns xlo..xlo+7, rows ylo..ylo+3); a
-    // column/row whose 1-D distance alone fails the test is never used
-#pragma unroll
-    for (int c = 0; c < 8; ++c) {
-      const double dx = SG_SUB(u0, (double)xlo + c);
-      const double dx2 = SG_MUL(dx, dx);
-      s.ex[c][j] = dx2 > thr ? 0.0 : sgad_exp_neg(SG_MUL(dx2, nh), tab);
-    }
-#pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      const double dy = SG_SUB(v0, (double)ylo + r);
-      const double dy2 = SG_MUL(dy, dy);
-      s.ey[r][j] = dy2 > thr ? 0.0 : sgad_exp_neg(SG_MUL(dy2, nh), tab);
-    }
-    s.ru[j] = (float)(u0 - (double)xlo);
-    s.rv[j] = (float)(v0 - (double)ylo);
-    s.thrf[j] = (float)thr;
-    s.k[j] = (uint32_t)k;
     s.gid[j] = __float_as_uint(bg2.y);
     if (BWD) {
-      b->nh[j] = nh;
       b->is3[j] = 1.0 / (s2 * sig);
       b->eidx[j] = e;
       if (coef) {
@@ -399,23 +418,7 @@ __device__ __forceinline__ int stage_chunk(WinStage<W>& s, BwdStage<W>* b,
       }
     }
   }
-  return __popc(km);
-}
-
-// Exact reference test d2 > 9 s2 for staged entry j at this lane's pixel:
-// fp32 decides outside a guard band (|error| < 2e-4 (thr + 1), K4),
-// fp64 decides inside it.
-template <int W>
-__device__ __forceinline__ bool passes(const WinStage<W>& s, int j, float lx, float ly,
-                                       double pxd, double pyd) {
-  const float dxf = s.ru[j] - lx, dyf = s.rv[j] - ly;
-  const float d2f = fmaf(dxf, dxf, dyf * dyf);
-  const float thrf = s.thrf[j];
-  const float band = 2e-4f * (thrf + 1.0f);
-  if (d2f > thrf + band) return false;
-  if (d2f < thrf - band) return true;
-  const double dx = SG_SUB(s.u0[j], pxd), dy = SG_SUB(s.v0[j], pyd);
-  return !(SG_ADD(SG_MUL(dx, dx), SG_MUL(dy, dy)) > s.thr[j]);
+  return transpose32(m, lane);
 }
 
 __device__ __forceinline__ void load_exp_table(double* tab) {
@@ -433,40 +436,34 @@ k_forward(const uint2* __restrict__ ranges, const uint32_t* __restrict__ lists,
           double* __restrict__ out_alpha, int32_t* __restrict__ out_count,
           double* __restrict__ t_final, int32_t* __restrict__ last_out,
           uint8_t* __restrict__ signs, sgad_loss_target tgt) {
-  constexpr int W = FWD_WIN;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  WinStage<W>* stage = reinterpret_cast<WinStage<W>*>(smem_raw);
+  WinStage* stage = reinterpret_cast<WinStage*>(smem_raw);
   __shared__ double tab[32];
   load_exp_table(tab);
   const TileGeom g = tile_geom(ntx, width, height);
-  WinStage<W>& s = stage[g.warp];
+  WinStage& s = stage[g.warp];
   const uint2 rg = ranges[g.tile];
   const double pxd = (double)g.px, pyd = (double)g.py;
-  const float xlo = (float)(g.tx * SGAD_TILE + (g.warp & 1) * 8);
-  const float ylo = (float)(g.ty * SGAD_TILE + (g.warp >> 1) * 4);
-  const int lxi = g.lane & 7, lyi = g.lane >> 3;
-  const float lx = (float)lxi, ly = (float)lyi;
+  const double xlo = (double)(g.tx * SGAD_TILE + (g.warp & 1) * 8);
+  const double ylo = (double)(g.ty * SGAD_TILE + (g.warp >> 1) * 4);
   double T = 1.0, C0 = 0.0, C1 = 0.0, C2 = 0.0, D = 0.0, A = 0.0;
   int cnt = 0, last = -1;
   bool done = !g.valid;
 
-  int64_t pos = rg.x;
-  while (pos < (int64_t)rg.y && !__all_sync(0xffffffffu, done)) {
-    int n = 0;
-    while (n <= W - 32 && pos < (int64_t)rg.y) {
-      n += stage_chunk<W, false>(s, nullptr, lists, rec, nullptr, col64, tab, pos, rg.x, rg.y,
-                                 xlo, ylo, g.lane, n, false);
-      pos += 32;
-    }
+  for (int64_t wb = rg.x; wb < (int64_t)rg.y; wb += WIN) {
+    if (__all_sync(0xffffffffu, done)) break;
+    const uint32_t b0 = stage_chunk<false>(s, nullptr, lists, rec, nullptr, col64, wb, rg.x, rg.y,
+                                           xlo, ylo, g.lane, 0);
+    const uint32_t b1 = stage_chunk<false>(s, nullptr, lists, rec, nullptr, col64, wb + 32, rg.x,
+                                           rg.y, xlo, ylo, g.lane, 32);
     __syncwarp();
-    unsigned long long mine = 0;
-    if (!done)
-      for (int j = 0; j < n; ++j)
-        if (passes(s, j, lx, ly, pxd, pyd)) mine |= 1ull << j;
+    unsigned long long mine = done ? 0ull : ((unsigned long long)b1 << 32) | b0;
     while (mine) {
       const int j = __ffsll((long long)mine) - 1;
       mine &= mine - 1;
-      const double w = SG_MUL(s.ex[lxi][j], s.ey[lyi][j]);
+      const double dx = SG_SUB(s.u0[j], pxd), dy = SG_SUB(s.v0[j], pyd);
+      const double d2 = SG_ADD(SG_MUL(dx, dx), SG_MUL(dy, dy));
+      const double w = sgad_exp_neg(SG_MUL(d2, s.nh[j]), tab);
       double a = SG_MUL(s.op[j], w);
       if (a > SGAD_ALPHA_MAX) a = SGAD_ALPHA_MAX;
       const double at = SG_MUL(a, T);
@@ -476,7 +473,7 @@ k_forward(const uint2* __restrict__ ranges, const uint32_t* __restrict__ lists,
       D = SG_FMA(s.z[j], at, D);
       A = SG_ADD(A, at);
       ++cnt;
-      last = (int)s.k[j];
+      last = (int)(wb + j);
       T = SG_MUL(T, SG_SUB(1.0, a));
       if (T < SGAD_TRANSMITTANCE_MIN) {
         done = true;
@@ -561,21 +558,18 @@ k_backward(const uint2* __restrict__ ranges, const uint32_t* __restrict__ lists,
            const uint8_t* __restrict__ signs, Upstream up, const double* __restrict__ g_color,
            const double* __restrict__ g_depth, const double* __restrict__ g_alpha,
            double* __restrict__ raw, float* __restrict__ grad_accum) {
-  constexpr int W = BWD_WIN;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  WinStage<W>* stage = reinterpret_cast<WinStage<W>*>(smem_raw);
-  BwdStage<W>* bstage = reinterpret_cast<BwdStage<W>*>(smem_raw + sizeof(WinStage<W>) * NWARP);
+  WinStage* stage = reinterpret_cast<WinStage*>(smem_raw);
+  BwdStage* bstage = reinterpret_cast<BwdStage*>(smem_raw + sizeof(WinStage) * NWARP);
   __shared__ double tab[32];
   load_exp_table(tab);
   const TileGeom g = tile_geom(ntx, width, height);
-  WinStage<W>& s = stage[g.warp];
-  BwdStage<W>& x = bstage[g.warp];
+  WinStage& s = stage[g.warp];
+  BwdStage& x = bstage[g.warp];
   const uint2 rg = ranges[g.tile];
   const double pxd = (double)g.px, pyd = (double)g.py;
-  const float xlo = (float)(g.tx * SGAD_TILE + (g.warp & 1) * 8);
-  const float ylo = (float)(g.ty * SGAD_TILE + (g.warp >> 1) * 4);
-  const int lxi = g.lane & 7, lyi = g.lane >> 3;
-  const float lx = (float)lxi, ly = (float)lyi;
+  const double xlo = (double)(g.tx * SGAD_TILE + (g.warp & 1) * 8);
+  const double ylo = (double)(g.ty * SGAD_TILE + (g.warp >> 1) * 4);
   const int64_t p = (int64_t)g.py * width + g.px;
 
   double gc0 = 0.0, gc1 = 0.0, gc2 = 0.0, gd = 0.0, ga = 0.0, T = 0.0;
@@ -605,24 +599,24 @@ k_backward(const uint2* __restrict__ ranges, const uint32_t* __restrict__ lists,
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) wend = max(wend, __shfl_xor_sync(0xffffffffu, wend, o));
   double sc0 = 0.0, sc1 = 0.0, sc2 = 0.0, sd = 0.0, sa = 0.0;
-  int64_t pos = wend;  // exclusive upper end of the unstaged part
-  while (pos > (int64_t)rg.x) {
-    int lo = W;  // staged slots are [lo, W), ascending in list order
-    while (lo >= 32 && pos > (int64_t)rg.x) {
-      const int64_t base = pos - 32;
-      lo -= stage_chunk<W, true>(s, &x, lists, rec, FUSED ? coef : nullptr, col64, tab, base, rg.x,
-                                 pos, xlo, ylo, g.lane, lo, true);
-      pos = base;
-    }
+  for (int64_t wt = wend; wt > (int64_t)rg.x; wt -= WIN) {
+    const int64_t wb = wt - WIN;  // window covers list positions [wb, wt)
+    const uint32_t b0 = stage_chunk<true>(s, &x, lists, rec, FUSED ? coef : nullptr, col64, wb,
+                                          rg.x, wt, xlo, ylo, g.lane, 0);
+    const uint32_t b1 = stage_chunk<true>(s, &x, lists, rec, FUSED ? coef : nullptr, col64,
+                                          wb + 32, rg.x, wt, xlo, ylo, g.lane, 32);
     __syncwarp();
-    unsigned long long mine = 0;
-    for (int j = lo; j < W; ++j)
-      if ((int)s.k[j] <= mylast && passes(s, j, lx, ly, pxd, pyd)) mine |= 1ull << j;
+    unsigned long long mine = ((unsigned long long)b1 << 32) | b0;
+    const int64_t lim = (int64_t)mylast - wb;  // bits above the lane's last contributor
+    if (lim < 0) mine = 0;
+    else if (lim < 63) mine &= (2ull << lim) - 1ull;
     while (mine) {
       const int j = 63 - __clzll((long long)mine);
       mine &= ~(1ull << j);
-      const double op = s.op[j], z = s.z[j];
-      const double w = SG_MUL(s.ex[lxi][j], s.ey[lyi][j]);
+      const double dx = SG_SUB(s.u0[j], pxd), dy = SG_SUB(s.v0[j], pyd);
+      const double d2 = SG_ADD(SG_MUL(dx, dx), SG_MUL(dy, dy));
+      const double nh = s.nh[j], op = s.op[j], z = s.z[j];
+      const double w = sgad_exp_neg(SG_MUL(d2, nh), tab);
       const double aw = SG_MUL(op, w);
       const bool clamped = aw > SGAD_ALPHA_MAX;
       const double a = clamped ? SGAD_ALPHA_MAX : aw;
@@ -637,12 +631,10 @@ k_backward(const uint2* __restrict__ ranges, const uint32_t* __restrict__ lists,
         const double gcol0 = gc0 * at, gcol1 = gc1 * at, gcol2 = gc2 * at, gz = gd * at;
         double gop = 0.0, gsig = 0.0, gu = 0.0, gv = 0.0;
         if (!clamped) {
-          const double dx = SG_SUB(s.u0[j], pxd), dy = SG_SUB(s.v0[j], pyd);
-          const double d2 = SG_ADD(SG_MUL(dx, dx), SG_MUL(dy, dy));
           const double gw = d_alpha * op;
           gop = d_alpha * w;
-          gsig = gw * w * d2 * x.is3[j];   // gw w d2 / (s2 sigma)
-          const double gd2 = gw * w * x.nh[j];  // gw (-0.5 w / s2)
+          gsig = gw * w * d2 * x.is3[j];  // gw w d2 / (s2 sigma)
+          const double gd2 = gw * w * nh;  // gw (-0.5 w / s2)
           gu = 2.0 * gd2 * dx;
           gv = 2.0 * gd2 * dy;
         }
@@ -745,8 +737,8 @@ __global__ void k_export_surv(const uint32_t* __restrict__ perm, const Record* _
   if (opacity) opacity[i] = r.opacity;
 }
 
-constexpr size_t FWD_SMEM = sizeof(WinStage<FWD_WIN>) * NWARP;
-constexpr size_t BWD_SMEM = (sizeof(WinStage<BWD_WIN>) + sizeof(BwdStage<BWD_WIN>)) * NWARP;
+constexpr size_t FWD_SMEM = sizeof(WinStage) * NWARP;
+constexpr size_t BWD_SMEM = (sizeof(WinStage) + sizeof(BwdStage)) * NWARP;
 
 // opt in to >48 KB dynamic shared memory once per process
 static int smem_attrs() {
