@@ -320,37 +320,44 @@ __device__ __forceinline__ uint32_t transpose32(uint32_t x, int lane) {
 
 // Exact pixel mask of one Gaussian over the warp's 8x4 rectangle: bit
 // (ly*8 + lx) set iff the reference test d2 > 9 s2 fails at pixel
-// (xlo+lx, ylo+ly).  fp32 decides outside a guard band of 2e-4 (thr + 1)
-// (its error is < 1e-6 (thr + 400) for any Gaussian that reaches the
-// rectangle; K4), fp64 decides inside it.
+// (xlo+lx, ylo+ly).  Per row, fp32 gives the column interval of certain
+// passes (shrunk by a guard band of 2e-4 (thr + 1) in d2) and of possible
+// passes (grown by it); only columns in between are decided by the exact
+// fp64 test, which is rare.  The fp32 error is < 1e-6 (thr + 400) for any
+// Gaussian that survived the rectangle cull (K4).
+__device__ __forceinline__ uint32_t col_range(float a, float b) {
+  // columns c in [ceil(a), floor(b)] intersected with [0, 7], as an 8-bit mask
+  const int lo = max((int)ceilf(a), 0), hi = min((int)floorf(b), 7);
+  return lo > hi ? 0u : ((0xFFu >> (7 - hi + lo)) << lo);
+}
+
 __device__ __forceinline__ uint32_t pixel_mask(double u0, double v0, double thr, double xlo,
                                                double ylo) {
   const float ru = (float)(u0 - xlo), rv = (float)(v0 - ylo), thrf = (float)thr;
   const float band = 2e-4f * (thrf + 1.0f);
-  const float hi = thrf + band, lo = thrf - band;
-  uint32_t m = 0;
+  uint32_t sure = 0, maybe = 0;
 #pragma unroll
   for (int r = 0; r < 4; ++r) {
     const float dyf = rv - (float)r;
-    const float dy2f = dyf * dyf;
-    if (dy2f > hi) continue;
-#pragma unroll
-    for (int c = 0; c < 8; ++c) {
-      const float dxf = ru - (float)c;
-      const float d2f = fmaf(dxf, dxf, dy2f);
-      bool pass;
-      if (d2f > hi) {
-        pass = false;
-      } else if (d2f < lo) {
-        pass = true;
-      } else {
-        const double dx = SG_SUB(u0, xlo + c), dy = SG_SUB(v0, ylo + r);
-        pass = !(SG_ADD(SG_MUL(dx, dx), SG_MUL(dy, dy)) > thr);
-      }
-      m |= (pass ? 1u : 0u) << (r * 8 + c);
+    const float dy2 = dyf * dyf;
+    const float rem_hi = thrf + band - dy2;
+    if (rem_hi < 0.0f) continue;
+    const float h_hi = sqrtf(rem_hi) * 1.000001f + 1e-5f;
+    maybe |= col_range(ru - h_hi, ru + h_hi) << (8 * r);
+    const float rem_lo = thrf - band - dy2;
+    if (rem_lo > 0.0f) {
+      const float h_lo = sqrtf(rem_lo) * 0.999999f - 1e-5f;
+      sure |= col_range(ru - h_lo, ru + h_lo) << (8 * r);
     }
   }
-  return m;
+  uint32_t unsure = maybe & ~sure;
+  while (unsure) {
+    const int bit = __ffs(unsure) - 1;
+    unsure &= unsure - 1;
+    const double dx = SG_SUB(u0, xlo + (bit & 7)), dy = SG_SUB(v0, ylo + (bit >> 3));
+    if (!(SG_ADD(SG_MUL(dx, dx), SG_MUL(dy, dy)) > thr)) sure |= 1u << bit;
+  }
+  return sure;
 }
 
 // One 32-entry chunk [base, base+32) clipped to [lo, hi): stage entries that
@@ -456,6 +463,9 @@ k_forward(const uint2* __restrict__ ranges, const uint32_t* __restrict__ lists,
                                            xlo, ylo, g.lane, 0);
     const uint32_t b1 = stage_chunk<false>(s, nullptr, lists, rec, nullptr, col64, wb + 32, rg.x,
                                            rg.y, xlo, ylo, g.lane, 32);
+    // pull the next window's record heads towards L1 while this one composites
+    for (int64_t q = wb + WIN + g.lane; q < min(wb + 2 * WIN, (int64_t)rg.y); q += 32)
+      asm volatile("prefetch.global.L1 [%0];" ::"l"(rec + lists[q]));
     __syncwarp();
     unsigned long long mine = done ? 0ull : ((unsigned long long)b1 << 32) | b0;
     while (mine) {
@@ -605,6 +615,8 @@ k_backward(const uint2* __restrict__ ranges, const uint32_t* __restrict__ lists,
                                           rg.x, wt, xlo, ylo, g.lane, 0);
     const uint32_t b1 = stage_chunk<true>(s, &x, lists, rec, FUSED ? coef : nullptr, col64,
                                           wb + 32, rg.x, wt, xlo, ylo, g.lane, 32);
+    for (int64_t q = wb - WIN + g.lane; q < wb; q += 32)
+      if (q >= (int64_t)rg.x) asm volatile("prefetch.global.L1 [%0];" ::"l"(rec + lists[q]));
     __syncwarp();
     unsigned long long mine = ((unsigned long long)b1 << 32) | b0;
     const int64_t lim = (int64_t)mylast - wb;  // bits above the lane's last contributor

@@ -178,3 +178,30 @@ def test_window_engine_step_adam():
     assert d[:, 3].max() <= cfg.lr_opacity * 1.0001 + 1e-7
     assert (d[:, 0] == 0).all()  # base depth is not learnable
     assert wm.grad.abs().max().item() == 0.0  # consumed and zeroed by Adam
+
+
+@pytest.mark.parametrize("seed", [11, 12])
+def test_random_footprints_bit_exact(seed):
+    """Gaussians with footprints from ~0.05 px to ~40 px, many centres near
+    pixel-boundary distances: the fp32-guarded pixel masks must reproduce the
+    reference test exactly, so images equal the oracle's bit for bit."""
+    from types import SimpleNamespace
+    from paper_2603_21055_b200.rasterizer import splat
+    wc = _window_np(n_frames=3, seed=seed)
+    rng = np.random.default_rng(seed)
+    maps_np = []
+    for i, p in enumerate(wc.params):
+        p.log_radius = p.log_radius + rng.normal(0.0, 1.5, p.log_radius.shape)
+        p.opacity_logit = rng.normal(0.0, 3.0, p.log_radius.shape)
+        maps_np.append(SimpleNamespace(frame_index=i, pose=wc.poses[i], intrinsics=wc.intr,
+                                       base_depth=p.base_depth, delta=p.delta,
+                                       log_radius=p.log_radius, opacity_logit=p.opacity_logit,
+                                       color=p.color, active_mask=p.active_mask))
+    maps = [dev_map(m) for m in maps_np]
+    for v in range(3):
+        pose = wc.poses[v]
+        out = splat(maps, pose, wc.intr)
+        ref = O.splat(maps_np, pose.rotation, pose.translation, wc.intr)
+        np.testing.assert_array_equal(out.contributors.cpu().numpy(), ref.contributors)
+        np.testing.assert_array_equal(out.color.cpu().numpy(), ref.color)
+        np.testing.assert_array_equal(out.depth.cpu().numpy(), ref.depth)
