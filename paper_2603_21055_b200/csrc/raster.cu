@@ -43,7 +43,7 @@ constexpr int RASTER_THREADS = 256;
 struct sgad_raster {
   sgad::DevBuf frames, status, counters, records, coef, keys0, keys1, vals0, vals1;
   sgad::DevBuf pcount, poffset, pkeys0, pkeys1, pvals0, pvals1, ranges, cub_tmp;
-  sgad::DevBuf trans_final, last_idx, signs, raw_grads, rank_of, scratch, col64;
+  sgad::DevBuf trans_final, last_idx, signs, raw_grads, rank_of, scratch, col64, zrange, k32a, k32b;
   int any_f64 = 0;
   std::vector<sgad_frame> host_frames;
   sgad_camera cam{};
@@ -122,9 +122,12 @@ k_project(const sgad_frame* __restrict__ frames, int n_frames, sgad_camera cam, 
           int ntx, int nty, int want_coef, Record* __restrict__ rec, ChainCoef* __restrict__ coef,
           double* __restrict__ col64,
           unsigned long long* __restrict__ keys, uint32_t* __restrict__ vals,
-          uint32_t* __restrict__ status, uint32_t* __restrict__ counters) {
+          uint32_t* __restrict__ status, uint32_t* __restrict__ counters,
+          unsigned long long* __restrict__ zrange) {
   typedef cub::BlockScan<uint32_t, PROJ_THREADS> Scan;
+  typedef cub::BlockReduce<unsigned long long, PROJ_THREADS> Red;
   __shared__ typename Scan::TempStorage scan_tmp;
+  __shared__ typename Red::TempStorage red_tmp;
   __shared__ uint32_t s_tile, s_prefix;
   if (threadIdx.x == 0) s_tile = atomicAdd(&counters[0], 1u);
   __syncthreads();
@@ -155,11 +158,12 @@ k_project(const sgad_frame* __restrict__ frames, int n_frames, sgad_camera cam, 
       c64[2] = plane_ld(f, 6 * hw + p);
       r.gid = gid | (f.learnable ? GID_LEARN : 0u);
       // tile bbox (rasterizer.py:187-199)
-      const double rr = SG_MUL(3.0, o.sig), t16 = (double)SGAD_TILE;
-      long long x0 = (long long)floor(SG_DIV(SG_SUB(o.u0, rr), t16));
-      long long x1 = (long long)floor(SG_DIV(SG_ADD(o.u0, rr), t16));
-      long long y0 = (long long)floor(SG_DIV(SG_SUB(o.v0, rr), t16));
-      long long y1 = (long long)floor(SG_DIV(SG_ADD(o.v0, rr), t16));
+      // (x) / 16 is exact as (x) * 0.0625 (power of two)
+      const double rr = SG_MUL(3.0, o.sig), it16 = 1.0 / (double)SGAD_TILE;
+      long long x0 = (long long)floor(SG_MUL(SG_SUB(o.u0, rr), it16));
+      long long x1 = (long long)floor(SG_MUL(SG_ADD(o.u0, rr), it16));
+      long long y0 = (long long)floor(SG_MUL(SG_SUB(o.v0, rr), it16));
+      long long y1 = (long long)floor(SG_MUL(SG_ADD(o.v0, rr), it16));
       x0 = x0 < 0 ? 0 : x0;
       y0 = y0 < 0 ? 0 : y0;
       x1 = x1 > ntx - 1 ? ntx - 1 : x1;
@@ -181,6 +185,15 @@ k_project(const sgad_frame* __restrict__ frames, int n_frames, sgad_camera cam, 
     }
   }
 
+  // depth range of the survivors (positive doubles order like their bits)
+  const unsigned long long zk = keep ? (unsigned long long)__double_as_longlong(r.z) : 0ull;
+  const unsigned long long zmax = Red(red_tmp).Reduce(zk, cub::Max());
+  __syncthreads();
+  const unsigned long long zmin = Red(red_tmp).Reduce(keep ? zk : ~0ull, cub::Min());
+  if (threadIdx.x == 0) {
+    if (zmin != ~0ull) atomicMin(zrange, zmin);
+    if (zmax) atomicMax(zrange + 1, zmax);
+  }
   uint32_t rank, agg;
   Scan(scan_tmp).ExclusiveSum(keep ? 1u : 0u, rank, agg);
   if (threadIdx.x == 0) {
@@ -212,6 +225,50 @@ k_project(const sgad_frame* __restrict__ frames, int n_frames, sgad_camera cam, 
     vals[slot] = slot;
   }
   if (threadIdx.x == 0 && (uint32_t)(tile + 1) * PROJ_THREADS >= n_total) counters[1] = s_prefix + agg;
+}
+
+// ------------------------------------------------------------------ K2
+// 32-bit monotone depth buckets: floor((z - zmin) * scale).  Sorting them
+// stably leaves only runs of equal buckets to be put in exact (z, emission)
+// order by k_depth_fixup -- 4 radix passes instead of 8 for the 63-bit key.
+__global__ void k_depth_key32(const unsigned long long* __restrict__ zkeys, uint32_t n,
+                              double zmin, double scale, uint32_t* __restrict__ k32,
+                              uint32_t* __restrict__ vals) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double z = __longlong_as_double((long long)zkeys[i]);
+  const double b = floor((z - zmin) * scale);
+  k32[i] = b >= 4294967295.0 ? 0xFFFFFFFFu : (uint32_t)b;
+  vals[i] = i;
+}
+
+// Runs of equal buckets are sorted by (z bits, emission index) in place;
+// runs longer than 64 raise *overflow and are redone with the full key.
+__global__ void k_depth_fixup(const uint32_t* __restrict__ k32, uint32_t n,
+                              const unsigned long long* __restrict__ zkeys,
+                              uint32_t* __restrict__ perm, uint32_t* __restrict__ overflow) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i + 1 >= n) return;
+  if (k32[i + 1] != k32[i] || (i > 0 && k32[i - 1] == k32[i])) return;  // not a run head
+  uint32_t end = i + 2;
+  while (end < n && k32[end] == k32[i] && end - i <= 64) ++end;
+  if (end - i > 64) {
+    atomicExch(overflow, 1u);
+    return;
+  }
+  for (uint32_t a = i + 1; a < end; ++a) {  // insertion sort, stable on (z, e)
+    const uint32_t e = perm[a];
+    const unsigned long long z = zkeys[e];
+    uint32_t b = a;
+    while (b > i) {
+      const uint32_t pe = perm[b - 1];
+      const unsigned long long pz = zkeys[pe];
+      if (pz < z || (pz == z && pe < e)) break;
+      perm[b] = pe;
+      --b;
+    }
+    perm[b] = e;
+  }
 }
 
 // ------------------------------------------------------------------ K3
@@ -550,6 +607,16 @@ __device__ __forceinline__ double sign_of(uint32_t code) {
   return code == 1u ? 1.0 : (code == 2u ? -1.0 : 0.0);
 }
 
+// 1/x for x in [1e-3, 1]: fp32 seed + two Newton steps (full fp64 accuracy,
+// a fraction of the IEEE division's cost; gradients carry a 1e-3 bar)
+__device__ __forceinline__ double fast_rcp(double x) {
+  double r = (double)__frcp_rn((float)x);
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+
 __device__ __forceinline__ void red_add_v4(float* addr, float a, float b, float c, float d) {
   asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(addr), "f"(a), "f"(b),
                "f"(c), "f"(d)
@@ -632,7 +699,7 @@ k_backward(const uint2* __restrict__ ranges, const uint32_t* __restrict__ lists,
       const double aw = SG_MUL(op, w);
       const bool clamped = aw > SGAD_ALPHA_MAX;
       const double a = clamped ? SGAD_ALPHA_MAX : aw;
-      const double iom = 1.0 / (1.0 - a);
+      const double iom = fast_rcp(1.0 - a);
       const double tb = T * iom;
       const double at = a * tb;
       const double c0 = s.rgb[0][j], c1 = s.rgb[1][j], c2 = s.rgb[2][j];
@@ -714,6 +781,11 @@ __global__ void k_chain_exact(const Record* __restrict__ rec, const double* __re
   out[3 * hw + p] += rg[0];
   out[4 * hw + p] += rg[1];
   out[5 * hw + p] += rg[2];
+}
+
+__global__ void k_iota(uint32_t* __restrict__ v, uint32_t n) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) v[i] = i;
 }
 
 __global__ void k_rank_of(const uint32_t* __restrict__ perm, uint32_t n, uint32_t* __restrict__ rank) {
@@ -803,7 +875,7 @@ int sgad_raster_destroy(sgad_raster* h) {
                     &h->keys1, &h->vals0, &h->vals1, &h->pcount, &h->poffset, &h->pkeys0,
                     &h->pkeys1, &h->pvals0, &h->pvals1, &h->ranges, &h->cub_tmp,
                     &h->trans_final, &h->last_idx, &h->signs, &h->raw_grads, &h->rank_of,
-                    &h->scratch, &h->col64};
+                    &h->scratch, &h->col64, &h->zrange, &h->k32a, &h->k32b};
   for (DevBuf* b : bufs) b->release();
   if (h->pinned) cudaFreeHost(h->pinned);
   delete h;
@@ -863,13 +935,19 @@ int sgad_raster_prepare(sgad_raster* h, const sgad_frame* frames, int32_t n_fram
                                   cudaMemcpyHostToDevice, st));
   SGAD_CHECK_CUDA(cudaMemsetAsync(h->status.p, 0, sizeof(uint32_t) * n_tiles_proj, st));
   SGAD_CHECK_CUDA(cudaMemsetAsync(h->counters.p, 0, sizeof(uint32_t) * 8, st));
+  SGAD_CHECK_CUDA(h->zrange.ensure(sizeof(unsigned long long) * 2));
+  SGAD_CHECK_CUDA(cudaMemsetAsync(h->zrange.p, 0xff, sizeof(unsigned long long), st));
+  SGAD_CHECK_CUDA(cudaMemsetAsync(h->zrange.as<unsigned long long>() + 1, 0, sizeof(unsigned long long), st));
   k_project<<<(unsigned)n_tiles_proj, PROJ_THREADS, 0, st>>>(
       h->frames.as<sgad_frame>(), n_frames, *cam, (uint32_t)n_total, h->ntx, h->nty, want_coef,
       h->records.as<Record>(), h->coef.as<ChainCoef>(), h->any_f64 ? h->col64.as<double>() : nullptr,
       h->keys0.as<unsigned long long>(),
-      h->vals0.as<uint32_t>(), h->status.as<uint32_t>(), h->counters.as<uint32_t>());
+      h->vals0.as<uint32_t>(), h->status.as<uint32_t>(), h->counters.as<uint32_t>(),
+      h->zrange.as<unsigned long long>());
   SGAD_LAUNCH_CHECK();
   SGAD_CHECK_CUDA(cudaMemcpyAsync(h->pinned, h->counters.as<uint32_t>() + 1, sizeof(uint32_t),
+                                  cudaMemcpyDeviceToHost, st));
+  SGAD_CHECK_CUDA(cudaMemcpyAsync(h->pinned + 4, h->zrange.p, 2 * sizeof(unsigned long long),
                                   cudaMemcpyDeviceToHost, st));
   SGAD_CHECK_CUDA(cudaStreamSynchronize(st));
   const uint32_t ns = h->pinned[0];
@@ -881,22 +959,38 @@ int sgad_raster_prepare(sgad_raster* h, const sgad_frame* frames, int32_t n_fram
     h->prepared = 1;
     return SGAD_OK;
   }
-  // K2: stable LSD radix sort of the fp64 depth bits (z > 0, so bit 63 is 0);
-  // ties keep emission = (frame, pixel) order, matching np.lexsort.
-  cub::DoubleBuffer<unsigned long long> dk(h->keys0.as<unsigned long long>(),
-                                           h->keys1.as<unsigned long long>());
-  cub::DoubleBuffer<uint32_t> dv(h->vals0.as<uint32_t>(), h->vals1.as<uint32_t>());
-  size_t tmp = 0;
-  SGAD_CHECK_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, dk, dv, (int)ns, 0, 63, st));
-  SGAD_CHECK_CUDA(h->cub_tmp.ensure(tmp));
-  SGAD_CHECK_CUDA(cub::DeviceRadixSort::SortPairs(h->cub_tmp.p, tmp, dk, dv, (int)ns, 0, 63, st));
-  uint32_t* perm = dv.Current();
-  // keep the permutation in vals0 for later kernels
-  if (perm != h->vals0.as<uint32_t>()) {
-    SGAD_CHECK_CUDA(cudaMemcpyAsync(h->vals0.p, perm, sizeof(uint32_t) * ns,
-                                    cudaMemcpyDeviceToDevice, st));
-    perm = h->vals0.as<uint32_t>();
+  // K2: depth order.  Stable sort of 32-bit monotone depth buckets, then the
+  // (rare, short) runs of equal buckets are ordered by exact (z, emission
+  // index) -- together the (z, frame, pixel) order of np.lexsort.
+  uint32_t* perm = h->vals0.as<uint32_t>();
+  {
+    unsigned long long zb[2];
+    memcpy(zb, h->pinned + 4, sizeof zb);
+    double zmin, zmax;
+    memcpy(&zmin, &zb[0], 8);
+    memcpy(&zmax, &zb[1], 8);
+    const double scale = zmax > zmin ? 4294967295.0 / (zmax - zmin) : 0.0;
+    SGAD_CHECK_CUDA(h->k32a.ensure(sizeof(uint32_t) * ns));
+    SGAD_CHECK_CUDA(h->k32b.ensure(sizeof(uint32_t) * ns));
+    k_depth_key32<<<blocks_for(ns, 256), 256, 0, st>>>(h->keys0.as<unsigned long long>(), ns, zmin,
+                                                       scale, h->k32a.as<uint32_t>(),
+                                                       h->vals1.as<uint32_t>());
+    SGAD_LAUNCH_CHECK();
+    cub::DoubleBuffer<uint32_t> dk(h->k32a.as<uint32_t>(), h->k32b.as<uint32_t>());
+    cub::DoubleBuffer<uint32_t> dv(h->vals1.as<uint32_t>(), h->vals0.as<uint32_t>());
+    size_t tmp = 0;
+    SGAD_CHECK_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, dk, dv, (int)ns, 0, 32, st));
+    SGAD_CHECK_CUDA(h->cub_tmp.ensure(tmp));
+    SGAD_CHECK_CUDA(cub::DeviceRadixSort::SortPairs(h->cub_tmp.p, tmp, dk, dv, (int)ns, 0, 32, st));
+    if (dv.Current() != perm)
+      SGAD_CHECK_CUDA(cudaMemcpyAsync(perm, dv.Current(), sizeof(uint32_t) * ns,
+                                      cudaMemcpyDeviceToDevice, st));
+    k_depth_fixup<<<blocks_for(ns, 256), 256, 0, st>>>(dk.Current(), ns,
+                                                       h->keys0.as<unsigned long long>(), perm,
+                                                       h->counters.as<uint32_t>() + 2);
+    SGAD_LAUNCH_CHECK();
   }
+  size_t tmp = 0;
   // K3: per-survivor tile counts in depth order, exclusive scan, emit, stable tile sort
   SGAD_CHECK_CUDA(h->pcount.ensure(sizeof(uint32_t) * (ns + 1)));
   SGAD_CHECK_CUDA(h->poffset.ensure(sizeof(uint32_t) * (ns + 1)));
@@ -912,7 +1006,37 @@ int sgad_raster_prepare(sgad_raster* h, const sgad_frame* frames, int32_t n_fram
                                                 h->poffset.as<uint32_t>(), (int)ns + 1, st));
   SGAD_CHECK_CUDA(cudaMemcpyAsync(h->pinned + 1, h->poffset.as<uint32_t>() + ns, sizeof(uint32_t),
                                   cudaMemcpyDeviceToHost, st));
+  SGAD_CHECK_CUDA(cudaMemcpyAsync(h->pinned + 2, h->counters.as<uint32_t>() + 2, sizeof(uint32_t),
+                                  cudaMemcpyDeviceToHost, st));
   SGAD_CHECK_CUDA(cudaStreamSynchronize(st));
+  if (h->pinned[2]) {
+    // a long run of equal depth buckets (e.g. a fronto-parallel plane seen
+    // head-on): fall back to the stable sort of the full 63-bit depth key
+    k_iota<<<blocks_for(ns, 256), 256, 0, st>>>(h->vals1.as<uint32_t>(), ns);
+    SGAD_LAUNCH_CHECK();
+    cub::DoubleBuffer<unsigned long long> dk(h->keys0.as<unsigned long long>(),
+                                             h->keys1.as<unsigned long long>());
+    cub::DoubleBuffer<uint32_t> dv(h->vals1.as<uint32_t>(), h->vals0.as<uint32_t>());
+    tmp = 0;
+    SGAD_CHECK_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, dk, dv, (int)ns, 0, 63, st));
+    SGAD_CHECK_CUDA(h->cub_tmp.ensure(tmp));
+    SGAD_CHECK_CUDA(cub::DeviceRadixSort::SortPairs(h->cub_tmp.p, tmp, dk, dv, (int)ns, 0, 63, st));
+    if (dv.Current() != perm)
+      SGAD_CHECK_CUDA(cudaMemcpyAsync(perm, dv.Current(), sizeof(uint32_t) * ns,
+                                      cudaMemcpyDeviceToDevice, st));
+    k_tile_count<<<blocks_for(ns, 256), 256, 0, st>>>(perm, h->records.as<Record>(), ns,
+                                                      h->pcount.as<uint32_t>());
+    SGAD_LAUNCH_CHECK();
+    tmp = 0;
+    SGAD_CHECK_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, h->pcount.as<uint32_t>(),
+                                                  h->poffset.as<uint32_t>(), (int)ns + 1, st));
+    SGAD_CHECK_CUDA(h->cub_tmp.ensure(tmp));
+    SGAD_CHECK_CUDA(cub::DeviceScan::ExclusiveSum(h->cub_tmp.p, tmp, h->pcount.as<uint32_t>(),
+                                                  h->poffset.as<uint32_t>(), (int)ns + 1, st));
+    SGAD_CHECK_CUDA(cudaMemcpyAsync(h->pinned + 1, h->poffset.as<uint32_t>() + ns,
+                                    sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+    SGAD_CHECK_CUDA(cudaStreamSynchronize(st));
+  }
   const uint32_t np_ = h->pinned[1];
   h->n_pairs = np_;
   *n_pairs = np_;
