@@ -205,16 +205,20 @@ def run_ours(args):
 
     # kernel timing hooks on the launching stream (torch current stream)
     stream = torch.cuda.current_stream()
-    ev = {"fwd": [], "bwd": []}
+    ev = {"fwd": [], "bwd": [], "prep": []}
     orig = wm.render_view_grads
 
     def timed_view(v, record=[False]):
         r = wm.raster
+        p0 = torch.cuda.Event(enable_timing=True)
+        p0.record(stream)
         ns, npairs = r.prepare(wm._frames[v], wm.cam, want_coef=True)
         wm.last_counts[v] = (ns, npairs)
         if ns:
             e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
             e0.record(stream)
+            if timed_view.on:
+                ev["prep"].append((p0, e0, ns, npairs))
             r.forward(target=wm._target(v))
             e1.record(stream)
             r.backward_fused(wm.grad)
@@ -274,6 +278,8 @@ def run_ours(args):
                 "traffic": None, "launch_ms": dom[1] / dom[3],
                 "bytes_per_launch": dom[2] / dom[3],
                 "forward_ms_per_view": f_ms / max(f_n, 1), "backward_ms_per_view": b_ms / max(b_n, 1),
+                "prepare_ms_per_view": sum(a.elapsed_time(b) for a, b, _, _ in ev["prep"]) /
+                max(len(ev["prep"]), 1),
                 "mean_survivors_per_view": mean_ns, "mean_pairs_per_view": mean_np}
 
     # e2e through the public API with host buffers (params + targets up, params down)

@@ -28,10 +28,11 @@ struct __align__(16) Record {
 };
 static_assert(sizeof(Record) == 64, "record must be one 64-byte line");
 
-struct ChainCoef {  // fused backward: d(param)/d(image-space quantity), fp32
+struct __align__(16) ChainCoef {  // fused backward: d(param)/d(image quantity), fp32
   float k_r;        // d sigma -> radius: fx / z
   float a_u, a_v, a_z, a_s;  // delta <- (u0, v0, z, sigma)
   float k_op;       // opacity -> logit: op (1 - op)
+  float pad_[2];    // one 32-byte sector per Gaussian
 };
 
 constexpr uint32_t GID_LEARN = 0x80000000u;
@@ -121,18 +122,11 @@ __global__ void __launch_bounds__(PROJ_THREADS)
 k_project(const sgad_frame* __restrict__ frames, int n_frames, sgad_camera cam, uint32_t n_total,
           int ntx, int nty, int want_coef, Record* __restrict__ rec, ChainCoef* __restrict__ coef,
           double* __restrict__ col64,
-          unsigned long long* __restrict__ keys, uint32_t* __restrict__ vals,
-          uint32_t* __restrict__ status, uint32_t* __restrict__ counters,
+          unsigned long long* __restrict__ keys, uint32_t* __restrict__ counters,
           unsigned long long* __restrict__ zrange) {
-  typedef cub::BlockScan<uint32_t, PROJ_THREADS> Scan;
   typedef cub::BlockReduce<unsigned long long, PROJ_THREADS> Red;
-  __shared__ typename Scan::TempStorage scan_tmp;
   __shared__ typename Red::TempStorage red_tmp;
-  __shared__ uint32_t s_tile, s_prefix;
-  if (threadIdx.x == 0) s_tile = atomicAdd(&counters[0], 1u);
-  __syncthreads();
-  const int tile = (int)s_tile;
-  const uint32_t gid = (uint32_t)tile * PROJ_THREADS + threadIdx.x;
+  const uint32_t gid = blockIdx.x * PROJ_THREADS + threadIdx.x;
 
   bool keep = false;
   Record r;
@@ -190,41 +184,27 @@ k_project(const sgad_frame* __restrict__ frames, int n_frames, sgad_camera cam, 
   const unsigned long long zmax = Red(red_tmp).Reduce(zk, cub::Max());
   __syncthreads();
   const unsigned long long zmin = Red(red_tmp).Reduce(keep ? zk : ~0ull, cub::Min());
+  __syncthreads();
+  const uint32_t cnt = (uint32_t)__syncthreads_count(keep);
   if (threadIdx.x == 0) {
     if (zmin != ~0ull) atomicMin(zrange, zmin);
     if (zmax) atomicMax(zrange + 1, zmax);
+    if (cnt) atomicAdd(&counters[1], cnt);
   }
-  uint32_t rank, agg;
-  Scan(scan_tmp).ExclusiveSum(keep ? 1u : 0u, rank, agg);
-  if (threadIdx.x == 0) {
-    if (tile == 0) {
-      st_volatile_u32(status, LB_FLAG_P | agg);
-      s_prefix = 0;
-    } else {
-      st_volatile_u32(status + tile, LB_FLAG_A | agg);
+  // records stay at their Gaussian id (emission order); culled ids get the
+  // sentinel depth key and sort behind every survivor
+  if (gid < n_total) {
+    keys[gid] = keep ? zk : ~0ull;
+    if (keep) {
+      rec[gid] = r;
+      if (want_coef) coef[gid] = c;
+      if (col64) {
+        col64[3 * (size_t)gid] = c64[0];
+        col64[3 * (size_t)gid + 1] = c64[1];
+        col64[3 * (size_t)gid + 2] = c64[2];
+      }
     }
   }
-  if (tile > 0 && threadIdx.x < 32) {
-    const uint32_t excl = lookback_exclusive(status, tile);
-    if (threadIdx.x == 0) {
-      st_volatile_u32(status + tile, LB_FLAG_P | (excl + agg));
-      s_prefix = excl;
-    }
-  }
-  __syncthreads();
-  const uint32_t slot = s_prefix + rank;
-  if (keep) {
-    rec[slot] = r;
-    if (want_coef) coef[slot] = c;
-    if (col64) {
-      col64[3 * slot] = c64[0];
-      col64[3 * slot + 1] = c64[1];
-      col64[3 * slot + 2] = c64[2];
-    }
-    keys[slot] = (unsigned long long)__double_as_longlong(r.z);
-    vals[slot] = slot;
-  }
-  if (threadIdx.x == 0 && (uint32_t)(tile + 1) * PROJ_THREADS >= n_total) counters[1] = s_prefix + agg;
 }
 
 // ------------------------------------------------------------------ K2
@@ -236,9 +216,13 @@ __global__ void k_depth_key32(const unsigned long long* __restrict__ zkeys, uint
                               uint32_t* __restrict__ vals) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  const double z = __longlong_as_double((long long)zkeys[i]);
-  const double b = floor((z - zmin) * scale);
-  k32[i] = b >= 4294967295.0 ? 0xFFFFFFFFu : (uint32_t)b;
+  const unsigned long long zk = zkeys[i];
+  if (zk == ~0ull) {
+    k32[i] = 0xFFFFFFFFu;  // culled: behind every survivor
+  } else {
+    const double b = floor((__longlong_as_double((long long)zk) - zmin) * scale);
+    k32[i] = b >= 4294967294.0 ? 0xFFFFFFFEu : (uint32_t)b;
+  }
   vals[i] = i;
 }
 
@@ -249,6 +233,7 @@ __global__ void k_depth_fixup(const uint32_t* __restrict__ k32, uint32_t n,
                               uint32_t* __restrict__ perm, uint32_t* __restrict__ overflow) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i + 1 >= n) return;
+  if (k32[i] == 0xFFFFFFFFu) return;  // the culled tail
   if (k32[i + 1] != k32[i] || (i > 0 && k32[i - 1] == k32[i])) return;  // not a run head
   uint32_t end = i + 2;
   while (end < n && k32[end] == k32[i] && end - i <= 64) ++end;
@@ -748,10 +733,12 @@ k_backward(const uint2* __restrict__ ranges, const uint32_t* __restrict__ lists,
 
 // Exact-mode chain rule (rasterizer.py:462-483) from per-survivor fp64 sums.
 __global__ void k_chain_exact(const Record* __restrict__ rec, const double* __restrict__ raw,
-                              uint32_t n_surv, const sgad_frame* __restrict__ frames, int n_frames,
+                              const uint32_t* __restrict__ perm, uint32_t n_surv,
+                              const sgad_frame* __restrict__ frames, int n_frames,
                               sgad_camera cam, double* const* __restrict__ map_grads) {
-  const uint32_t e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= n_surv) return;
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_surv) return;
+  const uint32_t e = perm[i];
   const uint32_t gidw = rec[e].gid;
   if (!(gidw & GID_LEARN)) return;
   const uint32_t gid = gidw & ~GID_LEARN;
@@ -922,7 +909,6 @@ int sgad_raster_prepare(sgad_raster* h, const sgad_frame* frames, int32_t n_fram
   }
   const int64_t n_tiles_proj = (n_total + PROJ_THREADS - 1) / PROJ_THREADS;
   SGAD_CHECK_CUDA(h->frames.ensure(sizeof(sgad_frame) * n_frames));
-  SGAD_CHECK_CUDA(h->status.ensure(sizeof(uint32_t) * n_tiles_proj));
   SGAD_CHECK_CUDA(h->counters.ensure(sizeof(uint32_t) * 8));
   SGAD_CHECK_CUDA(h->records.ensure(sizeof(Record) * n_total));
   if (want_coef) SGAD_CHECK_CUDA(h->coef.ensure(sizeof(ChainCoef) * n_total));
@@ -933,7 +919,6 @@ int sgad_raster_prepare(sgad_raster* h, const sgad_frame* frames, int32_t n_fram
   SGAD_CHECK_CUDA(h->vals1.ensure(sizeof(uint32_t) * n_total));
   SGAD_CHECK_CUDA(cudaMemcpyAsync(h->frames.p, frames, sizeof(sgad_frame) * n_frames,
                                   cudaMemcpyHostToDevice, st));
-  SGAD_CHECK_CUDA(cudaMemsetAsync(h->status.p, 0, sizeof(uint32_t) * n_tiles_proj, st));
   SGAD_CHECK_CUDA(cudaMemsetAsync(h->counters.p, 0, sizeof(uint32_t) * 8, st));
   SGAD_CHECK_CUDA(h->zrange.ensure(sizeof(unsigned long long) * 2));
   SGAD_CHECK_CUDA(cudaMemsetAsync(h->zrange.p, 0xff, sizeof(unsigned long long), st));
@@ -941,8 +926,7 @@ int sgad_raster_prepare(sgad_raster* h, const sgad_frame* frames, int32_t n_fram
   k_project<<<(unsigned)n_tiles_proj, PROJ_THREADS, 0, st>>>(
       h->frames.as<sgad_frame>(), n_frames, *cam, (uint32_t)n_total, h->ntx, h->nty, want_coef,
       h->records.as<Record>(), h->coef.as<ChainCoef>(), h->any_f64 ? h->col64.as<double>() : nullptr,
-      h->keys0.as<unsigned long long>(),
-      h->vals0.as<uint32_t>(), h->status.as<uint32_t>(), h->counters.as<uint32_t>(),
+      h->keys0.as<unsigned long long>(), h->counters.as<uint32_t>(),
       h->zrange.as<unsigned long long>());
   SGAD_LAUNCH_CHECK();
   SGAD_CHECK_CUDA(cudaMemcpyAsync(h->pinned, h->counters.as<uint32_t>() + 1, sizeof(uint32_t),
@@ -969,19 +953,20 @@ int sgad_raster_prepare(sgad_raster* h, const sgad_frame* frames, int32_t n_fram
     double zmin, zmax;
     memcpy(&zmin, &zb[0], 8);
     memcpy(&zmax, &zb[1], 8);
-    const double scale = zmax > zmin ? 4294967295.0 / (zmax - zmin) : 0.0;
-    SGAD_CHECK_CUDA(h->k32a.ensure(sizeof(uint32_t) * ns));
-    SGAD_CHECK_CUDA(h->k32b.ensure(sizeof(uint32_t) * ns));
-    k_depth_key32<<<blocks_for(ns, 256), 256, 0, st>>>(h->keys0.as<unsigned long long>(), ns, zmin,
+    const double scale = zmax > zmin ? 4294967294.0 / (zmax - zmin) : 0.0;
+    const uint32_t nt = (uint32_t)n_total;  // culled ids carry the sentinel key
+    SGAD_CHECK_CUDA(h->k32a.ensure(sizeof(uint32_t) * nt));
+    SGAD_CHECK_CUDA(h->k32b.ensure(sizeof(uint32_t) * nt));
+    k_depth_key32<<<blocks_for(nt, 256), 256, 0, st>>>(h->keys0.as<unsigned long long>(), nt, zmin,
                                                        scale, h->k32a.as<uint32_t>(),
                                                        h->vals1.as<uint32_t>());
     SGAD_LAUNCH_CHECK();
     cub::DoubleBuffer<uint32_t> dk(h->k32a.as<uint32_t>(), h->k32b.as<uint32_t>());
     cub::DoubleBuffer<uint32_t> dv(h->vals1.as<uint32_t>(), h->vals0.as<uint32_t>());
     size_t tmp = 0;
-    SGAD_CHECK_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, dk, dv, (int)ns, 0, 32, st));
+    SGAD_CHECK_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, dk, dv, (int)nt, 0, 32, st));
     SGAD_CHECK_CUDA(h->cub_tmp.ensure(tmp));
-    SGAD_CHECK_CUDA(cub::DeviceRadixSort::SortPairs(h->cub_tmp.p, tmp, dk, dv, (int)ns, 0, 32, st));
+    SGAD_CHECK_CUDA(cub::DeviceRadixSort::SortPairs(h->cub_tmp.p, tmp, dk, dv, (int)nt, 0, 32, st));
     if (dv.Current() != perm)
       SGAD_CHECK_CUDA(cudaMemcpyAsync(perm, dv.Current(), sizeof(uint32_t) * ns,
                                       cudaMemcpyDeviceToDevice, st));
@@ -1012,15 +997,16 @@ int sgad_raster_prepare(sgad_raster* h, const sgad_frame* frames, int32_t n_fram
   if (h->pinned[2]) {
     // a long run of equal depth buckets (e.g. a fronto-parallel plane seen
     // head-on): fall back to the stable sort of the full 63-bit depth key
-    k_iota<<<blocks_for(ns, 256), 256, 0, st>>>(h->vals1.as<uint32_t>(), ns);
+    const uint32_t nt = (uint32_t)n_total;
+    k_iota<<<blocks_for(nt, 256), 256, 0, st>>>(h->vals1.as<uint32_t>(), nt);
     SGAD_LAUNCH_CHECK();
     cub::DoubleBuffer<unsigned long long> dk(h->keys0.as<unsigned long long>(),
                                              h->keys1.as<unsigned long long>());
     cub::DoubleBuffer<uint32_t> dv(h->vals1.as<uint32_t>(), h->vals0.as<uint32_t>());
     tmp = 0;
-    SGAD_CHECK_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, dk, dv, (int)ns, 0, 63, st));
+    SGAD_CHECK_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, dk, dv, (int)nt, 0, 64, st));
     SGAD_CHECK_CUDA(h->cub_tmp.ensure(tmp));
-    SGAD_CHECK_CUDA(cub::DeviceRadixSort::SortPairs(h->cub_tmp.p, tmp, dk, dv, (int)ns, 0, 63, st));
+    SGAD_CHECK_CUDA(cub::DeviceRadixSort::SortPairs(h->cub_tmp.p, tmp, dk, dv, (int)nt, 0, 64, st));
     if (dv.Current() != perm)
       SGAD_CHECK_CUDA(cudaMemcpyAsync(perm, dv.Current(), sizeof(uint32_t) * ns,
                                       cudaMemcpyDeviceToDevice, st));
@@ -1139,8 +1125,8 @@ int sgad_raster_backward(sgad_raster* h, int32_t mode, const double* g_color,
   SGAD_REQUIRE(mode == 0 && g_color && g_depth && g_alpha && map_grads,
                "exact backward needs upstream images and map_grads");
   const int n_frames = (int)h->host_frames.size();
-  SGAD_CHECK_CUDA(h->raw_grads.ensure(sizeof(double) * 8 * h->n_surv));
-  SGAD_CHECK_CUDA(cudaMemsetAsync(h->raw_grads.p, 0, sizeof(double) * 8 * h->n_surv, st));
+  SGAD_CHECK_CUDA(h->raw_grads.ensure(sizeof(double) * 8 * h->n_total));
+  SGAD_CHECK_CUDA(cudaMemsetAsync(h->raw_grads.p, 0, sizeof(double) * 8 * h->n_total, st));
   SGAD_CHECK_CUDA(h->scratch.ensure(sizeof(double*) * n_frames));
   SGAD_CHECK_CUDA(cudaMemcpyAsync(h->scratch.p, map_grads, sizeof(double*) * n_frames,
                                   cudaMemcpyHostToDevice, st));
@@ -1151,8 +1137,8 @@ int sgad_raster_backward(sgad_raster* h, int32_t mode, const double* g_color,
       nullptr, up, g_color, g_depth, g_alpha, h->raw_grads.as<double>(), nullptr);
   SGAD_LAUNCH_CHECK();
   k_chain_exact<<<blocks_for(h->n_surv, 256), 256, 0, st>>>(
-      h->records.as<Record>(), h->raw_grads.as<double>(), (uint32_t)h->n_surv,
-      h->frames.as<sgad_frame>(), n_frames, h->cam, h->scratch.as<double*>());
+      h->records.as<Record>(), h->raw_grads.as<double>(), h->vals0.as<uint32_t>(),
+      (uint32_t)h->n_surv, h->frames.as<sgad_frame>(), n_frames, h->cam, h->scratch.as<double*>());
   SGAD_LAUNCH_CHECK();
   // the pointer table is read by the kernel; keep the host copy alive until done
   SGAD_CHECK_CUDA(cudaStreamSynchronize(st));
