@@ -311,23 +311,24 @@ __device__ __forceinline__ TileGeom tile_geom(int ntx, int width, int height) {
 }
 
 // Each warp owns one 8x4 sub-tile and walks the tile's depth-ordered list on
-// its own (no block barriers: sub-tiles finish at different list positions),
-// 64 list entries (two chunks) per window:
-//   1. entry-major masks: lane j loads list entry j of a 32-entry chunk, culls
-//      it against the rectangle in fp32, and for survivors evaluates the
-//      reference test d2 > 9 s2 at all 32 pixels (fp32 outside a guard band,
-//      fp64 inside it) -> a 32-bit pixel mask M_j; entries with M_j != 0 are
-//      staged in the warp's shared-memory slots;
-//   2. a 5-round shuffle transpose turns the 32 entry masks into one bitmask
-//      per lane (= per pixel) over the window's entries;
-//   3. every lane pops its own bits in list order and composites in fp64, so
+// its own (no block barriers: sub-tiles finish at different list positions).
+//   1. entry-major exact masks: lane i loads list entry i of a 32-entry
+//      chunk, culls it against the rectangle in fp32 and, for survivors,
+//      evaluates the reference test d2 > 9 s2 at all 32 pixels (fp32 row
+//      intervals outside a guard band, fp64 inside it) -> 32-bit pixel mask;
+//   2. entries that reach at least one pixel are compacted into the warp's
+//      shared-memory window (33..64 useful entries per window), their masks
+//      gathered into slot-owner lanes with shuffles;
+//   3. two 32x32 bit transposes turn the entry masks into one 64-bit mask per
+//      lane (= per pixel) over the window;
+//   4. every lane pops its own bits in list order and composites in fp64:
 //      lanes work on different Gaussians at the same time.
 constexpr int NWARP = RASTER_THREADS / 32;
 constexpr int WIN = 64;
 
 struct WinStage {
   double u0[WIN], v0[WIN], nh[WIN], op[WIN], z[WIN], rgb[3][WIN];
-  uint32_t gid[WIN];
+  uint32_t k[WIN], gid[WIN];
 };
 
 struct BwdStage {  // backward-only per-warp slots
@@ -402,20 +403,36 @@ __device__ __forceinline__ uint32_t pixel_mask(double u0, double v0, double thr,
   return sure;
 }
 
-// One 32-entry chunk [base, base+32) clipped to [lo, hi): stage entries that
-// touch at least one pixel at slots slot0 + lane; returns this lane's bits.
-template <bool BWD>
-__device__ __forceinline__ uint32_t stage_chunk(WinStage& s, BwdStage* b,
-                                                const uint32_t* __restrict__ lists,
-                                                const Record* __restrict__ rec,
-                                                const ChainCoef* __restrict__ coef,
-                                                const double* __restrict__ col64, int64_t base,
-                                                int64_t lo, int64_t hi, double xlo, double ylo,
-                                                int lane, int slot0) {
+// position of the q-th (0-based) set bit of m (q < popc(m))
+__device__ __forceinline__ int nth_set_bit(uint32_t m, int q) {
+  int pos = 0, c;
+  c = __popc(m & 0xFFFFu);
+  if (q >= c) { q -= c; m >>= 16; pos += 16; }
+  c = __popc(m & 0xFFu);
+  if (q >= c) { q -= c; m >>= 8; pos += 8; }
+  c = __popc(m & 0xFu);
+  if (q >= c) { q -= c; m >>= 4; pos += 4; }
+  c = __popc(m & 0x3u);
+  if (q >= c) { q -= c; m >>= 2; pos += 2; }
+  if (q >= (int)(m & 1u)) pos += 1;
+  return pos;
+}
+
+// One 32-entry chunk [base, base+32) clipped to [lo, hi): entries that reach
+// at least one pixel are appended to the window at slots n, n+1, ... in
+// ascending (DESC = false) or descending (DESC = true) list order; their
+// pixel masks land in the slot-owner lanes' registers mlo/mhi.  Returns the
+// number appended (warp-uniform).
+template <bool DESC, bool BWD>
+__device__ __forceinline__ int fill_chunk(WinStage& s, BwdStage* b, const uint32_t* __restrict__ lists,
+                                          const Record* __restrict__ rec,
+                                          const ChainCoef* __restrict__ coef,
+                                          const double* __restrict__ col64, int64_t base,
+                                          int64_t lo, int64_t hi, double xlo, double ylo, int lane,
+                                          int n, uint32_t& mlo, uint32_t& mhi) {
   const int64_t k = base + lane;
-  uint32_t m = 0;
-  uint32_t e = 0;
-  double u0 = 0.0, v0 = 0.0, sig = 0.0, op = 0.0, thr = 0.0;
+  uint32_t m = 0, e = 0;
+  double u0 = 0.0, v0 = 0.0, sig = 0.0, op = 0.0;
   if (k >= lo && k < hi) {
     e = lists[k];
     load_head(rec, e, u0, v0, sig, op);
@@ -425,13 +442,13 @@ __device__ __forceinline__ uint32_t stage_chunk(WinStage& s, BwdStage* b,
     const float xl = (float)xlo, yl = (float)ylo;
     const float dx = fmaxf(fmaxf(xl - uf, uf - (xl + 7.0f)), 0.0f);
     const float dy = fmaxf(fmaxf(yl - vf, vf - (yl + 3.0f)), 0.0f);
-    if (dx * dx + dy * dy <= rr * rr) {
-      thr = SG_MUL(9.0, SG_MUL(sig, sig));
-      m = pixel_mask(u0, v0, thr, xlo, ylo);
-    }
+    if (dx * dx + dy * dy <= rr * rr) m = pixel_mask(u0, v0, SG_MUL(9.0, SG_MUL(sig, sig)), xlo, ylo);
   }
+  const uint32_t keep = __ballot_sync(0xffffffffu, m != 0);
+  const int c = __popc(keep);
   if (m) {
-    const int j = slot0 + lane;
+    const int rank = DESC ? __popc(lane == 31 ? 0u : (keep >> (lane + 1))) : __popc(keep & ((1u << lane) - 1u));
+    const int j = n + rank;
     // second half of the record: z | r, g | b, gid  (16-byte aligned loads)
     const double2* tp = reinterpret_cast<const double2*>(rec + e) + 2;
     const double2 t0 = __ldg(tp), t1 = __ldg(tp + 1);
@@ -452,22 +469,32 @@ __device__ __forceinline__ uint32_t stage_chunk(WinStage& s, BwdStage* b,
       s.rgb[1][j] = rg2.y;
       s.rgb[2][j] = bg2.x;
     }
+    s.k[j] = (uint32_t)k;
     s.gid[j] = __float_as_uint(bg2.y);
     if (BWD) {
       b->is3[j] = 1.0 / (s2 * sig);
       b->eidx[j] = e;
       if (coef) {
-        const ChainCoef cc = coef[e];
-        b->coef[0][j] = cc.k_r;
-        b->coef[1][j] = cc.a_u;
-        b->coef[2][j] = cc.a_v;
-        b->coef[3][j] = cc.a_z;
-        b->coef[4][j] = cc.a_s;
-        b->coef[5][j] = cc.k_op;
+        const float4* cp = reinterpret_cast<const float4*>(coef + e);
+        const float4 c0 = __ldg(cp), c1 = __ldg(cp + 1);
+        b->coef[0][j] = c0.x;
+        b->coef[1][j] = c0.y;
+        b->coef[2][j] = c0.z;
+        b->coef[3][j] = c0.w;
+        b->coef[4][j] = c1.x;
+        b->coef[5][j] = c1.y;
       }
     }
   }
-  return transpose32(m, lane);
+  // slot n + q is owned by lane (n + q) & 31 (register mlo for slots < 32,
+  // mhi above); it pulls the mask of the q-th kept entry
+  const int q = (lane - n) & 31;
+  const int src = q < c ? nth_set_bit(keep, DESC ? c - 1 - q : q) : 0;
+  const uint32_t val = __shfl_sync(0xffffffffu, m, src);
+  if (q < c) {
+    if (n + q < 32) mlo = val; else mhi = val;
+  }
+  return c;
 }
 
 __device__ __forceinline__ void load_exp_table(double* tab) {
@@ -499,17 +526,19 @@ k_forward(const uint2* __restrict__ ranges, const uint32_t* __restrict__ lists,
   int cnt = 0, last = -1;
   bool done = !g.valid;
 
-  for (int64_t wb = rg.x; wb < (int64_t)rg.y; wb += WIN) {
-    if (__all_sync(0xffffffffu, done)) break;
-    const uint32_t b0 = stage_chunk<false>(s, nullptr, lists, rec, nullptr, col64, wb, rg.x, rg.y,
-                                           xlo, ylo, g.lane, 0);
-    const uint32_t b1 = stage_chunk<false>(s, nullptr, lists, rec, nullptr, col64, wb + 32, rg.x,
-                                           rg.y, xlo, ylo, g.lane, 32);
-    // pull the next window's record heads towards L1 while this one composites
-    for (int64_t q = wb + WIN + g.lane; q < min(wb + 2 * WIN, (int64_t)rg.y); q += 32)
-      asm volatile("prefetch.global.L1 [%0];" ::"l"(rec + lists[q]));
+  int64_t pos = rg.x;
+  while (pos < (int64_t)rg.y && !__all_sync(0xffffffffu, done)) {
+    int n = 0;
+    uint32_t mlo = 0, mhi = 0;
+    while (n <= 32 && pos < (int64_t)rg.y) {
+      n += fill_chunk<false, false>(s, nullptr, lists, rec, nullptr, col64, pos, rg.x, rg.y, xlo,
+                                    ylo, g.lane, n, mlo, mhi);
+      pos += 32;
+    }
     __syncwarp();
-    unsigned long long mine = done ? 0ull : ((unsigned long long)b1 << 32) | b0;
+    const unsigned long long bits = ((unsigned long long)transpose32(mhi, g.lane) << 32) |
+                                    transpose32(mlo, g.lane);
+    unsigned long long mine = done ? 0ull : bits;
     while (mine) {
       const int j = __ffsll((long long)mine) - 1;
       mine &= mine - 1;
@@ -525,7 +554,7 @@ k_forward(const uint2* __restrict__ ranges, const uint32_t* __restrict__ lists,
       D = SG_FMA(s.z[j], at, D);
       A = SG_ADD(A, at);
       ++cnt;
-      last = (int)(wb + j);
+      last = (int)s.k[j];
       T = SG_MUL(T, SG_SUB(1.0, a));
       if (T < SGAD_TRANSMITTANCE_MIN) {
         done = true;
@@ -661,22 +690,31 @@ k_backward(const uint2* __restrict__ ranges, const uint32_t* __restrict__ lists,
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) wend = max(wend, __shfl_xor_sync(0xffffffffu, wend, o));
   double sc0 = 0.0, sc1 = 0.0, sc2 = 0.0, sd = 0.0, sa = 0.0;
-  for (int64_t wt = wend; wt > (int64_t)rg.x; wt -= WIN) {
-    const int64_t wb = wt - WIN;  // window covers list positions [wb, wt)
-    const uint32_t b0 = stage_chunk<true>(s, &x, lists, rec, FUSED ? coef : nullptr, col64, wb,
-                                          rg.x, wt, xlo, ylo, g.lane, 0);
-    const uint32_t b1 = stage_chunk<true>(s, &x, lists, rec, FUSED ? coef : nullptr, col64,
-                                          wb + 32, rg.x, wt, xlo, ylo, g.lane, 32);
-    for (int64_t q = wb - WIN + g.lane; q < wb; q += 32)
-      if (q >= (int64_t)rg.x) asm volatile("prefetch.global.L1 [%0];" ::"l"(rec + lists[q]));
+  int64_t pos = wend;  // exclusive upper end of the part not yet staged
+  while (pos > (int64_t)rg.x) {
+    int n = 0;
+    uint32_t mlo = 0, mhi = 0;
+    while (n <= 32 && pos > (int64_t)rg.x) {
+      const int64_t base = pos - 32;
+      n += fill_chunk<true, true>(s, &x, lists, rec, FUSED ? coef : nullptr, col64, base, rg.x,
+                                  pos, xlo, ylo, g.lane, n, mlo, mhi);
+      pos = base;
+    }
     __syncwarp();
-    unsigned long long mine = ((unsigned long long)b1 << 32) | b0;
-    const int64_t lim = (int64_t)mylast - wb;  // bits above the lane's last contributor
-    if (lim < 0) mine = 0;
-    else if (lim < 63) mine &= (2ull << lim) - 1ull;
+    unsigned long long mine = ((unsigned long long)transpose32(mhi, g.lane) << 32) |
+                              transpose32(mlo, g.lane);
+    // slots run in descending list order: drop the leading slots above this
+    // lane's last contributor (binary search on the staged positions)
+    int lo_s = 0, hi_s = n;
+    while (lo_s < hi_s) {
+      const int mid = (lo_s + hi_s) >> 1;
+      if ((int)s.k[mid] > mylast) lo_s = mid + 1; else hi_s = mid;
+    }
+    if (lo_s >= 64) mine = 0;
+    else mine &= ~((1ull << lo_s) - 1ull);
     while (mine) {
-      const int j = 63 - __clzll((long long)mine);
-      mine &= ~(1ull << j);
+      const int j = __ffsll((long long)mine) - 1;
+      mine &= mine - 1;
       const double dx = SG_SUB(s.u0[j], pxd), dy = SG_SUB(s.v0[j], pyd);
       const double d2 = SG_ADD(SG_MUL(dx, dx), SG_MUL(dy, dy));
       const double nh = s.nh[j], op = s.op[j], z = s.z[j];
