@@ -423,19 +423,39 @@ __device__ __forceinline__ int nth_set_bit(uint32_t m, int q) {
 // ascending (DESC = false) or descending (DESC = true) list order; their
 // pixel masks land in the slot-owner lanes' registers mlo/mhi.  Returns the
 // number appended (warp-uniform).
+struct Head {  // one lane's list entry of a chunk, loaded one chunk ahead
+  int64_t k;
+  uint32_t e;
+  bool valid;
+  double u0, v0, sig, op;
+};
+
+__device__ __forceinline__ Head load_entry(const uint32_t* __restrict__ lists,
+                                           const Record* __restrict__ rec, int64_t base,
+                                           int64_t lo, int64_t hi, int lane) {
+  Head h;
+  h.k = base + lane;
+  h.valid = h.k >= lo && h.k < hi;
+  h.e = 0;
+  h.u0 = h.v0 = h.sig = h.op = 0.0;
+  if (h.valid) {
+    h.e = lists[h.k];
+    load_head(rec, h.e, h.u0, h.v0, h.sig, h.op);
+  }
+  return h;
+}
+
 template <bool DESC, bool BWD>
-__device__ __forceinline__ int fill_chunk(WinStage& s, BwdStage* b, const uint32_t* __restrict__ lists,
+__device__ __forceinline__ int fill_chunk(WinStage& s, BwdStage* b, const Head& hd,
                                           const Record* __restrict__ rec,
                                           const ChainCoef* __restrict__ coef,
-                                          const double* __restrict__ col64, int64_t base,
-                                          int64_t lo, int64_t hi, double xlo, double ylo, int lane,
-                                          int n, uint32_t& mlo, uint32_t& mhi) {
-  const int64_t k = base + lane;
-  uint32_t m = 0, e = 0;
-  double u0 = 0.0, v0 = 0.0, sig = 0.0, op = 0.0;
-  if (k >= lo && k < hi) {
-    e = lists[k];
-    load_head(rec, e, u0, v0, sig, op);
+                                          const double* __restrict__ col64, double xlo, double ylo,
+                                          int lane, int n, uint32_t& mlo, uint32_t& mhi) {
+  const int64_t k = hd.k;
+  const uint32_t e = hd.e;
+  const double u0 = hd.u0, v0 = hd.v0, sig = hd.sig, op = hd.op;
+  uint32_t m = 0;
+  if (hd.valid) {
     // cheap conservative cull of the whole rectangle first
     const float uf = (float)u0, vf = (float)v0;
     const float rr = (float)(3.0 * sig) * 1.0001f + 0.01f;
@@ -527,12 +547,15 @@ k_forward(const uint2* __restrict__ ranges, const uint32_t* __restrict__ lists,
   bool done = !g.valid;
 
   int64_t pos = rg.x;
+  Head nx = load_entry(lists, rec, pos, rg.x, rg.y, g.lane);
   while (pos < (int64_t)rg.y && !__all_sync(0xffffffffu, done)) {
     int n = 0;
     uint32_t mlo = 0, mhi = 0;
     while (n <= 32 && pos < (int64_t)rg.y) {
-      n += fill_chunk<false, false>(s, nullptr, lists, rec, nullptr, col64, pos, rg.x, rg.y, xlo,
-                                    ylo, g.lane, n, mlo, mhi);
+      const Head cur = nx;
+      nx = load_entry(lists, rec, pos + 32, rg.x, rg.y, g.lane);  // one chunk ahead
+      n += fill_chunk<false, false>(s, nullptr, cur, rec, nullptr, col64, xlo, ylo, g.lane, n,
+                                    mlo, mhi);
       pos += 32;
     }
     __syncwarp();
@@ -691,13 +714,17 @@ k_backward(const uint2* __restrict__ ranges, const uint32_t* __restrict__ lists,
   for (int o = 16; o > 0; o >>= 1) wend = max(wend, __shfl_xor_sync(0xffffffffu, wend, o));
   double sc0 = 0.0, sc1 = 0.0, sc2 = 0.0, sd = 0.0, sa = 0.0;
   int64_t pos = wend;  // exclusive upper end of the part not yet staged
+  const int64_t top = wend;
+  Head nx = load_entry(lists, rec, pos - 32, rg.x, top, g.lane);
   while (pos > (int64_t)rg.x) {
     int n = 0;
     uint32_t mlo = 0, mhi = 0;
     while (n <= 32 && pos > (int64_t)rg.x) {
       const int64_t base = pos - 32;
-      n += fill_chunk<true, true>(s, &x, lists, rec, FUSED ? coef : nullptr, col64, base, rg.x,
-                                  pos, xlo, ylo, g.lane, n, mlo, mhi);
+      const Head cur = nx;
+      nx = load_entry(lists, rec, base - 32, rg.x, top, g.lane);  // one chunk ahead
+      n += fill_chunk<true, true>(s, &x, cur, rec, FUSED ? coef : nullptr, col64, xlo, ylo,
+                                  g.lane, n, mlo, mhi);
       pos = base;
     }
     __syncwarp();
