@@ -517,15 +517,16 @@ __device__ __forceinline__ int fill_chunk(WinStage& s, BwdStage* b, const Head& 
   return c;
 }
 
+__device__ const double kExp2Table[32] = {SGAD_EXP2_TABLE};
+
 __device__ __forceinline__ void load_exp_table(double* tab) {
-  const double t[32] = {SGAD_EXP2_TABLE};
-  if (threadIdx.x < 32) tab[threadIdx.x] = t[threadIdx.x];
+  if (threadIdx.x < 32) tab[threadIdx.x] = kExp2Table[threadIdx.x];
   __syncthreads();
 }
 
 // ------------------------------------------------------------------ K4
 template <bool IMAGES, bool STATE, bool LOSS>
-__global__ void __launch_bounds__(RASTER_THREADS)
+__global__ void __launch_bounds__(RASTER_THREADS, 3)
 k_forward(const uint2* __restrict__ ranges, const uint32_t* __restrict__ lists,
           const Record* __restrict__ rec, const double* __restrict__ col64, int ntx, int width,
           int height, double* __restrict__ out_color, double* __restrict__ out_depth,
