@@ -14,7 +14,8 @@ import threading
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsgad.so")
+# SGAD_LIB overrides the library path (A/B experiments with alternative builds)
+LIB_PATH = os.environ.get("SGAD_LIB") or os.path.join(_HERE, "libsgad.so")
 
 SGAD_OK = 0
 _ERRORS = {-1: ValueError, -2: RuntimeError, -3: MemoryError, -4: RuntimeError}

@@ -526,7 +526,7 @@ __device__ __forceinline__ void load_exp_table(double* tab) {
 
 // ------------------------------------------------------------------ K4
 template <bool IMAGES, bool STATE, bool LOSS>
-__global__ void __launch_bounds__(RASTER_THREADS, 3)
+__global__ void __launch_bounds__(RASTER_THREADS)
 k_forward(const uint2* __restrict__ ranges, const uint32_t* __restrict__ lists,
           const Record* __restrict__ rec, const double* __restrict__ col64, int ntx, int width,
           int height, double* __restrict__ out_color, double* __restrict__ out_depth,
@@ -715,15 +715,14 @@ k_backward(const uint2* __restrict__ ranges, const uint32_t* __restrict__ lists,
   for (int o = 16; o > 0; o >>= 1) wend = max(wend, __shfl_xor_sync(0xffffffffu, wend, o));
   double sc0 = 0.0, sc1 = 0.0, sc2 = 0.0, sd = 0.0, sa = 0.0;
   int64_t pos = wend;  // exclusive upper end of the part not yet staged
-  const int64_t top = wend;
-  Head nx = load_entry(lists, rec, pos - 32, rg.x, top, g.lane);
   while (pos > (int64_t)rg.x) {
     int n = 0;
     uint32_t mlo = 0, mhi = 0;
     while (n <= 32 && pos > (int64_t)rg.x) {
       const int64_t base = pos - 32;
-      const Head cur = nx;
-      nx = load_entry(lists, rec, base - 32, rg.x, top, g.lane);  // one chunk ahead
+      // (no load-ahead here: the backward is register-bound, extra live
+      // registers cost more occupancy than the latency they hide)
+      const Head cur = load_entry(lists, rec, base, rg.x, pos, g.lane);
       n += fill_chunk<true, true>(s, &x, cur, rec, FUSED ? coef : nullptr, col64, xlo, ylo,
                                   g.lane, n, mlo, mhi);
       pos = base;
