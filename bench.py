@@ -273,9 +273,16 @@ def run_ours(args):
     counts = list(wm.last_counts.values())
     mean_ns = float(np.mean([c[0] for c in counts])) if counts else 0.0
     mean_np = float(np.mean([c[1] for c in counts])) if counts else 0.0
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            traffic = json.load(f)["dram_bytes_per_launch"].get(dom[0])
+    except Exception:
+        pass
     roofline = {"bound": "hbm", "kernel": dom[0], "achieved": achieved, "peak": peak,
                 "peak_source": peak_kind, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": None, "launch_ms": dom[1] / dom[3],
+                "traffic": traffic, "traffic_source": "profiles/traffic.json (ncu --set full)",
+                "launch_ms": dom[1] / dom[3],
                 "bytes_per_launch": dom[2] / dom[3],
                 "forward_ms_per_view": f_ms / max(f_n, 1), "backward_ms_per_view": b_ms / max(b_n, 1),
                 "prepare_ms_per_view": sum(a.elapsed_time(b) for a, b, _, _ in ev["prep"]) /
