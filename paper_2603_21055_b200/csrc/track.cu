@@ -332,11 +332,14 @@ k_track_fit(FitArgs a, double* __restrict__ centers, double* __restrict__ cov,
 // point density (surfaces: ~3 points per occupied cell).  A query searches
 // Chebyshev rings of cells around its (clamped) cell, pruning cells whose box
 // is farther than the best distance so far, and stops when no unvisited cell
-// can hold a closer point.  Queries still unresolved after MAX_RINGS rings
+// can hold a closer point.  A query not settled within MAX_RINGS rings moves
+// to the next, 4x coarser grid level (keeping its best candidate); queries
+// still unresolved after the coarsest level (far from every surface)
 // (far from every surface) fall back to an exact block-parallel scan, so the
 // result is always the exact Euclidean nearest neighbour (ties -> lower index),
 // as scipy cKDTree gives the reference (tracker.py:125-128).
-constexpr int MAX_RINGS = 4;
+constexpr int MAX_RINGS = 2;
+constexpr int NLEV = 4;
 constexpr unsigned long long HASH_EMPTY = ~0ull;
 
 __device__ __forceinline__ unsigned long long dkey(double x) {
@@ -426,17 +429,21 @@ __global__ void k_cell_table(const unsigned long long* __restrict__ keys, int64_
   if (i == n - 1) start[head_scan[i]] = (uint32_t)n;
 }
 
-struct GridView {
+struct LevelView {
   Grid g;
   const unsigned long long* hkeys;
   const uint32_t* hvals;
   const uint32_t* start;
   const uint32_t* items;
+};
+
+struct GridView {
+  LevelView lv[NLEV];
   const double* pts;
   int64_t n;
 };
 
-__device__ __forceinline__ int hash_find(const GridView& v, unsigned long long k) {
+__device__ __forceinline__ int hash_find(const LevelView& v, unsigned long long k) {
   unsigned long long s = hash64(k) & v.g.hmask;
   while (true) {
     const unsigned long long hk = v.hkeys[s];
@@ -446,13 +453,13 @@ __device__ __forceinline__ int hash_find(const GridView& v, unsigned long long k
   }
 }
 
-// Bounded ring search; returns false if MAX_RINGS rings did not settle it.
-__device__ bool grid_nearest(const GridView& v, const double* q, int64_t& best_j, double& best_d2) {
+// Bounded ring search on one level, refining (best_j, best_d2); returns
+// false if MAX_RINGS rings did not settle it.
+__device__ bool grid_nearest(const LevelView& v, const double* pts, const double* q,
+                             int64_t& best_j, double& best_d2) {
   const Grid& g = v.g;
   int c0[3];
   for (int k = 0; k < 3; ++k) c0[k] = cell_coord(q[k], g.lo[k], g.h, g.dim[k]);
-  best_j = -1;
-  best_d2 = INFINITY;
   for (int r = 0; r <= MAX_RINGS; ++r) {
     const int x0 = max(c0[0] - r, 0), x1 = min(c0[0] + r, g.dim[0] - 1);
     const int y0 = max(c0[1] - r, 0), y1 = min(c0[1] + r, g.dim[1] - 1);
@@ -473,8 +480,8 @@ __device__ bool grid_nearest(const GridView& v, const double* q, int64_t& best_j
           if (c < 0) continue;
           for (uint32_t t = v.start[c]; t < v.start[c + 1]; ++t) {
             const uint32_t j = v.items[t];
-            const double dx = q[0] - v.pts[3 * j], dy = q[1] - v.pts[3 * j + 1],
-                         dz = q[2] - v.pts[3 * j + 2];
+            const double dx = q[0] - pts[3 * j], dy = q[1] - pts[3 * j + 1],
+                         dz = q[2] - pts[3 * j + 2];
             const double d2 = dx * dx + dy * dy + dz * dz;
             if (d2 < best_d2 || (d2 == best_d2 && (int64_t)j < best_j)) {
               best_d2 = d2;
@@ -536,14 +543,16 @@ __global__ void k_nearest(GridView v, NNArgs a) {
   if (i >= a.m) return;
   double q[3];
   query_point(a, i, q);
-  int64_t j;
-  double d2;
-  if (grid_nearest(v, q, j, d2)) {
-    a.idx[i] = j;
-    a.d2[i] = d2;
-  } else {
-    a.unresolved[atomicAdd(a.n_unres, 1u)] = (uint32_t)i;
+  int64_t j = -1;
+  double d2 = INFINITY;
+  for (int l = 0; l < NLEV; ++l) {
+    if (grid_nearest(v.lv[l], v.pts, q, j, d2)) {
+      a.idx[i] = j;
+      a.d2[i] = d2;
+      return;
+    }
   }
+  a.unresolved[atomicAdd(a.n_unres, 1u)] = (uint32_t)i;
 }
 
 // Exact fallback: one block per unresolved query scans every centre.
@@ -779,7 +788,8 @@ struct sgad_geomset {
   sgad::DevBuf pts, cov, nrm, bbox, keys0, keys1, idx0, idx1, head, headscan, start, hkeys, hvals,
       cub_tmp;
   sgad::DevBuf w, b, acc, partial, poses, nn_j, nn_d2, unres, counter;
-  sgad::Grid grid{};
+  sgad::Grid grid[sgad::NLEV]{};
+  sgad::DevBuf lhkeys[sgad::NLEV], lhvals[sgad::NLEV], lstart[sgad::NLEV], litems[sgad::NLEV];
   int64_t n = 0;
   unsigned long long* pinned = nullptr;
 };
@@ -842,6 +852,12 @@ int sgad_geomset_destroy(sgad_geomset* g) {
                     &g->cub_tmp, &g->w, &g->b, &g->acc, &g->partial, &g->poses, &g->nn_j,
                     &g->nn_d2, &g->unres, &g->counter};
   for (DevBuf* b : bufs) b->release();
+  for (int l = 0; l < NLEV; ++l) {
+    g->lhkeys[l].release();
+    g->lhvals[l].release();
+    g->lstart[l].release();
+    g->litems[l].release();
+  }
   if (g->pinned) cudaFreeHost(g->pinned);
   delete g;
   return SGAD_OK;
@@ -949,31 +965,42 @@ int sgad_geomset_set(sgad_geomset* g, const double* centers, const double* cov,
     rc = grid_sort(g, gr, st, &n_cells, &ks, &is);
     if (rc) return rc;
   }
-  unsigned long long hsize = 1024;
-  while (hsize < 2ull * (unsigned long long)n_cells) hsize <<= 1;
-  gr.hmask = hsize - 1;
-  g->grid = gr;
-  SGAD_CHECK_CUDA(g->start.ensure(sizeof(uint32_t) * (n_cells + 1)));
-  SGAD_CHECK_CUDA(g->hkeys.ensure(sizeof(unsigned long long) * hsize));
-  SGAD_CHECK_CUDA(g->hvals.ensure(sizeof(uint32_t) * hsize));
-  SGAD_CHECK_CUDA(cudaMemsetAsync(g->hkeys.p, 0xff, sizeof(unsigned long long) * hsize, st));
-  k_cell_table<<<nblk(n, 256), 256, 0, st>>>(ks, n, g->headscan.as<uint32_t>(), g->start.as<uint32_t>(),
-                                             g->hkeys.as<unsigned long long>(), g->hvals.as<uint32_t>(),
-                                             gr.hmask);
-  SGAD_LAUNCH_CHECK();
-  // keep the sorted point order (items) in idx0
-  if (is != g->idx0.as<uint32_t>())
-    SGAD_CHECK_CUDA(cudaMemcpyAsync(g->idx0.p, is, sizeof(uint32_t) * n, cudaMemcpyDeviceToDevice, st));
+  // level l uses cells 4^l times larger; each level is an exact hash grid
+  for (int l = 0; l < NLEV; ++l) {
+    if (l > 0) {
+      grid_dims(gr, ext, gr.h * 4.0);
+      rc = grid_sort(g, gr, st, &n_cells, &ks, &is);
+      if (rc) return rc;
+    }
+    unsigned long long hsize = 1024;
+    while (hsize < 2ull * (unsigned long long)n_cells) hsize <<= 1;
+    gr.hmask = hsize - 1;
+    g->grid[l] = gr;
+    SGAD_CHECK_CUDA(g->lstart[l].ensure(sizeof(uint32_t) * (n_cells + 1)));
+    SGAD_CHECK_CUDA(g->lhkeys[l].ensure(sizeof(unsigned long long) * hsize));
+    SGAD_CHECK_CUDA(g->lhvals[l].ensure(sizeof(uint32_t) * hsize));
+    SGAD_CHECK_CUDA(g->litems[l].ensure(sizeof(uint32_t) * n));
+    SGAD_CHECK_CUDA(cudaMemsetAsync(g->lhkeys[l].p, 0xff, sizeof(unsigned long long) * hsize, st));
+    k_cell_table<<<nblk(n, 256), 256, 0, st>>>(ks, n, g->headscan.as<uint32_t>(),
+                                               g->lstart[l].as<uint32_t>(),
+                                               g->lhkeys[l].as<unsigned long long>(),
+                                               g->lhvals[l].as<uint32_t>(), gr.hmask);
+    SGAD_LAUNCH_CHECK();
+    SGAD_CHECK_CUDA(cudaMemcpyAsync(g->litems[l].p, is, sizeof(uint32_t) * n,
+                                    cudaMemcpyDeviceToDevice, st));
+  }
   return SGAD_OK;
 }
 
 static GridView view_of(sgad_geomset* g) {
   GridView v;
-  v.g = g->grid;
-  v.hkeys = g->hkeys.as<unsigned long long>();
-  v.hvals = g->hvals.as<uint32_t>();
-  v.start = g->start.as<uint32_t>();
-  v.items = g->idx0.as<uint32_t>();
+  for (int l = 0; l < NLEV; ++l) {
+    v.lv[l].g = g->grid[l];
+    v.lv[l].hkeys = g->lhkeys[l].as<unsigned long long>();
+    v.lv[l].hvals = g->lhvals[l].as<uint32_t>();
+    v.lv[l].start = g->lstart[l].as<uint32_t>();
+    v.lv[l].items = g->litems[l].as<uint32_t>();
+  }
   v.pts = g->pts.as<double>();
   v.n = g->n;
   return v;
