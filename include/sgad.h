@@ -166,12 +166,14 @@ int sgad_geomset_nearest(sgad_geomset* g, const double* queries, int64_t m, int6
 /* One GICP linearisation (tracker.py:286-321) at pose (rot row-major, trans).
  * local: centers [m,3], cov [m,6] in the local camera frame.
  * metric_mode 0 point2surf, 1 point2point; gate `dist_max`.
+ * warm_start != 0 seeds the exact nearest-neighbour search with the previous
+ * call's neighbours (same local set; the result is still the exact 1-NN).
  * out (device double[29]): H upper triangle (21, row-major), g (6), cost, inliers.
  * The frozen weights W (6 per correspondence, 0 for rejected) and the matched
  * target centres are kept in the geomset for sgad_track_cost. */
 int sgad_track_normal_eqs(sgad_geomset* g, const double* local_centers, const double* local_cov,
                           int64_t m, const double* rot, const double* trans, int32_t metric_mode,
-                          double dist_max, double* out, void* stream);
+                          double dist_max, int32_t warm_start, double* out, void* stream);
 
 /* Copy the per-correspondence acceptance flags of the last
  * sgad_track_normal_eqs call (device uint8 [m]). */

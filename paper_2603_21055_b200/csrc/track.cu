@@ -515,6 +515,7 @@ __device__ bool grid_nearest(const LevelView& v, const double* pts, const double
 struct NNArgs {
   const double* queries;  // [m, 3]
   int64_t m;
+  int warm;               // idx[] holds a previous nearest neighbour per query
   int transform;          // apply pose P to the queries first
   double r[9], t[3];
   int64_t* idx;
@@ -545,7 +546,17 @@ __global__ void k_nearest(GridView v, NNArgs a) {
   query_point(a, i, q);
   int64_t j = -1;
   double d2 = INFINITY;
-  for (int l = 0; l < NLEV; ++l) {
+  int l0 = 0;
+  if (a.warm) {
+    // warm start from the previous iteration's neighbour: its distance bounds
+    // the answer, so start at the finest level whose ring reach covers it
+    j = a.idx[i];
+    const double dx = q[0] - v.pts[3 * j], dy = q[1] - v.pts[3 * j + 1], dz = q[2] - v.pts[3 * j + 2];
+    d2 = dx * dx + dy * dy + dz * dz;
+    const double reach = sqrt(d2);
+    while (l0 < NLEV - 1 && MAX_RINGS * v.lv[l0].g.h < reach) ++l0;
+  }
+  for (int l = l0; l < NLEV; ++l) {
     if (grid_nearest(v.lv[l], v.pts, q, j, d2)) {
       a.idx[i] = j;
       a.d2[i] = d2;
@@ -791,6 +802,7 @@ struct sgad_geomset {
   sgad::Grid grid[sgad::NLEV]{};
   sgad::DevBuf lhkeys[sgad::NLEV], lhvals[sgad::NLEV], lstart[sgad::NLEV], litems[sgad::NLEV];
   int64_t n = 0;
+  int64_t nn_m = -1;  // queries whose neighbours nn_j holds (warm start)
   unsigned long long* pinned = nullptr;
 };
 
@@ -912,6 +924,7 @@ int sgad_geomset_set(sgad_geomset* g, const double* centers, const double* cov,
   SGAD_REQUIRE(n < (1ll << 31), "sgad_geomset_set: too many points");
   cudaStream_t st = (cudaStream_t)stream_;
   g->n = n;
+  g->nn_m = -1;
   SGAD_CHECK_CUDA(g->pts.ensure(sizeof(double) * 3 * n));
   SGAD_CHECK_CUDA(g->cov.ensure(sizeof(double) * 6 * n));
   SGAD_CHECK_CUDA(g->nrm.ensure(sizeof(double) * 3 * n));
@@ -1008,13 +1021,14 @@ static GridView view_of(sgad_geomset* g) {
 
 // exact 1-NN for m queries (optionally transformed by rot/trans) into idx/d2
 static int run_nearest(sgad_geomset* g, const double* queries, int64_t m, const double* rot,
-                       const double* trans, int64_t* idx, double* d2, cudaStream_t st) {
+                       const double* trans, int64_t* idx, double* d2, int warm, cudaStream_t st) {
   SGAD_CHECK_CUDA(g->unres.ensure(sizeof(uint32_t) * m));
   SGAD_CHECK_CUDA(g->counter.ensure(sizeof(uint32_t) * 4));
   SGAD_CHECK_CUDA(cudaMemsetAsync(g->counter.p, 0, sizeof(uint32_t), st));
   NNArgs a;
   a.queries = queries;
   a.m = m;
+  a.warm = warm;
   a.transform = rot != nullptr;
   for (int k = 0; k < 9; ++k) a.r[k] = rot ? rot[k] : 0.0;
   for (int k = 0; k < 3; ++k) a.t[k] = trans ? trans[k] : 0.0;
@@ -1037,7 +1051,7 @@ int sgad_geomset_nearest(sgad_geomset* g, const double* queries, int64_t m, int6
   if (m == 0) return SGAD_OK;
   cudaStream_t st = (cudaStream_t)stream_;
   SGAD_CHECK_CUDA(g->nn_d2.ensure(sizeof(double) * m));
-  int rc = run_nearest(g, queries, m, nullptr, nullptr, idx, g->nn_d2.as<double>(), st);
+  int rc = run_nearest(g, queries, m, nullptr, nullptr, idx, g->nn_d2.as<double>(), 0, st);
   if (rc) return rc;
   if (dist) {
     k_sqrt<<<nblk(m, 256), 256, 0, st>>>(g->nn_d2.as<double>(), m, dist);
@@ -1048,7 +1062,7 @@ int sgad_geomset_nearest(sgad_geomset* g, const double* queries, int64_t m, int6
 
 int sgad_track_normal_eqs(sgad_geomset* g, const double* local_centers, const double* local_cov,
                           int64_t m, const double* rot, const double* trans, int32_t metric_mode,
-                          double dist_max, double* out, void* stream_) {
+                          double dist_max, int32_t warm_start, double* out, void* stream_) {
   SGAD_REQUIRE(g && g->n > 0, "global set is empty");
   SGAD_REQUIRE(local_centers && local_cov && rot && trans && out && m > 0,
                "sgad_track_normal_eqs: bad arguments");
@@ -1058,9 +1072,12 @@ int sgad_track_normal_eqs(sgad_geomset* g, const double* local_centers, const do
   SGAD_CHECK_CUDA(g->b.ensure(sizeof(double) * 3 * m));
   SGAD_CHECK_CUDA(g->acc.ensure(m));
   SGAD_CHECK_CUDA(g->partial.ensure(sizeof(double) * NE_VALS * nb));
+  const bool warm = warm_start && g->nn_m == m && g->nn_j.cap >= sizeof(int64_t) * m;
   SGAD_CHECK_CUDA(g->nn_j.ensure(sizeof(int64_t) * m));
   SGAD_CHECK_CUDA(g->nn_d2.ensure(sizeof(double) * m));
-  int rc = run_nearest(g, local_centers, m, rot, trans, g->nn_j.as<int64_t>(), g->nn_d2.as<double>(), st);
+  g->nn_m = m;
+  int rc = run_nearest(g, local_centers, m, rot, trans, g->nn_j.as<int64_t>(), g->nn_d2.as<double>(),
+                       warm ? 1 : 0, st);
   if (rc) return rc;
   PoseArg P;
   for (int k = 0; k < 9; ++k) P.r[k] = rot[k];

@@ -297,6 +297,7 @@ class GicpSolver:
         self.costs = torch.empty(8, dtype=torch.float64, device=local.centers.device)
         self.host = torch.empty(29 + 8, dtype=torch.float64).pin_memory()
         self.metric = METRIC_MODES.index(cfg.metric_mode)
+        self._warm = 0
 
     def linearize(self, pose: Pose):
         """K8 at ``pose``: returns (H 6x6, g 6, cost, inliers)."""
@@ -304,7 +305,9 @@ class GicpSolver:
         tr = (ctypes.c_double * 3)(*np.asarray(pose.translation, dtype=np.float64).reshape(3))
         N.call("sgad_track_normal_eqs", self.g._h, self.local.centers.data_ptr(),
                self.local.cov6.data_ptr(), self.m, rot, tr, self.metric,
-               float(self.cfg.correspondence_dist_max), self.out.data_ptr(), N.stream_ptr())
+               float(self.cfg.correspondence_dist_max), self._warm, self.out.data_ptr(),
+               N.stream_ptr())
+        self._warm = 1  # later iterations seed the exact NN search with these neighbours
         h = self.host[:29]
         h.copy_(self.out)  # synchronising copy into pinned memory
         v = h.numpy()
