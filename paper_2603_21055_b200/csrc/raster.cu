@@ -13,6 +13,7 @@
 // indices in depth order.  Per-view scratch is owned by the sgad_raster handle.
 #include <cub/cub.cuh>
 #include <stdarg.h>
+#include <stddef.h>
 #include <algorithm>
 #include <vector>
 
@@ -22,11 +23,19 @@ namespace sgad {
 
 struct __align__(16) Record {
   double u0, v0, sigma, opacity, z;
+  double nh;             // -0.5 / sigma^2 (the compositing exponent scale)
   float r, g, b;
   uint32_t gid;          // bit 31: learnable
+};
+
+struct TileBox {         // inclusive tile bbox of a survivor (rasterizer.py:187-199)
   uint16_t tx0, tx1, ty0, ty1;
 };
 static_assert(sizeof(Record) == 64, "record must be one 64-byte line");
+// K4/K5 read the record as four 16-byte vectors: (u0, v0) (sigma, opacity) (z, nh) (r, g, b, gid)
+static_assert(offsetof(Record, sigma) == 16 && offsetof(Record, z) == 32 &&
+              offsetof(Record, nh) == 40 && offsetof(Record, r) == 48 && offsetof(Record, gid) == 60,
+              "record field offsets");
 
 struct __align__(16) ChainCoef {  // fused backward: d(param)/d(image quantity), fp32
   float k_r;        // d sigma -> radius: fx / z
@@ -44,7 +53,7 @@ constexpr int RASTER_THREADS = 256;
 struct sgad_raster {
   sgad::DevBuf frames, status, counters, records, coef, keys0, keys1, vals0, vals1;
   sgad::DevBuf pcount, poffset, pkeys0, pkeys1, pvals0, pvals1, ranges, cub_tmp;
-  sgad::DevBuf trans_final, last_idx, signs, raw_grads, rank_of, scratch, col64, zrange, k32a, k32b;
+  sgad::DevBuf trans_final, last_idx, signs, raw_grads, rank_of, scratch, col64, zrange, k32a, k32b, bbox;
   int any_f64 = 0;
   std::vector<sgad_frame> host_frames;
   sgad_camera cam{};
@@ -120,7 +129,8 @@ __device__ __forceinline__ bool project_point(const sgad_frame& f, int64_t p, in
 
 __global__ void __launch_bounds__(PROJ_THREADS)
 k_project(const sgad_frame* __restrict__ frames, int n_frames, sgad_camera cam, uint32_t n_total,
-          int ntx, int nty, int want_coef, Record* __restrict__ rec, ChainCoef* __restrict__ coef,
+          int ntx, int nty, int want_coef, Record* __restrict__ rec, TileBox* __restrict__ box,
+          ChainCoef* __restrict__ coef,
           double* __restrict__ col64,
           unsigned long long* __restrict__ keys, uint32_t* __restrict__ counters,
           unsigned long long* __restrict__ zrange) {
@@ -130,6 +140,7 @@ k_project(const sgad_frame* __restrict__ frames, int n_frames, sgad_camera cam, 
 
   bool keep = false;
   Record r;
+  TileBox bx;
   ChainCoef c;
   double c64[3];
   if (gid < n_total) {
@@ -143,6 +154,7 @@ k_project(const sgad_frame* __restrict__ frames, int n_frames, sgad_camera cam, 
       r.v0 = o.v0;
       r.sigma = o.sig;
       r.opacity = o.op;
+      r.nh = SG_DIV(-0.5, SG_MUL(o.sig, o.sig));
       r.z = o.z;
       r.r = (float)plane_ld(f, 4 * hw + p);
       r.g = (float)plane_ld(f, 5 * hw + p);
@@ -162,10 +174,10 @@ k_project(const sgad_frame* __restrict__ frames, int n_frames, sgad_camera cam, 
       y0 = y0 < 0 ? 0 : y0;
       x1 = x1 > ntx - 1 ? ntx - 1 : x1;
       y1 = y1 > nty - 1 ? nty - 1 : y1;
-      r.tx0 = (uint16_t)x0;
-      r.tx1 = (uint16_t)x1;
-      r.ty0 = (uint16_t)y0;
-      r.ty1 = (uint16_t)y1;
+      bx.tx0 = (uint16_t)x0;
+      bx.tx1 = (uint16_t)x1;
+      bx.ty0 = (uint16_t)y0;
+      bx.ty1 = (uint16_t)y1;
       if (want_coef) {
         const double sgn = o.bd >= 0.0 ? 1.0 : -1.0;
         const double iz = 1.0 / o.z;
@@ -197,6 +209,7 @@ k_project(const sgad_frame* __restrict__ frames, int n_frames, sgad_camera cam, 
     keys[gid] = keep ? zk : ~0ull;
     if (keep) {
       rec[gid] = r;
+      box[gid] = bx;
       if (want_coef) coef[gid] = c;
       if (col64) {
         col64[3 * (size_t)gid] = c64[0];
@@ -257,21 +270,21 @@ __global__ void k_depth_fixup(const uint32_t* __restrict__ k32, uint32_t n,
 }
 
 // ------------------------------------------------------------------ K3
-__global__ void k_tile_count(const uint32_t* __restrict__ perm, const Record* __restrict__ rec,
+__global__ void k_tile_count(const uint32_t* __restrict__ perm, const TileBox* __restrict__ box,
                              uint32_t n, uint32_t* __restrict__ cnt) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  const Record& r = rec[perm[i]];
+  const TileBox r = box[perm[i]];
   cnt[i] = (uint32_t)(r.tx1 - r.tx0 + 1) * (uint32_t)(r.ty1 - r.ty0 + 1);
 }
 
-__global__ void k_tile_emit(const uint32_t* __restrict__ perm, const Record* __restrict__ rec,
+__global__ void k_tile_emit(const uint32_t* __restrict__ perm, const TileBox* __restrict__ box,
                             const uint32_t* __restrict__ off, uint32_t n, int ntx,
                             uint32_t* __restrict__ pkeys, uint32_t* __restrict__ pvals) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const uint32_t e = perm[i];
-  const Record& r = rec[e];
+  const TileBox r = box[e];
   uint32_t o = off[i];
   for (int ty = r.ty0; ty <= r.ty1; ++ty)
     for (int tx = r.tx0; tx <= r.tx1; ++tx) {
@@ -316,36 +329,29 @@ __device__ __forceinline__ TileGeom tile_geom(int ntx, int width, int height) {
 //      chunk, culls it against the rectangle in fp32 and, for survivors,
 //      evaluates the reference test d2 > 9 s2 at all 32 pixels (fp32 row
 //      intervals outside a guard band, fp64 inside it) -> 32-bit pixel mask;
-//   2. entries that reach at least one pixel are compacted into the warp's
-//      shared-memory window (33..64 useful entries per window), their masks
+//   2. entries that reach at least one pixel are compacted into a window of
+//      33..64 slots (record index + list position per slot), their masks
 //      gathered into slot-owner lanes with shuffles;
 //   3. two 32x32 bit transposes turn the entry masks into one 64-bit mask per
 //      lane (= per pixel) over the window;
-//   4. every lane pops its own bits in list order and composites in fp64:
-//      lanes work on different Gaussians at the same time.
+//   4. every lane pops its own bits in list order and composites in fp64,
+//      reading the entry's record through L1.
+// Windows live in a per-warp ring of RING slots and every lane consumes them
+// at its own pace.  Depth order sweeps across a surface, so a pixel's
+// contributors arrive in bursts that differ from lane to lane; with one
+// window at a time the warp paid every window's busiest lane (8 of 32 lanes
+// busy at C4), with a ring deep enough to hold a sub-tile's whole sweep the
+// lanes stay busy (K4).  A window is staged when a lane has run dry
+// and the slot it needs is no longer read by any lane.
 constexpr int NWARP = RASTER_THREADS / 32;
 constexpr int WIN = 64;
+constexpr int RING = 12;
 
-struct WinStage {
-  double u0[WIN], v0[WIN], nh[WIN], op[WIN], z[WIN], rgb[3][WIN];
-  uint32_t k[WIN], gid[WIN];
+struct WarpRing {
+  uint32_t e[RING][WIN];                  // record index of each slot
+  int32_t k[RING][WIN];                   // list position of each slot
+  unsigned long long mask[RING][32];      // per-lane bits over the slots
 };
-
-struct BwdStage {  // backward-only per-warp slots
-  double is3[WIN];  // 1 / (s2 sigma)
-  uint32_t eidx[WIN];
-  float coef[6][WIN];
-};
-
-__device__ __forceinline__ void load_head(const Record* rec, uint32_t e, double& u0, double& v0,
-                                          double& sig, double& op) {
-  const double2* hp = reinterpret_cast<const double2*>(rec + e);  // u0, v0 | sigma, opacity
-  const double2 a = __ldg(hp), b = __ldg(hp + 1);
-  u0 = a.x;
-  v0 = a.y;
-  sig = b.x;
-  op = b.y;
-}
 
 // 32x32 bit transpose across the warp: lane i holds row i on entry, column i
 // on exit.
@@ -418,11 +424,6 @@ __device__ __forceinline__ int nth_set_bit(uint32_t m, int q) {
   return pos;
 }
 
-// One 32-entry chunk [base, base+32) clipped to [lo, hi): entries that reach
-// at least one pixel are appended to the window at slots n, n+1, ... in
-// ascending (DESC = false) or descending (DESC = true) list order; their
-// pixel masks land in the slot-owner lanes' registers mlo/mhi.  Returns the
-// number appended (warp-uniform).
 struct Head {  // one lane's list entry of a chunk, loaded one chunk ahead
   int64_t k;
   uint32_t e;
@@ -439,72 +440,43 @@ __device__ __forceinline__ Head load_entry(const uint32_t* __restrict__ lists,
   h.e = 0;
   h.u0 = h.v0 = h.sig = h.op = 0.0;
   if (h.valid) {
-    h.e = lists[h.k];
-    load_head(rec, h.e, h.u0, h.v0, h.sig, h.op);
+    h.e = __ldg(lists + h.k);
+    const double2* hp = reinterpret_cast<const double2*>(rec + h.e);  // u0, v0 | sigma, op
+    const double2 a = __ldg(hp), b = __ldg(hp + 1);
+    h.u0 = a.x;
+    h.v0 = a.y;
+    h.sig = b.x;
+    h.op = b.y;
   }
   return h;
 }
 
-template <bool DESC, bool BWD>
-__device__ __forceinline__ int fill_chunk(WinStage& s, BwdStage* b, const Head& hd,
-                                          const Record* __restrict__ rec,
-                                          const ChainCoef* __restrict__ coef,
-                                          const double* __restrict__ col64, double xlo, double ylo,
-                                          int lane, int n, uint32_t& mlo, uint32_t& mhi) {
-  const int64_t k = hd.k;
-  const uint32_t e = hd.e;
-  const double u0 = hd.u0, v0 = hd.v0, sig = hd.sig, op = hd.op;
+// One 32-entry chunk: entries that reach at least one pixel are appended to
+// window slots n, n+1, ... in ascending (DESC = false) or descending (DESC =
+// true) list order; their pixel masks land in the slot-owner lanes' registers
+// mlo/mhi.  Returns the number appended (warp-uniform).
+template <bool DESC>
+__device__ __forceinline__ int fill_chunk(uint32_t* __restrict__ se, int32_t* __restrict__ sk,
+                                          const Head& hd, double xlo, double ylo, int lane, int n,
+                                          uint32_t& mlo, uint32_t& mhi) {
   uint32_t m = 0;
   if (hd.valid) {
     // cheap conservative cull of the whole rectangle first
-    const float uf = (float)u0, vf = (float)v0;
-    const float rr = (float)(3.0 * sig) * 1.0001f + 0.01f;
+    const float uf = (float)hd.u0, vf = (float)hd.v0;
+    const float rr = (float)(3.0 * hd.sig) * 1.0001f + 0.01f;
     const float xl = (float)xlo, yl = (float)ylo;
     const float dx = fmaxf(fmaxf(xl - uf, uf - (xl + 7.0f)), 0.0f);
     const float dy = fmaxf(fmaxf(yl - vf, vf - (yl + 3.0f)), 0.0f);
-    if (dx * dx + dy * dy <= rr * rr) m = pixel_mask(u0, v0, SG_MUL(9.0, SG_MUL(sig, sig)), xlo, ylo);
+    if (dx * dx + dy * dy <= rr * rr)
+      m = pixel_mask(hd.u0, hd.v0, SG_MUL(9.0, SG_MUL(hd.sig, hd.sig)), xlo, ylo);
   }
   const uint32_t keep = __ballot_sync(0xffffffffu, m != 0);
   const int c = __popc(keep);
   if (m) {
-    const int rank = DESC ? __popc(lane == 31 ? 0u : (keep >> (lane + 1))) : __popc(keep & ((1u << lane) - 1u));
-    const int j = n + rank;
-    // second half of the record: z | r, g | b, gid  (16-byte aligned loads)
-    const double2* tp = reinterpret_cast<const double2*>(rec + e) + 2;
-    const double2 t0 = __ldg(tp), t1 = __ldg(tp + 1);
-    const float2 rg2 = *reinterpret_cast<const float2*>(&t0.y);
-    const float2 bg2 = *reinterpret_cast<const float2*>(&t1.x);
-    const double s2 = SG_MUL(sig, sig);
-    s.u0[j] = u0;
-    s.v0[j] = v0;
-    s.nh[j] = SG_DIV(-0.5, s2);
-    s.op[j] = op;
-    s.z[j] = t0.x;
-    if (col64) {  // fp64 drop-in maps keep exact fp64 colours
-      s.rgb[0][j] = col64[3 * (size_t)e];
-      s.rgb[1][j] = col64[3 * (size_t)e + 1];
-      s.rgb[2][j] = col64[3 * (size_t)e + 2];
-    } else {
-      s.rgb[0][j] = rg2.x;
-      s.rgb[1][j] = rg2.y;
-      s.rgb[2][j] = bg2.x;
-    }
-    s.k[j] = (uint32_t)k;
-    s.gid[j] = __float_as_uint(bg2.y);
-    if (BWD) {
-      b->is3[j] = 1.0 / (s2 * sig);
-      b->eidx[j] = e;
-      if (coef) {
-        const float4* cp = reinterpret_cast<const float4*>(coef + e);
-        const float4 c0 = __ldg(cp), c1 = __ldg(cp + 1);
-        b->coef[0][j] = c0.x;
-        b->coef[1][j] = c0.y;
-        b->coef[2][j] = c0.z;
-        b->coef[3][j] = c0.w;
-        b->coef[4][j] = c1.x;
-        b->coef[5][j] = c1.y;
-      }
-    }
+    const int rank = DESC ? __popc(lane == 31 ? 0u : (keep >> (lane + 1)))
+                          : __popc(keep & ((1u << lane) - 1u));
+    se[n + rank] = hd.e;
+    sk[n + rank] = (int32_t)hd.k;
   }
   // slot n + q is owned by lane (n + q) & 31 (register mlo for slots < 32,
   // mhi above); it pulls the mask of the q-th kept entry
@@ -517,11 +489,142 @@ __device__ __forceinline__ int fill_chunk(WinStage& s, BwdStage* b, const Head& 
   return c;
 }
 
+// ---- forward: window-synchronous, entry data staged in shared memory ----
+// The forward's per-contribution work is light, so it keeps one window at a
+// time with the entries' fields in shared memory (short-latency loads); the
+// backward's heavy contributions pay for the ring below (K4/K5).
+struct FwdStage {
+  double u0[WIN], v0[WIN], nh[WIN], op[WIN], z[WIN], rgb[3][WIN];
+  int32_t k[WIN];
+};
+
+__device__ __forceinline__ int fill_chunk_fwd(FwdStage& s, const Head& hd,
+                                              const Record* __restrict__ rec,
+                                              const double* __restrict__ col64, double xlo,
+                                              double ylo, int lane, int n, uint32_t& mlo,
+                                              uint32_t& mhi) {
+  uint32_t m = 0;
+  if (hd.valid) {
+    const float uf = (float)hd.u0, vf = (float)hd.v0;
+    const float rr = (float)(3.0 * hd.sig) * 1.0001f + 0.01f;
+    const float xl = (float)xlo, yl = (float)ylo;
+    const float dx = fmaxf(fmaxf(xl - uf, uf - (xl + 7.0f)), 0.0f);
+    const float dy = fmaxf(fmaxf(yl - vf, vf - (yl + 3.0f)), 0.0f);
+    if (dx * dx + dy * dy <= rr * rr)
+      m = pixel_mask(hd.u0, hd.v0, SG_MUL(9.0, SG_MUL(hd.sig, hd.sig)), xlo, ylo);
+  }
+  const uint32_t keep = __ballot_sync(0xffffffffu, m != 0);
+  const int c = __popc(keep);
+  if (m) {
+    const int j = n + __popc(keep & ((1u << lane) - 1u));
+    const double2* rp = reinterpret_cast<const double2*>(rec + hd.e);
+    const double2 zn = __ldg(rp + 2);                                        // z, nh
+    const float4 cg = __ldg(reinterpret_cast<const float4*>(rp + 3));        // r, g, b, gid
+    s.u0[j] = hd.u0;
+    s.v0[j] = hd.v0;
+    s.nh[j] = zn.y;
+    s.op[j] = hd.op;
+    s.z[j] = zn.x;
+    if (col64) {  // fp64 drop-in maps keep exact fp64 colours
+      s.rgb[0][j] = __ldg(col64 + 3 * (size_t)hd.e);
+      s.rgb[1][j] = __ldg(col64 + 3 * (size_t)hd.e + 1);
+      s.rgb[2][j] = __ldg(col64 + 3 * (size_t)hd.e + 2);
+    } else {
+      s.rgb[0][j] = cg.x;
+      s.rgb[1][j] = cg.y;
+      s.rgb[2][j] = cg.z;
+    }
+    s.k[j] = (int32_t)hd.k;
+  }
+  const int q = (lane - n) & 31;
+  const int src = q < c ? nth_set_bit(keep, q) : 0;
+  const uint32_t val = __shfl_sync(0xffffffffu, m, src);
+  if (q < c) {
+    if (n + q < 32) mlo = val; else mhi = val;
+  }
+  return c;
+}
+
+// Stage the next window into ring slot `slot`: whole 32-entry chunks from
+// `pos` (ascending) or below `pos` (descending) until more than 32 slots are
+// used, each chunk's list entries and record heads loaded one chunk ahead.
+// Returns the per-lane 64-bit mask; pos advances.
+template <bool DESC>
+__device__ __forceinline__ unsigned long long stage_window(
+    WarpRing& rg, int slot, const uint32_t* __restrict__ lists, const Record* __restrict__ rec,
+    int64_t& pos, int64_t lo, int64_t hi, double xlo, double ylo, int lane, int& n) {
+  n = 0;
+  uint32_t mlo = 0, mhi = 0;
+  if (!DESC) {
+    Head nx = load_entry(lists, rec, pos, lo, hi, lane);
+    while (n <= 32 && pos < hi) {
+      const Head hc = nx;
+      nx = load_entry(lists, rec, pos + 32, lo, hi, lane);
+      n += fill_chunk<false>(rg.e[slot], rg.k[slot], hc, xlo, ylo, lane, n, mlo, mhi);
+      pos += 32;
+    }
+  } else {
+    const int64_t top = pos;
+    Head nx = load_entry(lists, rec, pos - 32, lo, top, lane);
+    while (n <= 32 && pos > lo) {
+      const Head hc = nx;
+      nx = load_entry(lists, rec, pos - 64, lo, top, lane);
+      n += fill_chunk<true>(rg.e[slot], rg.k[slot], hc, xlo, ylo, lane, n, mlo, mhi);
+      pos -= 32;
+    }
+    if (pos < lo) pos = lo;
+  }
+  __syncwarp();
+  return ((unsigned long long)transpose32(mhi, lane) << 32) | transpose32(mlo, lane);
+}
+
+// One contribution's record fields, loaded a step ahead of their use.
+struct Contrib {
+  double u0, v0, sig, op, z, nh;
+  float r, g, b;
+  uint32_t gid, e;
+  int32_t k;
+};
+
+__device__ __forceinline__ void load_contrib(Contrib& q, const WarpRing& rg, int slot, int j,
+                                             const Record* __restrict__ rec) {
+  q.e = rg.e[slot][j];
+  q.k = rg.k[slot][j];
+  const double2* rp = reinterpret_cast<const double2*>(rec + q.e);
+  const double2 uv = __ldg(rp), so = __ldg(rp + 1), zn = __ldg(rp + 2);
+  const float4 cg = __ldg(reinterpret_cast<const float4*>(rp + 3));
+  q.u0 = uv.x;
+  q.v0 = uv.y;
+  q.sig = so.x;
+  q.op = so.y;
+  q.z = zn.x;
+  q.nh = zn.y;
+  q.r = cg.x;
+  q.g = cg.y;
+  q.b = cg.z;
+  q.gid = __float_as_uint(cg.w);
+}
+
 __device__ const double kExp2Table[32] = {SGAD_EXP2_TABLE};
 
 __device__ __forceinline__ void load_exp_table(double* tab) {
   if (threadIdx.x < 32) tab[threadIdx.x] = kExp2Table[threadIdx.x];
   __syncthreads();
+}
+
+// Per-lane ring cursor: the lane's current window (cw) and its remaining bits.
+struct Cursor {
+  unsigned long long cur;
+  int cw;
+};
+
+// advance a dry lane to the next staged window that has bits for it
+__device__ __forceinline__ void advance(Cursor& c, const WarpRing& rg, int w_head, int lane,
+                                        bool done) {
+  while (!done && c.cur == 0ull && c.cw + 1 < w_head) {
+    ++c.cw;
+    c.cur = rg.mask[c.cw % RING][lane];
+  }
 }
 
 // ------------------------------------------------------------------ K4
@@ -534,11 +637,10 @@ k_forward(const uint2* __restrict__ ranges, const uint32_t* __restrict__ lists,
           double* __restrict__ t_final, int32_t* __restrict__ last_out,
           uint8_t* __restrict__ signs, sgad_loss_target tgt) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  WinStage* stage = reinterpret_cast<WinStage*>(smem_raw);
+  FwdStage& s = reinterpret_cast<FwdStage*>(smem_raw)[threadIdx.x >> 5];
   __shared__ double tab[32];
   load_exp_table(tab);
   const TileGeom g = tile_geom(ntx, width, height);
-  WinStage& s = stage[g.warp];
   const uint2 rg = ranges[g.tile];
   const double pxd = (double)g.px, pyd = (double)g.py;
   const double xlo = (double)(g.tx * SGAD_TILE + (g.warp & 1) * 8);
@@ -555,8 +657,7 @@ k_forward(const uint2* __restrict__ ranges, const uint32_t* __restrict__ lists,
     while (n <= 32 && pos < (int64_t)rg.y) {
       const Head cur = nx;
       nx = load_entry(lists, rec, pos + 32, rg.x, rg.y, g.lane);  // one chunk ahead
-      n += fill_chunk<false, false>(s, nullptr, cur, rec, nullptr, col64, xlo, ylo, g.lane, n,
-                                    mlo, mhi);
+      n += fill_chunk_fwd(s, cur, rec, col64, xlo, ylo, g.lane, n, mlo, mhi);
       pos += 32;
     }
     __syncwarp();
@@ -578,7 +679,7 @@ k_forward(const uint2* __restrict__ ranges, const uint32_t* __restrict__ lists,
       D = SG_FMA(s.z[j], at, D);
       A = SG_ADD(A, at);
       ++cnt;
-      last = (int)s.k[j];
+      last = s.k[j];
       T = SG_MUL(T, SG_SUB(1.0, a));
       if (T < SGAD_TRANSMITTANCE_MIN) {
         done = true;
@@ -645,8 +746,9 @@ __device__ __forceinline__ double sign_of(uint32_t code) {
   return code == 1u ? 1.0 : (code == 2u ? -1.0 : 0.0);
 }
 
-// 1/x for x in [1e-3, 1]: fp32 seed + two Newton steps (full fp64 accuracy,
-// a fraction of the IEEE division's cost; gradients carry a 1e-3 bar)
+// 1/x: fp32 seed + two Newton steps (full fp64 accuracy for x within the
+// fp32 range, a fraction of the IEEE division's cost; gradients carry a 1e-3
+// bar, the exact drop-in backward 1e-9)
 __device__ __forceinline__ double fast_rcp(double x) {
   double r = (double)__frcp_rn((float)x);
   double e = fma(-x, r, 1.0);
@@ -674,13 +776,10 @@ k_backward(const uint2* __restrict__ ranges, const uint32_t* __restrict__ lists,
            const double* __restrict__ g_depth, const double* __restrict__ g_alpha,
            double* __restrict__ raw, float* __restrict__ grad_accum) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  WinStage* stage = reinterpret_cast<WinStage*>(smem_raw);
-  BwdStage* bstage = reinterpret_cast<BwdStage*>(smem_raw + sizeof(WinStage) * NWARP);
+  WarpRing& ring = reinterpret_cast<WarpRing*>(smem_raw)[threadIdx.x >> 5];
   __shared__ double tab[32];
   load_exp_table(tab);
   const TileGeom g = tile_geom(ntx, width, height);
-  WinStage& s = stage[g.warp];
-  BwdStage& x = bstage[g.warp];
   const uint2 rg = ranges[g.tile];
   const double pxd = (double)g.px, pyd = (double)g.py;
   const double xlo = (double)(g.tx * SGAD_TILE + (g.warp & 1) * 8);
@@ -713,38 +812,46 @@ k_backward(const uint2* __restrict__ ranges, const uint32_t* __restrict__ lists,
   int wend = mylast + 1;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) wend = max(wend, __shfl_xor_sync(0xffffffffu, wend, o));
+  const bool done = mylast < 0;  // nothing to propagate for this pixel
   double sc0 = 0.0, sc1 = 0.0, sc2 = 0.0, sd = 0.0, sa = 0.0;
   int64_t pos = wend;  // exclusive upper end of the part not yet staged
-  while (pos > (int64_t)rg.x) {
-    int n = 0;
-    uint32_t mlo = 0, mhi = 0;
-    while (n <= 32 && pos > (int64_t)rg.x) {
-      const int64_t base = pos - 32;
-      // (no load-ahead here: the backward is register-bound, extra live
-      // registers cost more occupancy than the latency they hide)
-      const Head cur = load_entry(lists, rec, base, rg.x, pos, g.lane);
-      n += fill_chunk<true, true>(s, &x, cur, rec, FUSED ? coef : nullptr, col64, xlo, ylo,
-                                  g.lane, n, mlo, mhi);
-      pos = base;
+  Cursor c{0ull, -1};
+  int w_head = 0;
+  Contrib cc;
+  while (true) {
+    advance(c, ring, w_head, g.lane, done);
+    if (pos > (int64_t)rg.x && __any_sync(0xffffffffu, !done && c.cur == 0ull) &&
+        !__any_sync(0xffffffffu, !done && c.cw == w_head - RING)) {
+      const int slot = w_head % RING;
+      int n;
+      unsigned long long bits = stage_window<true>(ring, slot, lists, rec, pos, rg.x, pos, xlo,
+                                                   ylo, g.lane, n);
+      // slots run in descending list order: drop the leading slots above this
+      // lane's last contributor (binary search on the staged positions)
+      int lo_s = 0, hi_s = n;
+      while (lo_s < hi_s) {
+        const int mid = (lo_s + hi_s) >> 1;
+        if (ring.k[slot][mid] > mylast) lo_s = mid + 1; else hi_s = mid;
+      }
+      if (lo_s >= 64) bits = 0ull;
+      else bits &= ~((1ull << lo_s) - 1ull);
+      ring.mask[slot][g.lane] = done ? 0ull : bits;
+      __syncwarp();
+      ++w_head;
+      continue;
     }
-    __syncwarp();
-    unsigned long long mine = ((unsigned long long)transpose32(mhi, g.lane) << 32) |
-                              transpose32(mlo, g.lane);
-    // slots run in descending list order: drop the leading slots above this
-    // lane's last contributor (binary search on the staged positions)
-    int lo_s = 0, hi_s = n;
-    while (lo_s < hi_s) {
-      const int mid = (lo_s + hi_s) >> 1;
-      if ((int)s.k[mid] > mylast) lo_s = mid + 1; else hi_s = mid;
+    if (!__any_sync(0xffffffffu, c.cur != 0ull)) break;
+    if (!c.cur) continue;
+    {
+      const int j = __ffsll((long long)c.cur) - 1;
+      c.cur &= c.cur - 1;
+      load_contrib(cc, ring, c.cw % RING, j, rec);
     }
-    if (lo_s >= 64) mine = 0;
-    else mine &= ~((1ull << lo_s) - 1ull);
-    while (mine) {
-      const int j = __ffsll((long long)mine) - 1;
-      mine &= mine - 1;
-      const double dx = SG_SUB(s.u0[j], pxd), dy = SG_SUB(s.v0[j], pyd);
+    {
+      const uint32_t e = cc.e;
+      const double dx = SG_SUB(cc.u0, pxd), dy = SG_SUB(cc.v0, pyd);
       const double d2 = SG_ADD(SG_MUL(dx, dx), SG_MUL(dy, dy));
-      const double nh = s.nh[j], op = s.op[j], z = s.z[j];
+      const double nh = cc.nh, op = cc.op, z = cc.z;
       const double w = sgad_exp_neg(SG_MUL(d2, nh), tab);
       const double aw = SG_MUL(op, w);
       const bool clamped = aw > SGAD_ALPHA_MAX;
@@ -752,8 +859,13 @@ k_backward(const uint2* __restrict__ ranges, const uint32_t* __restrict__ lists,
       const double iom = fast_rcp(1.0 - a);
       const double tb = T * iom;
       const double at = a * tb;
-      const double c0 = s.rgb[0][j], c1 = s.rgb[1][j], c2 = s.rgb[2][j];
-      if (s.gid[j] & GID_LEARN) {
+      double c0 = cc.r, c1 = cc.g, c2 = cc.b;
+      if (col64) {
+        c0 = __ldg(col64 + 3 * (size_t)e);
+        c1 = __ldg(col64 + 3 * (size_t)e + 1);
+        c2 = __ldg(col64 + 3 * (size_t)e + 2);
+      }
+      if (cc.gid & GID_LEARN) {
         const double d_alpha = gc0 * (c0 * tb - sc0 * iom) + gc1 * (c1 * tb - sc1 * iom) +
                                gc2 * (c2 * tb - sc2 * iom) + gd * (z * tb - sd * iom) +
                                ga * (tb - sa * iom);
@@ -762,19 +874,21 @@ k_backward(const uint2* __restrict__ ranges, const uint32_t* __restrict__ lists,
         if (!clamped) {
           const double gw = d_alpha * op;
           gop = d_alpha * w;
-          gsig = gw * w * d2 * x.is3[j];  // gw w d2 / (s2 sigma)
+          // gw w d2 / (s2 sigma) = gw w d2 (-2 nh) / sigma
+          gsig = gw * w * d2 * (-2.0 * nh) * fast_rcp(cc.sig);
           const double gd2 = gw * w * nh;  // gw (-0.5 w / s2)
           gu = 2.0 * gd2 * dx;
           gv = 2.0 * gd2 * dy;
         }
         if (FUSED) {
-          float* dst = grad_accum + (size_t)(s.gid[j] & ~GID_LEARN) * 8;
-          red_add_v4(dst, (float)(x.coef[1][j] * gu + x.coef[2][j] * gv + x.coef[3][j] * gz +
-                                  x.coef[4][j] * gsig),
-                     (float)(x.coef[0][j] * gsig), (float)(x.coef[5][j] * gop), (float)gcol0);
+          const float4* cp = reinterpret_cast<const float4*>(coef + e);
+          const float4 k0 = __ldg(cp), k1 = __ldg(cp + 1);
+          float* dst = grad_accum + (size_t)(cc.gid & ~GID_LEARN) * 8;
+          red_add_v4(dst, (float)(k0.y * gu + k0.z * gv + k0.w * gz + k1.x * gsig),
+                     (float)(k0.x * gsig), (float)(k1.y * gop), (float)gcol0);
           red_add_v2(dst + 4, (float)gcol1, (float)gcol2);
         } else {
-          double* dst = raw + (size_t)x.eidx[j] * 8;
+          double* dst = raw + (size_t)e * 8;
           atomicAdd(dst + 0, gcol0);
           atomicAdd(dst + 1, gcol1);
           atomicAdd(dst + 2, gcol2);
@@ -792,7 +906,6 @@ k_backward(const uint2* __restrict__ ranges, const uint32_t* __restrict__ lists,
       sa += at;
       T = tb;
     }
-    __syncwarp();
   }
 }
 
@@ -873,8 +986,8 @@ __global__ void k_export_surv(const uint32_t* __restrict__ perm, const Record* _
   if (opacity) opacity[i] = r.opacity;
 }
 
-constexpr size_t FWD_SMEM = sizeof(WinStage) * NWARP;
-constexpr size_t BWD_SMEM = (sizeof(WinStage) + sizeof(BwdStage)) * NWARP;
+constexpr size_t FWD_SMEM = sizeof(FwdStage) * NWARP;
+constexpr size_t BWD_SMEM = sizeof(WarpRing) * NWARP;
 
 // opt in to >48 KB dynamic shared memory once per process
 static int smem_attrs() {
@@ -927,7 +1040,7 @@ int sgad_raster_destroy(sgad_raster* h) {
                     &h->keys1, &h->vals0, &h->vals1, &h->pcount, &h->poffset, &h->pkeys0,
                     &h->pkeys1, &h->pvals0, &h->pvals1, &h->ranges, &h->cub_tmp,
                     &h->trans_final, &h->last_idx, &h->signs, &h->raw_grads, &h->rank_of,
-                    &h->scratch, &h->col64, &h->zrange, &h->k32a, &h->k32b};
+                    &h->scratch, &h->col64, &h->zrange, &h->k32a, &h->k32b, &h->bbox};
   for (DevBuf* b : bufs) b->release();
   if (h->pinned) cudaFreeHost(h->pinned);
   delete h;
@@ -976,6 +1089,7 @@ int sgad_raster_prepare(sgad_raster* h, const sgad_frame* frames, int32_t n_fram
   SGAD_CHECK_CUDA(h->frames.ensure(sizeof(sgad_frame) * n_frames));
   SGAD_CHECK_CUDA(h->counters.ensure(sizeof(uint32_t) * 8));
   SGAD_CHECK_CUDA(h->records.ensure(sizeof(Record) * n_total));
+  SGAD_CHECK_CUDA(h->bbox.ensure(sizeof(TileBox) * n_total));
   if (want_coef) SGAD_CHECK_CUDA(h->coef.ensure(sizeof(ChainCoef) * n_total));
   if (h->any_f64) SGAD_CHECK_CUDA(h->col64.ensure(sizeof(double) * 3 * n_total));
   SGAD_CHECK_CUDA(h->keys0.ensure(sizeof(unsigned long long) * n_total));
@@ -990,8 +1104,8 @@ int sgad_raster_prepare(sgad_raster* h, const sgad_frame* frames, int32_t n_fram
   SGAD_CHECK_CUDA(cudaMemsetAsync(h->zrange.as<unsigned long long>() + 1, 0, sizeof(unsigned long long), st));
   k_project<<<(unsigned)n_tiles_proj, PROJ_THREADS, 0, st>>>(
       h->frames.as<sgad_frame>(), n_frames, *cam, (uint32_t)n_total, h->ntx, h->nty, want_coef,
-      h->records.as<Record>(), h->coef.as<ChainCoef>(), h->any_f64 ? h->col64.as<double>() : nullptr,
-      h->keys0.as<unsigned long long>(), h->counters.as<uint32_t>(),
+      h->records.as<Record>(), h->bbox.as<TileBox>(), h->coef.as<ChainCoef>(),
+      h->any_f64 ? h->col64.as<double>() : nullptr, h->keys0.as<unsigned long long>(), h->counters.as<uint32_t>(),
       h->zrange.as<unsigned long long>());
   SGAD_LAUNCH_CHECK();
   SGAD_CHECK_CUDA(cudaMemcpyAsync(h->pinned, h->counters.as<uint32_t>() + 1, sizeof(uint32_t),
@@ -1044,7 +1158,7 @@ int sgad_raster_prepare(sgad_raster* h, const sgad_frame* frames, int32_t n_fram
   // K3: per-survivor tile counts in depth order, exclusive scan, emit, stable tile sort
   SGAD_CHECK_CUDA(h->pcount.ensure(sizeof(uint32_t) * (ns + 1)));
   SGAD_CHECK_CUDA(h->poffset.ensure(sizeof(uint32_t) * (ns + 1)));
-  k_tile_count<<<blocks_for(ns, 256), 256, 0, st>>>(perm, h->records.as<Record>(), ns,
+  k_tile_count<<<blocks_for(ns, 256), 256, 0, st>>>(perm, h->bbox.as<TileBox>(), ns,
                                                     h->pcount.as<uint32_t>());
   SGAD_LAUNCH_CHECK();
   SGAD_CHECK_CUDA(cudaMemsetAsync(h->pcount.as<uint32_t>() + ns, 0, sizeof(uint32_t), st));
@@ -1075,7 +1189,7 @@ int sgad_raster_prepare(sgad_raster* h, const sgad_frame* frames, int32_t n_fram
     if (dv.Current() != perm)
       SGAD_CHECK_CUDA(cudaMemcpyAsync(perm, dv.Current(), sizeof(uint32_t) * ns,
                                       cudaMemcpyDeviceToDevice, st));
-    k_tile_count<<<blocks_for(ns, 256), 256, 0, st>>>(perm, h->records.as<Record>(), ns,
+    k_tile_count<<<blocks_for(ns, 256), 256, 0, st>>>(perm, h->bbox.as<TileBox>(), ns,
                                                       h->pcount.as<uint32_t>());
     SGAD_LAUNCH_CHECK();
     tmp = 0;
@@ -1095,7 +1209,7 @@ int sgad_raster_prepare(sgad_raster* h, const sgad_frame* frames, int32_t n_fram
   SGAD_CHECK_CUDA(h->pkeys1.ensure(sizeof(uint32_t) * (np_ + 1)));
   SGAD_CHECK_CUDA(h->pvals0.ensure(sizeof(uint32_t) * (np_ + 1)));
   SGAD_CHECK_CUDA(h->pvals1.ensure(sizeof(uint32_t) * (np_ + 1)));
-  k_tile_emit<<<blocks_for(ns, 256), 256, 0, st>>>(perm, h->records.as<Record>(),
+  k_tile_emit<<<blocks_for(ns, 256), 256, 0, st>>>(perm, h->bbox.as<TileBox>(),
                                                    h->poffset.as<uint32_t>(), ns, h->ntx,
                                                    h->pkeys0.as<uint32_t>(), h->pvals0.as<uint32_t>());
   SGAD_LAUNCH_CHECK();
