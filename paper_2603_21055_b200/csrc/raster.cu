@@ -96,15 +96,44 @@ struct Proj {
   double dir[3], y[3];
 };
 
+// The seven parameter planes of pixel p, loaded together up front (the loads
+// are independent, so they are all in flight before the first use).
+struct Params {
+  double base, delta, logr, logit, r, g, b;
+};
+
+__device__ __forceinline__ Params load_params(const sgad_frame& f, int64_t p, int64_t hw) {
+  Params q;
+  if (f.planes_f64) {
+    const double* P = reinterpret_cast<const double*>(f.planes) + p;
+    q.base = __ldg(P);
+    q.delta = __ldg(P + hw);
+    q.logr = __ldg(P + 2 * hw);
+    q.logit = __ldg(P + 3 * hw);
+    q.r = __ldg(P + 4 * hw);
+    q.g = __ldg(P + 5 * hw);
+    q.b = __ldg(P + 6 * hw);
+  } else {
+    const float* P = reinterpret_cast<const float*>(f.planes) + p;
+    q.base = (double)__ldg(P);
+    q.delta = (double)__ldg(P + hw);
+    q.logr = (double)__ldg(P + 2 * hw);
+    q.logit = (double)__ldg(P + 3 * hw);
+    q.r = (double)__ldg(P + 4 * hw);
+    q.g = (double)__ldg(P + 5 * hw);
+    q.b = (double)__ldg(P + 6 * hw);
+  }
+  return q;
+}
+
 // rasterizer.py:86-116 for one active pixel p of frame f; true if it survives
 // the near-plane and on-screen culls.  Operation order matches the reference.
-__device__ __forceinline__ bool project_point(const sgad_frame& f, int64_t p, int64_t hw,
+__device__ __forceinline__ bool project_point(const sgad_frame& f, int64_t p, const Params& q,
                                               const sgad_camera& cam, Proj& o) {
   const double xx = (double)(p % f.width), yy = (double)(p / f.width);
-  const double base = plane_ld(f, p), delta = plane_ld(f, hw + p), logr = plane_ld(f, 2 * hw + p);
   const double r0 = SG_DIV(SG_SUB(xx, f.cx), f.fx);
   const double r1 = SG_DIV(SG_SUB(yy, f.cy), f.fy);
-  o.bd = SG_ADD(base, delta);
+  o.bd = SG_ADD(q.base, q.delta);
   const double dadj = fabs(o.bd);
 #pragma unroll
   for (int j = 0; j < 3; ++j) {
@@ -114,7 +143,7 @@ __device__ __forceinline__ bool project_point(const sgad_frame& f, int64_t p, in
   }
   o.z = o.y[2];
   if (!(o.z > SGAD_Z_NEAR)) return false;
-  const double radius = sgad_exp(logr);
+  const double radius = sgad_exp(q.logr);
   o.u0 = SG_ADD(SG_DIV(SG_MUL(cam.fx, o.y[0]), o.z), cam.cx);
   o.v0 = SG_ADD(SG_DIV(SG_MUL(cam.fy, o.y[1]), o.z), cam.cy);
   o.sig = SG_DIV(SG_MUL(radius, cam.fx), o.z);
@@ -123,48 +152,63 @@ __device__ __forceinline__ bool project_point(const sgad_frame& f, int64_t p, in
   if (!(SG_ADD(o.u0, margin) >= 0.0 && SG_SUB(o.u0, margin) <= wlim &&
         SG_ADD(o.v0, margin) >= 0.0 && SG_SUB(o.v0, margin) <= hlim))
     return false;
-  o.op = sgad_sigmoid(plane_ld(f, 3 * hw + p));
+  o.op = sgad_sigmoid(q.logit);
   return true;
 }
 
 __global__ void __launch_bounds__(PROJ_THREADS)
-k_project(const sgad_frame* __restrict__ frames, int n_frames, sgad_camera cam, uint32_t n_total,
-          int ntx, int nty, int want_coef, Record* __restrict__ rec, TileBox* __restrict__ box,
-          ChainCoef* __restrict__ coef,
-          double* __restrict__ col64,
-          unsigned long long* __restrict__ keys, uint32_t* __restrict__ counters,
+k_project(const sgad_frame* __restrict__ frames, sgad_camera cam, int ntx, int nty,
+          int want_coef, Record* __restrict__ rec, TileBox* __restrict__ box,
+          ChainCoef* __restrict__ coef, double* __restrict__ col64,
+          unsigned long long* __restrict__ zkey, uint32_t* __restrict__ counters,
           unsigned long long* __restrict__ zrange) {
-  typedef cub::BlockReduce<unsigned long long, PROJ_THREADS> Red;
-  __shared__ typename Red::TempStorage red_tmp;
-  const uint32_t gid = blockIdx.x * PROJ_THREADS + threadIdx.x;
+  // one block = 256 consecutive pixels of frame blockIdx.y; the frame
+  // descriptor is copied to shared memory (no per-thread frame search), and
+  // the 64-byte records and 32-byte chain coefficients are staged in shared
+  // memory so the global stores are whole contiguous lines
+  __shared__ sgad_frame fsh;
+  __shared__ __align__(16) Record rs[PROJ_THREADS];
+  __shared__ __align__(16) ChainCoef cs[PROJ_THREADS];
+  __shared__ unsigned long long red_z[2][PROJ_THREADS / 32];
+  __shared__ uint32_t red_n[PROJ_THREADS / 32];
+  constexpr int FW = (int)(sizeof(sgad_frame) / 4);
+  static_assert(sizeof(sgad_frame) % 4 == 0, "frame descriptor size");
+  for (int i = threadIdx.x; i < FW; i += PROJ_THREADS)
+    reinterpret_cast<uint32_t*>(&fsh)[i] = reinterpret_cast<const uint32_t*>(frames + blockIdx.y)[i];
+  __syncthreads();
+  const sgad_frame& f = fsh;
+  const int64_t hw = (int64_t)f.height * f.width;
+  const int64_t p0 = (int64_t)blockIdx.x * PROJ_THREADS;
+  if (p0 >= hw) return;  // block-uniform
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t p = p0 + threadIdx.x;
+  const uint32_t gid = (uint32_t)(f.gauss_offset + p);
 
   bool keep = false;
-  Record r;
-  TileBox bx;
-  ChainCoef c;
-  double c64[3];
-  if (gid < n_total) {
-    const sgad_frame& f = frames[find_frame(frames, n_frames, gid)];
-    const int64_t hw = (int64_t)f.height * f.width;
-    const int64_t p = (int64_t)gid - f.gauss_offset;
-    Proj o;
-    if (p < hw && f.mask[p] && project_point(f, p, hw, cam, o)) {
+  Proj o;
+  if (p < hw) {
+    const bool active = f.mask[p] != 0;
+    const Params q = load_params(f, p, hw);
+    if (active && project_point(f, p, q, cam, o)) {
       keep = true;
+      Record r;
       r.u0 = o.u0;
       r.v0 = o.v0;
       r.sigma = o.sig;
       r.opacity = o.op;
-      r.nh = SG_DIV(-0.5, SG_MUL(o.sig, o.sig));
       r.z = o.z;
-      r.r = (float)plane_ld(f, 4 * hw + p);
-      r.g = (float)plane_ld(f, 5 * hw + p);
-      r.b = (float)plane_ld(f, 6 * hw + p);
-      c64[0] = plane_ld(f, 4 * hw + p);
-      c64[1] = plane_ld(f, 5 * hw + p);
-      c64[2] = plane_ld(f, 6 * hw + p);
+      r.nh = SG_DIV(-0.5, SG_MUL(o.sig, o.sig));
+      r.r = (float)q.r;
+      r.g = (float)q.g;
+      r.b = (float)q.b;
+      if (col64) {
+        col64[3 * (size_t)gid] = q.r;
+        col64[3 * (size_t)gid + 1] = q.g;
+        col64[3 * (size_t)gid + 2] = q.b;
+      }
       r.gid = gid | (f.learnable ? GID_LEARN : 0u);
-      // tile bbox (rasterizer.py:187-199)
-      // (x) / 16 is exact as (x) * 0.0625 (power of two)
+      rs[threadIdx.x] = r;
+      // tile bbox (rasterizer.py:187-199); (x) / 16 is exact as (x) * 0.0625
       const double rr = SG_MUL(3.0, o.sig), it16 = 1.0 / (double)SGAD_TILE;
       long long x0 = (long long)floor(SG_MUL(SG_SUB(o.u0, rr), it16));
       long long x1 = (long long)floor(SG_MUL(SG_ADD(o.u0, rr), it16));
@@ -174,11 +218,14 @@ k_project(const sgad_frame* __restrict__ frames, int n_frames, sgad_camera cam, 
       y0 = y0 < 0 ? 0 : y0;
       x1 = x1 > ntx - 1 ? ntx - 1 : x1;
       y1 = y1 > nty - 1 ? nty - 1 : y1;
+      TileBox bx;
       bx.tx0 = (uint16_t)x0;
       bx.tx1 = (uint16_t)x1;
       bx.ty0 = (uint16_t)y0;
       bx.ty1 = (uint16_t)y1;
+      box[gid] = bx;
       if (want_coef) {
+        ChainCoef c;
         const double sgn = o.bd >= 0.0 ? 1.0 : -1.0;
         const double iz = 1.0 / o.z;
         c.k_r = (float)(cam.fx * iz);
@@ -187,36 +234,56 @@ k_project(const sgad_frame* __restrict__ frames, int n_frames, sgad_camera cam, 
         c.a_z = (float)(sgn * o.dir[2]);
         c.a_s = (float)(-sgn * o.dir[2] * o.sig * iz);
         c.k_op = (float)(o.op * (1.0 - o.op));
+        c.pad_[0] = c.pad_[1] = 0.0f;
+        cs[threadIdx.x] = c;
       }
     }
   }
-
-  // depth range of the survivors (positive doubles order like their bits)
-  const unsigned long long zk = keep ? (unsigned long long)__double_as_longlong(r.z) : 0ull;
-  const unsigned long long zmax = Red(red_tmp).Reduce(zk, cub::Max());
+  // depth keys: records stay at their Gaussian id; culled ids carry the
+  // sentinel and sort behind every survivor
+  const unsigned long long zk = keep ? (unsigned long long)__double_as_longlong(o.z) : ~0ull;
+  if (p < hw) zkey[gid] = zk;
+  // survivors and their depth range (positive doubles order like their
+  // bits): warp shuffles, then one atomic per block
+  unsigned long long zmn = zk, zmx = keep ? zk : 0ull;
+  uint32_t ns = keep ? 1u : 0u;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    zmn = min(zmn, __shfl_xor_sync(0xffffffffu, zmn, off));
+    zmx = max(zmx, __shfl_xor_sync(0xffffffffu, zmx, off));
+    ns += __shfl_xor_sync(0xffffffffu, ns, off);
+  }
+  if (lane == 0) {
+    red_z[0][warp] = zmn;
+    red_z[1][warp] = zmx;
+    red_n[warp] = ns;
+  }
   __syncthreads();
-  const unsigned long long zmin = Red(red_tmp).Reduce(keep ? zk : ~0ull, cub::Min());
-  __syncthreads();
-  const uint32_t cnt = (uint32_t)__syncthreads_count(keep);
   if (threadIdx.x == 0) {
-    if (zmin != ~0ull) atomicMin(zrange, zmin);
-    if (zmax) atomicMax(zrange + 1, zmax);
-    if (cnt) atomicAdd(&counters[1], cnt);
-  }
-  // records stay at their Gaussian id (emission order); culled ids get the
-  // sentinel depth key and sort behind every survivor
-  if (gid < n_total) {
-    keys[gid] = keep ? zk : ~0ull;
-    if (keep) {
-      rec[gid] = r;
-      box[gid] = bx;
-      if (want_coef) coef[gid] = c;
-      if (col64) {
-        col64[3 * (size_t)gid] = c64[0];
-        col64[3 * (size_t)gid + 1] = c64[1];
-        col64[3 * (size_t)gid + 2] = c64[2];
-      }
+    for (int w = 1; w < PROJ_THREADS / 32; ++w) {
+      zmn = min(zmn, red_z[0][w]);
+      zmx = max(zmx, red_z[1][w]);
+      ns += red_n[w];
     }
+    if (ns) {
+      atomicAdd(&counters[1], ns);
+      atomicMin(zrange, zmn);
+      atomicMax(zrange + 1, zmx);
+    }
+  }
+  // coalesced stores of the staged records (culled slots carry stale bytes;
+  // nothing reads a record whose depth key is the sentinel)
+  const int nvalid = (int)min((int64_t)PROJ_THREADS, hw - p0);
+  const uint32_t gid0 = (uint32_t)(f.gauss_offset + p0);
+  {
+    const uint4* src = reinterpret_cast<const uint4*>(rs);
+    uint4* dst = reinterpret_cast<uint4*>(rec + gid0);
+    for (int i = threadIdx.x; i < nvalid * 4; i += PROJ_THREADS) dst[i] = src[i];
+  }
+  if (want_coef) {
+    const uint4* src = reinterpret_cast<const uint4*>(cs);
+    uint4* dst = reinterpret_cast<uint4*>(coef + gid0);
+    for (int i = threadIdx.x; i < nvalid * 2; i += PROJ_THREADS) dst[i] = src[i];
   }
 }
 
@@ -927,7 +994,7 @@ __global__ void k_chain_exact(const Record* __restrict__ rec, const double* __re
   const int64_t hw = (int64_t)f.height * f.width;
   const int64_t p = (int64_t)gid - f.gauss_offset;
   Proj o;
-  project_point(f, p, hw, cam, o);
+  project_point(f, p, load_params(f, p, hw), cam, o);
   const double* rg = raw + (size_t)e * 8;
   const double g_op = rg[3], g_u0 = rg[4], g_v0 = rg[5], g_sig = rg[6], g_z = rg[7];
   const double z = o.z, z2 = SG_MUL(z, z);
@@ -1066,10 +1133,12 @@ int sgad_raster_prepare(sgad_raster* h, const sgad_frame* frames, int32_t n_fram
   h->n_tiles = h->ntx * h->nty;
   SGAD_REQUIRE(h->ntx <= 65535 && h->nty <= 65535, "image too large");
   h->host_frames.assign(frames, frames + n_frames);
-  int64_t n_total = 0;
+  int64_t n_total = 0, max_hw = 0;
   for (int i = 0; i < n_frames; ++i) {
     SGAD_REQUIRE(frames[i].gauss_offset == n_total, "frames must be packed: gauss_offset[%d]", i);
-    n_total += (int64_t)frames[i].height * frames[i].width;
+    const int64_t hw = (int64_t)frames[i].height * frames[i].width;
+    n_total += hw;
+    max_hw = hw > max_hw ? hw : max_hw;
   }
   SGAD_REQUIRE(n_total < (1ll << 30), "too many Gaussians (%lld)", (long long)n_total);
   h->n_total = n_total;
@@ -1085,7 +1154,6 @@ int sgad_raster_prepare(sgad_raster* h, const sgad_frame* frames, int32_t n_fram
     h->prepared = 1;
     return SGAD_OK;
   }
-  const int64_t n_tiles_proj = (n_total + PROJ_THREADS - 1) / PROJ_THREADS;
   SGAD_CHECK_CUDA(h->frames.ensure(sizeof(sgad_frame) * n_frames));
   SGAD_CHECK_CUDA(h->counters.ensure(sizeof(uint32_t) * 8));
   SGAD_CHECK_CUDA(h->records.ensure(sizeof(Record) * n_total));
@@ -1102,10 +1170,11 @@ int sgad_raster_prepare(sgad_raster* h, const sgad_frame* frames, int32_t n_fram
   SGAD_CHECK_CUDA(h->zrange.ensure(sizeof(unsigned long long) * 2));
   SGAD_CHECK_CUDA(cudaMemsetAsync(h->zrange.p, 0xff, sizeof(unsigned long long), st));
   SGAD_CHECK_CUDA(cudaMemsetAsync(h->zrange.as<unsigned long long>() + 1, 0, sizeof(unsigned long long), st));
-  k_project<<<(unsigned)n_tiles_proj, PROJ_THREADS, 0, st>>>(
-      h->frames.as<sgad_frame>(), n_frames, *cam, (uint32_t)n_total, h->ntx, h->nty, want_coef,
-      h->records.as<Record>(), h->bbox.as<TileBox>(), h->coef.as<ChainCoef>(),
-      h->any_f64 ? h->col64.as<double>() : nullptr, h->keys0.as<unsigned long long>(), h->counters.as<uint32_t>(),
+  const dim3 pgrid((unsigned)((max_hw + PROJ_THREADS - 1) / PROJ_THREADS), (unsigned)n_frames);
+  k_project<<<pgrid, PROJ_THREADS, 0, st>>>(
+      h->frames.as<sgad_frame>(), *cam, h->ntx, h->nty, want_coef, h->records.as<Record>(),
+      h->bbox.as<TileBox>(), h->coef.as<ChainCoef>(), h->any_f64 ? h->col64.as<double>() : nullptr,
+      h->keys0.as<unsigned long long>(), h->counters.as<uint32_t>(),
       h->zrange.as<unsigned long long>());
   SGAD_LAUNCH_CHECK();
   SGAD_CHECK_CUDA(cudaMemcpyAsync(h->pinned, h->counters.as<uint32_t>() + 1, sizeof(uint32_t),

@@ -205,3 +205,39 @@ def test_random_footprints_bit_exact(seed):
         np.testing.assert_array_equal(out.contributors.cpu().numpy(), ref.contributors)
         np.testing.assert_array_equal(out.color.cpu().numpy(), ref.color)
         np.testing.assert_array_equal(out.depth.cpu().numpy(), ref.depth)
+
+
+@pytest.mark.parametrize("scale", [1.2, 2.5, 4.0])
+def test_tile_size_classes_bit_exact(scale):
+    """Tile buckets of every size class of the shared-memory depth sort (<= 2048,
+    <= 4096, <= 8192 pairs) and beyond it (the segmented-sort fallback): a third
+    of the Gaussians get footprints of tens of pixels so that some tiles collect
+    well over 8192 pairs.  Indices, ranges and images must equal the oracle's."""
+    from types import SimpleNamespace
+    from paper_2603_21055_b200.rasterizer import splat
+    wc = _window_np(n_frames=3, seed=5, w=96, h=64, fx=80.0)
+    rng = np.random.default_rng(17)
+    maps_np = []
+    for i, p in enumerate(wc.params):
+        big = rng.random(p.log_radius.shape) < (0.6 if scale > 3.0 else 0.34)
+        p.log_radius = p.log_radius + np.where(big, scale * rng.random(p.log_radius.shape) + 1.0,
+                                               0.0)
+        maps_np.append(SimpleNamespace(frame_index=i, pose=wc.poses[i], intrinsics=wc.intr,
+                                       base_depth=p.base_depth, delta=p.delta,
+                                       log_radius=p.log_radius, opacity_logit=p.opacity_logit,
+                                       color=p.color, active_mask=p.active_mask))
+    pose = wc.poses[1]
+    maps = check_view(maps_np, pose, wc.intr)
+    from paper_2603_21055_b200.rasterizer import inspect_view
+    _, ranges, _ = inspect_view(maps, pose, wc.intr)
+    sizes = ranges[:, 1] - ranges[:, 0]
+    if scale > 3.0:
+        assert sizes.max() > 8192, sizes.max()
+    elif scale > 2.0:
+        assert sizes.max() > 4096, sizes.max()
+    else:
+        assert sizes.max() > 2048, sizes.max()
+    out = splat(maps, pose, wc.intr)
+    ref = O.splat(maps_np, pose.rotation, pose.translation, wc.intr)
+    np.testing.assert_array_equal(out.contributors.cpu().numpy(), ref.contributors)
+    np.testing.assert_array_equal(out.color.cpu().numpy(), ref.color)
