@@ -53,7 +53,7 @@ constexpr int RASTER_THREADS = 256;
 struct sgad_raster {
   sgad::DevBuf frames, status, counters, records, coef, keys0, keys1, vals0, vals1;
   sgad::DevBuf pcount, poffset, pkeys0, pkeys1, pvals0, pvals1, ranges, cub_tmp;
-  sgad::DevBuf trans_final, last_idx, signs, raw_grads, rank_of, scratch, col64, zrange, k32a, k32b, bbox;
+  sgad::DevBuf trans_final, last_idx, signs, raw_grads, rank_of, scratch, col64, zrange, k32a, k32b, bbox, runs;
   int any_f64 = 0;
   std::vector<sgad_frame> host_frames;
   sgad_camera cam{};
@@ -306,19 +306,29 @@ __global__ void k_depth_key32(const unsigned long long* __restrict__ zkeys, uint
   vals[i] = i;
 }
 
-// Runs of equal buckets are sorted by (z bits, emission index) in place;
-// runs longer than 64 raise *overflow and are redone with the full key.
+// Runs of equal buckets are sorted by (z bits, emission index) in place:
+// runs of up to 64 by this thread (insertion sort), longer runs are queued for
+// k_long_runs (a fronto-parallel plane seen head-on gives long runs of
+// exactly equal depth); runs beyond LONG_RUN_MAX raise *overflow and the
+// whole order is redone with the full 63-bit key.
+constexpr uint32_t LONG_RUN_MAX = 8192;
+
 __global__ void k_depth_fixup(const uint32_t* __restrict__ k32, uint32_t n,
                               const unsigned long long* __restrict__ zkeys,
-                              uint32_t* __restrict__ perm, uint32_t* __restrict__ overflow) {
+                              uint32_t* __restrict__ perm, uint32_t* __restrict__ overflow,
+                              uint32_t* __restrict__ n_long, uint2* __restrict__ long_runs) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i + 1 >= n) return;
   if (k32[i] == 0xFFFFFFFFu) return;  // the culled tail
   if (k32[i + 1] != k32[i] || (i > 0 && k32[i - 1] == k32[i])) return;  // not a run head
   uint32_t end = i + 2;
-  while (end < n && k32[end] == k32[i] && end - i <= 64) ++end;
-  if (end - i > 64) {
+  while (end < n && k32[end] == k32[i] && end - i <= LONG_RUN_MAX) ++end;
+  if (end - i > LONG_RUN_MAX) {
     atomicExch(overflow, 1u);
+    return;
+  }
+  if (end - i > 64) {
+    long_runs[atomicAdd(n_long, 1u)] = make_uint2(i, end - i);
     return;
   }
   for (uint32_t a = i + 1; a < end; ++a) {  // insertion sort, stable on (z, e)
@@ -333,6 +343,54 @@ __global__ void k_depth_fixup(const uint32_t* __restrict__ k32, uint32_t n,
       --b;
     }
     perm[b] = e;
+  }
+}
+
+// Long runs of equal depth buckets: a bitonic sort of (z bits, emission
+// index) in shared memory, one block per run (blocks loop over the queue).
+__global__ void __launch_bounds__(1024)
+k_long_runs(const uint2* __restrict__ long_runs, const uint32_t* __restrict__ n_long,
+            const unsigned long long* __restrict__ zkeys, uint32_t* __restrict__ perm) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  unsigned long long* zs = reinterpret_cast<unsigned long long*>(smem_raw);  // [LONG_RUN_MAX]
+  uint32_t* es = reinterpret_cast<uint32_t*>(zs + LONG_RUN_MAX);              // [LONG_RUN_MAX]
+  const uint32_t nr = *n_long;
+  for (uint32_t r = blockIdx.x; r < nr; r += gridDim.x) {
+    const uint2 ru = long_runs[r];
+    uint32_t P = 1;
+    while (P < ru.y) P <<= 1;
+    for (uint32_t i = threadIdx.x; i < P; i += blockDim.x) {
+      if (i < ru.y) {
+        const uint32_t e = perm[ru.x + i];
+        zs[i] = zkeys[e];
+        es[i] = e;
+      } else {
+        zs[i] = ~0ull;
+        es[i] = ~0u;
+      }
+    }
+    __syncthreads();
+    for (uint32_t k = 2; k <= P; k <<= 1) {
+      for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+        for (uint32_t i = threadIdx.x; i < P; i += blockDim.x) {
+          const uint32_t x = i ^ j;
+          if (x > i) {
+            const bool gt = zs[i] > zs[x] || (zs[i] == zs[x] && es[i] > es[x]);
+            if (((i & k) == 0) == gt) {
+              const unsigned long long tz = zs[i];
+              zs[i] = zs[x];
+              zs[x] = tz;
+              const uint32_t te = es[i];
+              es[i] = es[x];
+              es[x] = te;
+            }
+          }
+        }
+        __syncthreads();
+      }
+    }
+    for (uint32_t i = threadIdx.x; i < ru.y; i += blockDim.x) perm[ru.x + i] = es[i];
+    __syncthreads();
   }
 }
 
@@ -1056,6 +1114,8 @@ __global__ void k_export_surv(const uint32_t* __restrict__ perm, const Record* _
 constexpr size_t FWD_SMEM = sizeof(FwdStage) * NWARP;
 constexpr size_t BWD_SMEM = sizeof(WarpRing) * NWARP;
 
+constexpr size_t LONG_RUN_SMEM = (sizeof(unsigned long long) + sizeof(uint32_t)) * LONG_RUN_MAX;
+
 // opt in to >48 KB dynamic shared memory once per process
 static int smem_attrs() {
   static int done = 0;
@@ -1067,6 +1127,7 @@ static int smem_attrs() {
   SGAD_CHECK_CUDA(cudaFuncSetAttribute(k_forward<false, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FWD_SMEM));
   SGAD_CHECK_CUDA(cudaFuncSetAttribute(k_backward<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)BWD_SMEM));
   SGAD_CHECK_CUDA(cudaFuncSetAttribute(k_backward<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)BWD_SMEM));
+  SGAD_CHECK_CUDA(cudaFuncSetAttribute(k_long_runs, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LONG_RUN_SMEM));
   done = 1;
   return SGAD_OK;
 }
@@ -1107,7 +1168,7 @@ int sgad_raster_destroy(sgad_raster* h) {
                     &h->keys1, &h->vals0, &h->vals1, &h->pcount, &h->poffset, &h->pkeys0,
                     &h->pkeys1, &h->pvals0, &h->pvals1, &h->ranges, &h->cub_tmp,
                     &h->trans_final, &h->last_idx, &h->signs, &h->raw_grads, &h->rank_of,
-                    &h->scratch, &h->col64, &h->zrange, &h->k32a, &h->k32b, &h->bbox};
+                    &h->scratch, &h->col64, &h->zrange, &h->k32a, &h->k32b, &h->bbox, &h->runs};
   for (DevBuf* b : bufs) b->release();
   if (h->pinned) cudaFreeHost(h->pinned);
   delete h;
@@ -1126,6 +1187,7 @@ int sgad_raster_prepare(sgad_raster* h, const sgad_frame* frames, int32_t n_fram
   SGAD_REQUIRE(h && cam && n_frames >= 0 && (n_frames == 0 || frames), "sgad_raster_prepare: bad args");
   SGAD_REQUIRE(cam->width > 0 && cam->height > 0, "sgad_raster_prepare: empty camera");
   cudaStream_t st = (cudaStream_t)stream_;
+  if (int rc = smem_attrs()) return rc;
   h->prepared = h->forwarded = h->fused_ready = 0;
   h->cam = *cam;
   h->ntx = (cam->width + SGAD_TILE - 1) / SGAD_TILE;
@@ -1218,9 +1280,16 @@ int sgad_raster_prepare(sgad_raster* h, const sgad_frame* frames, int32_t n_fram
     if (dv.Current() != perm)
       SGAD_CHECK_CUDA(cudaMemcpyAsync(perm, dv.Current(), sizeof(uint32_t) * ns,
                                       cudaMemcpyDeviceToDevice, st));
+    SGAD_CHECK_CUDA(h->runs.ensure(sizeof(uint2) * (ns / 65 + 1)));
     k_depth_fixup<<<blocks_for(ns, 256), 256, 0, st>>>(dk.Current(), ns,
                                                        h->keys0.as<unsigned long long>(), perm,
-                                                       h->counters.as<uint32_t>() + 2);
+                                                       h->counters.as<uint32_t>() + 2,
+                                                       h->counters.as<uint32_t>() + 3,
+                                                       h->runs.as<uint2>());
+    SGAD_LAUNCH_CHECK();
+    k_long_runs<<<148, 1024, LONG_RUN_SMEM, st>>>(h->runs.as<uint2>(),
+                                                  h->counters.as<uint32_t>() + 3,
+                                                  h->keys0.as<unsigned long long>(), perm);
     SGAD_LAUNCH_CHECK();
   }
   size_t tmp = 0;

@@ -241,3 +241,31 @@ def test_tile_size_classes_bit_exact(scale):
     ref = O.splat(maps_np, pose.rotation, pose.translation, wc.intr)
     np.testing.assert_array_equal(out.contributors.cpu().numpy(), ref.contributors)
     np.testing.assert_array_equal(out.color.cpu().numpy(), ref.color)
+
+
+@pytest.mark.parametrize("size", [(64, 48), (160, 120)])
+def test_fronto_parallel_runs_bit_exact(size):
+    """A plane seen head-on at exactly equal depth: thousands of survivors
+    share one depth bucket (the long-run sort), and the other frames'
+    Gaussians on the same plane land in that bucket with depths a few ulps
+    away -- the tile lists must still follow the exact (z, frame, pixel) order."""
+    from types import SimpleNamespace
+    w, h = size
+    wc = _window_np(n_frames=3, seed=9, w=w, h=h, fx=w * 0.9)
+    rng = np.random.default_rng(3)
+    maps_np = []
+    for i, p in enumerate(wc.params):
+        if i == 0:
+            p.base_depth = np.full_like(p.base_depth, 2.0)
+            p.delta = np.zeros_like(p.delta)
+        else:
+            p.base_depth = np.full_like(p.base_depth, 2.0)
+            p.delta = (rng.normal(0.0, 1e-9, p.delta.shape)).astype(np.float32).astype(np.float64)
+        p.active_mask = np.ones_like(p.active_mask)
+        maps_np.append(SimpleNamespace(frame_index=i, pose=wc.poses[i], intrinsics=wc.intr,
+                                       base_depth=p.base_depth, delta=p.delta,
+                                       log_radius=p.log_radius, opacity_logit=p.opacity_logit,
+                                       color=p.color, active_mask=p.active_mask))
+    from paper_2603_21055_b200.geometry import Pose
+    check_view(maps_np, Pose.identity(), wc.intr)
+    check_view(maps_np, wc.poses[1], wc.intr)
