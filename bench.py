@@ -200,42 +200,22 @@ def run_ours(args):
     views = list(range(rank, len(wc.poses), world))
     wm = WindowMapper(wc.frames, wc.poses, wc.intr, wc.params, MapperConfig(tau=0.0),
                       views=views, device=dev)
+    if os.environ.get("SGAD_PIPELINE") == "0":  # A/B: no prepare/composite overlap
+        wm.pipelined = False
     n_g = wm.n_gaussians
     n_views_total = len(wc.poses)
 
-    # kernel timing hooks on the launching stream (torch current stream)
+    # per-view kernel timing: CUDA events recorded by the window engine on the
+    # streams the kernels run on (prepare on its side stream, compositing on
+    # the main stream)
     stream = torch.cuda.current_stream()
-    ev = {"fwd": [], "bwd": [], "prep": []}
-    orig = wm.render_view_grads
-
-    def timed_view(v, record=[False]):
-        r = wm.raster
-        p0 = torch.cuda.Event(enable_timing=True)
-        p0.record(stream)
-        ns, npairs = r.prepare(wm._frames[v], wm.cam, want_coef=True)
-        wm.last_counts[v] = (ns, npairs)
-        if ns:
-            e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
-            e0.record(stream)
-            if timed_view.on:
-                ev["prep"].append((p0, e0, ns, npairs))
-            r.forward(target=wm._target(v))
-            e1.record(stream)
-            r.backward_fused(wm.grad)
-            e2.record(stream)
-            if timed_view.on:
-                ev["fwd"].append((e0, e1, ns, npairs))
-                ev["bwd"].append((e1, e2, ns, npairs))
-
-    timed_view.on = False
-    wm.render_view_grads = timed_view
+    timing = []
 
     for _ in range(args.warmup):
         wm.step()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    timed_view.on = True
     sampler = ClockSampler(local)
     start = torch.cuda.Event(enable_timing=True)
     stop = torch.cuda.Event(enable_timing=True)
@@ -243,7 +223,7 @@ def run_ours(args):
         torch.cuda.synchronize()
         start.record(stream)
         for _ in range(args.steps):
-            wm.step()
+            wm.step(timing=timing)
         stop.record(stream)
         torch.cuda.synchronize()
     if world > 1:
@@ -259,14 +239,16 @@ def run_ours(args):
     # roofline of the compositing kernels (SURVEY 8d algorithmic bytes)
     hw = wm.HW
 
-    def kstats(lst, extra_surv):
-        tot_ms = sum(a.elapsed_time(b) for a, b, _, _ in lst)
+    def kstats(kind, extra_surv):
+        lst = [t for t in timing if t[0] == kind]
+        tot_ms = sum(a.elapsed_time(b) for _, a, b, _, _, _ in lst)
         tot_bytes = sum(36 * npairs + 20 * hw + (32 * ns if extra_surv else 0)
-                        for _, _, ns, npairs in lst)
+                        for _, _, _, _, ns, npairs in lst)
         return tot_ms, tot_bytes, len(lst)
 
-    f_ms, f_bytes, f_n = kstats(ev["fwd"], False)
-    b_ms, b_bytes, b_n = kstats(ev["bwd"], True)
+    f_ms, f_bytes, f_n = kstats("fwd", False)
+    b_ms, b_bytes, b_n = kstats("bwd", True)
+    p_ms, _, p_n = kstats("prep", False)
     peak, peak_kind = load_peaks()
     dom = ("k_backward", b_ms, b_bytes, b_n) if b_ms >= f_ms else ("k_forward", f_ms, f_bytes, f_n)
     achieved = dom[2] / dom[3] / (dom[1] / dom[3] / 1e3) / 1e9
@@ -285,8 +267,8 @@ def run_ours(args):
                 "launch_ms": dom[1] / dom[3],
                 "bytes_per_launch": dom[2] / dom[3],
                 "forward_ms_per_view": f_ms / max(f_n, 1), "backward_ms_per_view": b_ms / max(b_n, 1),
-                "prepare_ms_per_view": sum(a.elapsed_time(b) for a, b, _, _ in ev["prep"]) /
-                max(len(ev["prep"]), 1),
+                "prepare_ms_per_view": p_ms / max(p_n, 1),
+                "prepare_overlapped": bool(wm.pipelined),
                 "mean_survivors_per_view": mean_ns, "mean_pairs_per_view": mean_np}
 
     # e2e through the public API with host buffers (params + targets up, params down)

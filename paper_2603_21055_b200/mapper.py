@@ -24,7 +24,7 @@ import torch
 from . import _native as N
 from .gaussians import PixelGaussianMap
 from .geometry import Intrinsics, Pose
-from .rasterizer import (MapGradients, RenderOutput, build_frames, camera_of, get_raster,
+from .rasterizer import (MapGradients, Raster, RenderOutput, build_frames, camera_of, get_raster,
                          learnable_set)
 
 
@@ -251,6 +251,8 @@ class WindowMapper:
         self._frames = {v: build_frames(self.maps, self.poses[v], learn)[0] for v in self.views}
         self.raster = get_raster(dev)
         self.last_counts = {}
+        self.pipelined = True   # prepare view i+1 while view i composites
+        self._pipe = None
 
     @property
     def n_gaussians(self) -> int:
@@ -261,23 +263,81 @@ class WindowMapper:
                             self.tmask[v].data_ptr(), self.cfg.rho, self.cfg.sigma,
                             self.n_depth[v], self.loss_acc[v].data_ptr())
 
-    def render_view_grads(self, v):
+    def render_view_grads(self, v, raster=None, stream=None):
         """Fused forward (+ tau=0 L1) and backward of one view into self.grad."""
-        r = self.raster
-        ns, npairs = r.prepare(self._frames[v], self.cam, want_coef=True)
+        r = raster or self.raster
+        ns, npairs = r.prepare(self._frames[v], self.cam, want_coef=True, stream=stream)
         self.last_counts[v] = (ns, npairs)
         if ns:
-            r.forward(target=self._target(v))
-            r.backward_fused(self.grad)
+            r.forward(target=self._target(v), stream=stream)
+            r.backward_fused(self.grad, stream=stream)
 
-    def step(self, sync_loss=False):
+    def _render_pipelined(self, timing=None):
+        """All assigned views, the preparation (projection, depth order, tile
+        lists) of view i+1 on a side stream while view i composites on the
+        main stream.  Two raster handles alternate; a handle is re-prepared
+        only after the compositing that used it has finished.  ``timing``
+        (optional list) receives (kind, start_event, end_event, view) tuples."""
+        if self._pipe is None:
+            self._pipe = ([Raster(self.dev), Raster(self.dev)], torch.cuda.Stream(self.dev))
+        rasters, prep = self._pipe
+        main = torch.cuda.current_stream(self.dev)
+        ev = torch.cuda.Event()
+        ev.record(main)           # parameters / loss accumulators are ready
+        prep.wait_event(ev)
+        used = [None, None]       # compositing done on each handle
+
+        def mark(stream):
+            e = torch.cuda.Event(enable_timing=timing is not None)
+            e.record(stream)
+            return e
+
+        for i, v in enumerate(self.views):
+            r = rasters[i % 2]
+            if used[i % 2] is not None:
+                prep.wait_event(used[i % 2])
+            p0 = mark(prep)
+            ns, npairs = r.prepare(self._frames[v], self.cam, want_coef=True, stream=prep)
+            self.last_counts[v] = (ns, npairs)
+            p1 = mark(prep)
+            main.wait_event(p1)
+            if ns:
+                f0 = mark(main)
+                r.forward(target=self._target(v), stream=main)
+                f1 = mark(main)
+                r.backward_fused(self.grad, stream=main)
+                b1 = mark(main)
+                if timing is not None:
+                    timing += [("prep", p0, p1, v, ns, npairs), ("fwd", f0, f1, v, ns, npairs),
+                               ("bwd", f1, b1, v, ns, npairs)]
+            used[i % 2] = mark(main)
+
+    def step(self, sync_loss=False, timing=None):
         """One window iteration: every assigned view fwd+bwd, gradient
         all-reduce across ranks, Adam.  Returns the summed loss (a device
         scalar unless ``sync_loss``)."""
         self.loss_acc.zero_()
         with torch.cuda.device(self.dev):
-            for v in self.views:
-                self.render_view_grads(v)
+            if self.pipelined:
+                self._render_pipelined(timing)
+            else:
+                main = torch.cuda.current_stream(self.dev)
+                for v in self.views:
+                    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+                    ev[0].record(main)
+                    r = self.raster
+                    ns, npairs = r.prepare(self._frames[v], self.cam, want_coef=True)
+                    self.last_counts[v] = (ns, npairs)
+                    ev[1].record(main)
+                    if ns:
+                        r.forward(target=self._target(v))
+                        ev[2].record(main)
+                        r.backward_fused(self.grad)
+                        ev[3].record(main)
+                        if timing is not None:
+                            timing += [("prep", ev[0], ev[1], v, ns, npairs),
+                                       ("fwd", ev[1], ev[2], v, ns, npairs),
+                                       ("bwd", ev[2], ev[3], v, ns, npairs)]
             allreduce_window(self.grad, self.loss_acc, self.pg)
             self.t += 1
             _adam(self.planes, self.grad, self.m, self.v, self.F, self.HW, self.cfg, self.t, False)
