@@ -492,13 +492,12 @@ __device__ __forceinline__ uint32_t transpose32(uint32_t x, int lane) {
   return x;
 }
 
-// Exact pixel mask of one Gaussian over the warp's 8x4 rectangle: bit
-// (ly*8 + lx) set iff the reference test d2 > 9 s2 fails at pixel
-// (xlo+lx, ylo+ly).  Per row, fp32 gives the column interval of certain
-// passes (shrunk by a guard band of 2e-4 (thr + 1) in d2) and of possible
-// passes (grown by it); only columns in between are decided by the exact
-// fp64 test, which is rare.  The fp32 error is < 1e-6 (thr + 400) for any
-// Gaussian that survived the rectangle cull (K4).
+// Pixel mask of one Gaussian over the warp's 8x4 rectangle: bit (ly*8 + lx)
+// is set if the reference test d2 > 9 s2 may fail at pixel (xlo+lx, ylo+ly).
+// Per row, fp32 gives the column interval of possible passes, grown by a
+// guard band of 2e-4 (thr + 1) in d2; the fp32 error is < 1e-6 (thr + 400)
+// for any Gaussian that survived the rectangle cull, so no pass is missed
+// (K4), and the exact fp64 test is made where d2 is computed.
 __device__ __forceinline__ uint32_t col_range(float a, float b) {
   // columns c in [ceil(a), floor(b)] intersected with [0, 7], as an 8-bit mask
   const int lo = max((int)ceilf(a), 0), hi = min((int)floorf(b), 7);
@@ -507,6 +506,29 @@ __device__ __forceinline__ uint32_t col_range(float a, float b) {
 
 __device__ __forceinline__ uint32_t pixel_mask(double u0, double v0, double thr, double xlo,
                                                double ylo) {
+  // superset of the pixels passing the test: fp32 column intervals grown by
+  // the guard band; the compositing loops decide the exact test in fp64 for
+  // every bit (they compute d2 anyway), so the mask never drops a pass
+  const float ru = (float)(u0 - xlo), rv = (float)(v0 - ylo), thrf = (float)thr;
+  const float band = 2e-4f * (thrf + 1.0f);
+  uint32_t maybe = 0;
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const float dyf = rv - (float)r;
+    const float rem_hi = thrf + band - dyf * dyf;
+    if (rem_hi >= 0.0f) {
+      const float h_hi = sqrtf(rem_hi) * 1.000001f + 1e-5f;
+      maybe |= col_range(ru - h_hi, ru + h_hi) << (8 * r);
+    }
+  }
+  return maybe;
+}
+
+// Exact variant for the backward (its contributions are expensive to start,
+// so no superset bits): columns between the fp32 intervals of certain and of
+// possible passes are decided by the fp64 test.
+__device__ __forceinline__ uint32_t pixel_mask_exact(double u0, double v0, double thr, double xlo,
+                                                     double ylo) {
   const float ru = (float)(u0 - xlo), rv = (float)(v0 - ylo), thrf = (float)thr;
   const float band = 2e-4f * (thrf + 1.0f);
   uint32_t sure = 0, maybe = 0;
@@ -593,7 +615,7 @@ __device__ __forceinline__ int fill_chunk(uint32_t* __restrict__ se, int32_t* __
     const float dx = fmaxf(fmaxf(xl - uf, uf - (xl + 7.0f)), 0.0f);
     const float dy = fmaxf(fmaxf(yl - vf, vf - (yl + 3.0f)), 0.0f);
     if (dx * dx + dy * dy <= rr * rr)
-      m = pixel_mask(hd.u0, hd.v0, SG_MUL(9.0, SG_MUL(hd.sig, hd.sig)), xlo, ylo);
+      m = pixel_mask_exact(hd.u0, hd.v0, SG_MUL(9.0, SG_MUL(hd.sig, hd.sig)), xlo, ylo);
   }
   const uint32_t keep = __ballot_sync(0xffffffffu, m != 0);
   const int c = __popc(keep);
@@ -619,7 +641,7 @@ __device__ __forceinline__ int fill_chunk(uint32_t* __restrict__ se, int32_t* __
 // time with the entries' fields in shared memory (short-latency loads); the
 // backward's heavy contributions pay for the ring below (K4/K5).
 struct FwdStage {
-  double u0[WIN], v0[WIN], nh[WIN], op[WIN], z[WIN], rgb[3][WIN];
+  double u0[WIN], v0[WIN], nh[WIN], op[WIN], z[WIN], rgb[3][WIN], thr[WIN];
   int32_t k[WIN];
 };
 
@@ -645,6 +667,7 @@ __device__ __forceinline__ int fill_chunk_fwd(FwdStage& s, const Head& hd,
     const double2* rp = reinterpret_cast<const double2*>(rec + hd.e);
     const double2 zn = __ldg(rp + 2);                                        // z, nh
     const float4 cg = __ldg(reinterpret_cast<const float4*>(rp + 3));        // r, g, b, gid
+    s.thr[j] = SG_MUL(9.0, SG_MUL(hd.sig, hd.sig));
     s.u0[j] = hd.u0;
     s.v0[j] = hd.v0;
     s.nh[j] = zn.y;
@@ -794,6 +817,7 @@ k_forward(const uint2* __restrict__ ranges, const uint32_t* __restrict__ lists,
       mine &= mine - 1;
       const double dx = SG_SUB(s.u0[j], pxd), dy = SG_SUB(s.v0[j], pyd);
       const double d2 = SG_ADD(SG_MUL(dx, dx), SG_MUL(dy, dy));
+      if (d2 > s.thr[j]) continue;  // rasterizer.py:248 (the mask is a superset)
       const double w = sgad_exp_neg(SG_MUL(d2, s.nh[j]), tab);
       double a = SG_MUL(s.op[j], w);
       if (a > SGAD_ALPHA_MAX) a = SGAD_ALPHA_MAX;
