@@ -79,6 +79,10 @@ typedef struct sgad_raster sgad_raster;
 
 const char* sgad_last_error(void);
 int sgad_version(void);
+/* Number of this library's own kernels launched so far in the process (the
+ * bench's gpu_launches; CUB's sort/scan kernels are library kernels and not
+ * counted). */
+int sgad_launch_count(int64_t* out);
 
 int sgad_raster_create(sgad_raster** out);
 int sgad_raster_destroy(sgad_raster* h);

@@ -48,6 +48,7 @@ assert ctypes.sizeof(Frame) == 176
 _SIGNATURES = {
     "sgad_last_error": (ctypes.c_char_p, []),
     "sgad_version": (_i32, []),
+    "sgad_launch_count": (_i32, [ctypes.POINTER(_i64)]),
     "sgad_raster_create": (_i32, [ctypes.POINTER(_vp)]),
     "sgad_raster_destroy": (_i32, [_vp]),
     "sgad_raster_prepare": (_i32, [_vp, ctypes.POINTER(Frame), _i32, ctypes.POINTER(Camera), _i32,
@@ -117,3 +118,10 @@ def ptr(t) -> int | None:
 def stream_ptr(stream=None) -> int:
     s = stream if stream is not None else torch.cuda.current_stream()
     return s.cuda_stream
+
+
+def launch_count() -> int:
+    """Kernels of libsgad launched so far in this process."""
+    n = _i64()
+    check(load().sgad_launch_count(ctypes.byref(n)))
+    return n.value

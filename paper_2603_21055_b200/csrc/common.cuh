@@ -5,12 +5,17 @@
 #include <stdint.h>
 #include <stdio.h>
 
+#include <atomic>
+
 #include "../../include/sgad.h"
 #include "../../include/sgad_numerics.h"
 
 namespace sgad {
 
 void set_error(const char* fmt, ...);
+
+// kernels of this library launched so far (sgad_launch_count)
+extern std::atomic<long long> g_launches;
 
 #define SGAD_CHECK_CUDA(x)                                                                  \
   do {                                                                                      \
@@ -31,6 +36,7 @@ void set_error(const char* fmt, ...);
 
 #define SGAD_LAUNCH_CHECK()                                                                 \
   do {                                                                                      \
+    ::sgad::g_launches.fetch_add(1, std::memory_order_relaxed);                             \
     cudaError_t e_ = cudaGetLastError();                                                    \
     if (e_ != cudaSuccess) {                                                                \
       ::sgad::set_error("%s:%d launch: %s", __FILE__, __LINE__, cudaGetErrorString(e_));    \

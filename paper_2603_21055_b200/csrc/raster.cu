@@ -68,6 +68,7 @@ struct sgad_raster {
 namespace sgad {
 
 static thread_local char g_err[1024] = "";
+std::atomic<long long> g_launches{0};
 
 void set_error(const char* fmt, ...) {
   va_list ap;
@@ -1172,6 +1173,12 @@ extern "C" {
 
 const char* sgad_last_error(void) { return g_err; }
 int sgad_version(void) { return 1; }
+
+int sgad_launch_count(int64_t* out) {
+  SGAD_REQUIRE(out != nullptr, "sgad_launch_count: null out");
+  *out = (int64_t)g_launches.load(std::memory_order_relaxed);
+  return SGAD_OK;
+}
 
 int sgad_raster_create(sgad_raster** out) {
   SGAD_REQUIRE(out != nullptr, "sgad_raster_create: null out");
