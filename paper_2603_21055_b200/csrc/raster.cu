@@ -471,7 +471,7 @@ __device__ __forceinline__ TileGeom tile_geom(int ntx, int width, int height) {
 // and the slot it needs is no longer read by any lane.
 constexpr int NWARP = RASTER_THREADS / 32;
 constexpr int WIN = 64;
-constexpr int RING = 12;
+constexpr int RING = 10;
 
 struct WarpRing {
   uint32_t e[RING][WIN];                  // record index of each slot
