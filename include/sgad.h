@@ -18,6 +18,8 @@
  *   sgad_raster_backward  <- rasterizer.py:272-363 (_backward_kernel) and the
  *                            chain rule :451-483 (splat_backward)
  *   sgad_adam_step        <- mapper.py:73-95 (MapOptimizer.step)
+ *   sgad_ssim             <- ssim.py:31-87 (ssim(..., with_grad)), the tau term
+ *                            of mapping_loss (mapper.py:126-147)
  *   sgad_track_fit        <- tracker.py:144-170, :193-230 (build_local_set with
  *                            the 5x5 window neighbourhood of north_star, delta D2)
  *   sgad_sym_eigh3        <- geometry.py:275-353 (sym_eigh3_batch)
@@ -111,9 +113,11 @@ int sgad_raster_forward(sgad_raster* h, double* out_color, double* out_depth, do
  *   fp64 outputs map_grads[f] (device [6, H, W]: delta, radius, opacity_logit,
  *   R, G, B; NULL entries for non-learnable maps).
  * mode 1 (fused): upstream comes from the fused loss of the preceding
- *   forward (target != NULL there); per-pixel gradients are chained, warp-
- *   reduced in fp32 and atomically added into grad_accum (device
- *   [N_total, 8] fp32: delta, radius, opacity_logit, R, G, B, -, -). */
+ *   forward (target != NULL there) -- or, for the colour channels, from
+ *   g_color when it is given (the tau != 0 objective: sgad_ssim's upstream);
+ *   per-contribution gradients are chained in fp64, rounded to fp32 and
+ *   atomically added into grad_accum (device [N_total, 8] fp32: delta,
+ *   radius, opacity_logit, R, G, B, -, -). */
 int sgad_raster_backward(sgad_raster* h, int32_t mode, const double* g_color,
                          const double* g_depth, const double* g_alpha, double* const* map_grads,
                          float* grad_accum, void* stream);
@@ -134,6 +138,20 @@ int sgad_raster_tile_count(sgad_raster* h, int64_t* n_tiles);
 int sgad_adam_step(void* params, void* grads, void* m, void* v, int64_t n_frames, int64_t hw,
                    const double* lr, double beta1, double beta2, double eps, double bc1,
                    double bc2, int32_t update_delta, int32_t f64, void* stream);
+
+/* ---- SSIM term (tau != 0 objective) ------------------------------------
+ * Replaces raysplat/ssim.py:31-87 (ssim(img_a, img_b, with_grad)) as used by
+ * mapper.py:126-147.  Images are device [H, W, C] interleaved, img_a fp64,
+ * img_b fp64 or fp32 (b_is_f32).  *sum_out (device double) += the SUM of the
+ * per-pixel, per-channel SSIM (the mean is sum / (H W C)).  With grad_out
+ * (device double [H, W, C]) and a workspace of sgad_ssim_workspace_size
+ * bytes, writes d(mean SSIM)/d(img_a); with upstream != 0 it writes instead
+ * the mapping loss's colour upstream  kc * sign(a - b) - tau * grad
+ * (mapper.py:145-147 with kc = rho / (3 H W)). */
+int sgad_ssim_workspace_size(int32_t height, int32_t width, int32_t channels, int64_t* bytes);
+int sgad_ssim(const double* img_a, const void* img_b, int32_t b_is_f32, int32_t height,
+              int32_t width, int32_t channels, double* sum_out, double* grad_out,
+              double* workspace, double kc, double tau, int32_t upstream, void* stream);
 
 /* ----------------------------------------------------------- tracking */
 

@@ -942,9 +942,15 @@ k_backward(const uint2* __restrict__ ranges, const uint32_t* __restrict__ lists,
     if (FUSED) {
       const uint32_t code = signs[p];
       // mapper.py:145-152: rho * sign / n_color; sigma * sign * mask / n_depth
-      gc0 = SG_MUL(up.kc, sign_of(code & 3u));
-      gc1 = SG_MUL(up.kc, sign_of((code >> 2) & 3u));
-      gc2 = SG_MUL(up.kc, sign_of((code >> 4) & 3u));
+      if (g_color) {  // tau != 0: colour upstream with the SSIM term (sgad_ssim)
+        gc0 = g_color[3 * p];
+        gc1 = g_color[3 * p + 1];
+        gc2 = g_color[3 * p + 2];
+      } else {
+        gc0 = SG_MUL(up.kc, sign_of(code & 3u));
+        gc1 = SG_MUL(up.kc, sign_of((code >> 2) & 3u));
+        gc2 = SG_MUL(up.kc, sign_of((code >> 4) & 3u));
+      }
       gd = SG_MUL(up.kd, sign_of((code >> 6) & 3u));
     } else {
       gc0 = g_color[3 * p];
@@ -1466,7 +1472,7 @@ int sgad_raster_backward(sgad_raster* h, int32_t mode, const double* g_color,
         h->coef.as<ChainCoef>(), h->any_f64 ? h->col64.as<double>() : nullptr, h->ntx,
         h->cam.width, h->cam.height,
         h->trans_final.as<double>(), h->last_idx.as<int32_t>(), h->signs.as<uint8_t>(), up,
-        nullptr, nullptr, nullptr, nullptr, grad_accum);
+        g_color, nullptr, nullptr, nullptr, grad_accum);
     SGAD_LAUNCH_CHECK();
     return SGAD_OK;
   }

@@ -102,8 +102,10 @@ class Raster:
         N.check(N.load().sgad_raster_backward(self.h, 0, N.ptr(g_color), N.ptr(g_depth),
                                               N.ptr(g_alpha), arr, None, N.stream_ptr(stream)))
 
-    def backward_fused(self, grad_accum, stream=None):
-        N.check(N.load().sgad_raster_backward(self.h, 1, None, None, None, None,
+    def backward_fused(self, grad_accum, g_color=None, stream=None):
+        """Fused backward into ``grad_accum``; ``g_color`` (device fp64
+        [H, W, 3]) overrides the colour upstream (the tau != 0 objective)."""
+        N.check(N.load().sgad_raster_backward(self.h, 1, N.ptr(g_color), None, None, None,
                                               N.ptr(grad_accum), N.stream_ptr(stream)))
 
     def survivors(self):

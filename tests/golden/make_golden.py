@@ -2,7 +2,7 @@
 
 Run in the build container (where /root/reference exists):
 
-    python tests/golden/make_golden.py
+    python tests/golden/make_golden.py [c1 window eig track ssim]
 
 The reference package is copied to a temporary directory first (so nothing is
 written under /root/reference: Numba's cache and __pycache__ land in the
@@ -39,6 +39,45 @@ def import_reference():
     import raysplat.tracker as T
     from raysplat.datasets import RgbdFrame
     return tmp, G, GEO, M, R, T, RgbdFrame
+
+
+def golden_ssim(M, G, GEO, R, RgbdFrame):
+    """raysplat/ssim.py on seeded image pairs (3-channel, 1-channel, a
+    constant pair, tiny and odd sizes) and the full tau = 0.2 mapping_loss of
+    configuration C1 (mapper.py:106-157 with the SSIM term)."""
+    import raysplat.ssim as S
+    from paper_2603_21055_b200 import scenes
+    rng = np.random.default_rng(2024)
+    d = {}
+    cases = {
+        "rgb": (rng.random((45, 61, 3)), None),
+        "gray": (rng.random((23, 17)), None),
+        "const": (np.full((12, 14, 3), 0.3), np.full((12, 14, 3), 0.7)),
+        "tiny": (rng.random((4, 6, 3)), None),
+    }
+    for name, (a, b) in cases.items():
+        if b is None:
+            b = np.clip(a + rng.normal(0.0, 0.15, a.shape), 0.0, 1.0)
+        v, g = S.ssim(a, b, with_grad=True)
+        d[f"{name}_a"], d[f"{name}_b"] = a, b
+        d[f"{name}_value"], d[f"{name}_grad"] = np.array(v), g
+    intr, frame, learn, target = scenes.config_c1()
+    ri = ref_intr(GEO, intr)
+    ident = GEO.Pose.identity()
+    m_learn = ref_map(G, GEO, learn, ri, ident, 0)
+    m_tgt = ref_map(G, GEO, target, ri, ident, 0)
+    t_out = R.splat([m_tgt], ident, ri)
+    t_color = np.clip(t_out.color, 0.0, 1.0).astype(np.float32)
+    t_depth = t_out.depth.astype(np.float32)
+    tf = RgbdFrame(color=t_color, depth=t_depth, valid_mask=frame.valid_mask.copy(),
+                   intrinsics=ri, timestamp=0.0, index=0)
+    cfg = M.MapperConfig(tau=0.2)
+    loss, grads, out = M.mapping_loss([m_learn], tf, ident, cfg)
+    d["c1_loss"] = np.array([loss.total, loss.color_l1, loss.ssim_term, loss.depth_l1])
+    d["c1_g_color"], d["c1_g_radius"] = grads.color, grads.radius
+    d["c1_g_logit"], d["c1_g_delta"] = grads.opacity_logit, grads.delta
+    d["c1_t_color"], d["c1_t_depth"], d["c1_t_mask"] = t_color, t_depth, frame.valid_mask
+    return d
 
 
 def ref_map(G, GEO, params, intr_ref, pose, frame_index):
@@ -271,12 +310,20 @@ def golden_track(T, GEO):
 
 def main():
     sys.path.insert(0, ROOT)
+    want = set(sys.argv[1:]) or {"c1", "window", "eig", "track", "ssim"}
     tmp, G, GEO, M, R, T, RgbdFrame = import_reference()
     try:
-        np.savez_compressed(os.path.join(HERE, "c1.npz"), **golden_c1(G, GEO, M, R, RgbdFrame))
-        np.savez_compressed(os.path.join(HERE, "window.npz"), **golden_window(G, GEO, R))
-        np.savez_compressed(os.path.join(HERE, "eig.npz"), **golden_eig(GEO))
-        np.savez_compressed(os.path.join(HERE, "track.npz"), **golden_track(T, GEO))
+        if "c1" in want:
+            np.savez_compressed(os.path.join(HERE, "c1.npz"), **golden_c1(G, GEO, M, R, RgbdFrame))
+        if "window" in want:
+            np.savez_compressed(os.path.join(HERE, "window.npz"), **golden_window(G, GEO, R))
+        if "eig" in want:
+            np.savez_compressed(os.path.join(HERE, "eig.npz"), **golden_eig(GEO))
+        if "track" in want:
+            np.savez_compressed(os.path.join(HERE, "track.npz"), **golden_track(T, GEO))
+        if "ssim" in want:
+            np.savez_compressed(os.path.join(HERE, "ssim.npz"),
+                                **golden_ssim(M, G, GEO, R, RgbdFrame))
     finally:
         shutil.rmtree(tmp, ignore_errors=True)
     for f in sorted(os.listdir(HERE)):
