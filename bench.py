@@ -38,6 +38,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c4", choices=["c3", "c4", "c5"])
+    ap.add_argument("--tau", type=float, default=0.0,
+                    help="SSIM weight of the objective (BASELINE C4: colour+depth L1, tau 0)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-track", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -198,7 +200,7 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=dev)
     wc = make_config(args.config, dev)
     views = list(range(rank, len(wc.poses), world))
-    wm = WindowMapper(wc.frames, wc.poses, wc.intr, wc.params, MapperConfig(tau=0.0),
+    wm = WindowMapper(wc.frames, wc.poses, wc.intr, wc.params, MapperConfig(tau=args.tau),
                       views=views, device=dev)
     if os.environ.get("SGAD_PIPELINE") == "0":  # A/B: no prepare/composite overlap
         wm.pipelined = False
@@ -279,6 +281,13 @@ def run_ours(args):
     if not args.no_e2e:
         e2e = measure_e2e(wm, args, dev, world)
 
+    ssim_line = None
+    if rank == 0:
+        try:
+            ssim_line = bench_ssim(dev)
+        except Exception as exc:
+            ssim_line = {"error": repr(exc)}
+
     track = None
     if not args.no_track and rank == 0:
         try:
@@ -297,7 +306,8 @@ def run_ours(args):
                 "dtype": "f64 composite / fp32 params", "data": "synthetic",
                 "config": {"workload": f"{args.config.upper()}: {wm.W}x{wm.H}, "
                                        f"{n_views_total}-keyframe window, all learnable, "
-                                       "tau=0 L1 colour+depth, Adam",
+                                       f"tau={args.tau:g} L1 colour+depth"
+                                       f"{' + SSIM' if args.tau else ''}, Adam",
                            "gaussians": n_g, "views_per_step": n_views_total,
                            "parallelism": f"views sharded over {world} GPU(s), NCCL all-reduce",
                            "l2": "inputs larger than L2 (params 183 MB + records ~350 MB/view)"},
@@ -305,7 +315,7 @@ def run_ours(args):
                 "keyframes_per_s": n_views_total * 1e3 / ms_step / 100.0,
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": launches,
-                "clocks": sampler.summary(), "tracking": track}
+                "clocks": sampler.summary(), "tracking": track, "ssim_term": ssim_line}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
@@ -355,6 +365,37 @@ def measure_e2e(wm, args, dev, world):
     return {"value": wm.n_gaussians * wm.F * steps / (ms / 1e3), "unit": UNIT,
             "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
             "ms_per_step": ms / steps, "steps": steps}
+
+
+def bench_ssim(dev, reps=20):
+    """SSIM term (tau != 0 objective) at C4 size: sgad_ssim with the fused
+    colour upstream on a 1200x680x3 pair (fp64 render, fp32 target), CUDA
+    events on the launching stream.  Algorithmic bytes per call: images read
+    twice (8 + 4 B per value), three fp64 maps written and read (48 B), the
+    upstream written (8 B) = 72 B per pixel-channel."""
+    import torch
+    from paper_2603_21055_b200.ssim import ssim_sum, workspace_bytes
+    h, w, c = 680, 1200, 3
+    g = torch.Generator(device=dev).manual_seed(5)
+    a = torch.rand((h, w, c), dtype=torch.float64, device=dev, generator=g)
+    b = torch.rand((h, w, c), dtype=torch.float32, device=dev, generator=g)
+    acc = torch.zeros((), dtype=torch.float64, device=dev)
+    up = torch.empty_like(a)
+    ws = torch.empty(workspace_bytes(h, w, c) // 8, dtype=torch.float64, device=dev)
+    for _ in range(3):
+        ssim_sum(a, b, acc, up, ws, kc=0.8 / a.numel(), tau=0.2, upstream=True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(reps):
+        ssim_sum(a, b, acc, up, ws, kc=0.8 / a.numel(), tau=0.2, upstream=True)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    peak, kind = load_peaks()
+    gbs = 72.0 * a.numel() / (ms / 1e3) / 1e9
+    return {"kernel": "sgad_ssim (stats + grad, fused upstream)", "ms_per_view": ms,
+            "achieved_gbs": gbs, "peak_gbs": peak, "frac": gbs / peak, "image": [h, w, c]}
 
 
 def bench_tracking(dev, iters=20, reps=5):
