@@ -294,6 +294,10 @@ def run_ours(args):
             track = bench_tracking(dev)
         except Exception as exc:  # tracking is the secondary metric
             track = {"error": repr(exc)}
+        try:
+            track["render_init"] = bench_render_init(dev)
+        except Exception as exc:
+            track["render_init"] = {"error": repr(exc)}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -396,6 +400,30 @@ def bench_ssim(dev, reps=20):
     gbs = 72.0 * a.numel() / (ms / 1e3) / 1e9
     return {"kernel": "sgad_ssim (stats + grad, fused upstream)", "ms_per_view": ms,
             "achieved_gbs": gbs, "peak_gbs": peak, "frac": gbs / peak, "image": [h, w, c]}
+
+
+def bench_render_init(dev, iters=3):
+    """Render-based pose initialiser (tracker.py:354-426) at C4 size (room
+    scene, 1200x680): wall time per IRLS-GN iteration (13 renders + halving
+    candidates on the GPU, 6x6 solves on the host)."""
+    import torch
+    from paper_2603_21055_b200 import scenes
+    from paper_2603_21055_b200.gaussians import PixelGaussianMap
+    from paper_2603_21055_b200.geometry import Pose
+    from paper_2603_21055_b200.tracker import init_pose_render
+    intr, fa, fb, p, truth = scenes.config_render_init(intr_kw=scenes.C4_INTR,
+                                                       scene=scenes.room_scene(0), device=dev)
+    m = PixelGaussianMap(0, Pose.identity(), intr, p.base_depth, p.delta, p.color, p.log_radius,
+                         p.opacity_logit, p.active_mask, dtype=torch.float64, device=dev)
+    init_pose_render(fb, m, Pose.identity(), iters=1)  # warm-up
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    pose, ok = init_pose_render(fb, m, Pose.identity(), iters=iters)
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    return {"metric": "render-based pose init (1200x680, IRLS-GN, central-difference "
+                      "Jacobian through the GPU rasterizer)",
+            "ms_per_iteration": dt / iters * 1e3, "iterations": iters, "ok": bool(ok)}
 
 
 def bench_tracking(dev, iters=20, reps=5):

@@ -236,3 +236,61 @@ def gicp_align(l_centers, l_cov, g_centers, g_cov, g_normals, init_rot, init_t, 
             diag.converged = True
             break
     return R, t, diag
+
+
+# ---------------------------------------------------------------------------
+# Render-based pose initialiser (tracker.py:354-426), restated on the oracle
+# rasterizer: L1 photometric + weighted, valid-masked L1 depth residuals, a
+# central-difference Jacobian through the renderer (step 1e-4 on each twist
+# component, applied on the left), three IRLS solves per linearisation
+# (weights 1 / max(|predicted residual|, 1e-3), least squares), up to 5 step
+# halvings, a coverage gate (alpha > 0.5 on >= 30 % of the pixels).
+
+def _compose(ra, ta, rb, tb):
+    return ra @ rb, ra @ tb + ta
+
+
+def init_pose_render(tcolor, tdepth, tmask, prev_map, init_rot, init_t, intr, iters=10,
+                     depth_weight=4.0, coverage_min=0.3):
+    from . import raster as R
+    tc = np.asarray(tcolor, dtype=np.float64)
+    td = np.asarray(tdepth, dtype=np.float64)
+    m = np.asarray(tmask, dtype=np.float64)
+
+    def resid(rot, t):
+        out = R.splat([prev_map], rot, t, intr)
+        return np.concatenate([(out.color - tc).ravel(),
+                               (depth_weight * m * (out.depth - td)).ravel()])
+
+    cover = float((R.splat([prev_map], init_rot, init_t, intr).alpha > 0.5).mean())
+    if cover < coverage_min:
+        return init_rot, init_t, False
+    rot, t = np.asarray(init_rot, dtype=np.float64), np.asarray(init_t, dtype=np.float64)
+    step = 1e-4
+    r = resid(rot, t)
+    for _ in range(iters):
+        jac = np.empty((r.size, 6))
+        for k in range(6):
+            tw = np.zeros(6)
+            tw[k] = step
+            ep, em = se3_exp(tw), se3_exp(-tw)
+            jac[:, k] = (resid(*_compose(*ep, rot, t)) - resid(*_compose(*em, rot, t))) / (2 * step)
+        xi = np.zeros(6)
+        for _irls in range(3):
+            wts = 1.0 / np.maximum(np.abs(r + jac @ xi), 1e-3)
+            xi = np.linalg.lstsq(jac.T @ (jac * wts[:, None]), -(jac.T @ (wts * r)), rcond=None)[0]
+        cost = float(np.abs(r).sum())
+        cand = _compose(*se3_exp(xi), rot, t)
+        rc = resid(*cand)
+        halvings = 0
+        while float(np.abs(rc).sum()) > cost and halvings < 5:
+            xi = 0.5 * xi
+            cand = _compose(*se3_exp(xi), rot, t)
+            rc = resid(*cand)
+            halvings += 1
+        if float(np.abs(rc).sum()) > cost:
+            break
+        (rot, t), r = cand, rc
+        if np.linalg.norm(xi) < 1e-7:
+            break
+    return rot, t, True

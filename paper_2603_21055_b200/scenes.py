@@ -329,6 +329,24 @@ def config_c1(device="cpu"):
     return intr, frame, random_params(frame, 1), random_params(frame, 2)
 
 
+def config_render_init(device="cpu", angle_deg=1.0, shift_m=0.02, seed=6, intr_kw=None,
+                       scene=None):
+    """Render-based pose initialisation case (tracker.py:354-426): the map of
+    frame A (identity pose, reference init_gaussians parameters) and a query
+    frame B of the same scene (default: C1) under a seeded SE(3) offset."""
+    intr = Intrinsics(**(intr_kw or C1_INTR))
+    prims = scene if scene is not None else plane_spheres_scene(0)
+    frame_a = render_frame(prims, Pose.identity(), intr, 0, device=device)
+    rng = np.random.default_rng(seed)
+    axis = rng.normal(size=3)
+    axis /= np.linalg.norm(axis)
+    shift = rng.normal(size=3)
+    shift *= shift_m / np.linalg.norm(shift)
+    truth = se3_exp(np.concatenate([axis * np.deg2rad(angle_deg), shift]))
+    frame_b = render_frame(prims, truth, intr, 1, device=device)
+    return intr, frame_a, frame_b, init_params(frame_a), truth
+
+
 def config_window(name: str, n_frames: int, intr_kw: dict, device="cpu", scene=None,
                   step_m=0.05, step_deg=2.0) -> WindowConfig:
     intr = Intrinsics(**intr_kw)

@@ -379,3 +379,104 @@ def gicp_align(local: LocalGeomSet, global_set: GlobalGeomSet, init: Pose, cfg: 
 def init_pose_constant_speed(prev: Pose, prev_prev: Pose) -> Pose:
     """tracker.py:349-351."""
     return prev.compose(prev_prev.inverse().compose(prev))
+
+
+class _RenderResiduals:
+    """Residual vector of tracker.py:379-383 on the GPU: the previous frame's
+    map rendered at a candidate pose (K1-K4 through one raster handle with
+    preallocated images), L1 photometric and valid-masked, weighted depth
+    residuals concatenated into one device fp64 vector."""
+
+    def __init__(self, frame, prev_map, depth_weight: float):
+        from .rasterizer import Raster, build_frames, camera_of  # noqa: F401
+        self.intr = frame.intrinsics
+        self.map = prev_map
+        dev = prev_map.planes.device
+        self.dev = dev
+        h, w = int(self.intr.height), int(self.intr.width)
+        self.tc = torch.as_tensor(np.asarray(frame.color, dtype=np.float64), device=dev)
+        self.td = torch.as_tensor(np.asarray(frame.depth, dtype=np.float64), device=dev)
+        self.wm = depth_weight * torch.as_tensor(np.asarray(frame.valid_mask, dtype=np.float64),
+                                                 device=dev)
+        self.color = torch.empty((h, w, 3), dtype=torch.float64, device=dev)
+        self.depth = torch.empty((h, w), dtype=torch.float64, device=dev)
+        self.alpha = torch.empty((h, w), dtype=torch.float64, device=dev)
+        self.raster = Raster(dev)
+        self.cam = camera_of(self.intr)
+        self.n = 4 * h * w
+
+    def render(self, pose: Pose) -> None:
+        from .rasterizer import build_frames
+        frames = build_frames([self.map], pose, set())[0]
+        ns, _ = self.raster.prepare(frames, self.cam)
+        if ns:
+            self.raster.forward(self.color, self.depth, self.alpha)
+        else:
+            self.color.zero_()
+            self.depth.zero_()
+            self.alpha.zero_()
+
+    def __call__(self, pose: Pose, out=None) -> torch.Tensor:
+        self.render(pose)
+        r = out if out is not None else torch.empty(self.n, dtype=torch.float64, device=self.dev)
+        nc = self.color.numel()
+        torch.sub(self.color.reshape(-1), self.tc.reshape(-1), out=r[:nc])
+        torch.mul(self.wm.reshape(-1), self.depth.reshape(-1) - self.td.reshape(-1), out=r[nc:])
+        return r
+
+    def coverage(self, pose: Pose) -> float:
+        self.render(pose)
+        return float((self.alpha > 0.5).double().mean())
+
+
+def init_pose_render(frame, prev_map, init: Pose, iters: int = 10, depth_weight: float = 4.0,
+                     coverage_min: float = 0.3):
+    """tracker.py:354-426: refine ``init`` by rendering ``prev_map`` (a device
+    PixelGaussianMap) against ``frame`` -- IRLS Gauss-Newton on the L1
+    photometric + weighted L1 depth residuals with a central-difference
+    Jacobian through the renderer.  Every render (13 per iteration plus the
+    step-halving candidates) runs on the sm_100a rasterizer; residuals, the
+    Jacobian and the 6x6 IRLS systems stay on the device and only the 6x6
+    least-squares solves run on the host, as in the reference.  Returns
+    ``(pose, ok)``; ``ok`` is False (and ``init`` returned) when the map
+    covers less than ``coverage_min`` of the frame."""
+    res = _RenderResiduals(frame, prev_map, depth_weight)
+    if res.coverage(init) < coverage_min:
+        return init, False
+    pose = init
+    h = 1e-4
+    r = res(pose).clone()
+    jac = torch.empty((res.n, 6), dtype=torch.float64, device=res.dev)
+    rp = torch.empty(res.n, dtype=torch.float64, device=res.dev)
+    rm = torch.empty(res.n, dtype=torch.float64, device=res.dev)
+    for _ in range(iters):
+        for k in range(6):
+            e = np.zeros(6)
+            e[k] = h
+            res(se3_exp(e).compose(pose), out=rp)
+            res(se3_exp(-e).compose(pose), out=rm)
+            torch.sub(rp, rm, out=jac[:, k])
+        jac.div_(2.0 * h)
+        # IRLS on the same linearisation: weights from the predicted residuals
+        xi = np.zeros(6)
+        for _inner in range(3):
+            r_pred = r + jac @ torch.as_tensor(xi, device=res.dev)
+            wts = 1.0 / torch.clamp(r_pred.abs(), min=1e-3)
+            hw = (jac.T @ (jac * wts[:, None])).cpu().numpy()
+            gw = (jac.T @ (wts * r)).cpu().numpy()
+            xi = np.linalg.lstsq(hw, -gw, rcond=None)[0]
+        cost = float(r.abs().sum())
+        candidate = se3_exp(xi).compose(pose)
+        r_cand = res(candidate)
+        halvings = 0
+        while float(r_cand.abs().sum()) > cost and halvings < MAX_STEP_HALVINGS:
+            xi = 0.5 * xi
+            candidate = se3_exp(xi).compose(pose)
+            r_cand = res(candidate)
+            halvings += 1
+        if float(r_cand.abs().sum()) > cost:
+            break
+        pose, r = candidate, r_cand.clone()
+        if np.linalg.norm(xi) < 1e-7:
+            break
+    return pose, True

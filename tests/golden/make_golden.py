@@ -2,7 +2,7 @@
 
 Run in the build container (where /root/reference exists):
 
-    python tests/golden/make_golden.py [c1 window eig track ssim]
+    python tests/golden/make_golden.py [c1 window eig track ssim render_init]
 
 The reference package is copied to a temporary directory first (so nothing is
 written under /root/reference: Numba's cache and __pycache__ land in the
@@ -308,9 +308,32 @@ def golden_track(T, GEO):
     return d
 
 
+def golden_render_init(G, GEO, T, RgbdFrame):
+    """tracker.py:354-426 (init_pose_render) on the C1 scene: the map of frame
+    A against frame B under a seeded offset, from the identity, plus a
+    low-coverage case (the map shifted out of view) that must return the
+    initial pose with ok = False."""
+    from paper_2603_21055_b200 import scenes
+    intr, fa, fb, params, truth = scenes.config_render_init()
+    ri = ref_intr(GEO, intr)
+    ident = GEO.Pose.identity()
+    m = ref_map(G, GEO, params, ri, ident, 0)
+    tf = RgbdFrame(color=fb.color, depth=fb.depth, valid_mask=fb.valid_mask, intrinsics=ri,
+                   timestamp=0.0, index=1)
+    d = {"truth_R": truth.rotation, "truth_t": truth.translation}
+    for iters in (1, 10):
+        pose, ok = T.init_pose_render(tf, m, ident, iters=iters)
+        d[f"it{iters}_R"], d[f"it{iters}_t"], d[f"it{iters}_ok"] = (pose.rotation,
+                                                                   pose.translation, np.array(ok))
+    far = GEO.Pose(np.eye(3), np.array([5.0, 0.0, 0.0]))
+    pose, ok = T.init_pose_render(tf, m, far, iters=3)
+    d["far_R"], d["far_t"], d["far_ok"] = pose.rotation, pose.translation, np.array(ok)
+    return d
+
+
 def main():
     sys.path.insert(0, ROOT)
-    want = set(sys.argv[1:]) or {"c1", "window", "eig", "track", "ssim"}
+    want = set(sys.argv[1:]) or {"c1", "window", "eig", "track", "ssim", "render_init"}
     tmp, G, GEO, M, R, T, RgbdFrame = import_reference()
     try:
         if "c1" in want:
@@ -321,6 +344,9 @@ def main():
             np.savez_compressed(os.path.join(HERE, "eig.npz"), **golden_eig(GEO))
         if "track" in want:
             np.savez_compressed(os.path.join(HERE, "track.npz"), **golden_track(T, GEO))
+        if "render_init" in want:
+            np.savez_compressed(os.path.join(HERE, "render_init.npz"),
+                                **golden_render_init(G, GEO, T, RgbdFrame))
         if "ssim" in want:
             np.savez_compressed(os.path.join(HERE, "ssim.npz"),
                                 **golden_ssim(M, G, GEO, R, RgbdFrame))
