@@ -441,7 +441,12 @@ def bench_tracking(dev, iters=20, reps=5):
     cfg = T.TrackerConfig(downsample_ratio=1, max_gicp_iters=iters, convergence_eps=0.0,
                           voxel_size=1e-4)
     g = T.GlobalGeomSet(cfg.voxel_size)
-    T.update_global_set(g, T.build_local_set(ref, cfg), Pose.identity())
+    ref_local = T.build_local_set(ref, cfg)
+    torch.cuda.synchronize()
+    t_ins = time.perf_counter()
+    T.update_global_set(g, ref_local, Pose.identity())
+    torch.cuda.synchronize()
+    insert_ms = (time.perf_counter() - t_ins) * 1e3
     local = T.build_local_set(qry, cfg)
     T.gicp_align(local, g, Pose.identity(), cfg)  # warm-up
     torch.cuda.synchronize()
@@ -458,7 +463,8 @@ def bench_tracking(dev, iters=20, reps=5):
     fit_ms = (time.perf_counter() - t1) / reps * 1e3
     return {"metric": "tracking GN iterations/s (1200x680, 5x5 window fit, exact NN, host solve)",
             "value": n_it / dt, "unit": "GN iters/s", "correspondences": len(local),
-            "iterations_per_run": diag.iterations, "fit_ms_per_frame": fit_ms}
+            "iterations_per_run": diag.iterations, "fit_ms_per_frame": fit_ms,
+            "global_insert_ms": insert_ms, "global_members": len(g)}
 
 
 def main():

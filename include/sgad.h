@@ -18,6 +18,7 @@
  *   sgad_raster_backward  <- rasterizer.py:272-363 (_backward_kernel) and the
  *                            chain rule :451-483 (splat_backward)
  *   sgad_adam_step        <- mapper.py:73-95 (MapOptimizer.step)
+ *   sgad_voxels_*         <- tracker.py:105-122 (GlobalGeomSet.insert cell gating)
  *   sgad_ssim             <- ssim.py:31-87 (ssim(..., with_grad)), the tau term
  *                            of mapping_loss (mapper.py:126-147)
  *   sgad_track_fit        <- tracker.py:144-170, :193-230 (build_local_set with
@@ -206,6 +207,20 @@ int sgad_track_accepted(sgad_geomset* g, uint8_t* out, int64_t m, void* stream);
  * (device). */
 int sgad_track_cost(sgad_geomset* g, const double* local_centers, int64_t m, const double* poses,
                     int32_t n_cand, double* out, void* stream);
+
+/* ---- voxel occupancy of the global geometry set -----------------------
+ * Replaces the cell gating of GlobalGeomSet.insert (tracker.py:105-122): a
+ * device hash table of occupied cells floor(center / voxel_size).  For a
+ * batch of centers (device [n, 3] fp64) keep[i] (device u8) = 1 iff row i's
+ * cell is not occupied by an earlier batch and no earlier row of this batch
+ * has the same cell; the kept cells become occupied; *n_keep (host) = the
+ * number kept.  Cells must satisfy |cell| < 2^20 per axis (else SGAD_E_INVALID
+ * and the batch is not inserted). */
+typedef struct sgad_voxels sgad_voxels;
+int sgad_voxels_create(sgad_voxels** out);
+int sgad_voxels_destroy(sgad_voxels* v);
+int sgad_voxels_gate(sgad_voxels* v, const double* centers, int64_t n, double voxel_size,
+                     uint8_t* keep, int64_t* n_keep, void* stream);
 
 #ifdef __cplusplus
 }

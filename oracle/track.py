@@ -294,3 +294,22 @@ def init_pose_render(tcolor, tdepth, tmask, prev_map, init_rot, init_t, intr, it
         if np.linalg.norm(xi) < 1e-7:
             break
     return rot, t, True
+
+
+class VoxelSet:
+    """Cell gating of GlobalGeomSet.insert (tracker.py:101-122) restated: at
+    most one member per cell floor(c / voxel), first come first served in row
+    order within a batch."""
+
+    def __init__(self, voxel):
+        self.voxel = voxel
+        self.cells = set()
+
+    def gate(self, centers):
+        keys = np.floor(np.asarray(centers, dtype=np.float64) / self.voxel).astype(np.int64)
+        keep = np.zeros(len(keys), dtype=bool)
+        for i, k in enumerate(map(tuple, keys)):
+            if k not in self.cells:
+                self.cells.add(k)
+                keep[i] = True
+        return keep

@@ -179,8 +179,9 @@ class GlobalGeomSet:
     """World-frame geometry Gaussians with an exact 1-NN index (tracker.py:81-133).
 
     Insertion keeps the reference's voxel gating (one member per cell, first
-    come first served) on the host; the members live on the device with a
-    uniform-grid index rebuilt per insert, like the reference's cKDTree."""
+    come first served in row order) with a device hash table of occupied
+    cells (csrc/voxels.cu); the members live on the device with a multi-level
+    grid index rebuilt per insert, like the reference's cKDTree."""
 
     def __init__(self, voxel_size: float = 0.02):
         if voxel_size <= 0:
@@ -192,51 +193,68 @@ class GlobalGeomSet:
         self.scales = torch.empty((0, 3), dtype=torch.float64, device=dev)
         self.normals = torch.empty((0, 3), dtype=torch.float64, device=dev)
         self.cov6 = torch.empty((0, 6), dtype=torch.float64, device=dev)
-        self._cells: set = set()
         h = ctypes.c_void_p()
         N.check(N.load().sgad_geomset_create(ctypes.byref(h)))
         self._h = h
+        v = ctypes.c_void_p()
+        N.check(N.load().sgad_voxels_create(ctypes.byref(v)))
+        self._vox = v
 
     def __del__(self):
         try:
+            lib = N.load(require_cuda=False)
             if self._h:
-                N.load(require_cuda=False).sgad_geomset_destroy(self._h)
+                lib.sgad_geomset_destroy(self._h)
                 self._h = None
+            if getattr(self, "_vox", None):
+                lib.sgad_voxels_destroy(self._vox)
+                self._vox = None
         except Exception:
             pass
 
     def __len__(self) -> int:
         return int(self.centers.shape[0])
 
+    def _gate(self, c: torch.Tensor) -> torch.Tensor:
+        keep = torch.empty(c.shape[0], dtype=torch.uint8, device=c.device)
+        n_keep = ctypes.c_int64()
+        rc = N.load().sgad_voxels_gate(self._vox, N.ptr(c), int(c.shape[0]),
+                                       float(self.voxel_size), N.ptr(keep),
+                                       ctypes.byref(n_keep), N.stream_ptr())
+        if rc != N.SGAD_OK:
+            raise TrackerError(N.load().sgad_last_error().decode())
+        return keep.bool()
+
     def insert(self, centers, rotations, scales, normals) -> int:
-        c = _t(centers)
-        keys = np.floor(c.cpu().numpy() / self.voxel_size).astype(np.int64)
-        keep, batch = [], set()
-        for i, key in enumerate(map(tuple, keys)):
-            if key in self._cells or key in batch:
-                continue
-            batch.add(key)
-            keep.append(i)
-        if keep:
-            idx = torch.as_tensor(keep, device=c.device)
-            rot, sc = _t(rotations)[idx], _t(scales)[idx]
-            self.centers = torch.cat([self.centers, c[idx]])
+        """tracker.py:105-122: rows whose voxel cell is free join the set (in
+        row order); returns the number added."""
+        c = _t(centers).reshape(-1, 3).contiguous()
+        keep = self._gate(c)
+        n = int(keep.sum())
+        if n:
+            rot, sc = _t(rotations)[keep], _t(scales)[keep]
+            self.centers = torch.cat([self.centers, c[keep]])
             self.rotations = torch.cat([self.rotations, rot])
             self.scales = torch.cat([self.scales, sc])
-            self.normals = torch.cat([self.normals, _t(normals)[idx]])
+            self.normals = torch.cat([self.normals, _t(normals)[keep]])
             self.cov6 = torch.cat([self.cov6, cov_packed(_cov_from(rot, sc))])
-            self._cells |= batch
             N.call("sgad_geomset_set", self._h, self.centers.data_ptr(), self.cov6.data_ptr(),
                    self.normals.data_ptr(), len(self), N.stream_ptr())
-        return len(keep)
+        return n
 
     def set_members(self, centers, cov6, normals, rotations=None, scales=None):
         """Replace the members wholesale (no voxel gating): the C2/C5 target set."""
         self.centers, self.cov6, self.normals = _t(centers), _t(cov6), _t(normals)
         self.rotations = _t(rotations) if rotations is not None else self.rotations[:0]
         self.scales = _t(scales) if scales is not None else self.scales[:0]
-        self._cells = set(map(tuple, np.floor(self.centers.cpu().numpy() /
-                                              self.voxel_size).astype(np.int64)))
+        # the occupancy restarts from exactly these members' cells
+        lib = N.load()
+        lib.sgad_voxels_destroy(self._vox)
+        v = ctypes.c_void_p()
+        N.check(lib.sgad_voxels_create(ctypes.byref(v)))
+        self._vox = v
+        if len(self):
+            self._gate(self.centers.contiguous())
         N.call("sgad_geomset_set", self._h, self.centers.data_ptr(), self.cov6.data_ptr(),
                self.normals.data_ptr(), len(self), N.stream_ptr())
 

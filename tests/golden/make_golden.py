@@ -2,7 +2,7 @@
 
 Run in the build container (where /root/reference exists):
 
-    python tests/golden/make_golden.py [c1 window eig track ssim render_init]
+    python tests/golden/make_golden.py [c1 window eig track ssim render_init voxels]
 
 The reference package is copied to a temporary directory first (so nothing is
 written under /root/reference: Numba's cache and __pycache__ land in the
@@ -331,9 +331,28 @@ def golden_render_init(G, GEO, T, RgbdFrame):
     return d
 
 
+def golden_voxels(T):
+    """GlobalGeomSet.insert (tracker.py:105-122) on seeded batches with many
+    cell collisions (within and across batches, negative coordinates)."""
+    rng = np.random.default_rng(31)
+    g = T.GlobalGeomSet(voxel_size=0.05)
+    d = {}
+    for b in range(3):
+        n = 4000
+        c = rng.uniform(-1.0, 1.0, (n, 3)) * np.array([1.0, 0.5, 0.25])
+        c[n // 2:] = c[: n - n // 2] + rng.normal(0, 0.01, (n - n // 2, 3))  # near-duplicates
+        rot = np.repeat(np.eye(3)[None], n, axis=0)
+        sc = rng.uniform(0.01, 0.1, (n, 3))
+        nr = np.tile([0.0, 0.0, -1.0], (n, 1))
+        added = g.insert(c, rot, sc, nr)
+        d[f"b{b}_centers"], d[f"b{b}_scales"], d[f"b{b}_added"] = c, sc, np.array(added)
+        d[f"b{b}_members"] = g.centers.copy()
+    return d
+
+
 def main():
     sys.path.insert(0, ROOT)
-    want = set(sys.argv[1:]) or {"c1", "window", "eig", "track", "ssim", "render_init"}
+    want = set(sys.argv[1:]) or {"c1", "window", "eig", "track", "ssim", "render_init", "voxels"}
     tmp, G, GEO, M, R, T, RgbdFrame = import_reference()
     try:
         if "c1" in want:
@@ -344,6 +363,8 @@ def main():
             np.savez_compressed(os.path.join(HERE, "eig.npz"), **golden_eig(GEO))
         if "track" in want:
             np.savez_compressed(os.path.join(HERE, "track.npz"), **golden_track(T, GEO))
+        if "voxels" in want:
+            np.savez_compressed(os.path.join(HERE, "voxels.npz"), **golden_voxels(T))
         if "render_init" in want:
             np.savez_compressed(os.path.join(HERE, "render_init.npz"),
                                 **golden_render_init(G, GEO, T, RgbdFrame))
