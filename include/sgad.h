@@ -19,6 +19,7 @@
  *                            chain rule :451-483 (splat_backward)
  *   sgad_adam_step        <- mapper.py:73-95 (MapOptimizer.step)
  *   sgad_voxels_*         <- tracker.py:105-122 (GlobalGeomSet.insert cell gating)
+ *   sgad_inpaint_jacobi   <- datasets.py:368-398 (inpaint_depth sweeps)
  *   sgad_ssim             <- ssim.py:31-87 (ssim(..., with_grad)), the tau term
  *                            of mapping_loss (mapper.py:126-147)
  *   sgad_track_fit        <- tracker.py:144-170, :193-230 (build_local_set with
@@ -139,6 +140,17 @@ int sgad_raster_tile_count(sgad_raster* h, int64_t* n_tiles);
 int sgad_adam_step(void* params, void* grads, void* m, void* v, int64_t n_frames, int64_t hw,
                    const double* lr, double beta1, double beta2, double eps, double bc1,
                    double bc2, int32_t update_delta, int32_t f64, void* stream);
+
+/* ---- harmonic depth inpainting ----------------------------------------
+ * Replaces the Jacobi loop of raysplat/datasets.py:388-397 (inpaint_depth):
+ * depth (device [H, W] fp64, holes already seeded with their nearest valid
+ * value) is relaxed in place over the pixels with hole[p] != 0 until the
+ * sweep whose largest update is below tol, or max_iters sweeps; scratch is a
+ * device [H, W] fp64 buffer; *sweeps (host) = sweeps applied.  Synchronises
+ * the stream. */
+int sgad_inpaint_jacobi(double* depth, const uint8_t* hole, int32_t height, int32_t width,
+                        int32_t max_iters, double tol, double* scratch, int32_t* sweeps,
+                        void* stream);
 
 /* ---- SSIM term (tau != 0 objective) ------------------------------------
  * Replaces raysplat/ssim.py:31-87 (ssim(img_a, img_b, with_grad)) as used by

@@ -313,3 +313,29 @@ class VoxelSet:
                 self.cells.add(k)
                 keep[i] = True
         return keep
+
+
+def inpaint_depth(depth, valid_mask, max_iters=200, tol=1e-5):
+    """datasets.py:368-398 restated: nearest-valid seeding (scipy's Euclidean
+    distance transform, the reference's call) then Jacobi sweeps of the
+    Laplace equation on the holes with edge-replicated borders, stopping
+    after the first sweep whose largest update is below ``tol``."""
+    from scipy import ndimage
+    z = np.asarray(depth, dtype=np.float64)
+    ok = np.asarray(valid_mask, dtype=bool) & (z > 0)
+    if not ok.any():
+        raise ValueError("cannot inpaint a frame with no valid depth")
+    if ok.all():
+        return z.copy()
+    _, (iy, ix) = ndimage.distance_transform_edt(~ok, return_indices=True)
+    cur = z[iy, ix]
+    cur[ok] = z[ok]
+    holes = ~ok
+    for _ in range(max_iters):
+        e = np.pad(cur, 1, mode="edge")
+        nxt = 0.25 * (e[:-2, 1:-1] + e[2:, 1:-1] + e[1:-1, :-2] + e[1:-1, 2:])
+        step = np.abs(nxt[holes] - cur[holes]).max()
+        cur[holes] = nxt[holes]
+        if step < tol:
+            break
+    return cur

@@ -155,3 +155,65 @@ def init_gaussians(frame, pose: Pose, base_depth=None, device=None,
         base_depth=np.where(active, base, 0.0), delta=np.zeros_like(base),
         color=np.asarray(frame.color, dtype=np.float64), log_radius=np.log(safe / frame.intrinsics.fx),
         opacity_logit=np.zeros_like(base), active_mask=active, device=device, dtype=dtype)
+
+
+# ---------------------------------------------------------------- map files
+# raysplat/gaussians.py:1-15 layout, little-endian: b"RSGM", u32 version 1,
+# u32 height, u32 width, i64 frame index, 12 f64 pose entries (rotation
+# row-major, translation), 7 f32 planes (base_depth, delta, radius,
+# opacity_logit, R, G, B), one u8 active flag per pixel.
+
+MAP_MAGIC = b"RSGM"
+MAP_VERSION = 1
+_MAP_HEAD = "<4sIIIq"
+
+
+class GaussianMapError(ValueError):
+    """A malformed or truncated map file (gaussians.py)."""
+
+
+def save_gaussian_map(path, gmap: PixelGaussianMap) -> None:
+    """gaussians.py:118-136."""
+    import struct
+    h, w = gmap.shape
+    p = gmap.planes.double().cpu().numpy()
+    planes = np.stack([p[0], p[1], np.exp(p[2]), p[3], p[4], p[5], p[6]]).astype("<f4")
+    pose = np.concatenate([np.asarray(gmap.pose.rotation, dtype=np.float64).reshape(9),
+                           np.asarray(gmap.pose.translation, dtype=np.float64)]).astype("<f8")
+    with open(path, "wb") as f:
+        f.write(struct.pack(_MAP_HEAD, MAP_MAGIC, MAP_VERSION, h, w, int(gmap.frame_index)))
+        f.write(pose.tobytes())
+        f.write(planes.tobytes())
+        f.write(gmap.mask_u8.cpu().numpy().astype(np.uint8).tobytes())
+
+
+def load_gaussian_map(path, intrinsics: Intrinsics, device=None,
+                      dtype=torch.float64) -> PixelGaussianMap:
+    """gaussians.py:139-180: errors name the offending path."""
+    import struct
+    from pathlib import Path
+    path = Path(path)
+    blob = path.read_bytes()
+    head = struct.calcsize(_MAP_HEAD)
+    if len(blob) < head + 96:
+        raise GaussianMapError(f"gaussian map file too short: {path}")
+    magic, version, h, w, frame_index = struct.unpack_from(_MAP_HEAD, blob, 0)
+    if magic != MAP_MAGIC:
+        raise GaussianMapError(f"bad magic in gaussian map file: {path}")
+    if version != MAP_VERSION:
+        raise GaussianMapError(f"unsupported gaussian map version {version} in {path}")
+    want = head + 96 + 28 * h * w + h * w
+    if len(blob) != want:
+        raise GaussianMapError(f"gaussian map file {path} has {len(blob)} bytes, expected {want}")
+    pose = np.frombuffer(blob, dtype="<f8", count=12, offset=head)
+    planes = np.frombuffer(blob, dtype="<f4", count=7 * h * w, offset=head + 96).reshape(7, h, w)
+    mask = np.frombuffer(blob, dtype=np.uint8, count=h * w, offset=head + 96 + 28 * h * w)
+    radius = planes[2].astype(np.float64)
+    if (radius <= 0).any():
+        raise GaussianMapError(f"non-positive radius in gaussian map file: {path}")
+    return PixelGaussianMap(
+        int(frame_index), Pose(pose[:9].reshape(3, 3).copy(), pose[9:].copy()), intrinsics,
+        planes[0].astype(np.float64), planes[1].astype(np.float64),
+        np.stack([planes[4], planes[5], planes[6]], axis=-1).astype(np.float64),
+        np.log(radius), planes[3].astype(np.float64), mask.reshape(h, w).astype(bool),
+        device=device, dtype=dtype)

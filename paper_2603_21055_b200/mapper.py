@@ -393,3 +393,65 @@ class WindowMapper:
         g = self.grad.view(self.F, self.H, self.W, 8).double().cpu().numpy()
         return [dict(delta=g[i, ..., 0], radius=g[i, ..., 1], opacity_logit=g[i, ..., 2],
                      color=g[i, ..., 3:6]) for i in range(self.F)]
+
+
+# ---------------------------------------------------------------- per-frame driver
+
+
+def target_schedule(iters: int, n_neighbors: int, min_current_fraction: float,
+                    seed: int = 0) -> list:
+    """mapper.py:175-194: slot 0 is the current frame, 1..n its neighbours;
+    strict alternation (current on even slots, neighbours round-robin from
+    ``seed`` on odd slots) with extra current slots whenever the current
+    frame's share would drop below ``min_current_fraction``."""
+    out, n_cur, n_nb = [], 0, 0
+    for i in range(iters):
+        if n_neighbors == 0 or n_cur < min_current_fraction * (i + 1) or i % 2 == 0:
+            out.append(0)
+            n_cur += 1
+        else:
+            out.append(1 + (seed + n_nb) % n_neighbors)
+            n_nb += 1
+    return out
+
+
+def assemble_base_depth(frame, pose: Pose, neighbor_maps) -> np.ndarray:
+    """mapper.py:197-214: sensor depth where valid; holes covered by the
+    neighbours (accumulated alpha > 0.5) take their alpha-normalised rendered
+    depth (GPU splat); remaining holes are inpainted (GPU Jacobi)."""
+    from .depthfill import inpaint_depth
+    from .rasterizer import splat
+    valid = np.asarray(frame.valid_mask, dtype=bool)
+    base = np.where(valid, np.asarray(frame.depth, dtype=np.float64), 0.0)
+    if valid.all():
+        return base
+    if neighbor_maps:
+        out = splat(list(neighbor_maps), pose, frame.intrinsics, normalize_depth=True)
+        a = out.alpha.cpu().numpy()
+        d = out.depth.cpu().numpy()
+        fill = (~valid) & (a > 0.5) & (d > 0)
+        base[fill] = d[fill]
+    if (base > 0).all():
+        return base
+    return inpaint_depth(base, base > 0)
+
+
+def map_frame(frame, pose: Pose, neighbors, cfg: MapperConfig, seed: int = 0):
+    """mapper.py:217-247: fit a frame's Gaussian map at a fixed pose against a
+    deterministic schedule of targets (the frame and its neighbours, whose
+    maps are rendered alongside but never updated).  ``neighbors`` holds
+    (frame, pose, PixelGaussianMap) triples; returns (map, losses)."""
+    from .gaussians import init_gaussians
+    if not np.asarray(frame.valid_mask, dtype=bool).any():
+        raise ValueError(f"frame {frame.index} has no valid depth to map")
+    neighbors = [n for n in neighbors if np.asarray(n[0].valid_mask, dtype=bool).any()]
+    neighbor_maps = [m for _, _, m in neighbors]
+    base = assemble_base_depth(frame, pose, neighbor_maps)
+    dev = neighbor_maps[0].planes.device if neighbor_maps else None
+    gmap = init_gaussians(frame, pose, base_depth=base, device=dev)
+    opt = MapOptimizer(gmap, cfg)
+    losses = []
+    for slot in target_schedule(cfg.mapping_iters, len(neighbors), cfg.min_current_fraction, seed):
+        t_frame, t_pose = (frame, pose) if slot == 0 else neighbors[slot - 1][:2]
+        losses.append(mapping_step(gmap, opt, t_frame, t_pose, neighbor_maps, cfg).total)
+    return gmap, losses

@@ -2,7 +2,7 @@
 
 Run in the build container (where /root/reference exists):
 
-    python tests/golden/make_golden.py [c1 window eig track ssim render_init voxels]
+    python tests/golden/make_golden.py [c1 window eig track ssim render_init voxels frame_driver]
 
 The reference package is copied to a temporary directory first (so nothing is
 written under /root/reference: Numba's cache and __pycache__ land in the
@@ -350,9 +350,56 @@ def golden_voxels(T):
     return d
 
 
+def golden_frame_driver(G, GEO, M, RgbdFrame):
+    """The per-frame mapping driver and its formats, from the reference:
+    target_schedule (mapper.py:175-194), inpaint_depth (datasets.py:368-398),
+    assemble_base_depth (:197-214), map_frame (:217-247, 4 iterations, tau
+    0.2) and the .bin map file bytes (gaussians.py:118-136)."""
+    import io
+    import tempfile as _tf
+    from raysplat.datasets import inpaint_depth
+    from paper_2603_21055_b200 import scenes
+    d = {}
+    cases = [(10, 0, 0.4, 0), (25, 1, 0.4, 0), (40, 3, 0.4, 2), (17, 2, 0.7, 5), (9, 4, 0.0, 1)]
+    for i, (it, n, frac, seed) in enumerate(cases):
+        d[f"sched{i}"] = np.array(M.target_schedule(it, n, frac, seed))
+        d[f"sched{i}_args"] = np.array([it, n, frac, seed])
+    intr, fa, fb, params, truth = scenes.config_render_init()
+    rng = np.random.default_rng(12)
+    holes = rng.random(fb.depth.shape) < 0.05
+    holes[40:70, 90:130] = True            # a block the neighbour covers
+    holes[:, :6] = True                    # a border strip
+    depth = np.where(holes, 0.0, fb.depth).astype(np.float32)
+    valid = fb.valid_mask & ~holes
+    d["inpaint_in"], d["inpaint_valid"] = depth.astype(np.float64), valid
+    d["inpaint_out"] = inpaint_depth(depth.astype(np.float64), valid)
+    d["inpaint_out_short"] = inpaint_depth(depth.astype(np.float64), valid, max_iters=7)
+    ri = ref_intr(GEO, intr)
+    ident = GEO.Pose.identity()
+    tpose = GEO.Pose(truth.rotation, truth.translation)
+    map_a = ref_map(G, GEO, params, ri, ident, 0)
+    fr_a = RgbdFrame(color=fa.color, depth=fa.depth, valid_mask=fa.valid_mask, intrinsics=ri,
+                     timestamp=0.0, index=0)
+    fr_b = RgbdFrame(color=fb.color, depth=depth, valid_mask=valid, intrinsics=ri,
+                     timestamp=1.0, index=1)
+    d["base_depth"] = M.assemble_base_depth(fr_b, tpose, [map_a])
+    d["target_depth"], d["target_valid"] = depth, valid
+    cfg = M.MapperConfig(mapping_iters=4)
+    gmap, losses = M.map_frame(fr_b, tpose, [(fr_a, ident, map_a)], cfg, seed=0)
+    d["mf_losses"] = np.array(losses)
+    for k in ("base_depth", "delta", "log_radius", "opacity_logit", "color", "active_mask"):
+        d[f"mf_{k}"] = getattr(gmap, k)
+    with _tf.TemporaryDirectory() as tmp:
+        path = os.path.join(tmp, "m.bin")
+        G.save_gaussian_map(path, gmap)
+        d["mapfile"] = np.frombuffer(open(path, "rb").read(), dtype=np.uint8).copy()
+    return d
+
+
 def main():
     sys.path.insert(0, ROOT)
-    want = set(sys.argv[1:]) or {"c1", "window", "eig", "track", "ssim", "render_init", "voxels"}
+    want = set(sys.argv[1:]) or {"c1", "window", "eig", "track", "ssim", "render_init", "voxels",
+                                    "frame_driver"}
     tmp, G, GEO, M, R, T, RgbdFrame = import_reference()
     try:
         if "c1" in want:
@@ -363,6 +410,9 @@ def main():
             np.savez_compressed(os.path.join(HERE, "eig.npz"), **golden_eig(GEO))
         if "track" in want:
             np.savez_compressed(os.path.join(HERE, "track.npz"), **golden_track(T, GEO))
+        if "frame_driver" in want:
+            np.savez_compressed(os.path.join(HERE, "frame_driver.npz"),
+                                **golden_frame_driver(G, GEO, M, RgbdFrame))
         if "voxels" in want:
             np.savez_compressed(os.path.join(HERE, "voxels.npz"), **golden_voxels(T))
         if "render_init" in want:
