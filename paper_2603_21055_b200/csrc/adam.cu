@@ -53,6 +53,40 @@ k_adam(P* __restrict__ params, P* __restrict__ grads, P* __restrict__ m,
   }
 }
 
+// The window engine's fp32 parameters (delta D4): the same update in fp32
+// arithmetic -- reciprocals of the bias corrections precomputed, fast exp /
+// sqrt -- so the step is bound by its 216 bytes per Gaussian, not by fp64
+// division and square-root sequences.
+template <>
+__global__ void __launch_bounds__(256)
+k_adam<float>(float* __restrict__ params, float* __restrict__ grads, float* __restrict__ m,
+              float* __restrict__ v, int64_t n_frames, int64_t hw, AdamArgs a) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_frames * hw) return;
+  const int64_t f = i / hw, p = i - f * hw;
+  float4* gp = reinterpret_cast<float4*>(grads + 8 * i);
+  const float4 g0 = gp[0], g1 = gp[1];
+  gp[0] = make_float4(0.f, 0.f, 0.f, 0.f);
+  gp[1] = make_float4(0.f, 0.f, 0.f, 0.f);
+  float* pf = params + f * 7 * hw + p;
+  float* mf = m + f * 6 * hw + p;
+  float* vf = v + f * 6 * hw + p;
+  const float b1 = (float)a.b1, b2 = (float)a.b2, eps = (float)a.eps;
+  const float ib1 = (float)(1.0 / a.bc1), ib2 = (float)(1.0 / a.bc2);
+  const float g[6] = {g0.x, g0.y * __expf(pf[2 * hw]), g0.z, g0.w, g1.x, g1.y};
+#pragma unroll
+  for (int c = 0; c < 6; ++c) {
+    if (c == 0 && !a.update_delta) continue;
+    const float mm = mf[c * hw] * b1 + (1.0f - b1) * g[c];
+    const float vv = vf[c * hw] * b2 + (1.0f - b2) * g[c] * g[c];
+    float prm = pf[(c + 1) * hw] - (float)a.lr[c] * (mm * ib1) / (sqrtf(vv * ib2) + eps);
+    if (c >= 3) prm = fminf(fmaxf(prm, 0.0f), 1.0f);  // colour clip, mapper.py:95
+    pf[(c + 1) * hw] = prm;
+    mf[c * hw] = mm;
+    vf[c * hw] = vv;
+  }
+}
+
 }  // namespace sgad
 
 extern "C" int sgad_adam_step(void* params, void* grads, void* m, void* v, int64_t n_frames,
