@@ -208,6 +208,8 @@ def run_ours(args):
                       views=views, device=dev)
     if os.environ.get("SGAD_PIPELINE") == "0":  # A/B: no prepare/composite overlap
         wm.pipelined = False
+    if os.environ.get("SGAD_FUSE") == "1":  # A/B: forward + backward as one kernel
+        wm.fuse_fwd_bwd = True
     n_g = wm.n_gaussians
     n_views_total = len(wc.poses)
 
@@ -248,18 +250,24 @@ def run_ours(args):
     # roofline of the compositing kernels (SURVEY 8d algorithmic bytes)
     hw = wm.HW
 
-    def kstats(kind, extra_surv):
+    def kstats(kind, extra_surv, both=False):
         lst = [t for t in timing if t[0] == kind]
         tot_ms = sum(a.elapsed_time(b) for _, a, b, _, _, _ in lst)
-        tot_bytes = sum(36 * npairs + 20 * hw + (32 * ns if extra_surv else 0)
-                        for _, _, _, _, ns, npairs in lst)
+        per = (lambda ns, npairs: 72 * npairs + 40 * hw + 32 * ns) if both else \
+            (lambda ns, npairs: 36 * npairs + 20 * hw + (32 * ns if extra_surv else 0))
+        tot_bytes = sum(per(ns, npairs) for _, _, _, _, ns, npairs in lst)
         return tot_ms, tot_bytes, len(lst)
 
     f_ms, f_bytes, f_n = kstats("fwd", False)
     b_ms, b_bytes, b_n = kstats("bwd", True)
+    fb_ms, fb_bytes, fb_n = kstats("fb", False, both=True)
     p_ms, _, p_n = kstats("prep", False)
     peak, peak_kind = load_peaks()
-    dom = ("k_backward", b_ms, b_bytes, b_n) if b_ms >= f_ms else ("k_forward", f_ms, f_bytes, f_n)
+    if fb_n:  # forward + loss + backward in one kernel (tau = 0)
+        dom = ("k_forward_backward", fb_ms, fb_bytes, fb_n)
+    else:
+        dom = ("k_backward", b_ms, b_bytes, b_n) if b_ms >= f_ms else \
+            ("k_forward", f_ms, f_bytes, f_n)
     achieved = dom[2] / dom[3] / (dom[1] / dom[3] / 1e3) / 1e9
     counts = list(wm.last_counts.values())
     mean_ns = float(np.mean([c[0] for c in counts])) if counts else 0.0
@@ -275,7 +283,9 @@ def run_ours(args):
                 "traffic": traffic, "traffic_source": "profiles/traffic.json (ncu --set full)",
                 "launch_ms": dom[1] / dom[3],
                 "bytes_per_launch": dom[2] / dom[3],
-                "forward_ms_per_view": f_ms / max(f_n, 1), "backward_ms_per_view": b_ms / max(b_n, 1),
+                "forward_ms_per_view": f_ms / max(f_n, 1) if f_n else None,
+                "backward_ms_per_view": b_ms / max(b_n, 1) if b_n else None,
+                "forward_backward_ms_per_view": fb_ms / fb_n if fb_n else None,
                 "prepare_ms_per_view": p_ms / max(p_n, 1),
                 "prepare_overlapped": bool(wm.pipelined),
                 "mean_survivors_per_view": mean_ns, "mean_pairs_per_view": mean_np}

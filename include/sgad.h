@@ -124,6 +124,15 @@ int sgad_raster_backward(sgad_raster* h, int32_t mode, const double* g_color,
                          const double* g_depth, const double* g_alpha, double* const* map_grads,
                          float* grad_accum, void* stream);
 
+/* Forward + fused L1 loss + fused backward of the prepared view in ONE
+ * kernel (the tau = 0 window step): each tile's backward sweep starts from
+ * the forward's per-pixel state in registers.  Same results as
+ * sgad_raster_forward(target) + sgad_raster_backward(mode 1) (the per-pixel
+ * state is not kept, so no separate backward may follow).  Requires
+ * want_coef at prepare and fp32 window parameters. */
+int sgad_raster_forward_backward(sgad_raster* h, const sgad_loss_target* target,
+                                 float* grad_accum, void* stream);
+
 /* Inspection (tests): survivors in sorted order and the tile lists with
  * entries expressed as sorted ranks (directly comparable to the reference's
  * `lists`).  Any pointer may be NULL.  ranges: [n_tiles, 2] int64 (start,end). */

@@ -62,6 +62,7 @@ _SIGNATURES = {
                                    _vp, ctypes.POINTER(_i64), ctypes.POINTER(_i64)]),
     "sgad_raster_forward": (_i32, [_vp, _vp, _vp, _vp, _vp, _i32, ctypes.POINTER(LossTarget), _vp]),
     "sgad_raster_backward": (_i32, [_vp, _i32, _vp, _vp, _vp, ctypes.POINTER(_vp), _vp, _vp]),
+    "sgad_raster_forward_backward": (_i32, [_vp, ctypes.POINTER(LossTarget), _vp, _vp]),
     "sgad_raster_get_survivors": (_i32, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "sgad_raster_get_tiles": (_i32, [_vp, _vp, _vp, _vp]),
     "sgad_raster_tile_count": (_i32, [_vp, ctypes.POINTER(_i64)]),

@@ -777,6 +777,110 @@ __device__ __forceinline__ void advance(Cursor& c, const WarpRing& rg, int w_hea
 }
 
 // ------------------------------------------------------------------ K4
+// Per-pixel compositing state carried from the forward sweep to the loss
+// epilogue (and, in the fused kernel, into the backward sweep).
+struct PixState {
+  double T, C0, C1, C2, D, A;
+  int cnt, last;
+};
+
+struct SweepGeom {
+  double pxd, pyd, xlo, ylo;
+};
+
+__device__ __forceinline__ SweepGeom sweep_geom(const TileGeom& g) {
+  SweepGeom q;
+  q.pxd = (double)g.px;
+  q.pyd = (double)g.py;
+  q.xlo = (double)(g.tx * SGAD_TILE + (g.warp & 1) * 8);
+  q.ylo = (double)(g.ty * SGAD_TILE + (g.warp >> 1) * 4);
+  return q;
+}
+
+// rasterizer.py:221-269 for the warp's 8x4 pixels over the tile list rg
+__device__ __forceinline__ PixState fwd_sweep(FwdStage& s, const TileGeom& g, const SweepGeom& q,
+                                              uint2 rg, const uint32_t* __restrict__ lists,
+                                              const Record* __restrict__ rec,
+                                              const double* __restrict__ col64,
+                                              const double* tab) {
+  PixState st{1.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0, -1};
+  bool done = !g.valid;
+  int64_t pos = rg.x;
+  Head nx = load_entry(lists, rec, pos, rg.x, rg.y, g.lane);
+  while (pos < (int64_t)rg.y && !__all_sync(0xffffffffu, done)) {
+    int n = 0;
+    uint32_t mlo = 0, mhi = 0;
+    while (n <= 32 && pos < (int64_t)rg.y) {
+      const Head cur = nx;
+      nx = load_entry(lists, rec, pos + 32, rg.x, rg.y, g.lane);  // one chunk ahead
+      n += fill_chunk_fwd(s, cur, rec, col64, q.xlo, q.ylo, g.lane, n, mlo, mhi);
+      pos += 32;
+    }
+    __syncwarp();
+    const unsigned long long bits = ((unsigned long long)transpose32(mhi, g.lane) << 32) |
+                                    transpose32(mlo, g.lane);
+    unsigned long long mine = done ? 0ull : bits;
+    while (mine) {
+      const int j = __ffsll((long long)mine) - 1;
+      mine &= mine - 1;
+      const double dx = SG_SUB(s.u0[j], q.pxd), dy = SG_SUB(s.v0[j], q.pyd);
+      const double d2 = SG_ADD(SG_MUL(dx, dx), SG_MUL(dy, dy));
+      if (d2 > s.thr[j]) continue;  // rasterizer.py:248 (the mask is a superset)
+      const double w = sgad_exp_neg(SG_MUL(d2, s.nh[j]), tab);
+      double a = SG_MUL(s.op[j], w);
+      if (a > SGAD_ALPHA_MAX) a = SGAD_ALPHA_MAX;
+      const double at = SG_MUL(a, st.T);
+      st.C0 = SG_FMA(s.rgb[0][j], at, st.C0);
+      st.C1 = SG_FMA(s.rgb[1][j], at, st.C1);
+      st.C2 = SG_FMA(s.rgb[2][j], at, st.C2);
+      st.D = SG_FMA(s.z[j], at, st.D);
+      st.A = SG_ADD(st.A, at);
+      ++st.cnt;
+      st.last = s.k[j];
+      st.T = SG_MUL(st.T, SG_SUB(1.0, a));
+      if (st.T < SGAD_TRANSMITTANCE_MIN) {
+        done = true;
+        mine = 0;
+      }
+    }
+    __syncwarp();
+  }
+  return st;
+}
+
+// mapper.py:118-152 (tau = 0): per-pixel L1 residual signs (2 bits per
+// channel) and the warp's |residual| sums added into loss_accum
+__device__ __forceinline__ uint8_t loss_epilogue(const PixState& st, const TileGeom& g, int64_t p,
+                                                 const sgad_loss_target& tgt) {
+  double lc = 0.0, ld = 0.0;
+  uint8_t code = 0;
+  if (g.valid) {
+    const double rc[3] = {SG_SUB(st.C0, (double)tgt.color[3 * p]),
+                          SG_SUB(st.C1, (double)tgt.color[3 * p + 1]),
+                          SG_SUB(st.C2, (double)tgt.color[3 * p + 2])};
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch) {
+      lc += fabs(rc[ch]);
+      code |= (uint8_t)((rc[ch] > 0.0 ? 1u : (rc[ch] < 0.0 ? 2u : 0u)) << (2 * ch));
+    }
+    if (tgt.mask[p]) {
+      const double rd = SG_SUB(st.D, (double)tgt.depth[p]);
+      ld = fabs(rd);
+      code |= (uint8_t)((rd > 0.0 ? 1u : (rd < 0.0 ? 2u : 0u)) << 6);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    lc += __shfl_xor_sync(0xffffffffu, lc, o);
+    ld += __shfl_xor_sync(0xffffffffu, ld, o);
+  }
+  if (g.lane == 0) {
+    atomicAdd(tgt.loss_accum, lc);
+    atomicAdd(tgt.loss_accum + 1, ld);
+  }
+  return code;
+}
+
 template <bool IMAGES, bool STATE, bool LOSS>
 __global__ void __launch_bounds__(RASTER_THREADS)
 k_forward(const uint2* __restrict__ ranges, const uint32_t* __restrict__ lists,
@@ -790,100 +894,28 @@ k_forward(const uint2* __restrict__ ranges, const uint32_t* __restrict__ lists,
   __shared__ double tab[32];
   load_exp_table(tab);
   const TileGeom g = tile_geom(ntx, width, height);
-  const uint2 rg = ranges[g.tile];
-  const double pxd = (double)g.px, pyd = (double)g.py;
-  const double xlo = (double)(g.tx * SGAD_TILE + (g.warp & 1) * 8);
-  const double ylo = (double)(g.ty * SGAD_TILE + (g.warp >> 1) * 4);
-  double T = 1.0, C0 = 0.0, C1 = 0.0, C2 = 0.0, D = 0.0, A = 0.0;
-  int cnt = 0, last = -1;
-  bool done = !g.valid;
-
-  int64_t pos = rg.x;
-  Head nx = load_entry(lists, rec, pos, rg.x, rg.y, g.lane);
-  while (pos < (int64_t)rg.y && !__all_sync(0xffffffffu, done)) {
-    int n = 0;
-    uint32_t mlo = 0, mhi = 0;
-    while (n <= 32 && pos < (int64_t)rg.y) {
-      const Head cur = nx;
-      nx = load_entry(lists, rec, pos + 32, rg.x, rg.y, g.lane);  // one chunk ahead
-      n += fill_chunk_fwd(s, cur, rec, col64, xlo, ylo, g.lane, n, mlo, mhi);
-      pos += 32;
-    }
-    __syncwarp();
-    const unsigned long long bits = ((unsigned long long)transpose32(mhi, g.lane) << 32) |
-                                    transpose32(mlo, g.lane);
-    unsigned long long mine = done ? 0ull : bits;
-    while (mine) {
-      const int j = __ffsll((long long)mine) - 1;
-      mine &= mine - 1;
-      const double dx = SG_SUB(s.u0[j], pxd), dy = SG_SUB(s.v0[j], pyd);
-      const double d2 = SG_ADD(SG_MUL(dx, dx), SG_MUL(dy, dy));
-      if (d2 > s.thr[j]) continue;  // rasterizer.py:248 (the mask is a superset)
-      const double w = sgad_exp_neg(SG_MUL(d2, s.nh[j]), tab);
-      double a = SG_MUL(s.op[j], w);
-      if (a > SGAD_ALPHA_MAX) a = SGAD_ALPHA_MAX;
-      const double at = SG_MUL(a, T);
-      C0 = SG_FMA(s.rgb[0][j], at, C0);
-      C1 = SG_FMA(s.rgb[1][j], at, C1);
-      C2 = SG_FMA(s.rgb[2][j], at, C2);
-      D = SG_FMA(s.z[j], at, D);
-      A = SG_ADD(A, at);
-      ++cnt;
-      last = s.k[j];
-      T = SG_MUL(T, SG_SUB(1.0, a));
-      if (T < SGAD_TRANSMITTANCE_MIN) {
-        done = true;
-        mine = 0;
-      }
-    }
-    __syncwarp();
-  }
-
+  const SweepGeom q = sweep_geom(g);
+  const PixState st = fwd_sweep(s, g, q, ranges[g.tile], lists, rec, col64, tab);
   const int64_t p = (int64_t)g.py * width + g.px;
   if (g.valid) {
     if (IMAGES) {
       if (out_color) {
-        out_color[3 * p] = C0;
-        out_color[3 * p + 1] = C1;
-        out_color[3 * p + 2] = C2;
+        out_color[3 * p] = st.C0;
+        out_color[3 * p + 1] = st.C1;
+        out_color[3 * p + 2] = st.C2;
       }
-      if (out_depth) out_depth[p] = D;
-      if (out_alpha) out_alpha[p] = A;
-      if (out_count) out_count[p] = cnt;
+      if (out_depth) out_depth[p] = st.D;
+      if (out_alpha) out_alpha[p] = st.A;
+      if (out_count) out_count[p] = st.cnt;
     }
     if (STATE) {
-      t_final[p] = T;
-      last_out[p] = last;
+      t_final[p] = st.T;
+      last_out[p] = st.last;
     }
   }
   if (LOSS) {
-    double lc = 0.0, ld = 0.0;
-    uint8_t code = 0;
-    if (g.valid) {
-      const double rc[3] = {SG_SUB(C0, (double)tgt.color[3 * p]),
-                            SG_SUB(C1, (double)tgt.color[3 * p + 1]),
-                            SG_SUB(C2, (double)tgt.color[3 * p + 2])};
-#pragma unroll
-      for (int ch = 0; ch < 3; ++ch) {
-        lc += fabs(rc[ch]);
-        code |= (uint8_t)((rc[ch] > 0.0 ? 1u : (rc[ch] < 0.0 ? 2u : 0u)) << (2 * ch));
-      }
-      if (tgt.mask[p]) {
-        const double rd = SG_SUB(D, (double)tgt.depth[p]);
-        ld = fabs(rd);
-        code |= (uint8_t)((rd > 0.0 ? 1u : (rd < 0.0 ? 2u : 0u)) << 6);
-      }
-      signs[p] = code;
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      lc += __shfl_xor_sync(0xffffffffu, lc, o);
-      ld += __shfl_xor_sync(0xffffffffu, ld, o);
-    }
-    if (g.lane == 0) {
-      atomicAdd(tgt.loss_accum, lc);
-      atomicAdd(tgt.loss_accum + 1, ld);
-    }
+    const uint8_t code = loss_epilogue(st, g, p, tgt);
+    if (g.valid) signs[p] = code;
   }
 }
 
@@ -916,55 +948,22 @@ __device__ __forceinline__ void red_add_v2(float* addr, float a, float b) {
   asm volatile("red.global.add.v2.f32 [%0], {%1, %2};" ::"l"(addr), "f"(a), "f"(b) : "memory");
 }
 
-template <bool FUSED>
-__global__ void __launch_bounds__(RASTER_THREADS)
-k_backward(const uint2* __restrict__ ranges, const uint32_t* __restrict__ lists,
-           const Record* __restrict__ rec, const ChainCoef* __restrict__ coef,
-           const double* __restrict__ col64, int ntx, int width, int height,
-           const double* __restrict__ t_final, const int32_t* __restrict__ last_idx,
-           const uint8_t* __restrict__ signs, Upstream up, const double* __restrict__ g_color,
-           const double* __restrict__ g_depth, const double* __restrict__ g_alpha,
-           double* __restrict__ raw, float* __restrict__ grad_accum) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  WarpRing& ring = reinterpret_cast<WarpRing*>(smem_raw)[threadIdx.x >> 5];
-  __shared__ double tab[32];
-  load_exp_table(tab);
-  const TileGeom g = tile_geom(ntx, width, height);
-  const uint2 rg = ranges[g.tile];
-  const double pxd = (double)g.px, pyd = (double)g.py;
-  const double xlo = (double)(g.tx * SGAD_TILE + (g.warp & 1) * 8);
-  const double ylo = (double)(g.ty * SGAD_TILE + (g.warp >> 1) * 4);
-  const int64_t p = (int64_t)g.py * width + g.px;
+struct PixUpstream {
+  double gc0, gc1, gc2, gd, ga;
+};
 
-  double gc0 = 0.0, gc1 = 0.0, gc2 = 0.0, gd = 0.0, ga = 0.0, T = 0.0;
-  int mylast = -1;
-  if (g.valid) {
-    if (FUSED) {
-      const uint32_t code = signs[p];
-      // mapper.py:145-152: rho * sign / n_color; sigma * sign * mask / n_depth
-      if (g_color) {  // tau != 0: colour upstream with the SSIM term (sgad_ssim)
-        gc0 = g_color[3 * p];
-        gc1 = g_color[3 * p + 1];
-        gc2 = g_color[3 * p + 2];
-      } else {
-        gc0 = SG_MUL(up.kc, sign_of(code & 3u));
-        gc1 = SG_MUL(up.kc, sign_of((code >> 2) & 3u));
-        gc2 = SG_MUL(up.kc, sign_of((code >> 4) & 3u));
-      }
-      gd = SG_MUL(up.kd, sign_of((code >> 6) & 3u));
-    } else {
-      gc0 = g_color[3 * p];
-      gc1 = g_color[3 * p + 1];
-      gc2 = g_color[3 * p + 2];
-      gd = g_depth[p];
-      ga = g_alpha[p];
-    }
-    const bool any = !(gc0 == 0.0 && gc1 == 0.0 && gc2 == 0.0 && gd == 0.0 && ga == 0.0);
-    if (any) {
-      mylast = last_idx[p];
-      T = t_final[p];
-    }
-  }
+// rasterizer.py:272-363 (+ the fused chain of :462-483) for the warp's
+// pixels: reverse sweep from each pixel's last contributor with transmittance
+// T_final, walking a ring of windows per warp (K5)
+template <bool FUSED>
+__device__ __forceinline__ void bwd_sweep(WarpRing& ring, const TileGeom& g, const SweepGeom& q,
+                                          uint2 rg, const uint32_t* __restrict__ lists,
+                                          const Record* __restrict__ rec,
+                                          const ChainCoef* __restrict__ coef,
+                                          const double* __restrict__ col64, const double* tab,
+                                          const PixUpstream& u, double T, int mylast,
+                                          double* __restrict__ raw,
+                                          float* __restrict__ grad_accum) {
   int wend = mylast + 1;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) wend = max(wend, __shfl_xor_sync(0xffffffffu, wend, o));
@@ -980,8 +979,8 @@ k_backward(const uint2* __restrict__ ranges, const uint32_t* __restrict__ lists,
         !__any_sync(0xffffffffu, !done && c.cw == w_head - RING)) {
       const int slot = w_head % RING;
       int n;
-      unsigned long long bits = stage_window<true>(ring, slot, lists, rec, pos, rg.x, pos, xlo,
-                                                   ylo, g.lane, n);
+      unsigned long long bits = stage_window<true>(ring, slot, lists, rec, pos, rg.x, pos, q.xlo,
+                                                   q.ylo, g.lane, n);
       // slots run in descending list order: drop the leading slots above this
       // lane's last contributor (binary search on the staged positions)
       int lo_s = 0, hi_s = n;
@@ -1005,7 +1004,7 @@ k_backward(const uint2* __restrict__ ranges, const uint32_t* __restrict__ lists,
     }
     {
       const uint32_t e = cc.e;
-      const double dx = SG_SUB(cc.u0, pxd), dy = SG_SUB(cc.v0, pyd);
+      const double dx = SG_SUB(cc.u0, q.pxd), dy = SG_SUB(cc.v0, q.pyd);
       const double d2 = SG_ADD(SG_MUL(dx, dx), SG_MUL(dy, dy));
       const double nh = cc.nh, op = cc.op, z = cc.z;
       const double w = sgad_exp_neg(SG_MUL(d2, nh), tab);
@@ -1022,10 +1021,10 @@ k_backward(const uint2* __restrict__ ranges, const uint32_t* __restrict__ lists,
         c2 = __ldg(col64 + 3 * (size_t)e + 2);
       }
       if (cc.gid & GID_LEARN) {
-        const double d_alpha = gc0 * (c0 * tb - sc0 * iom) + gc1 * (c1 * tb - sc1 * iom) +
-                               gc2 * (c2 * tb - sc2 * iom) + gd * (z * tb - sd * iom) +
-                               ga * (tb - sa * iom);
-        const double gcol0 = gc0 * at, gcol1 = gc1 * at, gcol2 = gc2 * at, gz = gd * at;
+        const double d_alpha = u.gc0 * (c0 * tb - sc0 * iom) + u.gc1 * (c1 * tb - sc1 * iom) +
+                               u.gc2 * (c2 * tb - sc2 * iom) + u.gd * (z * tb - sd * iom) +
+                               u.ga * (tb - sa * iom);
+        const double gcol0 = u.gc0 * at, gcol1 = u.gc1 * at, gcol2 = u.gc2 * at, gz = u.gd * at;
         double gop = 0.0, gsig = 0.0, gu = 0.0, gv = 0.0;
         if (!clamped) {
           const double gw = d_alpha * op;
@@ -1063,6 +1062,101 @@ k_backward(const uint2* __restrict__ ranges, const uint32_t* __restrict__ lists,
       T = tb;
     }
   }
+}
+
+__device__ __forceinline__ PixUpstream fused_upstream(uint32_t code, const double* g_color,
+                                                      int64_t p, const Upstream& up) {
+  // mapper.py:145-152: rho * sign / n_color; sigma * sign * mask / n_depth
+  PixUpstream u;
+  if (g_color) {  // tau != 0: colour upstream with the SSIM term (sgad_ssim)
+    u.gc0 = g_color[3 * p];
+    u.gc1 = g_color[3 * p + 1];
+    u.gc2 = g_color[3 * p + 2];
+  } else {
+    u.gc0 = SG_MUL(up.kc, sign_of(code & 3u));
+    u.gc1 = SG_MUL(up.kc, sign_of((code >> 2) & 3u));
+    u.gc2 = SG_MUL(up.kc, sign_of((code >> 4) & 3u));
+  }
+  u.gd = SG_MUL(up.kd, sign_of((code >> 6) & 3u));
+  u.ga = 0.0;
+  return u;
+}
+
+__device__ __forceinline__ bool any_upstream(const PixUpstream& u) {
+  return !(u.gc0 == 0.0 && u.gc1 == 0.0 && u.gc2 == 0.0 && u.gd == 0.0 && u.ga == 0.0);
+}
+
+template <bool FUSED>
+__global__ void __launch_bounds__(RASTER_THREADS)
+k_backward(const uint2* __restrict__ ranges, const uint32_t* __restrict__ lists,
+           const Record* __restrict__ rec, const ChainCoef* __restrict__ coef,
+           const double* __restrict__ col64, int ntx, int width, int height,
+           const double* __restrict__ t_final, const int32_t* __restrict__ last_idx,
+           const uint8_t* __restrict__ signs, Upstream up, const double* __restrict__ g_color,
+           const double* __restrict__ g_depth, const double* __restrict__ g_alpha,
+           double* __restrict__ raw, float* __restrict__ grad_accum) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  WarpRing& ring = reinterpret_cast<WarpRing*>(smem_raw)[threadIdx.x >> 5];
+  __shared__ double tab[32];
+  load_exp_table(tab);
+  const TileGeom g = tile_geom(ntx, width, height);
+  const SweepGeom q = sweep_geom(g);
+  const int64_t p = (int64_t)g.py * width + g.px;
+  PixUpstream u{0.0, 0.0, 0.0, 0.0, 0.0};
+  double T = 0.0;
+  int mylast = -1;
+  if (g.valid) {
+    if (FUSED) {
+      u = fused_upstream(signs[p], g_color, p, up);
+    } else {
+      u.gc0 = g_color[3 * p];
+      u.gc1 = g_color[3 * p + 1];
+      u.gc2 = g_color[3 * p + 2];
+      u.gd = g_depth[p];
+      u.ga = g_alpha[p];
+    }
+    if (any_upstream(u)) {
+      mylast = last_idx[p];
+      T = t_final[p];
+    }
+  }
+  bwd_sweep<FUSED>(ring, g, q, ranges[g.tile], lists, rec, coef, col64, tab, u, T, mylast, raw,
+                   grad_accum);
+}
+
+// K4+K5 fused (tau = 0 window step): the tile's forward sweep, the L1 loss
+// epilogue, then its backward sweep from the state still in registers --
+// no per-pixel state round trip through HBM, and the tile's list entries and
+// records are re-read while still in L2.  Each warp's shared memory holds
+// first its forward staging window, then its backward ring.
+constexpr size_t FB_SLAB = sizeof(WarpRing) > sizeof(FwdStage) ? sizeof(WarpRing)
+                                                                : sizeof(FwdStage);
+
+__global__ void __launch_bounds__(RASTER_THREADS)
+k_forward_backward(const uint2* __restrict__ ranges, const uint32_t* __restrict__ lists,
+                   const Record* __restrict__ rec, const ChainCoef* __restrict__ coef, int ntx,
+                   int width, int height, sgad_loss_target tgt, Upstream up,
+                   float* __restrict__ grad_accum) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  unsigned char* slab = smem_raw + FB_SLAB * (threadIdx.x >> 5);
+  __shared__ double tab[32];
+  load_exp_table(tab);
+  const TileGeom g = tile_geom(ntx, width, height);
+  const SweepGeom q = sweep_geom(g);
+  const uint2 rg = ranges[g.tile];
+  const PixState st = fwd_sweep(*reinterpret_cast<FwdStage*>(slab), g, q, rg, lists, rec,
+                                nullptr, tab);
+  const int64_t p = (int64_t)g.py * width + g.px;
+  const uint8_t code = loss_epilogue(st, g, p, tgt);
+  __syncwarp();
+  PixUpstream u{0.0, 0.0, 0.0, 0.0, 0.0};
+  int mylast = -1;
+  if (g.valid) {
+    u = fused_upstream(code, nullptr, p, up);
+    if (any_upstream(u)) mylast = st.last;
+  }
+  bwd_sweep<true>(*reinterpret_cast<WarpRing*>(slab), g, q, rg, lists, rec, coef, nullptr, tab, u,
+                  st.T, mylast, nullptr, grad_accum);
 }
 
 // Exact-mode chain rule (rasterizer.py:462-483) from per-survivor fp64 sums.
@@ -1143,6 +1237,7 @@ __global__ void k_export_surv(const uint32_t* __restrict__ perm, const Record* _
 }
 
 constexpr size_t FWD_SMEM = sizeof(FwdStage) * NWARP;
+constexpr size_t FB_SMEM = FB_SLAB * NWARP;
 constexpr size_t BWD_SMEM = sizeof(WarpRing) * NWARP;
 
 constexpr size_t LONG_RUN_SMEM = (sizeof(unsigned long long) + sizeof(uint32_t)) * LONG_RUN_MAX;
@@ -1158,6 +1253,7 @@ static int smem_attrs() {
   SGAD_CHECK_CUDA(cudaFuncSetAttribute(k_forward<false, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FWD_SMEM));
   SGAD_CHECK_CUDA(cudaFuncSetAttribute(k_backward<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)BWD_SMEM));
   SGAD_CHECK_CUDA(cudaFuncSetAttribute(k_backward<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)BWD_SMEM));
+  SGAD_CHECK_CUDA(cudaFuncSetAttribute(k_forward_backward, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FB_SMEM));
   SGAD_CHECK_CUDA(cudaFuncSetAttribute(k_long_runs, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LONG_RUN_SMEM));
   done = 1;
   return SGAD_OK;
@@ -1496,6 +1592,30 @@ int sgad_raster_backward(sgad_raster* h, int32_t mode, const double* g_color,
   SGAD_LAUNCH_CHECK();
   // the pointer table is read by the kernel; keep the host copy alive until done
   SGAD_CHECK_CUDA(cudaStreamSynchronize(st));
+  return SGAD_OK;
+}
+
+int sgad_raster_forward_backward(sgad_raster* h, const sgad_loss_target* target,
+                                 float* grad_accum, void* stream_) {
+  SGAD_REQUIRE(h && h->prepared && target && grad_accum && h->have_coef,
+               "sgad_raster_forward_backward: prepare with chain coefficients, a target and "
+               "grad_accum are required");
+  SGAD_REQUIRE(!h->any_f64, "sgad_raster_forward_backward: fp32 window parameters only");
+  SGAD_REQUIRE(target->color && target->depth && target->mask && target->loss_accum,
+               "sgad_raster_forward_backward: incomplete loss target");
+  cudaStream_t st = (cudaStream_t)stream_;
+  if (h->n_surv == 0) return SGAD_OK;
+  if (int rc = smem_attrs()) return rc;
+  const int64_t npx = (int64_t)h->cam.width * h->cam.height;
+  Upstream up;
+  up.kc = target->rho / (double)(3 * npx);
+  up.kd = target->n_depth > 0 ? target->sigma / (double)target->n_depth : 0.0;
+  k_forward_backward<<<dim3((unsigned)h->n_tiles), dim3(RASTER_THREADS), FB_SMEM, st>>>(
+      h->ranges.as<uint2>(), h->pvals0.as<uint32_t>(), h->records.as<Record>(),
+      h->coef.as<ChainCoef>(), h->ntx, h->cam.width, h->cam.height, *target, up, grad_accum);
+  SGAD_LAUNCH_CHECK();
+  h->forwarded = 0;
+  h->fused_ready = 0;
   return SGAD_OK;
 }
 

@@ -108,6 +108,11 @@ class Raster:
         N.check(N.load().sgad_raster_backward(self.h, 1, N.ptr(g_color), None, None, None,
                                               N.ptr(grad_accum), N.stream_ptr(stream)))
 
+    def forward_backward(self, target, grad_accum, stream=None):
+        """Forward + fused L1 loss + fused backward in one kernel (tau = 0)."""
+        N.check(N.load().sgad_raster_forward_backward(self.h, ctypes.byref(target),
+                                                      N.ptr(grad_accum), N.stream_ptr(stream)))
+
     def survivors(self):
         n = self.n_surv
         dev = self.device

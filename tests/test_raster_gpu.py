@@ -132,13 +132,16 @@ def _window_np(n_frames=3, seed=7, fx=60.0, w=64, h=48):
     return wc
 
 
-def test_window_engine_fused_vs_oracle():
+@pytest.mark.parametrize("one_kernel", [True, False])
+def test_window_engine_fused_vs_oracle(one_kernel):
     """Fused loss + fused fp32 backward of the WindowMapper vs the oracle's
-    all-learnable window gradients (delta D1) on identical fp32 parameters."""
+    all-learnable window gradients (delta D1) on identical fp32 parameters --
+    as one forward+backward kernel and as the two kernels."""
     from paper_2603_21055_b200.mapper import MapperConfig, WindowMapper
     from types import SimpleNamespace
     wc = _window_np()
     wm = WindowMapper(wc.frames, wc.poses, wc.intr, wc.params, MapperConfig(tau=0.0))
+    wm.fuse_fwd_bwd = one_kernel
     maps_np = []
     for i, p in enumerate(wc.params):
         maps_np.append(SimpleNamespace(frame_index=i, pose=wc.poses[i], intrinsics=wc.intr,

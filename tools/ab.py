@@ -8,7 +8,9 @@ for lib in sys.argv[1:]:
     for l in out.stdout.splitlines():
         if l.startswith("{"):
             d = json.loads(l); r = d["roofline"]
+            f = lambda k: "   -  " if r.get(k) is None else f"{r[k]:.3f}"
             print(f"{lib:30s} step {d['ms_per_step']:.2f} ms  prep {r['prepare_ms_per_view']:.3f}  "
-                  f"fwd {r['forward_ms_per_view']:.3f}  bwd {r['backward_ms_per_view']:.3f}", flush=True)
+                  f"fwd {f('forward_ms_per_view')}  bwd {f('backward_ms_per_view')}  "
+                  f"fb {f('forward_backward_ms_per_view')}", flush=True)
     if out.returncode:
         print(lib, "failed", out.stderr[-500:])
