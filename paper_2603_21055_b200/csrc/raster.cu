@@ -764,15 +764,19 @@ __device__ __forceinline__ void load_exp_table(double* tab) {
 // Per-lane ring cursor: the lane's current window (cw) and its remaining bits.
 struct Cursor {
   unsigned long long cur;
-  int cw;
+  int cw;    // window index
+  int slot;  // cw % RING, kept incrementally
 };
 
 // advance a dry lane to the next staged window that has bits for it
 __device__ __forceinline__ void advance(Cursor& c, const WarpRing& rg, int w_head, int lane,
                                         bool done) {
-  while (!done && c.cur == 0ull && c.cw + 1 < w_head) {
+  if (done || c.cur != 0ull) return;
+  while (c.cw + 1 < w_head) {
     ++c.cw;
-    c.cur = rg.mask[c.cw % RING][lane];
+    c.slot = c.slot + 1 == RING ? 0 : c.slot + 1;
+    c.cur = rg.mask[c.slot][lane];
+    if (c.cur) break;
   }
 }
 
@@ -928,11 +932,13 @@ __device__ __forceinline__ double sign_of(uint32_t code) {
   return code == 1u ? 1.0 : (code == 2u ? -1.0 : 0.0);
 }
 
-// 1/x: fp32 seed + two Newton steps (full fp64 accuracy for x within the
-// fp32 range, a fraction of the IEEE division's cost; gradients carry a 1e-3
-// bar, the exact drop-in backward 1e-9)
+// 1/x: approximate fp32 seed (one MUFU.RCP) + two Newton steps in fp64
+// (full fp64 accuracy for x within the fp32 range, a fraction of the IEEE
+// division's cost; gradients carry a 1e-3 bar, the exact drop-in backward 1e-9)
 __device__ __forceinline__ double fast_rcp(double x) {
-  double r = (double)__frcp_rn((float)x);
+  float r32;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r32) : "f"((float)x));
+  double r = (double)r32;
   double e = fma(-x, r, 1.0);
   r = fma(r, e, r);
   e = fma(-x, r, 1.0);
@@ -970,14 +976,14 @@ __device__ __forceinline__ void bwd_sweep(WarpRing& ring, const TileGeom& g, con
   const bool done = mylast < 0;  // nothing to propagate for this pixel
   double sc0 = 0.0, sc1 = 0.0, sc2 = 0.0, sd = 0.0, sa = 0.0;
   int64_t pos = wend;  // exclusive upper end of the part not yet staged
-  Cursor c{0ull, -1};
-  int w_head = 0;
+  Cursor c{0ull, -1, RING - 1};
+  int w_head = 0, head_slot = 0;  // head_slot = w_head % RING
   Contrib cc;
   while (true) {
     advance(c, ring, w_head, g.lane, done);
     if (pos > (int64_t)rg.x && __any_sync(0xffffffffu, !done && c.cur == 0ull) &&
         !__any_sync(0xffffffffu, !done && c.cw == w_head - RING)) {
-      const int slot = w_head % RING;
+      const int slot = head_slot;
       int n;
       unsigned long long bits = stage_window<true>(ring, slot, lists, rec, pos, rg.x, pos, q.xlo,
                                                    q.ylo, g.lane, n);
@@ -993,6 +999,7 @@ __device__ __forceinline__ void bwd_sweep(WarpRing& ring, const TileGeom& g, con
       ring.mask[slot][g.lane] = done ? 0ull : bits;
       __syncwarp();
       ++w_head;
+      head_slot = head_slot + 1 == RING ? 0 : head_slot + 1;
       continue;
     }
     if (!__any_sync(0xffffffffu, c.cur != 0ull)) break;
@@ -1000,7 +1007,7 @@ __device__ __forceinline__ void bwd_sweep(WarpRing& ring, const TileGeom& g, con
     {
       const int j = __ffsll((long long)c.cur) - 1;
       c.cur &= c.cur - 1;
-      load_contrib(cc, ring, c.cw % RING, j, rec);
+      load_contrib(cc, ring, c.slot, j, rec);
     }
     {
       const uint32_t e = cc.e;
