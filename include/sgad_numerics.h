@@ -120,8 +120,14 @@ SGAD_HD double sgad_exp_neg(double x, const double* tab) {
   p = SG_FMA(p, r, 1.0);
   const int ni = (int)n;
   const int j = ni & 31;
-  const int k = (ni - j) / 32;
+  const int k = ni >> 5; /* == (ni - j) / 32: ni - j is a multiple of 32 */
+#if defined(__CUDA_ARCH__)
+  /* x * 2^k by adding k to the exponent field: exact (identical to the
+   * multiplication) while the result stays normal, i.e. x > -700 here */
+  return __longlong_as_double(__double_as_longlong(SG_MUL(tab[j], p)) + ((long long)k << 52));
+#else
   return SG_MUL(SG_MUL(tab[j], p), sgad_pow2i(k));
+#endif
 }
 
 /* raysplat/gaussians.py:36-42: branch-stable logistic */

@@ -821,11 +821,18 @@ __device__ __forceinline__ PixState fwd_sweep(FwdStage& s, const TileGeom& g, co
       pos += 32;
     }
     __syncwarp();
-    const unsigned long long bits = ((unsigned long long)transpose32(mhi, g.lane) << 32) |
-                                    transpose32(mlo, g.lane);
-    unsigned long long mine = done ? 0ull : bits;
-    while (mine) {
-      const int j = __ffsll((long long)mine) - 1;
+    // this lane's bits over the window: slots 0..31, then 32..63 (list order)
+    uint32_t mine_lo = transpose32(mlo, g.lane), mine_hi = transpose32(mhi, g.lane);
+    if (done) mine_lo = mine_hi = 0u;
+    int base = 0;
+    uint32_t mine = mine_lo;
+    while (true) {
+      if (!mine) {
+        if (base || !mine_hi) break;
+        base = 32;
+        mine = mine_hi;
+      }
+      const int j = base + __ffs(mine) - 1;
       mine &= mine - 1;
       const double dx = SG_SUB(s.u0[j], q.pxd), dy = SG_SUB(s.v0[j], q.pyd);
       const double d2 = SG_ADD(SG_MUL(dx, dx), SG_MUL(dy, dy));
@@ -844,7 +851,7 @@ __device__ __forceinline__ PixState fwd_sweep(FwdStage& s, const TileGeom& g, co
       st.T = SG_MUL(st.T, SG_SUB(1.0, a));
       if (st.T < SGAD_TRANSMITTANCE_MIN) {
         done = true;
-        mine = 0;
+        break;
       }
     }
     __syncwarp();
