@@ -20,6 +20,7 @@
  *   sgad_adam_step        <- mapper.py:73-95 (MapOptimizer.step)
  *   sgad_voxels_*         <- tracker.py:105-122 (GlobalGeomSet.insert cell gating)
  *   sgad_inpaint_jacobi   <- datasets.py:368-398 (inpaint_depth sweeps)
+ *   sgad_irls_normal_eqs  <- tracker.py:400-410 (init_pose_render IRLS systems)
  *   sgad_ssim             <- ssim.py:31-87 (ssim(..., with_grad)), the tau term
  *                            of mapping_loss (mapper.py:126-147)
  *   sgad_track_fit        <- tracker.py:144-170, :193-230 (build_local_set with
@@ -149,6 +150,17 @@ int sgad_raster_tile_count(sgad_raster* h, int64_t* n_tiles);
 int sgad_adam_step(void* params, void* grads, void* m, void* v, int64_t n_frames, int64_t hw,
                    const double* lr, double beta1, double beta2, double eps, double bc1,
                    double bc2, int32_t update_delta, int32_t f64, void* stream);
+
+/* ---- render-based pose initialiser ------------------------------------
+ * One IRLS linearisation of tracker.py:400-410: rows (device fp64 [12, n]) are
+ * the residuals at the poses exp(+h e_k) o pose, exp(-h e_k) o pose for k =
+ * 0..5 (rows 2k, 2k+1), r (device [n]) the residual at the pose; with
+ * J = (rows[2k] - rows[2k+1]) / 2h and w = 1 / max(|r + J xi|, 1e-3) (xi: 6
+ * host doubles) writes out (device double[27]) = the 21 upper-triangle
+ * entries of J^T diag(w) J (row-major) then J^T (w r).  partial: device
+ * scratch of 592 * 27 doubles.  Deterministic. */
+int sgad_irls_normal_eqs(const double* rows, const double* r, int64_t n, const double* xi,
+                         double h, double* partial, double* out, void* stream);
 
 /* ---- harmonic depth inpainting ----------------------------------------
  * Replaces the Jacobi loop of raysplat/datasets.py:388-397 (inpaint_depth):

@@ -52,6 +52,7 @@ _SIGNATURES = {
     "sgad_voxels_create": (_i32, [ctypes.POINTER(_vp)]),
     "sgad_voxels_destroy": (_i32, [_vp]),
     "sgad_voxels_gate": (_i32, [_vp, _vp, _i64, _f64, _vp, ctypes.POINTER(_i64), _vp]),
+    "sgad_irls_normal_eqs": (_i32, [_vp, _vp, _i64, ctypes.POINTER(_f64), _f64, _vp, _vp, _vp]),
     "sgad_inpaint_jacobi": (_i32, [_vp, _vp, _i32, _i32, _i32, _f64, _vp, ctypes.POINTER(_i32),
                                    _vp]),
     "sgad_ssim_workspace_size": (_i32, [_i32, _i32, _i32, ctypes.POINTER(_i64)]),

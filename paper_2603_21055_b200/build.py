@@ -11,7 +11,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libsgad.so")
-SOURCES = ["raster.cu", "adam.cu", "track.cu", "ssim.cu", "voxels.cu", "inpaint.cu"]
+SOURCES = ["raster.cu", "adam.cu", "track.cu", "ssim.cu", "voxels.cu", "inpaint.cu", "irls.cu"]
 HEADERS = ["common.cuh"]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

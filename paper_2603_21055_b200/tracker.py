@@ -401,12 +401,14 @@ def init_pose_constant_speed(prev: Pose, prev_prev: Pose) -> Pose:
 
 class _RenderResiduals:
     """Residual vector of tracker.py:379-383 on the GPU: the previous frame's
-    map rendered at a candidate pose (K1-K4 through one raster handle with
-    preallocated images), L1 photometric and valid-masked, weighted depth
-    residuals concatenated into one device fp64 vector."""
+    map rendered at a candidate pose (K1-K4 with preallocated images), L1
+    photometric and valid-masked, weighted depth residuals concatenated into
+    one device fp64 vector.  Two raster handles on two streams let a batch of
+    renders (the Jacobian's 12) overlap one render's preparation with the
+    previous one's compositing."""
 
     def __init__(self, frame, prev_map, depth_weight: float):
-        from .rasterizer import Raster, build_frames, camera_of  # noqa: F401
+        from .rasterizer import Raster, camera_of
         self.intr = frame.intrinsics
         self.map = prev_map
         dev = prev_map.planes.device
@@ -416,35 +418,58 @@ class _RenderResiduals:
         self.td = torch.as_tensor(np.asarray(frame.depth, dtype=np.float64), device=dev)
         self.wm = depth_weight * torch.as_tensor(np.asarray(frame.valid_mask, dtype=np.float64),
                                                  device=dev)
-        self.color = torch.empty((h, w, 3), dtype=torch.float64, device=dev)
-        self.depth = torch.empty((h, w), dtype=torch.float64, device=dev)
-        self.alpha = torch.empty((h, w), dtype=torch.float64, device=dev)
-        self.raster = Raster(dev)
+        self.img = [tuple(torch.empty(shape, dtype=torch.float64, device=dev)
+                          for shape in ((h, w, 3), (h, w), (h, w))) for _ in range(2)]
+        self.rasters = [Raster(dev), Raster(dev)]
+        self.streams = [torch.cuda.Stream(dev), torch.cuda.Stream(dev)]
         self.cam = camera_of(self.intr)
         self.n = 4 * h * w
 
-    def render(self, pose: Pose) -> None:
+    def _render(self, k: int, pose: Pose, stream) -> None:
         from .rasterizer import build_frames
+        color, depth, alpha = self.img[k]
         frames = build_frames([self.map], pose, set())[0]
-        ns, _ = self.raster.prepare(frames, self.cam)
+        r = self.rasters[k]
+        ns, _ = r.prepare(frames, self.cam, stream=stream)
         if ns:
-            self.raster.forward(self.color, self.depth, self.alpha)
+            r.forward(color, depth, alpha, stream=stream)
         else:
-            self.color.zero_()
-            self.depth.zero_()
-            self.alpha.zero_()
+            with torch.cuda.stream(stream):
+                color.zero_()
+                depth.zero_()
+                alpha.zero_()
+
+    def _residual(self, k: int, out: torch.Tensor) -> None:
+        color, depth, _ = self.img[k]
+        nc = color.numel()
+        torch.sub(color.reshape(-1), self.tc.reshape(-1), out=out[:nc])
+        torch.mul(self.wm.reshape(-1), depth.reshape(-1) - self.td.reshape(-1), out=out[nc:])
+
+    def batch(self, poses, out: torch.Tensor) -> torch.Tensor:
+        """Residual rows out[i] for poses[i], renders alternating over the two
+        handles/streams; the current stream waits for all of them."""
+        main = torch.cuda.current_stream(self.dev)
+        start = torch.cuda.Event()
+        start.record(main)
+        for st in self.streams:
+            st.wait_event(start)
+        for i, pose in enumerate(poses):
+            k = i & 1
+            st = self.streams[k]
+            self._render(k, pose, st)
+            with torch.cuda.stream(st):
+                self._residual(k, out[i])
+        for st in self.streams:
+            main.wait_stream(st)
+        return out
 
     def __call__(self, pose: Pose, out=None) -> torch.Tensor:
-        self.render(pose)
         r = out if out is not None else torch.empty(self.n, dtype=torch.float64, device=self.dev)
-        nc = self.color.numel()
-        torch.sub(self.color.reshape(-1), self.tc.reshape(-1), out=r[:nc])
-        torch.mul(self.wm.reshape(-1), self.depth.reshape(-1) - self.td.reshape(-1), out=r[nc:])
-        return r
+        return self.batch([pose], r[None])[0]
 
     def coverage(self, pose: Pose) -> float:
-        self.render(pose)
-        return float((self.alpha > 0.5).double().mean())
+        self.batch([pose], torch.empty((1, self.n), dtype=torch.float64, device=self.dev))
+        return float((self.img[0][2] > 0.5).double().mean())
 
 
 def init_pose_render(frame, prev_map, init: Pose, iters: int = 10, depth_weight: float = 4.0,
@@ -464,25 +489,26 @@ def init_pose_render(frame, prev_map, init: Pose, iters: int = 10, depth_weight:
     pose = init
     h = 1e-4
     r = res(pose).clone()
-    jac = torch.empty((res.n, 6), dtype=torch.float64, device=res.dev)
-    rp = torch.empty(res.n, dtype=torch.float64, device=res.dev)
-    rm = torch.empty(res.n, dtype=torch.float64, device=res.dev)
+    rows = torch.empty((12, res.n), dtype=torch.float64, device=res.dev)
+    partial = torch.empty(592 * 27, dtype=torch.float64, device=res.dev)
+    sums = torch.empty(27, dtype=torch.float64, device=res.dev)
     for _ in range(iters):
+        # the 12 central-difference renders as one batch (residual rows)
+        probes = []
         for k in range(6):
             e = np.zeros(6)
             e[k] = h
-            res(se3_exp(e).compose(pose), out=rp)
-            res(se3_exp(-e).compose(pose), out=rm)
-            torch.sub(rp, rm, out=jac[:, k])
-        jac.div_(2.0 * h)
-        # IRLS on the same linearisation: weights from the predicted residuals
+            probes += [se3_exp(e).compose(pose), se3_exp(-e).compose(pose)]
+        res.batch(probes, rows)
+        # IRLS on the same linearisation: weights from the predicted residuals;
+        # J^T W J and J^T W r in one pass over the rows (sgad_irls_normal_eqs)
         xi = np.zeros(6)
         for _inner in range(3):
-            r_pred = r + jac @ torch.as_tensor(xi, device=res.dev)
-            wts = 1.0 / torch.clamp(r_pred.abs(), min=1e-3)
-            hw = (jac.T @ (jac * wts[:, None])).cpu().numpy()
-            gw = (jac.T @ (wts * r)).cpu().numpy()
-            xi = np.linalg.lstsq(hw, -gw, rcond=None)[0]
+            xi_c = (ctypes.c_double * 6)(*xi)
+            N.call("sgad_irls_normal_eqs", rows.data_ptr(), r.data_ptr(), int(res.n), xi_c,
+                   float(h), partial.data_ptr(), sums.data_ptr(), N.stream_ptr())
+            v = sums.cpu().numpy()
+            xi = np.linalg.lstsq(_sym6(v[:21]), -v[21:], rcond=None)[0]
         cost = float(r.abs().sum())
         candidate = se3_exp(xi).compose(pose)
         r_cand = res(candidate)
