@@ -14,6 +14,7 @@
 #include <cub/cub.cuh>
 #include <stdarg.h>
 #include <stddef.h>
+#include <stdlib.h>
 #include <algorithm>
 #include <vector>
 
@@ -53,7 +54,7 @@ constexpr int RASTER_THREADS = 256;
 struct sgad_raster {
   sgad::DevBuf frames, status, counters, records, coef, keys0, keys1, vals0, vals1;
   sgad::DevBuf pcount, poffset, pkeys0, pkeys1, pvals0, pvals1, ranges, cub_tmp;
-  sgad::DevBuf trans_final, last_idx, signs, raw_grads, rank_of, scratch, col64, zrange, k32a, k32b, bbox, runs;
+  sgad::DevBuf trans_final, last_idx, signs, raw_grads, rank_of, scratch, col64, zrange, k32a, k32b, bbox, runs, raw32;
   int any_f64 = 0;
   std::vector<sgad_frame> host_frames;
   sgad_camera cam{};
@@ -68,6 +69,13 @@ struct sgad_raster {
 namespace sgad {
 
 static thread_local char g_err[1024] = "";
+// fused backward variant: chain rule per Gaussian after the sweep (1, the
+// default: 2.20 vs 2.36 ms per C4 view) or per contribution (0); the
+// environment variable SGAD_LATE_CHAIN=0 selects the latter (A/B)
+static int g_late_chain = [] {
+  const char* e = getenv("SGAD_LATE_CHAIN");
+  return e && e[0] == '0' ? 0 : 1;
+}();
 std::atomic<long long> g_launches{0};
 
 void set_error(const char* fmt, ...) {
@@ -968,7 +976,7 @@ struct PixUpstream {
 // rasterizer.py:272-363 (+ the fused chain of :462-483) for the warp's
 // pixels: reverse sweep from each pixel's last contributor with transmittance
 // T_final, walking a ring of windows per warp (K5)
-template <bool FUSED>
+template <bool FUSED, bool LATE = false>
 __device__ __forceinline__ void bwd_sweep(WarpRing& ring, const TileGeom& g, const SweepGeom& q,
                                           uint2 rg, const uint32_t* __restrict__ lists,
                                           const Record* __restrict__ rec,
@@ -1049,7 +1057,13 @@ __device__ __forceinline__ void bwd_sweep(WarpRing& ring, const TileGeom& g, con
           gu = 2.0 * gd2 * dx;
           gv = 2.0 * gd2 * dy;
         }
-        if (FUSED) {
+        if (FUSED && LATE) {
+          // image-space gradients; k_chain_late applies the chain rule per
+          // Gaussian after the sweep (grad_accum is the view's raw buffer)
+          float* dst = grad_accum + (size_t)e * 8;
+          red_add_v4(dst, (float)gu, (float)gv, (float)gz, (float)gsig);
+          red_add_v4(dst + 4, (float)gop, (float)gcol0, (float)gcol1, (float)gcol2);
+        } else if (FUSED) {
           const float4* cp = reinterpret_cast<const float4*>(coef + e);
           const float4 k0 = __ldg(cp), k1 = __ldg(cp + 1);
           float* dst = grad_accum + (size_t)(cc.gid & ~GID_LEARN) * 8;
@@ -1100,7 +1114,7 @@ __device__ __forceinline__ bool any_upstream(const PixUpstream& u) {
   return !(u.gc0 == 0.0 && u.gc1 == 0.0 && u.gc2 == 0.0 && u.gd == 0.0 && u.ga == 0.0);
 }
 
-template <bool FUSED>
+template <bool FUSED, bool LATE = false>
 __global__ void __launch_bounds__(RASTER_THREADS)
 k_backward(const uint2* __restrict__ ranges, const uint32_t* __restrict__ lists,
            const Record* __restrict__ rec, const ChainCoef* __restrict__ coef,
@@ -1134,8 +1148,40 @@ k_backward(const uint2* __restrict__ ranges, const uint32_t* __restrict__ lists,
       T = t_final[p];
     }
   }
-  bwd_sweep<FUSED>(ring, g, q, ranges[g.tile], lists, rec, coef, col64, tab, u, T, mylast, raw,
-                   grad_accum);
+  bwd_sweep<FUSED, LATE>(ring, g, q, ranges[g.tile], lists, rec, coef, col64, tab, u, T, mylast,
+                         raw, grad_accum);
+}
+
+// Chain rule (rasterizer.py:462-483) per Gaussian for the late-chain fused
+// backward: raw image-space gradients (g_u0, g_v0, g_z, g_sigma, g_op,
+// g_rgb) -> window parameter gradients, added into grad_accum; the raw slot
+// is cleared for the next view.  One thread per Gaussian id, no atomics.
+__global__ void k_chain_late(float* __restrict__ raw, const ChainCoef* __restrict__ coef,
+                             const Record* __restrict__ rec, uint32_t n,
+                             float* __restrict__ grad_accum) {
+  const uint32_t e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n) return;
+  float4* rp = reinterpret_cast<float4*>(raw + (size_t)e * 8);
+  const float4 r0 = rp[0], r1 = rp[1];
+  if (r0.x == 0.f && r0.y == 0.f && r0.z == 0.f && r0.w == 0.f && r1.x == 0.f && r1.y == 0.f &&
+      r1.z == 0.f && r1.w == 0.f)
+    return;  // not reached by this view (or culled)
+  const float4* cp = reinterpret_cast<const float4*>(coef + e);
+  const float4 k0 = __ldg(cp), k1 = __ldg(cp + 1);
+  const uint32_t gid = __ldg(&rec[e].gid) & ~GID_LEARN;
+  float4* dst = reinterpret_cast<float4*>(grad_accum + (size_t)gid * 8);
+  float4 a = dst[0];
+  float2 b = *reinterpret_cast<float2*>(grad_accum + (size_t)gid * 8 + 4);
+  a.x += k0.y * r0.x + k0.z * r0.y + k0.w * r0.z + k1.x * r0.w;  // delta
+  a.y += k0.x * r0.w;                                             // radius
+  a.z += k1.y * r1.x;                                             // opacity logit
+  a.w += r1.y;
+  b.x += r1.z;
+  b.y += r1.w;
+  dst[0] = a;
+  *reinterpret_cast<float2*>(grad_accum + (size_t)gid * 8 + 4) = b;
+  rp[0] = make_float4(0.f, 0.f, 0.f, 0.f);
+  rp[1] = make_float4(0.f, 0.f, 0.f, 0.f);
 }
 
 // K4+K5 fused (tau = 0 window step): the tile's forward sweep, the L1 loss
@@ -1267,6 +1313,7 @@ static int smem_attrs() {
   SGAD_CHECK_CUDA(cudaFuncSetAttribute(k_forward<false, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FWD_SMEM));
   SGAD_CHECK_CUDA(cudaFuncSetAttribute(k_backward<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)BWD_SMEM));
   SGAD_CHECK_CUDA(cudaFuncSetAttribute(k_backward<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)BWD_SMEM));
+  SGAD_CHECK_CUDA(cudaFuncSetAttribute(k_backward<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)BWD_SMEM));
   SGAD_CHECK_CUDA(cudaFuncSetAttribute(k_forward_backward, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FB_SMEM));
   SGAD_CHECK_CUDA(cudaFuncSetAttribute(k_long_runs, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LONG_RUN_SMEM));
   done = 1;
@@ -1315,7 +1362,7 @@ int sgad_raster_destroy(sgad_raster* h) {
                     &h->keys1, &h->vals0, &h->vals1, &h->pcount, &h->poffset, &h->pkeys0,
                     &h->pkeys1, &h->pvals0, &h->pvals1, &h->ranges, &h->cub_tmp,
                     &h->trans_final, &h->last_idx, &h->signs, &h->raw_grads, &h->rank_of,
-                    &h->scratch, &h->col64, &h->zrange, &h->k32a, &h->k32b, &h->bbox, &h->runs};
+                    &h->scratch, &h->col64, &h->zrange, &h->k32a, &h->k32b, &h->bbox, &h->runs, &h->raw32};
   for (DevBuf* b : bufs) b->release();
   if (h->pinned) cudaFreeHost(h->pinned);
   delete h;
@@ -1577,6 +1624,26 @@ int sgad_raster_backward(sgad_raster* h, int32_t mode, const double* g_color,
     Upstream up;
     up.kc = h->rho / (double)(3 * npx);
     up.kd = h->n_depth > 0 ? h->sigma_d / (double)h->n_depth : 0.0;
+    if (g_late_chain) {
+      // image-space gradients into the handle's raw buffer, then the chain
+      // rule per Gaussian (k_chain_late); the raw buffer is kept zeroed
+      const size_t bytes = sizeof(float) * 8 * (size_t)h->n_total;
+      if (h->raw32.cap < bytes || !h->raw32.p) {
+        SGAD_CHECK_CUDA(h->raw32.ensure(bytes));
+        SGAD_CHECK_CUDA(cudaMemsetAsync(h->raw32.p, 0, h->raw32.cap, st));
+      }
+      k_backward<true, true><<<grid, block, BWD_SMEM, st>>>(
+          h->ranges.as<uint2>(), h->pvals0.as<uint32_t>(), h->records.as<Record>(),
+          h->coef.as<ChainCoef>(), h->any_f64 ? h->col64.as<double>() : nullptr, h->ntx,
+          h->cam.width, h->cam.height, h->trans_final.as<double>(), h->last_idx.as<int32_t>(),
+          h->signs.as<uint8_t>(), up, g_color, nullptr, nullptr, nullptr, h->raw32.as<float>());
+      SGAD_LAUNCH_CHECK();
+      k_chain_late<<<blocks_for(h->n_total, 256), 256, 0, st>>>(
+          h->raw32.as<float>(), h->coef.as<ChainCoef>(), h->records.as<Record>(),
+          (uint32_t)h->n_total, grad_accum);
+      SGAD_LAUNCH_CHECK();
+      return SGAD_OK;
+    }
     k_backward<true><<<grid, block, BWD_SMEM, st>>>(
         h->ranges.as<uint2>(), h->pvals0.as<uint32_t>(), h->records.as<Record>(),
         h->coef.as<ChainCoef>(), h->any_f64 ? h->col64.as<double>() : nullptr, h->ntx,
