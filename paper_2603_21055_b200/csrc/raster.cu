@@ -1051,8 +1051,10 @@ __device__ __forceinline__ void bwd_sweep(WarpRing& ring, const TileGeom& g, con
         if (!clamped) {
           const double gw = d_alpha * op;
           gop = d_alpha * w;
-          // gw w d2 / (s2 sigma) = gw w d2 (-2 nh) / sigma
-          gsig = gw * w * d2 * (-2.0 * nh) * fast_rcp(cc.sig);
+          // gw w d2 / (s2 sigma) = gw w d2 (-2 nh) / sigma; the late chain
+          // divides by sigma once per Gaussian (k_chain_late)
+          gsig = gw * w * d2 * (-2.0 * nh);
+          if (!LATE) gsig *= fast_rcp(cc.sig);
           const double gd2 = gw * w * nh;  // gw (-0.5 w / s2)
           gu = 2.0 * gd2 * dx;
           gv = 2.0 * gd2 * dy;
@@ -1169,11 +1171,12 @@ __global__ void k_chain_late(float* __restrict__ raw, const ChainCoef* __restric
   const float4* cp = reinterpret_cast<const float4*>(coef + e);
   const float4 k0 = __ldg(cp), k1 = __ldg(cp + 1);
   const uint32_t gid = __ldg(&rec[e].gid) & ~GID_LEARN;
+  const float gsig = (float)((double)r0.w / __ldg(&rec[e].sigma));  // raw slot holds gsig * sigma
   float4* dst = reinterpret_cast<float4*>(grad_accum + (size_t)gid * 8);
   float4 a = dst[0];
   float2 b = *reinterpret_cast<float2*>(grad_accum + (size_t)gid * 8 + 4);
-  a.x += k0.y * r0.x + k0.z * r0.y + k0.w * r0.z + k1.x * r0.w;  // delta
-  a.y += k0.x * r0.w;                                             // radius
+  a.x += k0.y * r0.x + k0.z * r0.y + k0.w * r0.z + k1.x * gsig;  // delta
+  a.y += k0.x * gsig;                                             // radius
   a.z += k1.y * r1.x;                                             // opacity logit
   a.w += r1.y;
   b.x += r1.z;
