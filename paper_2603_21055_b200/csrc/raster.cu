@@ -54,7 +54,7 @@ constexpr int RASTER_THREADS = 256;
 struct sgad_raster {
   sgad::DevBuf frames, status, counters, records, coef, keys0, keys1, vals0, vals1;
   sgad::DevBuf pcount, poffset, pkeys0, pkeys1, pvals0, pvals1, ranges, cub_tmp;
-  sgad::DevBuf trans_final, last_idx, signs, raw_grads, rank_of, scratch, col64, zrange, k32a, k32b, bbox, runs, raw32;
+  sgad::DevBuf trans_final, last_idx, signs, raw_grads, rank_of, scratch, col64, zrange, k32a, k32b, bbox, runs, raw32, cl_e, cl_k, cl_m, cl_n;
   int any_f64 = 0;
   std::vector<sgad_frame> host_frames;
   sgad_camera cam{};
@@ -654,11 +654,28 @@ struct FwdStage {
   int32_t k[WIN];
 };
 
+// Per-warp compact lists written by a forward that keeps state for the
+// backward: every list entry that reaches the warp's rectangle, in list
+// order, with its exact pixel mask -- the backward stages its windows from
+// these instead of culling the tile list again.  Warp w of a tile with list
+// range [x, y) owns slots [8x + w (y - x), 8x + (w + 1)(y - x)).
+struct CList {
+  uint32_t* e;
+  int32_t* k;
+  uint32_t* m;
+  uint32_t* count;  // [n_tiles * 8] entries written per warp
+};
+
+__device__ __forceinline__ int64_t clist_base(uint2 rg, int warp) {
+  return 8 * (int64_t)rg.x + (int64_t)warp * (int64_t)(rg.y - rg.x);
+}
+
+template <bool EXACT>
 __device__ __forceinline__ int fill_chunk_fwd(FwdStage& s, const Head& hd,
                                               const Record* __restrict__ rec,
                                               const double* __restrict__ col64, double xlo,
                                               double ylo, int lane, int n, uint32_t& mlo,
-                                              uint32_t& mhi) {
+                                              uint32_t& mhi, const CList& cl, int64_t cbase) {
   uint32_t m = 0;
   if (hd.valid) {
     const float uf = (float)hd.u0, vf = (float)hd.v0;
@@ -667,12 +684,18 @@ __device__ __forceinline__ int fill_chunk_fwd(FwdStage& s, const Head& hd,
     const float dx = fmaxf(fmaxf(xl - uf, uf - (xl + 7.0f)), 0.0f);
     const float dy = fmaxf(fmaxf(yl - vf, vf - (yl + 3.0f)), 0.0f);
     if (dx * dx + dy * dy <= rr * rr)
-      m = pixel_mask(hd.u0, hd.v0, SG_MUL(9.0, SG_MUL(hd.sig, hd.sig)), xlo, ylo);
+      m = EXACT ? pixel_mask_exact(hd.u0, hd.v0, SG_MUL(9.0, SG_MUL(hd.sig, hd.sig)), xlo, ylo)
+                : pixel_mask(hd.u0, hd.v0, SG_MUL(9.0, SG_MUL(hd.sig, hd.sig)), xlo, ylo);
   }
   const uint32_t keep = __ballot_sync(0xffffffffu, m != 0);
   const int c = __popc(keep);
   if (m) {
     const int j = n + __popc(keep & ((1u << lane) - 1u));
+    if (EXACT) {  // the backward's compact list (cbase = this chunk's first slot - n)
+      cl.e[cbase + j] = hd.e;
+      cl.k[cbase + j] = (int32_t)hd.k;
+      cl.m[cbase + j] = m;
+    }
     const double2* rp = reinterpret_cast<const double2*>(rec + hd.e);
     const double2 zn = __ldg(rp + 2);                                        // z, nh
     const float4 cg = __ldg(reinterpret_cast<const float4*>(rp + 3));        // r, g, b, gid
@@ -809,15 +832,19 @@ __device__ __forceinline__ SweepGeom sweep_geom(const TileGeom& g) {
   return q;
 }
 
-// rasterizer.py:221-269 for the warp's 8x4 pixels over the tile list rg
+// rasterizer.py:221-269 for the warp's 8x4 pixels over the tile list rg;
+// with EXACT the masks are exact and the warp's compact list is written
+template <bool EXACT>
 __device__ __forceinline__ PixState fwd_sweep(FwdStage& s, const TileGeom& g, const SweepGeom& q,
                                               uint2 rg, const uint32_t* __restrict__ lists,
                                               const Record* __restrict__ rec,
                                               const double* __restrict__ col64,
-                                              const double* tab) {
+                                              const double* tab, const CList& cl) {
   PixState st{1.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0, -1};
   bool done = !g.valid;
   int64_t pos = rg.x;
+  const int64_t cbase = clist_base(rg, g.warp);
+  int64_t nw = 0;  // compact entries written so far
   Head nx = load_entry(lists, rec, pos, rg.x, rg.y, g.lane);
   while (pos < (int64_t)rg.y && !__all_sync(0xffffffffu, done)) {
     int n = 0;
@@ -825,9 +852,11 @@ __device__ __forceinline__ PixState fwd_sweep(FwdStage& s, const TileGeom& g, co
     while (n <= 32 && pos < (int64_t)rg.y) {
       const Head cur = nx;
       nx = load_entry(lists, rec, pos + 32, rg.x, rg.y, g.lane);  // one chunk ahead
-      n += fill_chunk_fwd(s, cur, rec, col64, q.xlo, q.ylo, g.lane, n, mlo, mhi);
+      n += fill_chunk_fwd<EXACT>(s, cur, rec, col64, q.xlo, q.ylo, g.lane, n, mlo, mhi, cl,
+                                 cbase + nw);
       pos += 32;
     }
+    nw += n;
     __syncwarp();
     // this lane's bits over the window: slots 0..31, then 32..63 (list order)
     uint32_t mine_lo = transpose32(mlo, g.lane), mine_hi = transpose32(mhi, g.lane);
@@ -864,6 +893,7 @@ __device__ __forceinline__ PixState fwd_sweep(FwdStage& s, const TileGeom& g, co
     }
     __syncwarp();
   }
+  if (EXACT && g.lane == 0) cl.count[(int64_t)g.tile * NWARP + g.warp] = (uint32_t)nw;
   return st;
 }
 
@@ -907,14 +937,14 @@ k_forward(const uint2* __restrict__ ranges, const uint32_t* __restrict__ lists,
           int height, double* __restrict__ out_color, double* __restrict__ out_depth,
           double* __restrict__ out_alpha, int32_t* __restrict__ out_count,
           double* __restrict__ t_final, int32_t* __restrict__ last_out,
-          uint8_t* __restrict__ signs, sgad_loss_target tgt) {
+          uint8_t* __restrict__ signs, sgad_loss_target tgt, CList cl) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   FwdStage& s = reinterpret_cast<FwdStage*>(smem_raw)[threadIdx.x >> 5];
   __shared__ double tab[32];
   load_exp_table(tab);
   const TileGeom g = tile_geom(ntx, width, height);
   const SweepGeom q = sweep_geom(g);
-  const PixState st = fwd_sweep(s, g, q, ranges[g.tile], lists, rec, col64, tab);
+  const PixState st = fwd_sweep<STATE>(s, g, q, ranges[g.tile], lists, rec, col64, tab, cl);
   const int64_t p = (int64_t)g.py * width + g.px;
   if (g.valid) {
     if (IMAGES) {
@@ -978,7 +1008,7 @@ struct PixUpstream {
 // T_final, walking a ring of windows per warp (K5)
 template <bool FUSED, bool LATE = false>
 __device__ __forceinline__ void bwd_sweep(WarpRing& ring, const TileGeom& g, const SweepGeom& q,
-                                          uint2 rg, const uint32_t* __restrict__ lists,
+                                          uint2 rg, const CList& cl,
                                           const Record* __restrict__ rec,
                                           const ChainCoef* __restrict__ coef,
                                           const double* __restrict__ col64, const double* tab,
@@ -990,18 +1020,42 @@ __device__ __forceinline__ void bwd_sweep(WarpRing& ring, const TileGeom& g, con
   for (int o = 16; o > 0; o >>= 1) wend = max(wend, __shfl_xor_sync(0xffffffffu, wend, o));
   const bool done = mylast < 0;  // nothing to propagate for this pixel
   double sc0 = 0.0, sc1 = 0.0, sc2 = 0.0, sd = 0.0, sa = 0.0;
-  int64_t pos = wend;  // exclusive upper end of the part not yet staged
+  // the warp's compact list (written by the forward): entries [0, cpos) are
+  // not staged yet; entries past the warp's last contributor are skipped
+  const int64_t cbase = clist_base(rg, g.warp);
+  // (plain loads: in k_forward_backward the same kernel wrote them)
+  __syncwarp();
+  int64_t cpos = (int64_t)cl.count[(int64_t)g.tile * NWARP + g.warp];
+  while (cpos > 0 && cl.k[cbase + cpos - 1] >= wend) --cpos;
   Cursor c{0ull, -1, RING - 1};
   int w_head = 0, head_slot = 0;  // head_slot = w_head % RING
   Contrib cc;
   while (true) {
     advance(c, ring, w_head, g.lane, done);
-    if (pos > (int64_t)rg.x && __any_sync(0xffffffffu, !done && c.cur == 0ull) &&
+    if (cpos > 0 && __any_sync(0xffffffffu, !done && c.cur == 0ull) &&
         !__any_sync(0xffffffffu, !done && c.cw == w_head - RING)) {
       const int slot = head_slot;
-      int n;
-      unsigned long long bits = stage_window<true>(ring, slot, lists, rec, pos, rg.x, pos, q.xlo,
-                                                   q.ylo, g.lane, n);
+      // the next (up to) 64 compact entries below cpos, descending: lane i
+      // takes slots i and 32 + i, whose masks are already exact
+      const int n = (int)min(cpos, (int64_t)WIN);
+      uint32_t mlo = 0, mhi = 0;
+      {
+        const int64_t i0 = cbase + cpos - 1 - g.lane, i1 = i0 - 32;
+        if (g.lane < n) {
+          ring.e[slot][g.lane] = cl.e[i0];
+          ring.k[slot][g.lane] = cl.k[i0];
+          mlo = cl.m[i0];
+        }
+        if (32 + g.lane < n) {
+          ring.e[slot][32 + g.lane] = cl.e[i1];
+          ring.k[slot][32 + g.lane] = cl.k[i1];
+          mhi = cl.m[i1];
+        }
+      }
+      cpos -= n;
+      __syncwarp();
+      unsigned long long bits = ((unsigned long long)transpose32(mhi, g.lane) << 32) |
+                                transpose32(mlo, g.lane);
       // slots run in descending list order: drop the leading slots above this
       // lane's last contributor (binary search on the staged positions)
       int lo_s = 0, hi_s = n;
@@ -1124,7 +1178,7 @@ k_backward(const uint2* __restrict__ ranges, const uint32_t* __restrict__ lists,
            const double* __restrict__ t_final, const int32_t* __restrict__ last_idx,
            const uint8_t* __restrict__ signs, Upstream up, const double* __restrict__ g_color,
            const double* __restrict__ g_depth, const double* __restrict__ g_alpha,
-           double* __restrict__ raw, float* __restrict__ grad_accum) {
+           double* __restrict__ raw, float* __restrict__ grad_accum, CList cl) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   WarpRing& ring = reinterpret_cast<WarpRing*>(smem_raw)[threadIdx.x >> 5];
   __shared__ double tab[32];
@@ -1150,7 +1204,7 @@ k_backward(const uint2* __restrict__ ranges, const uint32_t* __restrict__ lists,
       T = t_final[p];
     }
   }
-  bwd_sweep<FUSED, LATE>(ring, g, q, ranges[g.tile], lists, rec, coef, col64, tab, u, T, mylast,
+  bwd_sweep<FUSED, LATE>(ring, g, q, ranges[g.tile], cl, rec, coef, col64, tab, u, T, mylast,
                          raw, grad_accum);
 }
 
@@ -1199,7 +1253,7 @@ __global__ void __launch_bounds__(RASTER_THREADS)
 k_forward_backward(const uint2* __restrict__ ranges, const uint32_t* __restrict__ lists,
                    const Record* __restrict__ rec, const ChainCoef* __restrict__ coef, int ntx,
                    int width, int height, sgad_loss_target tgt, Upstream up,
-                   float* __restrict__ grad_accum) {
+                   float* __restrict__ grad_accum, CList cl) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   unsigned char* slab = smem_raw + FB_SLAB * (threadIdx.x >> 5);
   __shared__ double tab[32];
@@ -1207,8 +1261,8 @@ k_forward_backward(const uint2* __restrict__ ranges, const uint32_t* __restrict_
   const TileGeom g = tile_geom(ntx, width, height);
   const SweepGeom q = sweep_geom(g);
   const uint2 rg = ranges[g.tile];
-  const PixState st = fwd_sweep(*reinterpret_cast<FwdStage*>(slab), g, q, rg, lists, rec,
-                                nullptr, tab);
+  const PixState st = fwd_sweep<true>(*reinterpret_cast<FwdStage*>(slab), g, q, rg, lists, rec,
+                                      nullptr, tab, cl);
   const int64_t p = (int64_t)g.py * width + g.px;
   const uint8_t code = loss_epilogue(st, g, p, tgt);
   __syncwarp();
@@ -1218,7 +1272,7 @@ k_forward_backward(const uint2* __restrict__ ranges, const uint32_t* __restrict_
     u = fused_upstream(code, nullptr, p, up);
     if (any_upstream(u)) mylast = st.last;
   }
-  bwd_sweep<true>(*reinterpret_cast<WarpRing*>(slab), g, q, rg, lists, rec, coef, nullptr, tab, u,
+  bwd_sweep<true>(*reinterpret_cast<WarpRing*>(slab), g, q, rg, cl, rec, coef, nullptr, tab, u,
                   st.T, mylast, nullptr, grad_accum);
 }
 
@@ -1335,6 +1389,21 @@ static int bits_for(uint32_t maxval) {
 
 using namespace sgad;
 
+// the per-warp compact lists of the prepared view (sized at the forward)
+static int ensure_clist(sgad_raster* h) {
+  const size_t n = 8 * (size_t)(h->n_pairs > 0 ? h->n_pairs : 1);
+  SGAD_CHECK_CUDA(h->cl_e.ensure(sizeof(uint32_t) * n));
+  SGAD_CHECK_CUDA(h->cl_k.ensure(sizeof(int32_t) * n));
+  SGAD_CHECK_CUDA(h->cl_m.ensure(sizeof(uint32_t) * n));
+  SGAD_CHECK_CUDA(h->cl_n.ensure(sizeof(uint32_t) * 8 * (size_t)(h->n_tiles > 0 ? h->n_tiles : 1)));
+  return SGAD_OK;
+}
+
+static CList clist_of(sgad_raster* h) {
+  return CList{h->cl_e.as<uint32_t>(), h->cl_k.as<int32_t>(), h->cl_m.as<uint32_t>(),
+               h->cl_n.as<uint32_t>()};
+}
+
 extern "C" {
 
 const char* sgad_last_error(void) { return g_err; }
@@ -1365,7 +1434,7 @@ int sgad_raster_destroy(sgad_raster* h) {
                     &h->keys1, &h->vals0, &h->vals1, &h->pcount, &h->poffset, &h->pkeys0,
                     &h->pkeys1, &h->pvals0, &h->pvals1, &h->ranges, &h->cub_tmp,
                     &h->trans_final, &h->last_idx, &h->signs, &h->raw_grads, &h->rank_of,
-                    &h->scratch, &h->col64, &h->zrange, &h->k32a, &h->k32b, &h->bbox, &h->runs, &h->raw32};
+                    &h->scratch, &h->col64, &h->zrange, &h->k32a, &h->k32b, &h->bbox, &h->runs, &h->raw32, &h->cl_e, &h->cl_k, &h->cl_m, &h->cl_n};
   for (DevBuf* b : bufs) b->release();
   if (h->pinned) cudaFreeHost(h->pinned);
   delete h;
@@ -1594,11 +1663,14 @@ int sgad_raster_forward(sgad_raster* h, double* out_color, double* out_depth, do
   const dim3 grid((unsigned)h->n_tiles), block(RASTER_THREADS);
   const double* col64 = h->any_f64 ? h->col64.as<double>() : nullptr;
   if (int rc = smem_attrs()) return rc;
+  if (state)
+    if (int rc = ensure_clist(h)) return rc;
+  const CList cl = clist_of(h);
 #define SGAD_FWD(I, S, L)                                                                      \
   k_forward<I, S, L><<<grid, block, FWD_SMEM, st>>>(                                                \
       h->ranges.as<uint2>(), h->pvals0.as<uint32_t>(), h->records.as<Record>(), col64, h->ntx, \
       h->cam.width, h->cam.height, out_color, out_depth, out_alpha, out_count,               \
-      h->trans_final.as<double>(), h->last_idx.as<int32_t>(), h->signs.as<uint8_t>(), tg)
+      h->trans_final.as<double>(), h->last_idx.as<int32_t>(), h->signs.as<uint8_t>(), tg, cl)
   if (images && state && loss) SGAD_FWD(true, true, true);
   else if (images && state) SGAD_FWD(true, true, false);
   else if (images) SGAD_FWD(true, false, false);
@@ -1639,7 +1711,8 @@ int sgad_raster_backward(sgad_raster* h, int32_t mode, const double* g_color,
           h->ranges.as<uint2>(), h->pvals0.as<uint32_t>(), h->records.as<Record>(),
           h->coef.as<ChainCoef>(), h->any_f64 ? h->col64.as<double>() : nullptr, h->ntx,
           h->cam.width, h->cam.height, h->trans_final.as<double>(), h->last_idx.as<int32_t>(),
-          h->signs.as<uint8_t>(), up, g_color, nullptr, nullptr, nullptr, h->raw32.as<float>());
+          h->signs.as<uint8_t>(), up, g_color, nullptr, nullptr, nullptr, h->raw32.as<float>(),
+          clist_of(h));
       SGAD_LAUNCH_CHECK();
       k_chain_late<<<blocks_for(h->n_total, 256), 256, 0, st>>>(
           h->raw32.as<float>(), h->coef.as<ChainCoef>(), h->records.as<Record>(),
@@ -1652,7 +1725,7 @@ int sgad_raster_backward(sgad_raster* h, int32_t mode, const double* g_color,
         h->coef.as<ChainCoef>(), h->any_f64 ? h->col64.as<double>() : nullptr, h->ntx,
         h->cam.width, h->cam.height,
         h->trans_final.as<double>(), h->last_idx.as<int32_t>(), h->signs.as<uint8_t>(), up,
-        g_color, nullptr, nullptr, nullptr, grad_accum);
+        g_color, nullptr, nullptr, nullptr, grad_accum, clist_of(h));
     SGAD_LAUNCH_CHECK();
     return SGAD_OK;
   }
@@ -1668,7 +1741,7 @@ int sgad_raster_backward(sgad_raster* h, int32_t mode, const double* g_color,
   k_backward<false><<<grid, block, BWD_SMEM, st>>>(
       h->ranges.as<uint2>(), h->pvals0.as<uint32_t>(), h->records.as<Record>(), nullptr,
       h->any_f64 ? h->col64.as<double>() : nullptr, h->ntx, h->cam.width, h->cam.height, h->trans_final.as<double>(), h->last_idx.as<int32_t>(),
-      nullptr, up, g_color, g_depth, g_alpha, h->raw_grads.as<double>(), nullptr);
+      nullptr, up, g_color, g_depth, g_alpha, h->raw_grads.as<double>(), nullptr, clist_of(h));
   SGAD_LAUNCH_CHECK();
   k_chain_exact<<<blocks_for(h->n_surv, 256), 256, 0, st>>>(
       h->records.as<Record>(), h->raw_grads.as<double>(), h->vals0.as<uint32_t>(),
@@ -1690,13 +1763,15 @@ int sgad_raster_forward_backward(sgad_raster* h, const sgad_loss_target* target,
   cudaStream_t st = (cudaStream_t)stream_;
   if (h->n_surv == 0) return SGAD_OK;
   if (int rc = smem_attrs()) return rc;
+  if (int rc = ensure_clist(h)) return rc;
   const int64_t npx = (int64_t)h->cam.width * h->cam.height;
   Upstream up;
   up.kc = target->rho / (double)(3 * npx);
   up.kd = target->n_depth > 0 ? target->sigma / (double)target->n_depth : 0.0;
   k_forward_backward<<<dim3((unsigned)h->n_tiles), dim3(RASTER_THREADS), FB_SMEM, st>>>(
       h->ranges.as<uint2>(), h->pvals0.as<uint32_t>(), h->records.as<Record>(),
-      h->coef.as<ChainCoef>(), h->ntx, h->cam.width, h->cam.height, *target, up, grad_accum);
+      h->coef.as<ChainCoef>(), h->ntx, h->cam.width, h->cam.height, *target, up, grad_accum,
+      clist_of(h));
   SGAD_LAUNCH_CHECK();
   h->forwarded = 0;
   h->fused_ready = 0;
