@@ -42,7 +42,7 @@ struct __align__(16) ChainCoef {  // fused backward: d(param)/d(image quantity),
   float k_r;        // d sigma -> radius: fx / z
   float a_u, a_v, a_z, a_s;  // delta <- (u0, v0, z, sigma)
   float k_op;       // opacity -> logit: op (1 - op)
-  float pad_[2];    // one 32-byte sector per Gaussian
+  float pad_[2];    // [0]: 1 / sigma (late chain); one 32-byte sector per Gaussian
 };
 
 constexpr uint32_t GID_LEARN = 0x80000000u;
@@ -243,7 +243,8 @@ k_project(const sgad_frame* __restrict__ frames, sgad_camera cam, int ntx, int n
         c.a_z = (float)(sgn * o.dir[2]);
         c.a_s = (float)(-sgn * o.dir[2] * o.sig * iz);
         c.k_op = (float)(o.op * (1.0 - o.op));
-        c.pad_[0] = c.pad_[1] = 0.0f;
+        c.pad_[0] = (float)(1.0 / o.sig);  // 1 / sigma for the late chain
+        c.pad_[1] = 0.0f;
         cs[threadIdx.x] = c;
       }
     }
@@ -1224,8 +1225,8 @@ __global__ void k_chain_late(float* __restrict__ raw, const ChainCoef* __restric
     return;  // not reached by this view (or culled)
   const float4* cp = reinterpret_cast<const float4*>(coef + e);
   const float4 k0 = __ldg(cp), k1 = __ldg(cp + 1);
-  const uint32_t gid = __ldg(&rec[e].gid) & ~GID_LEARN;
-  const float gsig = (float)((double)r0.w / __ldg(&rec[e].sigma));  // raw slot holds gsig * sigma
+  const uint32_t gid = e;  // records and gradients are indexed by Gaussian id
+  const float gsig = r0.w * k1.z;  // the raw slot holds gsig * sigma; k1.z = 1 / sigma
   float4* dst = reinterpret_cast<float4*>(grad_accum + (size_t)gid * 8);
   float4 a = dst[0];
   float2 b = *reinterpret_cast<float2*>(grad_accum + (size_t)gid * 8 + 4);
