@@ -484,7 +484,6 @@ constexpr int RING = 10;
 
 struct WarpRing {
   uint32_t e[RING][WIN];                  // record index of each slot
-  int32_t k[RING][WIN];                   // list position of each slot
   unsigned long long mask[RING][32];      // per-lane bits over the slots
 };
 
@@ -608,44 +607,6 @@ __device__ __forceinline__ Head load_entry(const uint32_t* __restrict__ lists,
   return h;
 }
 
-// One 32-entry chunk: entries that reach at least one pixel are appended to
-// window slots n, n+1, ... in ascending (DESC = false) or descending (DESC =
-// true) list order; their pixel masks land in the slot-owner lanes' registers
-// mlo/mhi.  Returns the number appended (warp-uniform).
-template <bool DESC>
-__device__ __forceinline__ int fill_chunk(uint32_t* __restrict__ se, int32_t* __restrict__ sk,
-                                          const Head& hd, double xlo, double ylo, int lane, int n,
-                                          uint32_t& mlo, uint32_t& mhi) {
-  uint32_t m = 0;
-  if (hd.valid) {
-    // cheap conservative cull of the whole rectangle first
-    const float uf = (float)hd.u0, vf = (float)hd.v0;
-    const float rr = (float)(3.0 * hd.sig) * 1.0001f + 0.01f;
-    const float xl = (float)xlo, yl = (float)ylo;
-    const float dx = fmaxf(fmaxf(xl - uf, uf - (xl + 7.0f)), 0.0f);
-    const float dy = fmaxf(fmaxf(yl - vf, vf - (yl + 3.0f)), 0.0f);
-    if (dx * dx + dy * dy <= rr * rr)
-      m = pixel_mask_exact(hd.u0, hd.v0, SG_MUL(9.0, SG_MUL(hd.sig, hd.sig)), xlo, ylo);
-  }
-  const uint32_t keep = __ballot_sync(0xffffffffu, m != 0);
-  const int c = __popc(keep);
-  if (m) {
-    const int rank = DESC ? __popc(lane == 31 ? 0u : (keep >> (lane + 1)))
-                          : __popc(keep & ((1u << lane) - 1u));
-    se[n + rank] = hd.e;
-    sk[n + rank] = (int32_t)hd.k;
-  }
-  // slot n + q is owned by lane (n + q) & 31 (register mlo for slots < 32,
-  // mhi above); it pulls the mask of the q-th kept entry
-  const int q = (lane - n) & 31;
-  const int src = q < c ? nth_set_bit(keep, DESC ? c - 1 - q : q) : 0;
-  const uint32_t val = __shfl_sync(0xffffffffu, m, src);
-  if (q < c) {
-    if (n + q < 32) mlo = val; else mhi = val;
-  }
-  return c;
-}
-
 // ---- forward: window-synchronous, entry data staged in shared memory ----
 // The forward's per-contribution work is light, so it keeps one window at a
 // time with the entries' fields in shared memory (short-latency loads); the
@@ -726,51 +687,16 @@ __device__ __forceinline__ int fill_chunk_fwd(FwdStage& s, const Head& hd,
   return c;
 }
 
-// Stage the next window into ring slot `slot`: whole 32-entry chunks from
-// `pos` (ascending) or below `pos` (descending) until more than 32 slots are
-// used, each chunk's list entries and record heads loaded one chunk ahead.
-// Returns the per-lane 64-bit mask; pos advances.
-template <bool DESC>
-__device__ __forceinline__ unsigned long long stage_window(
-    WarpRing& rg, int slot, const uint32_t* __restrict__ lists, const Record* __restrict__ rec,
-    int64_t& pos, int64_t lo, int64_t hi, double xlo, double ylo, int lane, int& n) {
-  n = 0;
-  uint32_t mlo = 0, mhi = 0;
-  if (!DESC) {
-    Head nx = load_entry(lists, rec, pos, lo, hi, lane);
-    while (n <= 32 && pos < hi) {
-      const Head hc = nx;
-      nx = load_entry(lists, rec, pos + 32, lo, hi, lane);
-      n += fill_chunk<false>(rg.e[slot], rg.k[slot], hc, xlo, ylo, lane, n, mlo, mhi);
-      pos += 32;
-    }
-  } else {
-    const int64_t top = pos;
-    Head nx = load_entry(lists, rec, pos - 32, lo, top, lane);
-    while (n <= 32 && pos > lo) {
-      const Head hc = nx;
-      nx = load_entry(lists, rec, pos - 64, lo, top, lane);
-      n += fill_chunk<true>(rg.e[slot], rg.k[slot], hc, xlo, ylo, lane, n, mlo, mhi);
-      pos -= 32;
-    }
-    if (pos < lo) pos = lo;
-  }
-  __syncwarp();
-  return ((unsigned long long)transpose32(mhi, lane) << 32) | transpose32(mlo, lane);
-}
-
-// One contribution's record fields, loaded a step ahead of their use.
+// One contribution's record fields.
 struct Contrib {
   double u0, v0, sig, op, z, nh;
   float r, g, b;
   uint32_t gid, e;
-  int32_t k;
 };
 
 __device__ __forceinline__ void load_contrib(Contrib& q, const WarpRing& rg, int slot, int j,
                                              const Record* __restrict__ rec) {
   q.e = rg.e[slot][j];
-  q.k = rg.k[slot][j];
   const double2* rp = reinterpret_cast<const double2*>(rec + q.e);
   const double2 uv = __ldg(rp), so = __ldg(rp + 1), zn = __ldg(rp + 2);
   const float4 cg = __ldg(reinterpret_cast<const float4*>(rp + 3));
@@ -1040,16 +966,17 @@ __device__ __forceinline__ void bwd_sweep(WarpRing& ring, const TileGeom& g, con
       // takes slots i and 32 + i, whose masks are already exact
       const int n = (int)min(cpos, (int64_t)WIN);
       uint32_t mlo = 0, mhi = 0;
+      int kv0 = 0, kv1 = 0;  // list positions of slots lane and 32 + lane
       {
         const int64_t i0 = cbase + cpos - 1 - g.lane, i1 = i0 - 32;
         if (g.lane < n) {
           ring.e[slot][g.lane] = cl.e[i0];
-          ring.k[slot][g.lane] = cl.k[i0];
+          kv0 = cl.k[i0];
           mlo = cl.m[i0];
         }
         if (32 + g.lane < n) {
           ring.e[slot][32 + g.lane] = cl.e[i1];
-          ring.k[slot][32 + g.lane] = cl.k[i1];
+          kv1 = cl.k[i1];
           mhi = cl.m[i1];
         }
       }
@@ -1058,11 +985,15 @@ __device__ __forceinline__ void bwd_sweep(WarpRing& ring, const TileGeom& g, con
       unsigned long long bits = ((unsigned long long)transpose32(mhi, g.lane) << 32) |
                                 transpose32(mlo, g.lane);
       // slots run in descending list order: drop the leading slots above this
-      // lane's last contributor (binary search on the staged positions)
-      int lo_s = 0, hi_s = n;
-      while (lo_s < hi_s) {
-        const int mid = (lo_s + hi_s) >> 1;
-        if (ring.k[slot][mid] > mylast) lo_s = mid + 1; else hi_s = mid;
+      // lane's last contributor (binary search over the slots' positions,
+      // held in the slot-owner lanes' registers)
+      int lo_s = 0;
+#pragma unroll
+      for (int step = 64; step >= 1; step >>= 1) {
+        const int cand = lo_s + step, sl = min(cand - 1, 63);
+        const int ka = __shfl_sync(0xffffffffu, kv0, sl & 31);
+        const int kb = __shfl_sync(0xffffffffu, kv1, sl & 31);
+        if (cand <= n && (sl < 32 ? ka : kb) > mylast) lo_s = cand;
       }
       if (lo_s >= 64) bits = 0ull;
       else bits &= ~((1ull << lo_s) - 1ull);
