@@ -57,13 +57,13 @@ k_adam(P* __restrict__ params, P* __restrict__ grads, P* __restrict__ m,
 // arithmetic -- reciprocals of the bias corrections precomputed, fast exp /
 // sqrt -- so the step is bound by its 216 bytes per Gaussian, not by fp64
 // division and square-root sequences.
-template <>
+// grid (ceil(hw / 256), n_frames): no 64-bit division per thread
 __global__ void __launch_bounds__(256)
-k_adam<float>(float* __restrict__ params, float* __restrict__ grads, float* __restrict__ m,
-              float* __restrict__ v, int64_t n_frames, int64_t hw, AdamArgs a) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n_frames * hw) return;
-  const int64_t f = i / hw, p = i - f * hw;
+k_adam_f32(float* __restrict__ params, float* __restrict__ grads, float* __restrict__ m,
+           float* __restrict__ v, int64_t hw, AdamArgs a) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= hw) return;
+  const int64_t f = blockIdx.y, i = f * hw + p;
   float4* gp = reinterpret_cast<float4*>(grads + 8 * i);
   const float4 g0 = gp[0], g1 = gp[1];
   gp[0] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -110,8 +110,9 @@ extern "C" int sgad_adam_step(void* params, void* grads, void* m, void* v, int64
     sgad::k_adam<double><<<nb, 256, 0, (cudaStream_t)stream>>>(
         (double*)params, (double*)grads, (double*)m, (double*)v, n_frames, hw, a);
   else
-    sgad::k_adam<float><<<nb, 256, 0, (cudaStream_t)stream>>>(
-        (float*)params, (float*)grads, (float*)m, (float*)v, n_frames, hw, a);
+    sgad::k_adam_f32<<<dim3((unsigned)((hw + 255) / 256), (unsigned)n_frames), 256, 0,
+                        (cudaStream_t)stream>>>((float*)params, (float*)grads, (float*)m,
+                                                (float*)v, hw, a);
   SGAD_LAUNCH_CHECK();
   return SGAD_OK;
 }
