@@ -139,7 +139,8 @@ __device__ __forceinline__ Params load_params(const sgad_frame& f, int64_t p, in
 // the near-plane and on-screen culls.  Operation order matches the reference.
 __device__ __forceinline__ bool project_point(const sgad_frame& f, int64_t p, const Params& q,
                                               const sgad_camera& cam, Proj& o) {
-  const double xx = (double)(p % f.width), yy = (double)(p / f.width);
+  const int pi = (int)p;  // < 2^30 (checked in sgad_raster_prepare)
+  const double xx = (double)(pi % f.width), yy = (double)(pi / f.width);
   const double r0 = SG_DIV(SG_SUB(xx, f.cx), f.fx);
   const double r1 = SG_DIV(SG_SUB(yy, f.cy), f.fy);
   o.bd = SG_ADD(q.base, q.delta);
