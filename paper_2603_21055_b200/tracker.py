@@ -399,6 +399,9 @@ def init_pose_constant_speed(prev: Pose, prev_prev: Pose) -> Pose:
     return prev.compose(prev_prev.inverse().compose(prev))
 
 
+_RENDER_POOL = {}
+
+
 class _RenderResiduals:
     """Residual vector of tracker.py:379-383 on the GPU: the previous frame's
     map rendered at a candidate pose (K1-K4 with preallocated images), L1
@@ -420,8 +423,13 @@ class _RenderResiduals:
                                                  device=dev)
         self.img = [tuple(torch.empty(shape, dtype=torch.float64, device=dev)
                           for shape in ((h, w, 3), (h, w), (h, w))) for _ in range(2)]
-        self.rasters = [Raster(dev), Raster(dev)]
-        self.streams = [torch.cuda.Stream(dev), torch.cuda.Stream(dev)]
+        # raster handles and streams are reused across calls (their grow-only
+        # scratch would otherwise be reallocated -- cudaFree synchronises)
+        key = (dev.index, "render_init")
+        if key not in _RENDER_POOL:
+            _RENDER_POOL[key] = ([Raster(dev), Raster(dev)],
+                                 [torch.cuda.Stream(dev), torch.cuda.Stream(dev)])
+        self.rasters, self.streams = _RENDER_POOL[key]
         self.cam = camera_of(self.intr)
         self.n = 4 * h * w
 
