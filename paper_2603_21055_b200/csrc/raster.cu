@@ -31,7 +31,16 @@ struct __align__(16) Record {
 
 struct TileBox {         // inclusive tile bbox of a survivor (rasterizer.py:187-199)
   uint16_t tx0, tx1, ty0, ty1;
+  int16_t px0, px1, py0, py1;  // pixel centres its 3-sigma disc may reach (conservative)
 };
+
+// Tile list values: the record index in the low 26 bits and, above it, which
+// of the tile's 8x4 warp rectangles the Gaussian's (conservative) 3-sigma box
+// reaches -- 2 column bits, 4 row bits -- so K4 culls a list entry against
+// its rectangle without loading the record.  Views with 2^26 or more
+// Gaussians store the bare index and K4 culls nothing at this stage.
+constexpr int LIST_IDX_BITS = 26;
+constexpr uint32_t LIST_IDX_MASK = (1u << LIST_IDX_BITS) - 1u;
 static_assert(sizeof(Record) == 64, "record must be one 64-byte line");
 // K4/K5 read the record as four 16-byte vectors: (u0, v0) (sigma, opacity) (z, nh) (r, g, b, gid)
 static_assert(offsetof(Record, sigma) == 16 && offsetof(Record, z) == 32 &&
@@ -61,6 +70,7 @@ struct sgad_raster {
   int64_t n_total = 0, n_surv = 0, n_pairs = 0;
   int32_t n_tiles = 0, ntx = 0, nty = 0;
   int prepared = 0, forwarded = 0, have_coef = 0, fused_ready = 0;
+  int packed = 0;  // tile list values carry the warp-rectangle bits (n_total < 2^26)
   double rho = 0, sigma_d = 0;
   int64_t n_depth = 0;
   uint32_t* pinned = nullptr;  // host-pinned counters
@@ -233,6 +243,14 @@ k_project(const sgad_frame* __restrict__ frames, sgad_camera cam, int ntx, int n
       bx.tx1 = (uint16_t)x1;
       bx.ty0 = (uint16_t)y0;
       bx.ty1 = (uint16_t)y1;
+      {  // pixel-centre range of the disc, grown by a margin far above fp rounding
+        const double R = SG_ADD(SG_MUL(rr, 1.0001), 0.01);
+        const double lim_x = (double)cam.width, lim_y = (double)cam.height;
+        bx.px0 = (int16_t)fmin(fmax(ceil(SG_SUB(o.u0, R)), -1.0), lim_x);
+        bx.px1 = (int16_t)fmin(fmax(floor(SG_ADD(o.u0, R)), -1.0), lim_x);
+        bx.py0 = (int16_t)fmin(fmax(ceil(SG_SUB(o.v0, R)), -1.0), lim_y);
+        bx.py1 = (int16_t)fmin(fmax(floor(SG_ADD(o.v0, R)), -1.0), lim_y);
+      }
       box[gid] = bx;
       if (want_coef) {
         ChainCoef c;
@@ -415,19 +433,28 @@ __global__ void k_tile_count(const uint32_t* __restrict__ perm, const TileBox* _
 }
 
 __global__ void k_tile_emit(const uint32_t* __restrict__ perm, const TileBox* __restrict__ box,
-                            const uint32_t* __restrict__ off, uint32_t n, int ntx,
+                            const uint32_t* __restrict__ off, uint32_t n, int ntx, int packed,
                             uint32_t* __restrict__ pkeys, uint32_t* __restrict__ pvals) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const uint32_t e = perm[i];
   const TileBox r = box[e];
   uint32_t o = off[i];
-  for (int ty = r.ty0; ty <= r.ty1; ++ty)
+  for (int ty = r.ty0; ty <= r.ty1; ++ty) {
+    uint32_t rows = 0;  // 4-row bands [by + 4b, by + 4b + 3] the box reaches
+    const int by = ty * SGAD_TILE;
+#pragma unroll
+    for (int b = 0; b < 4; ++b)
+      rows |= (r.py0 <= by + 4 * b + 3 && r.py1 >= by + 4 * b) ? (1u << b) : 0u;
     for (int tx = r.tx0; tx <= r.tx1; ++tx) {
+      const int bx = tx * SGAD_TILE;
+      const uint32_t cols = ((r.px0 <= bx + 7 && r.px1 >= bx) ? 1u : 0u) |
+                            ((r.px0 <= bx + 15 && r.px1 >= bx + 8) ? 2u : 0u);
       pkeys[o] = (uint32_t)(ty * ntx + tx);
-      pvals[o] = e;
+      pvals[o] = packed ? e | ((cols | rows << 2) << LIST_IDX_BITS) : e;
       ++o;
     }
+  }
 }
 
 __global__ void k_tile_ranges(const uint32_t* __restrict__ pkeys, uint32_t n,
@@ -581,31 +608,11 @@ __device__ __forceinline__ int nth_set_bit(uint32_t m, int q) {
   return pos;
 }
 
-struct Head {  // one lane's list entry of a chunk, loaded one chunk ahead
-  int64_t k;
-  uint32_t e;
-  bool valid;
-  double u0, v0, sig, op;
-};
-
-__device__ __forceinline__ Head load_entry(const uint32_t* __restrict__ lists,
-                                           const Record* __restrict__ rec, int64_t base,
-                                           int64_t lo, int64_t hi, int lane) {
-  Head h;
-  h.k = base + lane;
-  h.valid = h.k >= lo && h.k < hi;
-  h.e = 0;
-  h.u0 = h.v0 = h.sig = h.op = 0.0;
-  if (h.valid) {
-    h.e = __ldg(lists + h.k);
-    const double2* hp = reinterpret_cast<const double2*>(rec + h.e);  // u0, v0 | sigma, op
-    const double2 a = __ldg(hp), b = __ldg(hp + 1);
-    h.u0 = a.x;
-    h.v0 = a.y;
-    h.sig = b.x;
-    h.op = b.y;
-  }
-  return h;
+// the list value of entry base + lane (0 past the range)
+__device__ __forceinline__ uint32_t load_value(const uint32_t* __restrict__ lists, int64_t base,
+                                               int64_t hi, int lane) {
+  const int64_t k = base + lane;
+  return k < hi ? __ldg(lists + k) : 0u;
 }
 
 // ---- forward: window-synchronous, entry data staged in shared memory ----
@@ -615,6 +622,10 @@ __device__ __forceinline__ Head load_entry(const uint32_t* __restrict__ lists,
 struct FwdStage {
   double u0[WIN], v0[WIN], nh[WIN], op[WIN], z[WIN], rgb[3][WIN], thr[WIN];
   int32_t k[WIN];
+  // cull queue (ring of WIN): list entries whose 3-sigma box reaches the
+  // warp's rectangle, waiting for their pixel masks
+  uint32_t qe[WIN];
+  int32_t qk[WIN];
 };
 
 // Per-warp compact lists written by a forward that keeps state for the
@@ -633,51 +644,58 @@ __device__ __forceinline__ int64_t clist_base(uint2 rg, int warp) {
   return 8 * (int64_t)rg.x + (int64_t)warp * (int64_t)(rg.y - rg.x);
 }
 
+// Pixel masks of up to 32 queued entries (one per lane, all lanes busy),
+// staged into window slots n.. in list order; returns how many had pixels.
 template <bool EXACT>
-__device__ __forceinline__ int fill_chunk_fwd(FwdStage& s, const Head& hd,
-                                              const Record* __restrict__ rec,
-                                              const double* __restrict__ col64, double xlo,
-                                              double ylo, int lane, int n, uint32_t& mlo,
-                                              uint32_t& mhi, const CList& cl, int64_t cbase) {
-  uint32_t m = 0;
-  if (hd.valid) {
-    const float uf = (float)hd.u0, vf = (float)hd.v0;
-    const float rr = (float)(3.0 * hd.sig) * 1.0001f + 0.01f;
-    const float xl = (float)xlo, yl = (float)ylo;
-    const float dx = fmaxf(fmaxf(xl - uf, uf - (xl + 7.0f)), 0.0f);
-    const float dy = fmaxf(fmaxf(yl - vf, vf - (yl + 3.0f)), 0.0f);
-    if (dx * dx + dy * dy <= rr * rr)
-      m = EXACT ? pixel_mask_exact(hd.u0, hd.v0, SG_MUL(9.0, SG_MUL(hd.sig, hd.sig)), xlo, ylo)
-                : pixel_mask(hd.u0, hd.v0, SG_MUL(9.0, SG_MUL(hd.sig, hd.sig)), xlo, ylo);
+__device__ __forceinline__ int stage_from_queue(FwdStage& s, int qh, int take,
+                                                const Record* __restrict__ rec,
+                                                const double* __restrict__ col64, double xlo,
+                                                double ylo, int lane, int n, uint32_t& mlo,
+                                                uint32_t& mhi, const CList& cl, int64_t cbase) {
+  uint32_t m = 0, e = 0;
+  int32_t k = 0;
+  double u0 = 0.0, v0 = 0.0, sig = 0.0, op = 0.0;
+  const double2* rp = nullptr;
+  if (lane < take) {
+    const int qi = (qh + lane) & (WIN - 1);
+    e = s.qe[qi];
+    k = s.qk[qi];
+    rp = reinterpret_cast<const double2*>(rec + e);
+    const double2 a = __ldg(rp), b = __ldg(rp + 1);  // u0, v0 | sigma, opacity
+    u0 = a.x;
+    v0 = a.y;
+    sig = b.x;
+    op = b.y;
+    const double thr = SG_MUL(9.0, SG_MUL(sig, sig));
+    m = EXACT ? pixel_mask_exact(u0, v0, thr, xlo, ylo) : pixel_mask(u0, v0, thr, xlo, ylo);
   }
   const uint32_t keep = __ballot_sync(0xffffffffu, m != 0);
   const int c = __popc(keep);
   if (m) {
     const int j = n + __popc(keep & ((1u << lane) - 1u));
-    if (EXACT) {  // the backward's compact list (cbase = this chunk's first slot - n)
-      cl.e[cbase + j] = hd.e;
-      cl.k[cbase + j] = (int32_t)hd.k;
+    if (EXACT) {  // the backward's compact list (cbase = this batch's first slot - n)
+      cl.e[cbase + j] = e;
+      cl.k[cbase + j] = k;
       cl.m[cbase + j] = m;
     }
-    const double2* rp = reinterpret_cast<const double2*>(rec + hd.e);
     const double2 zn = __ldg(rp + 2);                                        // z, nh
     const float4 cg = __ldg(reinterpret_cast<const float4*>(rp + 3));        // r, g, b, gid
-    s.thr[j] = SG_MUL(9.0, SG_MUL(hd.sig, hd.sig));
-    s.u0[j] = hd.u0;
-    s.v0[j] = hd.v0;
+    if (!EXACT) s.thr[j] = SG_MUL(9.0, SG_MUL(sig, sig));
+    s.u0[j] = u0;
+    s.v0[j] = v0;
     s.nh[j] = zn.y;
-    s.op[j] = hd.op;
+    s.op[j] = op;
     s.z[j] = zn.x;
     if (col64) {  // fp64 drop-in maps keep exact fp64 colours
-      s.rgb[0][j] = __ldg(col64 + 3 * (size_t)hd.e);
-      s.rgb[1][j] = __ldg(col64 + 3 * (size_t)hd.e + 1);
-      s.rgb[2][j] = __ldg(col64 + 3 * (size_t)hd.e + 2);
+      s.rgb[0][j] = __ldg(col64 + 3 * (size_t)e);
+      s.rgb[1][j] = __ldg(col64 + 3 * (size_t)e + 1);
+      s.rgb[2][j] = __ldg(col64 + 3 * (size_t)e + 2);
     } else {
       s.rgb[0][j] = cg.x;
       s.rgb[1][j] = cg.y;
       s.rgb[2][j] = cg.z;
     }
-    s.k[j] = (int32_t)hd.k;
+    s.k[j] = k;
   }
   const int q = (lane - n) & 31;
   const int src = q < c ? nth_set_bit(keep, q) : 0;
@@ -765,7 +783,7 @@ __device__ __forceinline__ SweepGeom sweep_geom(const TileGeom& g) {
 template <bool EXACT>
 __device__ __forceinline__ PixState fwd_sweep(FwdStage& s, const TileGeom& g, const SweepGeom& q,
                                               uint2 rg, const uint32_t* __restrict__ lists,
-                                              const Record* __restrict__ rec,
+                                              int packed, const Record* __restrict__ rec,
                                               const double* __restrict__ col64,
                                               const double* tab, const CList& cl) {
   PixState st{1.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0, -1};
@@ -773,16 +791,42 @@ __device__ __forceinline__ PixState fwd_sweep(FwdStage& s, const TileGeom& g, co
   int64_t pos = rg.x;
   const int64_t cbase = clist_base(rg, g.warp);
   int64_t nw = 0;  // compact entries written so far
-  Head nx = load_entry(lists, rec, pos, rg.x, rg.y, g.lane);
-  while (pos < (int64_t)rg.y && !__all_sync(0xffffffffu, done)) {
+  int qh = 0, qn = 0;  // cull queue head and fill (warp-uniform)
+  // list-value bits of this warp's rectangle (column g.warp & 1, band g.warp >> 1)
+  const uint32_t need =
+      packed ? (1u << (LIST_IDX_BITS + (g.warp & 1))) | (1u << (LIST_IDX_BITS + 2 + (g.warp >> 1)))
+             : 0u;
+  const uint32_t idx_mask = packed ? LIST_IDX_MASK : ~0u;
+  uint32_t nx0 = load_value(lists, pos, rg.y, g.lane);       // values two chunks ahead
+  uint32_t nx1 = load_value(lists, pos + 32, rg.y, g.lane);
+  while ((pos < (int64_t)rg.y || qn > 0) && !__all_sync(0xffffffffu, done)) {
     int n = 0;
     uint32_t mlo = 0, mhi = 0;
-    while (n <= 32 && pos < (int64_t)rg.y) {
-      const Head cur = nx;
-      nx = load_entry(lists, rec, pos + 32, rg.x, rg.y, g.lane);  // one chunk ahead
-      n += fill_chunk_fwd<EXACT>(s, cur, rec, col64, q.xlo, q.ylo, g.lane, n, mlo, mhi, cl,
-                                 cbase + nw);
-      pos += 32;
+    while (n <= 32) {
+      // cull whole chunks into the queue until 32 wait (the masks are then
+      // computed with every lane busy)
+      while (qn < 32 && pos < (int64_t)rg.y) {
+        const uint32_t cur = nx0;
+        nx0 = nx1;
+        nx1 = load_value(lists, pos + 64, rg.y, g.lane);
+        const bool hit = pos + g.lane < (int64_t)rg.y && (cur & need) == need;
+        const uint32_t b = __ballot_sync(0xffffffffu, hit);
+        if (hit) {
+          const int qi = (qh + qn + __popc(b & ((1u << g.lane) - 1u))) & (WIN - 1);
+          s.qe[qi] = cur & idx_mask;
+          s.qk[qi] = (int32_t)(pos + g.lane);
+        }
+        qn += __popc(b);
+        pos += 32;
+      }
+      if (qn == 0) break;
+      __syncwarp();
+      const int take = min(qn, 32);
+      n += stage_from_queue<EXACT>(s, qh, take, rec, col64, q.xlo, q.ylo, g.lane, n, mlo, mhi,
+                                   cl, cbase + nw);
+      qh = (qh + take) & (WIN - 1);
+      qn -= take;
+      __syncwarp();  // queue slots read above may be refilled next
     }
     nw += n;
     __syncwarp();
@@ -801,7 +845,8 @@ __device__ __forceinline__ PixState fwd_sweep(FwdStage& s, const TileGeom& g, co
       mine &= mine - 1;
       const double dx = SG_SUB(s.u0[j], q.pxd), dy = SG_SUB(s.v0[j], q.pyd);
       const double d2 = SG_ADD(SG_MUL(dx, dx), SG_MUL(dy, dy));
-      if (d2 > s.thr[j]) continue;  // rasterizer.py:248 (the mask is a superset)
+      if (!EXACT && d2 > s.thr[j]) continue;  // rasterizer.py:248 (superset masks only;
+                                              // exact masks already made this test)
       const double w = sgad_exp_neg(SG_MUL(d2, s.nh[j]), tab);
       double a = SG_MUL(s.op[j], w);
       if (a > SGAD_ALPHA_MAX) a = SGAD_ALPHA_MAX;
@@ -860,7 +905,7 @@ __device__ __forceinline__ uint8_t loss_epilogue(const PixState& st, const TileG
 
 template <bool IMAGES, bool STATE, bool LOSS>
 __global__ void __launch_bounds__(RASTER_THREADS)
-k_forward(const uint2* __restrict__ ranges, const uint32_t* __restrict__ lists,
+k_forward(const uint2* __restrict__ ranges, const uint32_t* __restrict__ lists, int packed,
           const Record* __restrict__ rec, const double* __restrict__ col64, int ntx, int width,
           int height, double* __restrict__ out_color, double* __restrict__ out_depth,
           double* __restrict__ out_alpha, int32_t* __restrict__ out_count,
@@ -872,7 +917,7 @@ k_forward(const uint2* __restrict__ ranges, const uint32_t* __restrict__ lists,
   load_exp_table(tab);
   const TileGeom g = tile_geom(ntx, width, height);
   const SweepGeom q = sweep_geom(g);
-  const PixState st = fwd_sweep<STATE>(s, g, q, ranges[g.tile], lists, rec, col64, tab, cl);
+  const PixState st = fwd_sweep<STATE>(s, g, q, ranges[g.tile], lists, packed, rec, col64, tab, cl);
   const int64_t p = (int64_t)g.py * width + g.px;
   if (g.valid) {
     if (IMAGES) {
@@ -1184,7 +1229,7 @@ constexpr size_t FB_SLAB = sizeof(WarpRing) > sizeof(FwdStage) ? sizeof(WarpRing
 
 __global__ void __launch_bounds__(RASTER_THREADS)
 k_forward_backward(const uint2* __restrict__ ranges, const uint32_t* __restrict__ lists,
-                   const Record* __restrict__ rec, const ChainCoef* __restrict__ coef, int ntx,
+                   int packed, const Record* __restrict__ rec, const ChainCoef* __restrict__ coef, int ntx,
                    int width, int height, sgad_loss_target tgt, Upstream up,
                    float* __restrict__ grad_accum, CList cl) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -1194,7 +1239,7 @@ k_forward_backward(const uint2* __restrict__ ranges, const uint32_t* __restrict_
   const TileGeom g = tile_geom(ntx, width, height);
   const SweepGeom q = sweep_geom(g);
   const uint2 rg = ranges[g.tile];
-  const PixState st = fwd_sweep<true>(*reinterpret_cast<FwdStage*>(slab), g, q, rg, lists, rec,
+  const PixState st = fwd_sweep<true>(*reinterpret_cast<FwdStage*>(slab), g, q, rg, lists, packed, rec,
                                       nullptr, tab, cl);
   const int64_t p = (int64_t)g.py * width + g.px;
   const uint8_t code = loss_epilogue(st, g, p, tgt);
@@ -1259,9 +1304,9 @@ __global__ void k_rank_of(const uint32_t* __restrict__ perm, uint32_t n, uint32_
 }
 
 __global__ void k_export_lists(const uint32_t* __restrict__ pvals, const uint32_t* __restrict__ rank,
-                               uint32_t n, int64_t* __restrict__ out) {
+                               uint32_t n, uint32_t idx_mask, int64_t* __restrict__ out) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) out[i] = rank[pvals[i]];
+  if (i < n) out[i] = rank[pvals[i] & idx_mask];
 }
 
 __global__ void k_export_ranges(const uint2* __restrict__ r, int n, int64_t* __restrict__ out) {
@@ -1403,6 +1448,7 @@ int sgad_raster_prepare(sgad_raster* h, const sgad_frame* frames, int32_t n_fram
   }
   SGAD_REQUIRE(n_total < (1ll << 30), "too many Gaussians (%lld)", (long long)n_total);
   h->n_total = n_total;
+  h->packed = n_total < (int64_t)(1u << sgad::LIST_IDX_BITS) ? 1 : 0;
   h->have_coef = want_coef != 0;
   h->any_f64 = 0;
   for (int i = 0; i < n_frames; ++i) h->any_f64 |= frames[i].planes_f64 ? 1 : 0;
@@ -1547,7 +1593,7 @@ int sgad_raster_prepare(sgad_raster* h, const sgad_frame* frames, int32_t n_fram
   SGAD_CHECK_CUDA(h->pvals0.ensure(sizeof(uint32_t) * (np_ + 1)));
   SGAD_CHECK_CUDA(h->pvals1.ensure(sizeof(uint32_t) * (np_ + 1)));
   k_tile_emit<<<blocks_for(ns, 256), 256, 0, st>>>(perm, h->bbox.as<TileBox>(),
-                                                   h->poffset.as<uint32_t>(), ns, h->ntx,
+                                                   h->poffset.as<uint32_t>(), ns, h->ntx, h->packed,
                                                    h->pkeys0.as<uint32_t>(), h->pvals0.as<uint32_t>());
   SGAD_LAUNCH_CHECK();
   cub::DoubleBuffer<uint32_t> pk(h->pkeys0.as<uint32_t>(), h->pkeys1.as<uint32_t>());
@@ -1601,7 +1647,8 @@ int sgad_raster_forward(sgad_raster* h, double* out_color, double* out_depth, do
   const CList cl = clist_of(h);
 #define SGAD_FWD(I, S, L)                                                                      \
   k_forward<I, S, L><<<grid, block, FWD_SMEM, st>>>(                                                \
-      h->ranges.as<uint2>(), h->pvals0.as<uint32_t>(), h->records.as<Record>(), col64, h->ntx, \
+      h->ranges.as<uint2>(), h->pvals0.as<uint32_t>(), h->packed, h->records.as<Record>(),     \
+      col64, h->ntx,                                                                         \
       h->cam.width, h->cam.height, out_color, out_depth, out_alpha, out_count,               \
       h->trans_final.as<double>(), h->last_idx.as<int32_t>(), h->signs.as<uint8_t>(), tg, cl)
   if (images && state && loss) SGAD_FWD(true, true, true);
@@ -1702,7 +1749,7 @@ int sgad_raster_forward_backward(sgad_raster* h, const sgad_loss_target* target,
   up.kc = target->rho / (double)(3 * npx);
   up.kd = target->n_depth > 0 ? target->sigma / (double)target->n_depth : 0.0;
   k_forward_backward<<<dim3((unsigned)h->n_tiles), dim3(RASTER_THREADS), FB_SMEM, st>>>(
-      h->ranges.as<uint2>(), h->pvals0.as<uint32_t>(), h->records.as<Record>(),
+      h->ranges.as<uint2>(), h->pvals0.as<uint32_t>(), h->packed, h->records.as<Record>(),
       h->coef.as<ChainCoef>(), h->ntx, h->cam.width, h->cam.height, *target, up, grad_accum,
       clist_of(h));
   SGAD_LAUNCH_CHECK();
@@ -1737,7 +1784,8 @@ int sgad_raster_get_tiles(sgad_raster* h, int64_t* ranges, int64_t* lists, void*
                                                           h->rank_of.as<uint32_t>());
     SGAD_LAUNCH_CHECK();
     k_export_lists<<<blocks_for(h->n_pairs, 256), 256, 0, st>>>(
-        h->pvals0.as<uint32_t>(), h->rank_of.as<uint32_t>(), (uint32_t)h->n_pairs, lists);
+        h->pvals0.as<uint32_t>(), h->rank_of.as<uint32_t>(), (uint32_t)h->n_pairs,
+        h->packed ? LIST_IDX_MASK : ~0u, lists);
     SGAD_LAUNCH_CHECK();
   }
   return SGAD_OK;
