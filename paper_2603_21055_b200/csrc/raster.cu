@@ -317,9 +317,12 @@ k_project(const sgad_frame* __restrict__ frames, sgad_camera cam, int ntx, int n
 }
 
 // ------------------------------------------------------------------ K2
-// 32-bit monotone depth buckets: floor((z - zmin) * scale).  Sorting them
+// 24-bit monotone depth buckets: floor((z - zmin) * scale).  Sorting them
 // stably leaves only runs of equal buckets to be put in exact (z, emission)
-// order by k_depth_fixup -- 4 radix passes instead of 8 for the 63-bit key.
+// order by k_depth_fixup -- 3 radix passes instead of 8 for the 63-bit key
+// (at C4 a bucket is ~1 um deep and nearly all runs are single entries).
+constexpr int DEPTH_KEY_BITS = 24;
+constexpr double DEPTH_KEY_TOP = (double)((1u << DEPTH_KEY_BITS) - 2u);  // survivors' largest
 __global__ void k_depth_key32(const unsigned long long* __restrict__ zkeys, uint32_t n,
                               double zmin, double scale, uint32_t* __restrict__ k32,
                               uint32_t* __restrict__ vals) {
@@ -327,10 +330,10 @@ __global__ void k_depth_key32(const unsigned long long* __restrict__ zkeys, uint
   if (i >= n) return;
   const unsigned long long zk = zkeys[i];
   if (zk == ~0ull) {
-    k32[i] = 0xFFFFFFFFu;  // culled: behind every survivor
+    k32[i] = 0xFFFFFFFFu;  // culled: behind every survivor (low 24 bits all set)
   } else {
     const double b = floor((__longlong_as_double((long long)zk) - zmin) * scale);
-    k32[i] = b >= 4294967294.0 ? 0xFFFFFFFEu : (uint32_t)b;
+    k32[i] = b >= DEPTH_KEY_TOP ? (uint32_t)DEPTH_KEY_TOP : (uint32_t)b;
   }
   vals[i] = i;
 }
@@ -608,6 +611,9 @@ __device__ __forceinline__ int nth_set_bit(uint32_t m, int q) {
   return pos;
 }
 
+#ifndef FWD_PREFETCH
+#define FWD_PREFETCH 2
+#endif
 // the list value of entry base + lane (0 past the range)
 __device__ __forceinline__ uint32_t load_value(const uint32_t* __restrict__ lists, int64_t base,
                                                int64_t hi, int lane) {
@@ -797,8 +803,9 @@ __device__ __forceinline__ PixState fwd_sweep(FwdStage& s, const TileGeom& g, co
       packed ? (1u << (LIST_IDX_BITS + (g.warp & 1))) | (1u << (LIST_IDX_BITS + 2 + (g.warp >> 1)))
              : 0u;
   const uint32_t idx_mask = packed ? LIST_IDX_MASK : ~0u;
-  uint32_t nx0 = load_value(lists, pos, rg.y, g.lane);       // values two chunks ahead
-  uint32_t nx1 = load_value(lists, pos + 32, rg.y, g.lane);
+  uint32_t nx[FWD_PREFETCH];  // list values FWD_PREFETCH chunks ahead
+#pragma unroll
+  for (int i = 0; i < FWD_PREFETCH; ++i) nx[i] = load_value(lists, pos + 32 * i, rg.y, g.lane);
   while ((pos < (int64_t)rg.y || qn > 0) && !__all_sync(0xffffffffu, done)) {
     int n = 0;
     uint32_t mlo = 0, mhi = 0;
@@ -806,9 +813,10 @@ __device__ __forceinline__ PixState fwd_sweep(FwdStage& s, const TileGeom& g, co
       // cull whole chunks into the queue until 32 wait (the masks are then
       // computed with every lane busy)
       while (qn < 32 && pos < (int64_t)rg.y) {
-        const uint32_t cur = nx0;
-        nx0 = nx1;
-        nx1 = load_value(lists, pos + 64, rg.y, g.lane);
+        const uint32_t cur = nx[0];
+#pragma unroll
+        for (int i = 0; i + 1 < FWD_PREFETCH; ++i) nx[i] = nx[i + 1];
+        nx[FWD_PREFETCH - 1] = load_value(lists, pos + 32 * FWD_PREFETCH, rg.y, g.lane);
         const bool hit = pos + g.lane < (int64_t)rg.y && (cur & need) == need;
         const uint32_t b = __ballot_sync(0xffffffffu, hit);
         if (hit) {
@@ -1498,7 +1506,7 @@ int sgad_raster_prepare(sgad_raster* h, const sgad_frame* frames, int32_t n_fram
     h->prepared = 1;
     return SGAD_OK;
   }
-  // K2: depth order.  Stable sort of 32-bit monotone depth buckets, then the
+  // K2: depth order.  Stable sort of 24-bit monotone depth buckets, then the
   // (rare, short) runs of equal buckets are ordered by exact (z, emission
   // index) -- together the (z, frame, pixel) order of np.lexsort.
   uint32_t* perm = h->vals0.as<uint32_t>();
@@ -1508,7 +1516,7 @@ int sgad_raster_prepare(sgad_raster* h, const sgad_frame* frames, int32_t n_fram
     double zmin, zmax;
     memcpy(&zmin, &zb[0], 8);
     memcpy(&zmax, &zb[1], 8);
-    const double scale = zmax > zmin ? 4294967294.0 / (zmax - zmin) : 0.0;
+    const double scale = zmax > zmin ? DEPTH_KEY_TOP / (zmax - zmin) : 0.0;
     const uint32_t nt = (uint32_t)n_total;  // culled ids carry the sentinel key
     SGAD_CHECK_CUDA(h->k32a.ensure(sizeof(uint32_t) * nt));
     SGAD_CHECK_CUDA(h->k32b.ensure(sizeof(uint32_t) * nt));
@@ -1519,9 +1527,11 @@ int sgad_raster_prepare(sgad_raster* h, const sgad_frame* frames, int32_t n_fram
     cub::DoubleBuffer<uint32_t> dk(h->k32a.as<uint32_t>(), h->k32b.as<uint32_t>());
     cub::DoubleBuffer<uint32_t> dv(h->vals1.as<uint32_t>(), h->vals0.as<uint32_t>());
     size_t tmp = 0;
-    SGAD_CHECK_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, dk, dv, (int)nt, 0, 32, st));
+    SGAD_CHECK_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, dk, dv, (int)nt, 0,
+                                                    DEPTH_KEY_BITS, st));
     SGAD_CHECK_CUDA(h->cub_tmp.ensure(tmp));
-    SGAD_CHECK_CUDA(cub::DeviceRadixSort::SortPairs(h->cub_tmp.p, tmp, dk, dv, (int)nt, 0, 32, st));
+    SGAD_CHECK_CUDA(cub::DeviceRadixSort::SortPairs(h->cub_tmp.p, tmp, dk, dv, (int)nt, 0,
+                                                    DEPTH_KEY_BITS, st));
     if (dv.Current() != perm)
       SGAD_CHECK_CUDA(cudaMemcpyAsync(perm, dv.Current(), sizeof(uint32_t) * ns,
                                       cudaMemcpyDeviceToDevice, st));
