@@ -427,13 +427,18 @@ k_long_runs(const uint2* __restrict__ long_runs, const uint32_t* __restrict__ n_
 }
 
 // ------------------------------------------------------------------ K3
-__global__ void k_tile_count(const uint32_t* __restrict__ perm, const TileBox* __restrict__ box,
-                             uint32_t n, uint32_t* __restrict__ cnt) {
-  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const TileBox r = box[perm[i]];
-  cnt[i] = (uint32_t)(r.tx1 - r.tx0 + 1) * (uint32_t)(r.ty1 - r.ty0 + 1);
-}
+// pair count of the i-th survivor in depth order (0 past the end), read by
+// the exclusive scan directly (no count array)
+struct TilePairCount {
+  const uint32_t* perm;
+  const TileBox* box;
+  uint32_t n;
+  __device__ __forceinline__ uint32_t operator()(uint32_t i) const {
+    if (i >= n) return 0u;
+    const TileBox r = box[perm[i]];
+    return (uint32_t)(r.tx1 - r.tx0 + 1) * (uint32_t)(r.ty1 - r.ty0 + 1);
+  }
+};
 
 __global__ void k_tile_emit(const uint32_t* __restrict__ perm, const TileBox* __restrict__ box,
                             const uint32_t* __restrict__ off, uint32_t n, int ntx, int packed,
@@ -1549,18 +1554,20 @@ int sgad_raster_prepare(sgad_raster* h, const sgad_frame* frames, int32_t n_fram
   }
   size_t tmp = 0;
   // K3: per-survivor tile counts in depth order, exclusive scan, emit, stable tile sort
-  SGAD_CHECK_CUDA(h->pcount.ensure(sizeof(uint32_t) * (ns + 1)));
   SGAD_CHECK_CUDA(h->poffset.ensure(sizeof(uint32_t) * (ns + 1)));
-  k_tile_count<<<blocks_for(ns, 256), 256, 0, st>>>(perm, h->bbox.as<TileBox>(), ns,
-                                                    h->pcount.as<uint32_t>());
-  SGAD_LAUNCH_CHECK();
-  SGAD_CHECK_CUDA(cudaMemsetAsync(h->pcount.as<uint32_t>() + ns, 0, sizeof(uint32_t), st));
-  tmp = 0;
-  SGAD_CHECK_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, h->pcount.as<uint32_t>(),
-                                                h->poffset.as<uint32_t>(), (int)ns + 1, st));
-  SGAD_CHECK_CUDA(h->cub_tmp.ensure(tmp));
-  SGAD_CHECK_CUDA(cub::DeviceScan::ExclusiveSum(h->cub_tmp.p, tmp, h->pcount.as<uint32_t>(),
-                                                h->poffset.as<uint32_t>(), (int)ns + 1, st));
+  const cub::TransformInputIterator<uint32_t, TilePairCount, cub::CountingInputIterator<uint32_t>>
+      pair_counts(cub::CountingInputIterator<uint32_t>(0u),
+                  TilePairCount{perm, h->bbox.as<TileBox>(), ns});
+  auto scan_counts = [&]() -> int {
+    size_t t2 = 0;
+    SGAD_CHECK_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, t2, pair_counts,
+                                                  h->poffset.as<uint32_t>(), (int)ns + 1, st));
+    SGAD_CHECK_CUDA(h->cub_tmp.ensure(t2));
+    SGAD_CHECK_CUDA(cub::DeviceScan::ExclusiveSum(h->cub_tmp.p, t2, pair_counts,
+                                                  h->poffset.as<uint32_t>(), (int)ns + 1, st));
+    return SGAD_OK;
+  };
+  if (int rc = scan_counts()) return rc;
   SGAD_CHECK_CUDA(cudaMemcpyAsync(h->pinned + 1, h->poffset.as<uint32_t>() + ns, sizeof(uint32_t),
                                   cudaMemcpyDeviceToHost, st));
   SGAD_CHECK_CUDA(cudaMemcpyAsync(h->pinned + 2, h->counters.as<uint32_t>() + 2, sizeof(uint32_t),
@@ -1582,15 +1589,7 @@ int sgad_raster_prepare(sgad_raster* h, const sgad_frame* frames, int32_t n_fram
     if (dv.Current() != perm)
       SGAD_CHECK_CUDA(cudaMemcpyAsync(perm, dv.Current(), sizeof(uint32_t) * ns,
                                       cudaMemcpyDeviceToDevice, st));
-    k_tile_count<<<blocks_for(ns, 256), 256, 0, st>>>(perm, h->bbox.as<TileBox>(), ns,
-                                                      h->pcount.as<uint32_t>());
-    SGAD_LAUNCH_CHECK();
-    tmp = 0;
-    SGAD_CHECK_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, h->pcount.as<uint32_t>(),
-                                                  h->poffset.as<uint32_t>(), (int)ns + 1, st));
-    SGAD_CHECK_CUDA(h->cub_tmp.ensure(tmp));
-    SGAD_CHECK_CUDA(cub::DeviceScan::ExclusiveSum(h->cub_tmp.p, tmp, h->pcount.as<uint32_t>(),
-                                                  h->poffset.as<uint32_t>(), (int)ns + 1, st));
+    if (int rc = scan_counts()) return rc;
     SGAD_CHECK_CUDA(cudaMemcpyAsync(h->pinned + 1, h->poffset.as<uint32_t>() + ns,
                                     sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
     SGAD_CHECK_CUDA(cudaStreamSynchronize(st));
