@@ -616,6 +616,13 @@ __device__ __forceinline__ int nth_set_bit(uint32_t m, int q) {
   return pos;
 }
 
+// 32-byte read-only load (one LDG.256: a record is two of them)
+__device__ __forceinline__ void ld256(const void* p, double& a, double& b, double& c, double& d) {
+  asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];"
+      : "=d"(a), "=d"(b), "=d"(c), "=d"(d)
+      : "l"(p));
+}
+
 #ifndef FWD_PREFETCH
 #define FWD_PREFETCH 2
 #endif
@@ -672,11 +679,7 @@ __device__ __forceinline__ int stage_from_queue(FwdStage& s, int qh, int take,
     e = s.qe[qi];
     k = s.qk[qi];
     rp = reinterpret_cast<const double2*>(rec + e);
-    const double2 a = __ldg(rp), b = __ldg(rp + 1);  // u0, v0 | sigma, opacity
-    u0 = a.x;
-    v0 = a.y;
-    sig = b.x;
-    op = b.y;
+    ld256(rp, u0, v0, sig, op);
     const double thr = SG_MUL(9.0, SG_MUL(sig, sig));
     m = EXACT ? pixel_mask_exact(u0, v0, thr, xlo, ylo) : pixel_mask(u0, v0, thr, xlo, ylo);
   }
@@ -689,8 +692,12 @@ __device__ __forceinline__ int stage_from_queue(FwdStage& s, int qh, int take,
       cl.k[cbase + j] = k;
       cl.m[cbase + j] = m;
     }
-    const double2 zn = __ldg(rp + 2);                                        // z, nh
-    const float4 cg = __ldg(reinterpret_cast<const float4*>(rp + 3));        // r, g, b, gid
+    double zz, nh, rg_, bgid;                                                // z, nh | r, g, b, gid
+    ld256(rp + 2, zz, nh, rg_, bgid);
+    const double2 zn = make_double2(zz, nh);
+    const float2 c01 = *reinterpret_cast<const float2*>(&rg_);
+    const float2 c2g = *reinterpret_cast<const float2*>(&bgid);
+    const float4 cg = make_float4(c01.x, c01.y, c2g.x, c2g.y);
     if (!EXACT) s.thr[j] = SG_MUL(9.0, SG_MUL(sig, sig));
     s.u0[j] = u0;
     s.v0[j] = v0;
@@ -727,19 +734,16 @@ struct Contrib {
 __device__ __forceinline__ void load_contrib(Contrib& q, const WarpRing& rg, int slot, int j,
                                              const Record* __restrict__ rec) {
   q.e = rg.e[slot][j];
-  const double2* rp = reinterpret_cast<const double2*>(rec + q.e);
-  const double2 uv = __ldg(rp), so = __ldg(rp + 1), zn = __ldg(rp + 2);
-  const float4 cg = __ldg(reinterpret_cast<const float4*>(rp + 3));
-  q.u0 = uv.x;
-  q.v0 = uv.y;
-  q.sig = so.x;
-  q.op = so.y;
-  q.z = zn.x;
-  q.nh = zn.y;
-  q.r = cg.x;
-  q.g = cg.y;
-  q.b = cg.z;
-  q.gid = __float_as_uint(cg.w);
+  const double* rp = reinterpret_cast<const double*>(rec + q.e);
+  double rg_, bgid;
+  ld256(rp, q.u0, q.v0, q.sig, q.op);
+  ld256(rp + 4, q.z, q.nh, rg_, bgid);
+  const float2 c01 = *reinterpret_cast<const float2*>(&rg_);
+  const float2 c2g = *reinterpret_cast<const float2*>(&bgid);
+  q.r = c01.x;
+  q.g = c01.y;
+  q.b = c2g.x;
+  q.gid = __float_as_uint(c2g.y);
 }
 
 __device__ const double kExp2Table[32] = {SGAD_EXP2_TABLE};
