@@ -73,13 +73,21 @@ k_adam_f32(float* __restrict__ params, float* __restrict__ grads, float* __restr
   float* vf = v + f * 6 * hw + p;
   const float b1 = (float)a.b1, b2 = (float)a.b2, eps = (float)a.eps;
   const float ib1 = (float)(1.0 / a.bc1), ib2 = (float)(1.0 / a.bc2);
-  const float g[6] = {g0.x, g0.y * __expf(pf[2 * hw]), g0.z, g0.w, g1.x, g1.y};
+  // every load issued before any store (18 independent streams in flight)
+  float m0[6], v0[6], p0[6];
+#pragma unroll
+  for (int c = 0; c < 6; ++c) {
+    m0[c] = mf[c * hw];
+    v0[c] = vf[c * hw];
+    p0[c] = pf[(c + 1) * hw];
+  }
+  const float g[6] = {g0.x, g0.y * __expf(p0[1]), g0.z, g0.w, g1.x, g1.y};
 #pragma unroll
   for (int c = 0; c < 6; ++c) {
     if (c == 0 && !a.update_delta) continue;
-    const float mm = mf[c * hw] * b1 + (1.0f - b1) * g[c];
-    const float vv = vf[c * hw] * b2 + (1.0f - b2) * g[c] * g[c];
-    float prm = pf[(c + 1) * hw] - (float)a.lr[c] * (mm * ib1) / (sqrtf(vv * ib2) + eps);
+    const float mm = m0[c] * b1 + (1.0f - b1) * g[c];
+    const float vv = v0[c] * b2 + (1.0f - b2) * g[c] * g[c];
+    float prm = p0[c] - (float)a.lr[c] * (mm * ib1) / (sqrtf(vv * ib2) + eps);
     if (c >= 3) prm = fminf(fmaxf(prm, 0.0f), 1.0f);  // colour clip, mapper.py:95
     pf[(c + 1) * hw] = prm;
     mf[c * hw] = mm;
