@@ -516,7 +516,10 @@ __device__ __forceinline__ TileGeom tile_geom(int ntx, int width, int height) {
 // and the slot it needs is no longer read by any lane.
 constexpr int NWARP = RASTER_THREADS / 32;
 constexpr int WIN = 64;
-constexpr int RING = 10;
+#ifndef SGAD_RING
+#define SGAD_RING 10
+#endif
+constexpr int RING = SGAD_RING;
 
 struct WarpRing {
   uint32_t e[RING][WIN];                  // record index of each slot

@@ -318,12 +318,15 @@ class WindowMapper:
         if ns:
             self._composite(r, v, stream)
 
-    def _render_pipelined(self, timing=None):
+    def _render_pipelined(self, timing=None, target_ready=None):
         """All assigned views, the preparation (projection, depth order, tile
         lists) of view i+1 on a side stream while view i composites on the
         main stream.  Two raster handles alternate; a handle is re-prepared
         only after the compositing that used it has finished.  ``timing``
-        (optional list) receives (kind, start_event, end_event, view) tuples."""
+        (optional list) receives (kind, start_event, end_event, view) tuples;
+        ``target_ready`` (optional {view: event}) holds back a view's
+        compositing until its target has arrived (targets uploaded while
+        earlier views composite)."""
         if self._pipe is None:
             self._pipe = ([Raster(self.dev), Raster(self.dev)], torch.cuda.Stream(self.dev))
         rasters, prep = self._pipe
@@ -347,6 +350,8 @@ class WindowMapper:
             self.last_counts[v] = (ns, npairs)
             p1 = mark(prep)
             main.wait_event(p1)
+            if target_ready is not None and v in target_ready:
+                main.wait_event(target_ready[v])
             if ns:
                 f0 = mark(main)
                 f1 = self._composite(r, v, main, marks=lambda: mark(main))
@@ -359,16 +364,20 @@ class WindowMapper:
                         timing += [("fwd", f0, f1, v, ns, npairs), ("bwd", f1, b1, v, ns, npairs)]
             used[i % 2] = mark(main)
 
-    def step(self, sync_loss=False, timing=None):
+    def step(self, sync_loss=False, timing=None, target_ready=None):
         """One window iteration: every assigned view fwd+bwd, gradient
         all-reduce across ranks, Adam.  Returns the summed loss (a device
-        scalar unless ``sync_loss``)."""
+        scalar unless ``sync_loss``).  ``target_ready`` ({view: CUDA event},
+        optional): a view composites only after its event."""
         self.loss_acc.zero_()
         with torch.cuda.device(self.dev):
             if self.pipelined:
-                self._render_pipelined(timing)
+                self._render_pipelined(timing, target_ready)
             else:
                 main = torch.cuda.current_stream(self.dev)
+                if target_ready is not None:
+                    for ev in target_ready.values():
+                        main.wait_event(ev)
                 for v in self.views:
                     ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
                     ev[0].record(main)
