@@ -1095,9 +1095,10 @@ __device__ __forceinline__ void bwd_sweep(WarpRing& ring, const TileGeom& g, con
         c2 = __ldg(col64 + 3 * (size_t)e + 2);
       }
       if (cc.gid & GID_LEARN) {
-        const double d_alpha = u.gc0 * (c0 * tb - sc0 * iom) + u.gc1 * (c1 * tb - sc1 * iom) +
-                               u.gc2 * (c2 * tb - sc2 * iom) + u.gd * (z * tb - sd * iom) +
-                               u.ga * (tb - sa * iom);
+        // (the fused loss has no alpha upstream: its term is compiled out)
+        double d_alpha = u.gc0 * (c0 * tb - sc0 * iom) + u.gc1 * (c1 * tb - sc1 * iom) +
+                         u.gc2 * (c2 * tb - sc2 * iom) + u.gd * (z * tb - sd * iom);
+        if (!FUSED) d_alpha += u.ga * (tb - sa * iom);
         const double gcol0 = u.gc0 * at, gcol1 = u.gc1 * at, gcol2 = u.gc2 * at, gz = u.gd * at;
         double gop = 0.0, gsig = 0.0, gu = 0.0, gv = 0.0;
         if (!clamped) {
@@ -1140,7 +1141,7 @@ __device__ __forceinline__ void bwd_sweep(WarpRing& ring, const TileGeom& g, con
       sc1 = fma(c1, at, sc1);
       sc2 = fma(c2, at, sc2);
       sd = fma(z, at, sd);
-      sa += at;
+      if (!FUSED) sa += at;
       T = tb;
     }
   }
