@@ -22,7 +22,7 @@
 #include <math.h>
 #include "../include/sgad_numerics.h"
 
-static const double TAB[32] = {SGAD_EXP2_TABLE};
+static const double TAB[SGAD_EXP2_TABLE_N] = {SGAD_EXP2_TABLE};
 
 /* Contributor weight, shared convention with the kernels: exp(d2 * nh),
  * nh = -0.5 / s2, through sgad_exp_neg (the reference evaluates

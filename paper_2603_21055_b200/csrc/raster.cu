@@ -11,6 +11,8 @@
 // Layout (HBM): survivors live in EMISSION order (frame, pixel) as 64-byte
 // records; the depth sort produces a permutation, tile lists hold emission
 // indices in depth order.  Per-view scratch is owned by the sgad_raster handle.
+#include <thrust/iterator/counting_iterator.h>
+#include <thrust/iterator/transform_iterator.h>
 #include <cub/cub.cuh>
 #include <stdarg.h>
 #include <stddef.h>
@@ -749,10 +751,10 @@ __device__ __forceinline__ void load_contrib(Contrib& q, const WarpRing& rg, int
   q.gid = __float_as_uint(c2g.y);
 }
 
-__device__ const double kExp2Table[32] = {SGAD_EXP2_TABLE};
+__device__ const double kExp2Table[SGAD_EXP2_TABLE_N] = {SGAD_EXP2_TABLE};
 
 __device__ __forceinline__ void load_exp_table(double* tab) {
-  if (threadIdx.x < 32) tab[threadIdx.x] = kExp2Table[threadIdx.x];
+  for (int i = threadIdx.x; i < SGAD_EXP2_TABLE_N; i += blockDim.x) tab[i] = kExp2Table[i];
   __syncthreads();
 }
 
@@ -933,7 +935,7 @@ k_forward(const uint2* __restrict__ ranges, const uint32_t* __restrict__ lists, 
           uint8_t* __restrict__ signs, sgad_loss_target tgt, CList cl) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   FwdStage& s = reinterpret_cast<FwdStage*>(smem_raw)[threadIdx.x >> 5];
-  __shared__ double tab[32];
+  __shared__ double tab[SGAD_EXP2_TABLE_N];
   load_exp_table(tab);
   const TileGeom g = tile_geom(ntx, width, height);
   const SweepGeom q = sweep_geom(g);
@@ -1180,7 +1182,7 @@ k_backward(const uint2* __restrict__ ranges, const uint32_t* __restrict__ lists,
            double* __restrict__ raw, float* __restrict__ grad_accum, CList cl) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   WarpRing& ring = reinterpret_cast<WarpRing*>(smem_raw)[threadIdx.x >> 5];
-  __shared__ double tab[32];
+  __shared__ double tab[SGAD_EXP2_TABLE_N];
   load_exp_table(tab);
   const TileGeom g = tile_geom(ntx, width, height);
   const SweepGeom q = sweep_geom(g);
@@ -1255,7 +1257,7 @@ k_forward_backward(const uint2* __restrict__ ranges, const uint32_t* __restrict_
                    float* __restrict__ grad_accum, CList cl) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   unsigned char* slab = smem_raw + FB_SLAB * (threadIdx.x >> 5);
-  __shared__ double tab[32];
+  __shared__ double tab[SGAD_EXP2_TABLE_N];
   load_exp_table(tab);
   const TileGeom g = tile_geom(ntx, width, height);
   const SweepGeom q = sweep_geom(g);
@@ -1563,9 +1565,8 @@ int sgad_raster_prepare(sgad_raster* h, const sgad_frame* frames, int32_t n_fram
   size_t tmp = 0;
   // K3: per-survivor tile counts in depth order, exclusive scan, emit, stable tile sort
   SGAD_CHECK_CUDA(h->poffset.ensure(sizeof(uint32_t) * (ns + 1)));
-  const cub::TransformInputIterator<uint32_t, TilePairCount, cub::CountingInputIterator<uint32_t>>
-      pair_counts(cub::CountingInputIterator<uint32_t>(0u),
-                  TilePairCount{perm, h->bbox.as<TileBox>(), ns});
+  const auto pair_counts = thrust::make_transform_iterator(
+      thrust::counting_iterator<uint32_t>(0u), TilePairCount{perm, h->bbox.as<TileBox>(), ns});
   auto scan_counts = [&]() -> int {
     size_t t2 = 0;
     SGAD_CHECK_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, t2, pair_counts,
