@@ -1474,7 +1474,10 @@ int sgad_raster_prepare(sgad_raster* h, const sgad_frame* frames, int32_t n_fram
   }
   SGAD_REQUIRE(n_total < (1ll << 30), "too many Gaussians (%lld)", (long long)n_total);
   h->n_total = n_total;
-  h->packed = n_total < (int64_t)(1u << sgad::LIST_IDX_BITS) ? 1 : 0;
+  // (SGAD_PACK=0 forces the bare-index lists of very large views: tests)
+  const char* pack_env = getenv("SGAD_PACK");
+  h->packed = n_total < (int64_t)(1u << sgad::LIST_IDX_BITS) && !(pack_env && pack_env[0] == '0')
+                  ? 1 : 0;
   h->have_coef = want_coef != 0;
   h->any_f64 = 0;
   for (int i = 0; i < n_frames; ++i) h->any_f64 |= frames[i].planes_f64 ? 1 : 0;
