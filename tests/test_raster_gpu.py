@@ -342,3 +342,42 @@ def test_unpacked_lists_same_results(monkeypatch):
     # loss and gradient sums are float atomics: equal up to summation order
     np.testing.assert_allclose(loss_u, loss_p, rtol=1e-12)
     np.testing.assert_allclose(grad_u, grad_p, rtol=1e-5, atol=1e-9)
+
+
+@pytest.mark.parametrize("hw", [4096, 4093])
+def test_window_adam_fp32_vs_numpy(hw):
+    """The window engine's fp32 Adam (vectorised kernel when hw % 4 == 0,
+    scalar otherwise) vs a numpy restatement of mapper.py:73-95 in fp64:
+    radius gradient chained to log radius, bias corrections, colour clip;
+    gradients consumed (zeroed)."""
+    import torch
+    from paper_2603_21055_b200.mapper import MapperConfig, _adam
+    cfg = MapperConfig(tau=0.0)
+    F = 3
+    rng = np.random.default_rng(hw)
+    params = rng.uniform(0.0, 1.0, (F, 7, hw)).astype(np.float32)
+    params[:, 2] = rng.normal(-4.0, 0.5, (F, hw))  # log radius
+    m = rng.normal(0.0, 1e-3, (F, 6, hw)).astype(np.float32)
+    v = rng.uniform(0.0, 1e-5, (F, 6, hw)).astype(np.float32)
+    g = rng.normal(0.0, 1e-2, (F * hw, 8)).astype(np.float32)
+    t = 5
+    dev = torch.device("cuda", 0)
+    P, M, V, G = (torch.from_numpy(x.copy()).to(dev) for x in (params, m, v, g))
+    _adam(P, G, M, V, F, hw, cfg, t, False)
+    torch.cuda.synchronize()
+    b1, b2, eps = cfg.adam_beta1, cfg.adam_beta2, cfg.adam_eps
+    lr = np.array(cfg.lrs())
+    gg = g.reshape(F, hw, 8).astype(np.float64)
+    grad = np.stack([gg[..., 0], gg[..., 1] * np.exp(params[:, 2].astype(np.float64)),
+                     gg[..., 2], gg[..., 3], gg[..., 4], gg[..., 5]], axis=1)  # [F, 6, hw]
+    m1 = b1 * m + (1 - b1) * grad
+    v1 = b2 * v + (1 - b2) * grad * grad
+    step = lr[None, :, None] * (m1 / (1 - b1**t)) / (np.sqrt(v1 / (1 - b2**t)) + eps)
+    p1 = params[:, 1:].astype(np.float64) - step
+    p1[:, 3:] = np.clip(p1[:, 3:], 0.0, 1.0)
+    # fp32 storage and arithmetic (1 - beta2 alone is 1.3e-5 off in fp32)
+    np.testing.assert_allclose(M.cpu().numpy(), m1, rtol=1e-5, atol=1e-9)
+    np.testing.assert_allclose(V.cpu().numpy(), v1, rtol=5e-5, atol=1e-12)
+    np.testing.assert_allclose(P.cpu().numpy()[:, 1:], p1, rtol=1e-5, atol=1e-6)
+    np.testing.assert_array_equal(P.cpu().numpy()[:, 0], params[:, 0])  # base depth untouched
+    assert G.abs().max().item() == 0.0
