@@ -326,10 +326,13 @@ k_project(const sgad_frame* __restrict__ frames, sgad_camera cam, int ntx, int n
 // stably leaves only runs of equal buckets to be put in exact (z, emission)
 // order by k_depth_fixup -- 3 radix passes instead of 8 for the 63-bit key
 // (at C4 a bucket is ~1 um deep and nearly all runs are single entries).
-constexpr int DEPTH_KEY_BITS = 24;
-constexpr double DEPTH_KEY_TOP = (double)((1u << DEPTH_KEY_BITS) - 2u);  // survivors' largest
+static int depth_key_bits() {  // SGAD_DEPTH_BITS (A/B): 16..32, default 24
+  const char* v = getenv("SGAD_DEPTH_BITS");
+  const int b = v ? atoi(v) : 24;
+  return b < 16 ? 16 : (b > 32 ? 32 : b);
+}
 __global__ void k_depth_key32(const unsigned long long* __restrict__ zkeys, uint32_t n,
-                              double zmin, double scale, uint32_t* __restrict__ k32,
+                              double zmin, double scale, double top, uint32_t* __restrict__ k32,
                               uint32_t* __restrict__ vals) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
@@ -338,7 +341,7 @@ __global__ void k_depth_key32(const unsigned long long* __restrict__ zkeys, uint
     k32[i] = 0xFFFFFFFFu;  // culled: behind every survivor (low 24 bits all set)
   } else {
     const double b = floor((__longlong_as_double((long long)zk) - zmin) * scale);
-    k32[i] = b >= DEPTH_KEY_TOP ? (uint32_t)DEPTH_KEY_TOP : (uint32_t)b;
+    k32[i] = b >= top ? (uint32_t)top : (uint32_t)b;  // top = 2^bits - 2 (survivors' largest)
   }
   vals[i] = i;
 }
@@ -1537,22 +1540,28 @@ int sgad_raster_prepare(sgad_raster* h, const sgad_frame* frames, int32_t n_fram
     double zmin, zmax;
     memcpy(&zmin, &zb[0], 8);
     memcpy(&zmax, &zb[1], 8);
-    const double scale = zmax > zmin ? DEPTH_KEY_TOP / (zmax - zmin) : 0.0;
+    const int kbits = depth_key_bits();
+    const double ktop = (double)(uint32_t)((kbits == 32 ? 0u : (1u << kbits)) - 2u);
+    const double scale = zmax > zmin ? ktop / (zmax - zmin) : 0.0;
+    // the permutation lands in vals0 after an even number of 8-bit passes if
+    // it starts there, after an odd number if it starts in vals1
+    const bool odd = ((kbits + 7) / 8) & 1;
+    uint32_t* v_first = odd ? h->vals1.as<uint32_t>() : h->vals0.as<uint32_t>();
+    uint32_t* v_second = odd ? h->vals0.as<uint32_t>() : h->vals1.as<uint32_t>();
     const uint32_t nt = (uint32_t)n_total;  // culled ids carry the sentinel key
     SGAD_CHECK_CUDA(h->k32a.ensure(sizeof(uint32_t) * nt));
     SGAD_CHECK_CUDA(h->k32b.ensure(sizeof(uint32_t) * nt));
     k_depth_key32<<<blocks_for(nt, 256), 256, 0, st>>>(h->keys0.as<unsigned long long>(), nt, zmin,
-                                                       scale, h->k32a.as<uint32_t>(),
-                                                       h->vals1.as<uint32_t>());
+                                                       scale, ktop, h->k32a.as<uint32_t>(),
+                                                       v_first);
     SGAD_LAUNCH_CHECK();
     cub::DoubleBuffer<uint32_t> dk(h->k32a.as<uint32_t>(), h->k32b.as<uint32_t>());
-    cub::DoubleBuffer<uint32_t> dv(h->vals1.as<uint32_t>(), h->vals0.as<uint32_t>());
+    cub::DoubleBuffer<uint32_t> dv(v_first, v_second);
     size_t tmp = 0;
-    SGAD_CHECK_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, dk, dv, (int)nt, 0,
-                                                    DEPTH_KEY_BITS, st));
+    SGAD_CHECK_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, dk, dv, (int)nt, 0, kbits, st));
     SGAD_CHECK_CUDA(h->cub_tmp.ensure(tmp));
-    SGAD_CHECK_CUDA(cub::DeviceRadixSort::SortPairs(h->cub_tmp.p, tmp, dk, dv, (int)nt, 0,
-                                                    DEPTH_KEY_BITS, st));
+    SGAD_CHECK_CUDA(cub::DeviceRadixSort::SortPairs(h->cub_tmp.p, tmp, dk, dv, (int)nt, 0, kbits,
+                                                    st));
     if (dv.Current() != perm)
       SGAD_CHECK_CUDA(cudaMemcpyAsync(perm, dv.Current(), sizeof(uint32_t) * ns,
                                       cudaMemcpyDeviceToDevice, st));
