@@ -65,7 +65,7 @@ constexpr int RASTER_THREADS = 256;
 struct sgad_raster {
   sgad::DevBuf frames, status, counters, records, coef, keys0, keys1, vals0, vals1;
   sgad::DevBuf pcount, poffset, pkeys0, pkeys1, pvals0, pvals1, ranges, cub_tmp;
-  sgad::DevBuf trans_final, last_idx, signs, raw_grads, rank_of, scratch, col64, zrange, k32a, k32b, bbox, runs, raw32, cl_e, cl_k, cl_m, cl_n;
+  sgad::DevBuf trans_final, last_idx, signs, raw_grads, rank_of, scratch, col64, zrange, k32a, k32b, bbox, runs, raw32, cl_e, cl_m, cl_n;
   int any_f64 = 0;
   std::vector<sgad_frame> host_frames;
   sgad_camera cam{};
@@ -650,21 +650,19 @@ __device__ __forceinline__ uint32_t load_value(const uint32_t* __restrict__ list
 // backward's heavy contributions pay for the ring below (K4/K5).
 struct FwdStage {
   double u0[WIN], v0[WIN], nh[WIN], op[WIN], z[WIN], rgb[3][WIN], thr[WIN];
-  int32_t k[WIN];
-  // cull queue (ring of WIN): list entries whose 3-sigma box reaches the
-  // warp's rectangle, waiting for their pixel masks
+  // cull queue (ring of WIN): record ids of list entries whose 3-sigma box
+  // reaches the warp's rectangle, waiting for their pixel masks
   uint32_t qe[WIN];
-  int32_t qk[WIN];
 };
 
 // Per-warp compact lists written by a forward that keeps state for the
 // backward: every list entry that reaches the warp's rectangle, in list
 // order, with its exact pixel mask -- the backward stages its windows from
 // these instead of culling the tile list again.  Warp w of a tile with list
-// range [x, y) owns slots [8x + w (y - x), 8x + (w + 1)(y - x)).
+// range [x, y) owns slots [8x + w (y - x), 8x + (w + 1)(y - x)).  A pixel's
+// last contributor is kept as its index in this list.
 struct CList {
   uint32_t* e;
-  int32_t* k;
   uint32_t* m;
   uint32_t* count;  // [n_tiles * 8] entries written per warp
 };
@@ -682,13 +680,11 @@ __device__ __forceinline__ int stage_from_queue(FwdStage& s, int qh, int take,
                                                 double ylo, int lane, int n, uint32_t& mlo,
                                                 uint32_t& mhi, const CList& cl, int64_t cbase) {
   uint32_t m = 0, e = 0;
-  int32_t k = 0;
   double u0 = 0.0, v0 = 0.0, sig = 0.0, op = 0.0;
   const double2* rp = nullptr;
   if (lane < take) {
     const int qi = (qh + lane) & (WIN - 1);
     e = s.qe[qi];
-    k = s.qk[qi];
     rp = reinterpret_cast<const double2*>(rec + e);
     ld256(rp, u0, v0, sig, op);
     const double thr = SG_MUL(9.0, SG_MUL(sig, sig));
@@ -700,7 +696,6 @@ __device__ __forceinline__ int stage_from_queue(FwdStage& s, int qh, int take,
     const int j = n + __popc(keep & ((1u << lane) - 1u));
     if (EXACT) {  // the backward's compact list (cbase = this batch's first slot - n)
       cl.e[cbase + j] = e;
-      cl.k[cbase + j] = k;
       cl.m[cbase + j] = m;
     }
     double zz, nh, rg_, bgid;                                                // z, nh | r, g, b, gid
@@ -724,7 +719,6 @@ __device__ __forceinline__ int stage_from_queue(FwdStage& s, int qh, int take,
       s.rgb[1][j] = cg.y;
       s.rgb[2][j] = cg.z;
     }
-    s.k[j] = k;
   }
   const int q = (lane - n) & 31;
   const int src = q < c ? nth_set_bit(keep, q) : 0;
@@ -842,7 +836,6 @@ __device__ __forceinline__ PixState fwd_sweep(FwdStage& s, const TileGeom& g, co
         if (hit) {
           const int qi = (qh + qn + __popc(b & ((1u << g.lane) - 1u))) & (WIN - 1);
           s.qe[qi] = cur & idx_mask;
-          s.qk[qi] = (int32_t)(pos + g.lane);
         }
         qn += __popc(b);
         pos += 32;
@@ -856,6 +849,7 @@ __device__ __forceinline__ PixState fwd_sweep(FwdStage& s, const TileGeom& g, co
       qn -= take;
       __syncwarp();  // queue slots read above may be refilled next
     }
+    const int wbase = (int)nw;  // compact-list index of slot 0
     nw += n;
     __syncwarp();
     // this lane's bits over the window: slots 0..31, then 32..63 (list order)
@@ -885,7 +879,7 @@ __device__ __forceinline__ PixState fwd_sweep(FwdStage& s, const TileGeom& g, co
       st.D = SG_FMA(s.z[j], at, st.D);
       st.A = SG_ADD(st.A, at);
       ++st.cnt;
-      st.last = s.k[j];
+      st.last = wbase + j;
       st.T = SG_MUL(st.T, SG_SUB(1.0, a));
       if (st.T < SGAD_TRANSMITTANCE_MIN) {
         done = true;
@@ -1027,7 +1021,7 @@ __device__ __forceinline__ void bwd_sweep(WarpRing& ring, const TileGeom& g, con
   // (plain loads: in k_forward_backward the same kernel wrote them)
   __syncwarp();
   int64_t cpos = (int64_t)cl.count[(int64_t)g.tile * NWARP + g.warp];
-  while (cpos > 0 && cl.k[cbase + cpos - 1] >= wend) --cpos;
+  if (cpos > wend) cpos = wend;  // entries past every lane's last contributor
   Cursor c{0ull, -1, RING - 1};
   int w_head = 0, head_slot = 0;  // head_slot = w_head % RING
   Contrib cc;
@@ -1040,35 +1034,24 @@ __device__ __forceinline__ void bwd_sweep(WarpRing& ring, const TileGeom& g, con
       // takes slots i and 32 + i, whose masks are already exact
       const int n = (int)min(cpos, (int64_t)WIN);
       uint32_t mlo = 0, mhi = 0;
-      int kv0 = 0, kv1 = 0;  // list positions of slots lane and 32 + lane
       {
         const int64_t i0 = cbase + cpos - 1 - g.lane, i1 = i0 - 32;
         if (g.lane < n) {
           ring.e[slot][g.lane] = cl.e[i0];
-          kv0 = cl.k[i0];
           mlo = cl.m[i0];
         }
         if (32 + g.lane < n) {
           ring.e[slot][32 + g.lane] = cl.e[i1];
-          kv1 = cl.k[i1];
           mhi = cl.m[i1];
         }
       }
+      // slot i holds compact entry cpos - 1 - i (descending): the leading
+      // slots above this lane's last contributor are dropped
+      const int lo_s = (int)max((int64_t)0, min((int64_t)n, cpos - 1 - (int64_t)mylast));
       cpos -= n;
       __syncwarp();
       unsigned long long bits = ((unsigned long long)transpose32(mhi, g.lane) << 32) |
                                 transpose32(mlo, g.lane);
-      // slots run in descending list order: drop the leading slots above this
-      // lane's last contributor (binary search over the slots' positions,
-      // held in the slot-owner lanes' registers)
-      int lo_s = 0;
-#pragma unroll
-      for (int step = 64; step >= 1; step >>= 1) {
-        const int cand = lo_s + step, sl = min(cand - 1, 63);
-        const int ka = __shfl_sync(0xffffffffu, kv0, sl & 31);
-        const int kb = __shfl_sync(0xffffffffu, kv1, sl & 31);
-        if (cand <= n && (sl < 32 ? ka : kb) > mylast) lo_s = cand;
-      }
       if (lo_s >= 64) bits = 0ull;
       else bits &= ~((1ull << lo_s) - 1ull);
       ring.mask[slot][g.lane] = done ? 0ull : bits;
@@ -1400,14 +1383,13 @@ using namespace sgad;
 static int ensure_clist(sgad_raster* h) {
   const size_t n = 8 * (size_t)(h->n_pairs > 0 ? h->n_pairs : 1);
   SGAD_CHECK_CUDA(h->cl_e.ensure(sizeof(uint32_t) * n));
-  SGAD_CHECK_CUDA(h->cl_k.ensure(sizeof(int32_t) * n));
   SGAD_CHECK_CUDA(h->cl_m.ensure(sizeof(uint32_t) * n));
   SGAD_CHECK_CUDA(h->cl_n.ensure(sizeof(uint32_t) * 8 * (size_t)(h->n_tiles > 0 ? h->n_tiles : 1)));
   return SGAD_OK;
 }
 
 static CList clist_of(sgad_raster* h) {
-  return CList{h->cl_e.as<uint32_t>(), h->cl_k.as<int32_t>(), h->cl_m.as<uint32_t>(),
+  return CList{h->cl_e.as<uint32_t>(), h->cl_m.as<uint32_t>(),
                h->cl_n.as<uint32_t>()};
 }
 
@@ -1441,7 +1423,7 @@ int sgad_raster_destroy(sgad_raster* h) {
                     &h->keys1, &h->vals0, &h->vals1, &h->pcount, &h->poffset, &h->pkeys0,
                     &h->pkeys1, &h->pvals0, &h->pvals1, &h->ranges, &h->cub_tmp,
                     &h->trans_final, &h->last_idx, &h->signs, &h->raw_grads, &h->rank_of,
-                    &h->scratch, &h->col64, &h->zrange, &h->k32a, &h->k32b, &h->bbox, &h->runs, &h->raw32, &h->cl_e, &h->cl_k, &h->cl_m, &h->cl_n};
+                    &h->scratch, &h->col64, &h->zrange, &h->k32a, &h->k32b, &h->bbox, &h->runs, &h->raw32, &h->cl_e, &h->cl_m, &h->cl_n};
   for (DevBuf* b : bufs) b->release();
   if (h->pinned) cudaFreeHost(h->pinned);
   delete h;
