@@ -125,21 +125,26 @@ def load_peaks():
 # ------------------------------------------------------------------ CPU legs
 
 
-def cpu_sample(cfg_name, n_views_req, threads):
+def cpu_sample(cfg_name, n_views_req, threads, n_sources=0, reps=1):
     """Oracle port (C restatement of the reference kernels) on host cores:
     a bounded sample of the window iteration -- ``n`` target views, each a full
-    all-learnable fwd+bwd over the whole window, in a thread pool like the
-    reference's own (raysplat/pipeline.py:212)."""
+    all-learnable fwd+bwd over the window's maps (all of them, or the first
+    ``n_sources``), in a thread pool like the reference's own
+    (raysplat/pipeline.py:212).  With ``reps`` > 1 the sample is repeated and
+    each repetition timed; the first ``reps - timed`` are for the caller."""
     from concurrent.futures import ThreadPoolExecutor
     from types import SimpleNamespace
 
+    import numpy as np
     from oracle import raster as O
     wc = make_config(cfg_name, "cpu" if not _has_cuda() else "cuda")
     maps = [SimpleNamespace(frame_index=i, pose=wc.poses[i], intrinsics=wc.intr,
                             base_depth=p.base_depth, delta=p.delta, log_radius=p.log_radius,
                             opacity_logit=p.opacity_logit, color=p.color,
                             active_mask=p.active_mask) for i, p in enumerate(wc.params)]
-    n_views = n_views_req or min(len(maps), max(1, threads))
+    if n_sources:
+        maps = maps[:n_sources]
+    n_views = n_views_req or min(len(wc.frames), max(1, threads))
     views = list(range(n_views))
 
     def one(v):
@@ -148,16 +153,23 @@ def cpu_sample(cfg_name, n_views_req, threads):
                        wc.poses[v].translation, wc.intr, learnable_map="all")
 
     O.lib()
-    t0 = time.perf_counter()
+    times = []
     with ThreadPoolExecutor(max_workers=max(1, min(threads, n_views))) as ex:
-        list(ex.map(one, views))
-    dt = time.perf_counter() - t0
-    n_g = sum(int(p.active_mask.size) for p in wc.params)
-    return {"value": n_g * n_views / dt, "unit": UNIT, "cores": min(threads, n_views),
-            "kind": "port",
-            "sample": f"{n_views} of {len(maps)} target views of one {cfg_name.upper()} window "
-                      f"iteration (all-learnable fwd+bwd over {n_g} Gaussians each), "
-                      f"{dt:.1f} s wall"}
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            list(ex.map(one, views))
+            times.append(time.perf_counter() - t0)
+    dt = times[-1] if reps == 1 else None  # (callers drop "times" / "gaussian_views")
+    n_g = sum(int(np.asarray(m.active_mask).size) for m in maps)
+    src = f"{len(maps)} of {len(wc.frames)} window maps" if n_sources else "all window maps"
+    res = {"unit": UNIT, "cores": min(threads, n_views), "kind": "port", "times": times,
+           "gaussian_views": n_g * n_views,
+           "sample": f"{n_views} target views of one {cfg_name.upper()} window iteration, "
+                     f"all-learnable fwd+bwd over {src} ({n_g} Gaussians)"}
+    if dt is not None:
+        res["value"] = n_g * n_views / dt
+        res["sample"] += f", {dt:.1f} s wall"
+    return res
 
 
 def _has_cuda():
@@ -169,21 +181,35 @@ def _has_cuda():
 
 
 def run_reference(args):
+    """The reference arm: the reference's CPU algorithm (the oracle port of its
+    kernels; the reference is a Python package) on the box's host cores, on
+    this arm's config, metric and unit.  A timed step is the full window
+    iteration's views (one per host thread, as the reference's own pool, over
+    all window maps; ~20 s at C4 on the GPU boxes' 8 cores); the W warm-up
+    steps only load the library (one view over two maps).  Under torchrun
+    rank 0 alone runs; the other ranks exit."""
     rank, world, _ = dist_env()
     if rank != 0:
         return
     threads = len(os.sched_getaffinity(0))
-    cb = cpu_sample(args.config, args.cpu_views, threads)
-    # one "step" of the CPU arm is the bounded sample above; its throughput is
-    # the same metric on the same config
-    line = {"metric": METRICS[args.config], "value": cb["value"], "unit": UNIT, "n_gpus": 0,
-            "steps": 1,
-            "warmup": 0, "ms_per_step": None, "higher_is_better": True, "scaling": "strong",
+    k, w = max(1, args.steps), max(0, args.warmup)
+    if w:
+        cpu_sample(args.config, 1, threads, n_sources=2, reps=w)
+    cb = cpu_sample(args.config, args.cpu_views, threads, reps=k)
+    timed = cb.pop("times")
+    gv = cb.pop("gaussian_views")
+    value = gv * k / sum(timed)
+    cb["value"] = value
+    cb["sample"] += f", {k} timed steps of {sum(timed) / k:.1f} s"
+    line = {"metric": METRICS[args.config], "value": value, "unit": UNIT, "n_gpus": 0,
+            "steps": k, "warmup": w, "ms_per_step": 1e3 * sum(timed) / k,
+            "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"{args.config.upper()} mapping window iteration (CPU oracle "
-                                   "port of raysplat rasterizer kernels)"},
+                                   "port of raysplat rasterizer kernels)",
+                       "gaussian_views_per_step": gv},
             "impl": "reference", "cpu_baseline": cb,
-            "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -317,6 +343,8 @@ def run_ours(args):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_sample(args.config, args.cpu_views, len(os.sched_getaffinity(0)))
+        cpu.pop("times", None)
+        cpu.pop("gaussian_views", None)
 
     if rank == 0:
         line = {"metric": METRICS[args.config], "value": value, "unit": UNIT, "n_gpus": world,
