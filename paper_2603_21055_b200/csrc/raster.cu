@@ -925,8 +925,11 @@ __device__ __forceinline__ uint8_t loss_epilogue(const PixState& st, const TileG
   return code;
 }
 
+#ifndef SGAD_FWD_MINB
+#define SGAD_FWD_MINB 4  // 64 registers: 3 blocks/SM 1.10 ms, 5 blocks 1.06 ms, 4 blocks 0.98 ms (C4 view)
+#endif
 template <bool IMAGES, bool STATE, bool LOSS>
-__global__ void __launch_bounds__(RASTER_THREADS)
+__global__ void __launch_bounds__(RASTER_THREADS, SGAD_FWD_MINB)
 k_forward(const uint2* __restrict__ ranges, const uint32_t* __restrict__ lists, int packed,
           const Record* __restrict__ rec, const double* __restrict__ col64, int ntx, int width,
           int height, double* __restrict__ out_color, double* __restrict__ out_depth,
