@@ -390,7 +390,8 @@ def measure_e2e(wm, args, dev, world):
     d2h = host_out.numel() * host_out.element_size() + host_loss.element_size()
     steps = max(2, args.steps // 2)
     main = torch.cuda.current_stream(dev)
-    copy = torch.cuda.Stream(dev)
+    copy = torch.cuda.Stream(dev)   # host -> device
+    back = torch.cuda.Stream(dev)   # device -> host (runs beside the next step's uploads)
     state = {"d2h_done": None, "step_done": None}
 
     def one():
@@ -416,11 +417,11 @@ def measure_e2e(wm, args, dev, world):
         done = torch.cuda.Event()
         done.record(main)
         state["step_done"] = done
-        with torch.cuda.stream(copy):
-            copy.wait_event(done)
+        with torch.cuda.stream(back):
+            back.wait_event(done)
             host_out.copy_(snap, non_blocking=True)
             d = torch.cuda.Event()
-            d.record(copy)
+            d.record(back)
             state["d2h_done"] = d
 
     one()
@@ -431,7 +432,7 @@ def measure_e2e(wm, args, dev, world):
     start.record()
     for _ in range(steps):
         one()
-    main.wait_stream(copy)  # the last read-back is inside the timed region
+    main.wait_stream(back)  # the last read-back is inside the timed region
     stop.record()
     torch.cuda.synchronize()
     ms = start.elapsed_time(stop)
@@ -443,9 +444,10 @@ def measure_e2e(wm, args, dev, world):
     return {"value": wm.n_gaussians * wm.F * steps / (ms / 1e3), "unit": UNIT,
             "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
             "ms_per_step": ms / steps, "steps": steps,
-            "copies": "pinned host buffers on a copy stream: parameters before the "
-                      "step's compositing, targets per view overlapping it, read-back of "
-                      "parameters + loss overlapping the next step"}
+            "copies": "pinned host buffers: uploads on a copy stream (parameters before "
+                      "the step's compositing, targets per view overlapping it), the "
+                      "read-back of parameters + loss on a second stream overlapping the "
+                      "next step"}
 
 
 def bench_ssim(dev, reps=20):
