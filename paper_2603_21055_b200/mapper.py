@@ -208,6 +208,34 @@ def allreduce_window(grad: torch.Tensor, loss_acc: torch.Tensor, group=None) -> 
     return True
 
 
+def frame_shard(n_frames: int, rank: int, world: int):
+    """Frames [f0, f1) whose Adam step ``rank`` owns when the optimizer is
+    sharded (contiguous blocks, so the gradient rows and parameter planes of a
+    block are contiguous and the collectives need no packing)."""
+    if world < 1 or not 0 <= rank < world or n_frames % world:
+        raise ValueError("the window's frames must split evenly over the ranks")
+    k = n_frames // world
+    return rank * k, (rank + 1) * k
+
+
+def reduce_scatter_window(grad: torch.Tensor, local: torch.Tensor, loss_acc: torch.Tensor,
+                          group=None) -> None:
+    """Sharded variant of the exchange step: the summed gradient
+    rows of this rank's frame block into ``local`` (reduce-scatter over the
+    frame-major [N, 8] buffer) and the per-view loss sums everywhere."""
+    dist = torch.distributed
+    dist.reduce_scatter_tensor(local, grad, group=group)
+    dist.all_reduce(loss_acc, group=group)
+
+
+def allgather_planes(planes: torch.Tensor, stage: torch.Tensor, f0: int, f1: int,
+                     group=None) -> None:
+    """Every rank's updated frame block back into everyone's [F, 7, H, W]
+    parameter tensor (all-gather of contiguous frame blocks)."""
+    stage.copy_(planes[f0:f1])
+    torch.distributed.all_gather_into_tensor(planes, stage, group=group)
+
+
 class WindowMapper:
     """All-learnable keyframe window, fp32 parameters, fused loss + backward.
 
@@ -280,6 +308,12 @@ class WindowMapper:
         # than the two kernels at C4, 3.84 vs 3.83 ms per view; kept as an option)
         self.fuse_fwd_bwd = False
         self._pipe = None
+        # world > 1: reduce-scatter the gradient by frame block, Adam on this
+        # rank's block only, all-gather the updated planes (instead of an
+        # all-reduce and a replicated Adam); falls back to the all-reduce when
+        # the frames do not split evenly over the ranks
+        self.shard_adam = True
+        self._shard = None
 
     @property
     def n_gaussians(self) -> int:
@@ -397,11 +431,14 @@ class WindowMapper:
                                            ("bwd", ev[2], ev[3], v, ns, npairs)]
                             else:
                                 timing.append(("fb", ev[1], ev[3], v, ns, npairs))
-            allreduce_window(self.grad, self.loss_acc, self.pg)
-            if self.adam_enabled:  # (tests inspect the reduced gradient with it off)
-                self.t += 1
-                _adam(self.planes, self.grad, self.m, self.v, self.F, self.HW, self.cfg, self.t,
-                      False)
+            if self.adam_enabled and self._sharded():
+                self._sharded_update()
+            else:
+                allreduce_window(self.grad, self.loss_acc, self.pg)
+                if self.adam_enabled:  # (tests inspect the reduced gradient with it off)
+                    self.t += 1
+                    _adam(self.planes, self.grad, self.m, self.v, self.F, self.HW, self.cfg,
+                          self.t, False)
         n_color = 3.0 * self.HW
         nd = torch.tensor([max(n, 1) for n in self.n_depth], dtype=torch.float64, device=self.dev)
         has_d = torch.tensor([n > 0 for n in self.n_depth], device=self.dev)
@@ -410,6 +447,31 @@ class WindowMapper:
                 self.cfg.sigma * torch.where(has_d, self.loss_acc[:, 1] / nd,
                                              torch.zeros_like(nd))).sum()
         return float(loss) if sync_loss else loss
+
+    def _sharded(self) -> bool:
+        dist = torch.distributed
+        if not (self.shard_adam and dist.is_available() and dist.is_initialized()):
+            return False
+        world = dist.get_world_size(self.pg)
+        return world > 1 and self.F % world == 0
+
+    def _sharded_update(self):
+        """Reduce-scatter -> Adam on this rank's frames -> all-gather."""
+        dist = torch.distributed
+        if self._shard is None:
+            world, rank = dist.get_world_size(self.pg), dist.get_rank(self.pg)
+            f0, f1 = frame_shard(self.F, rank, world)
+            local = torch.empty(((f1 - f0) * self.HW, 8), dtype=torch.float32, device=self.dev)
+            stage = torch.empty((f1 - f0,) + tuple(self.planes.shape[1:]),
+                                dtype=self.planes.dtype, device=self.dev)
+            self._shard = (f0, f1, local, stage)
+        f0, f1, local, stage = self._shard
+        reduce_scatter_window(self.grad, local, self.loss_acc, self.pg)
+        self.grad.zero_()  # this step's contributions are all in the scattered blocks
+        self.t += 1
+        _adam(self.planes[f0:f1], local, self.m[f0:f1], self.v[f0:f1], f1 - f0, self.HW,
+              self.cfg, self.t, False)
+        allgather_planes(self.planes, stage, f0, f1, self.pg)
 
     def grads_numpy(self):
         """Current gradient buffer as per-frame MapGradients-like dicts (host)."""
