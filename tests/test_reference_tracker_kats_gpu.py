@@ -200,3 +200,50 @@ def test_too_few_inliers_returns_the_initial_pose_flagged():
     init = Pose(np.eye(3), np.array([50.0, 50.0, 50.0]))  # off every surface
     pose, diag = gicp_align(local, g, init, TrackerConfig())
     assert diag.failed and np.array_equal(pose.translation, init.translation)
+
+
+# ------------------------------------------------------------------ 3x3 eig (T3)
+# raysplat tests/test_geometry.py TestSym3Eig :186-244 on sym_eigh3_batch
+
+def eig(mats):
+    from paper_2603_21055_b200.tracker import sym_eigh3_batch
+    rot, vals = sym_eigh3_batch(np.asarray(mats, dtype=np.float64).reshape(-1, 3, 3))
+    return n(rot), n(vals)
+
+
+def test_eig_known_diagonal():
+    r, v = eig(np.diag([4.0, 1.0, 0.25]))
+    np.testing.assert_allclose(v[0], [4.0, 1.0, 0.25], atol=1e-12)
+    np.testing.assert_allclose(np.abs(r[0]), np.eye(3), atol=1e-12)
+
+
+def test_eig_identity():
+    r, v = eig(np.eye(3))
+    np.testing.assert_allclose(v[0], np.ones(3), atol=1e-12)
+    np.testing.assert_allclose(r[0] @ r[0].T, np.eye(3), atol=1e-12)
+
+
+def test_eig_random_spd_reconstruction():
+    rng = np.random.default_rng(31)
+    a = rng.normal(size=(500, 3, 3))
+    m = a @ a.transpose(0, 2, 1) + 1e-6 * np.eye(3)
+    r, v = eig(m)
+    recon = np.einsum("nij,nj,nkj->nik", r, v, r)
+    assert np.linalg.norm(recon - m, axis=(1, 2)).max() < 1e-7
+    np.testing.assert_allclose(np.einsum("nij,nkj->nik", r, r),
+                               np.broadcast_to(np.eye(3), (500, 3, 3)), atol=1e-9)
+    assert (np.linalg.det(r) > 0).all()
+    assert (v[:, 0] >= v[:, 1]).all() and (v[:, 1] >= v[:, 2]).all()
+
+
+def test_eig_rank_deficient():
+    r, v = eig(np.diag([2.0, 1.0, 0.0]))
+    np.testing.assert_allclose(v[0], [2.0, 1.0, 0.0], atol=1e-12)
+    np.testing.assert_allclose(np.abs(r[0][:, 2]), [0.0, 0.0, 1.0], atol=1e-12)
+
+
+def test_eig_near_degenerate_pair():
+    m = np.diag([1.0, 1.0 + 1e-13, 2.0])
+    r, v = eig(m)
+    recon = r[0] @ np.diag(v[0]) @ r[0].T
+    assert np.linalg.norm(recon - m) < 1e-7
