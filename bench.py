@@ -356,7 +356,9 @@ def run_ours(args):
                                        f"tau={args.tau:g} L1 colour+depth"
                                        f"{' + SSIM' if args.tau else ''}, Adam",
                            "gaussians": n_g, "views_per_step": n_views_total,
-                           "parallelism": f"views sharded over {world} GPU(s), NCCL all-reduce",
+                           "parallelism": (f"views sharded over {world} GPU(s); gradient reduce-scatter by "
+                                   "frame block, Adam per block, parameter all-gather (NCCL)"
+                                   if world > 1 else "1 GPU"),
                            "l2": "inputs larger than L2 (params 183 MB + records ~350 MB/view)"},
                 "window_iters_per_s": 1e3 / ms_step,
                 "keyframes_per_s": n_views_total * 1e3 / ms_step / 100.0,
