@@ -10,7 +10,11 @@
 //
 // Layout (HBM): survivors live in EMISSION order (frame, pixel) as 64-byte
 // records; the depth sort produces a permutation, tile lists hold emission
-// indices in depth order.  Per-view scratch is owned by the sgad_raster handle.
+// indices in depth order (plus, in the top bits, the warp rectangles each
+// entry reaches).  A forward that keeps state writes per-warp compact lists
+// (entries reaching the warp's 8x4 pixels + exact masks) that the backward
+// walks instead of the tile lists.  Per-view scratch is owned by the
+// sgad_raster handle.  DESIGN.md section 4 has the measured design notes.
 #include <thrust/iterator/counting_iterator.h>
 #include <thrust/iterator/transform_iterator.h>
 #include <cub/cub.cuh>
