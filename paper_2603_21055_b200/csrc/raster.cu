@@ -508,24 +508,25 @@ __device__ __forceinline__ TileGeom tile_geom(int ntx, int width, int height) {
 
 // Each warp owns one 8x4 sub-tile and walks the tile's depth-ordered list on
 // its own (no block barriers: sub-tiles finish at different list positions).
-//   1. entry-major exact masks: lane i loads list entry i of a 32-entry
-//      chunk, culls it against the rectangle in fp32 and, for survivors,
-//      evaluates the reference test d2 > 9 s2 at all 32 pixels (fp32 row
-//      intervals outside a guard band, fp64 inside it) -> 32-bit pixel mask;
-//   2. entries that reach at least one pixel are compacted into a window of
-//      33..64 slots (record index + list position per slot), their masks
-//      gathered into slot-owner lanes with shuffles;
-//   3. two 32x32 bit transposes turn the entry masks into one 64-bit mask per
-//      lane (= per pixel) over the window;
-//   4. every lane pops its own bits in list order and composites in fp64,
-//      reading the entry's record through L1.
-// Windows live in a per-warp ring of RING slots and every lane consumes them
-// at its own pace.  Depth order sweeps across a surface, so a pixel's
-// contributors arrive in bursts that differ from lane to lane; with one
-// window at a time the warp paid every window's busiest lane (8 of 32 lanes
-// busy at C4), with a ring deep enough to hold a sub-tile's whole sweep the
-// lanes stay busy (K4).  A window is staged when a lane has run dry
-// and the slot it needs is no longer read by any lane.
+// Forward (K4):
+//   1. lane i reads list value i of a 32-entry chunk (two chunks ahead) and
+//      keeps it if its warp-rectangle bits say the entry's 3-sigma box reaches
+//      the sub-tile; kept entries queue up in shared memory;
+//   2. 32 queued entries at a time, one per lane: the record is loaded and the
+//      reference test d2 > 9 s2 evaluated at all 32 pixels (fp32 row
+//      intervals outside a guard band, fp64 inside it) -> exact pixel mask;
+//   3. entries with pixels fill a window of 33..64 slots (fields staged in
+//      shared memory; with state, also appended to the warp's compact list),
+//      and two 32x32 bit transposes give each lane (pixel) its 64 bits;
+//   4. every lane pops its own bits in list order and composites in fp64.
+// Backward (K5): windows are staged from the compact list in reverse into a
+// per-warp ring of RING windows, each lane consumes them at its own pace and
+// reads the entry's record through L1.  Depth order sweeps across a surface,
+// so a pixel's contributors arrive in bursts that differ from lane to lane;
+// with one window at a time the warp paid every window's busiest lane (8 of
+// 32 lanes busy at C4), with the ring the lanes stay busy (K4/K5).
+// A window is staged when a lane has run dry and the slot it needs is no
+// longer read by any lane.
 constexpr int NWARP = RASTER_THREADS / 32;
 constexpr int WIN = 64;
 #ifndef SGAD_RING
