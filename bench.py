@@ -5,13 +5,17 @@ Gaussians/s at 1200x680, 8-keyframe window; tracking GN iterations/s).
 
 One step = one window iteration of configuration C4: every keyframe's view is
 rendered (K1-K4 with the fused tau=0 L1 loss), back-propagated (K5) onto all
-6.5 M pixel-aligned Gaussians, the gradients are all-reduced over ranks
-(NCCL) and one Adam kernel updates the window.  Views are sharded over ranks
-(weak in views per rank... the window is fixed, so total work is fixed:
-``scaling`` = "strong").  Inputs are synthetic (seeded room scene).
+6.5 M pixel-aligned Gaussians, the gradients are exchanged over ranks (NCCL
+reduce-scatter by frame block, Adam per block, all-gather) and Adam updates
+the window.  Views are sharded over ranks; the window is fixed, so total work
+is fixed (``scaling`` = "strong").  Inputs are synthetic (seeded room scene,
+DESIGN.md).  ``--gpus N`` without a torchrun environment re-executes itself
+under torch.distributed.run with N ranks.
 
-``--impl reference`` times the CPU oracle port of the reference path (the
-reference is a Python/Numba package) on the host cores, rank 0 only.
+``--impl reference`` times the reference itself (the raysplat package from
+baseline/_ref, its Numba kernels and MapOptimizer) on the host cores, rank 0
+only; the CPU legs of our line (the reference, the oracle port, tracking)
+run in child processes (bench_cpu.py).
 """
 
 from __future__ import annotations
@@ -47,7 +51,6 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-track", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--cpu-views", type=int, default=0, help="views in the CPU sample (0: auto)")
     return ap.parse_args()
 
 
@@ -125,89 +128,45 @@ def load_peaks():
 # ------------------------------------------------------------------ CPU legs
 
 
-def cpu_sample(cfg_name, n_views_req, threads, n_sources=0, reps=1):
-    """Oracle port (C restatement of the reference kernels) on host cores:
-    a bounded sample of the window iteration -- ``n`` target views, each a full
-    all-learnable fwd+bwd over the window's maps (all of them, or the first
-    ``n_sources``), in a thread pool like the reference's own
-    (raysplat/pipeline.py:212).  With ``reps`` > 1 the sample is repeated and
-    each repetition timed; the first ``reps - timed`` are for the caller."""
-    from concurrent.futures import ThreadPoolExecutor
-    from types import SimpleNamespace
-
-    import numpy as np
-    from oracle import raster as O
-    wc = make_config(cfg_name, "cpu" if not _has_cuda() else "cuda")
-    maps = [SimpleNamespace(frame_index=i, pose=wc.poses[i], intrinsics=wc.intr,
-                            base_depth=p.base_depth, delta=p.delta, log_radius=p.log_radius,
-                            opacity_logit=p.opacity_logit, color=p.color,
-                            active_mask=p.active_mask) for i, p in enumerate(wc.params)]
-    if n_sources:
-        maps = maps[:n_sources]
-    n_views = n_views_req or min(len(wc.frames), max(1, threads))
-    views = list(range(n_views))
-
-    def one(v):
-        fr = wc.frames[v]
-        O.mapping_loss(maps, fr.color, fr.depth, fr.valid_mask, wc.poses[v].rotation,
-                       wc.poses[v].translation, wc.intr, learnable_map="all")
-
-    O.lib()
-    times = []
-    with ThreadPoolExecutor(max_workers=max(1, min(threads, n_views))) as ex:
-        for _ in range(reps):
-            t0 = time.perf_counter()
-            list(ex.map(one, views))
-            times.append(time.perf_counter() - t0)
-    dt = times[-1] if reps == 1 else None  # (callers drop "times" / "gaussian_views")
-    n_g = sum(int(np.asarray(m.active_mask).size) for m in maps)
-    src = f"{len(maps)} of {len(wc.frames)} window maps" if n_sources else "all window maps"
-    res = {"unit": UNIT, "cores": min(threads, n_views), "kind": "port", "times": times,
-           "gaussian_views": n_g * n_views,
-           "sample": f"{n_views} target views of one {cfg_name.upper()} window iteration, "
-                     f"all-learnable fwd+bwd over {src} ({n_g} Gaussians)"}
-    if dt is not None:
-        res["value"] = n_g * n_views / dt
-        res["sample"] += f", {dt:.1f} s wall"
-    return res
-
-
-def _has_cuda():
-    try:
-        import torch
-        return torch.cuda.is_available()
-    except Exception:
-        return False
+def workload_config(cfg_name, tau, world):
+    """The ``config`` object of both arms' lines (identical by construction)."""
+    from paper_2603_21055_b200 import scenes
+    intr = {"c3": scenes.C3_INTR, "c4": scenes.C4_INTR, "c5": scenes.C4_INTR}[cfg_name]
+    n_views = 32 if cfg_name == "c5" else 8
+    w, h = intr["width"], intr["height"]
+    return {"workload": f"{cfg_name.upper()}: {w}x{h}, {n_views}-keyframe window, all learnable, "
+                        f"tau={tau:g} L1 colour+depth{' + SSIM' if tau else ''}, Adam",
+            "gaussians": n_views * w * h, "views_per_step": n_views,
+            "parallelism": (f"views sharded over {world} GPU(s); gradient reduce-scatter by "
+                            "frame block, Adam per block, parameter all-gather (NCCL)"
+                            if world > 1 else "1 GPU"),
+            "l2": "inputs larger than L2 (params 183 MB + records ~350 MB/view at C4)"}
 
 
 def run_reference(args):
-    """The reference arm: the reference's CPU algorithm (the oracle port of its
-    kernels; the reference is a Python package) on the box's host cores, on
-    this arm's config, metric and unit.  A timed step is the full window
-    iteration's views (one per host thread, as the reference's own pool, over
-    all window maps; ~20 s at C4 on the GPU boxes' 8 cores); the W warm-up
-    steps only load the library (one view over two maps).  Under torchrun
-    rank 0 alone runs; the other ranks exit."""
+    """The reference arm: the reference's own CPU implementation -- the
+    raysplat package itself (``baseline/_ref``: its Numba kernels, loss,
+    chain rule and MapOptimizer, bench_cpu.py / oracle/refwindow.py) -- on the
+    box's host cores, on this arm's config, metric and unit.  A step is a
+    bounded sample of the window iteration: every view (one per host thread)
+    over the first m window maps, m sized so a step takes ~``150 / K`` s, then
+    the reference Adam on those maps.  Under torchrun rank 0 alone runs; the
+    other ranks exit."""
     rank, world, _ = dist_env()
     if rank != 0:
         return
+    import bench_cpu
     threads = len(os.sched_getaffinity(0))
     k, w = max(1, args.steps), max(0, args.warmup)
-    if w:
-        cpu_sample(args.config, 1, threads, n_sources=2, reps=w)
-    cb = cpu_sample(args.config, args.cpu_views, threads, reps=k)
-    timed = cb.pop("times")
-    gv = cb.pop("gaussian_views")
-    value = gv * k / sum(timed)
-    cb["value"] = value
-    cb["sample"] += f", {k} timed steps of {sum(timed) / k:.1f} s"
-    line = {"metric": METRICS[args.config], "value": value, "unit": UNIT, "n_gpus": 0,
+    target = max(2.0, min(20.0, 150.0 / k))
+    cb = bench_cpu.map_leg("reference", args.config, target, threads, steps=k, warmup=w, log=True)
+    value = cb["value"]
+    timed = cb.pop("times_s")
+    line = {"metric": METRICS[args.config], "value": value, "unit": UNIT, "n_gpus": world,
             "steps": k, "warmup": w, "ms_per_step": 1e3 * sum(timed) / k,
             "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"{args.config.upper()} mapping window iteration (CPU oracle "
-                                   "port of raysplat rasterizer kernels)",
-                       "gaussian_views_per_step": gv},
+            "config": workload_config(args.config, args.tau, world),
             "impl": "reference", "cpu_baseline": cb,
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
@@ -225,10 +184,18 @@ def run_ours(args):
     from paper_2603_21055_b200.mapper import MapperConfig, WindowMapper
 
     rank, world, local = dist_env()
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+    if torch.cuda.device_count() < world:
+        raise SystemExit(f"bench.py: {world} ranks but {torch.cuda.device_count()} visible GPU(s)")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
+        assert dist.get_world_size() == args.gpus
+        print(f"bench.py: rank {dist.get_rank()}/{dist.get_world_size()} on cuda:{local} "
+              f"({torch.cuda.get_device_name(dev)}), NCCL {torch.cuda.nccl.version()}",
+              file=sys.stderr, flush=True)
     wc = make_config(args.config, dev)
     views = list(range(rank, len(wc.poses), world))
     wm = WindowMapper(wc.frames, wc.poses, wc.intr, wc.params, MapperConfig(tau=args.tau),
@@ -329,42 +296,54 @@ def run_ours(args):
         except Exception as exc:
             ssim_line = {"error": repr(exc)}
 
-    track = None
+    track = track_c2 = None
     if not args.no_track and rank == 0:
         try:
-            track = bench_tracking(dev)
+            track = bench_tracking(dev, "c4size")
         except Exception as exc:  # tracking is the secondary metric
             track = {"error": repr(exc)}
+        try:
+            track_c2 = bench_tracking(dev, "c2")
+        except Exception as exc:
+            track_c2 = {"error": repr(exc)}
         try:
             track["render_init"] = bench_render_init(dev)
         except Exception as exc:
             track["render_init"] = {"error": repr(exc)}
 
-    cpu = None
+    cpu = cpu_port = cpu_c1 = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_sample(args.config, args.cpu_views, len(os.sched_getaffinity(0)))
-        cpu.pop("times", None)
-        cpu.pop("gaussian_views", None)
+        # the reference itself (kind "reference") and the oracle port beside it,
+        # each in a process of its own (bench_cpu.py)
+        import bench_cpu
+        cpu = bench_cpu.run_subprocess(["map-ref", "--config", args.config, "--target-s", "15"])
+        cpu_port = bench_cpu.run_subprocess(["map-port", "--config", args.config,
+                                             "--target-s", "15"])
+        cpu_c1 = bench_cpu.run_subprocess(["ref-c1"])
+        for c in (cpu, cpu_port):
+            c.pop("times_s", None)
+        if track is not None and "error" not in track:
+            track["cpu_baseline"] = bench_cpu.run_subprocess(
+                ["track-port", "--track", "c4size", "--iters", "2"], threads=1)
+        if track_c2 is not None and "error" not in track_c2:
+            track_c2["cpu_baseline"] = bench_cpu.run_subprocess(
+                ["track-port", "--track", "c2", "--iters", "5"], threads=1)
+            track_c2["cpu_baseline_all_cores"] = bench_cpu.run_subprocess(
+                ["track-port", "--track", "c2", "--iters", "5"])
 
     if rank == 0:
         line = {"metric": METRICS[args.config], "value": value, "unit": UNIT, "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
                 "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
                 "dtype": "f64 composite / fp32 params", "data": "synthetic",
-                "config": {"workload": f"{args.config.upper()}: {wm.W}x{wm.H}, "
-                                       f"{n_views_total}-keyframe window, all learnable, "
-                                       f"tau={args.tau:g} L1 colour+depth"
-                                       f"{' + SSIM' if args.tau else ''}, Adam",
-                           "gaussians": n_g, "views_per_step": n_views_total,
-                           "parallelism": (f"views sharded over {world} GPU(s); gradient reduce-scatter by "
-                                   "frame block, Adam per block, parameter all-gather (NCCL)"
-                                   if world > 1 else "1 GPU"),
-                           "l2": "inputs larger than L2 (params 183 MB + records ~350 MB/view)"},
+                "config": workload_config(args.config, args.tau, world),
                 "window_iters_per_s": 1e3 / ms_step,
                 "keyframes_per_s": n_views_total * 1e3 / ms_step / 100.0,
-                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+                "roofline": roofline, "cpu_baseline": cpu, "cpu_baseline_port": cpu_port,
+                "cpu_reference_c1": cpu_c1, "e2e": e2e,
                 "gpu_launches": launches,
-                "clocks": sampler.summary(), "tracking": track, "ssim_term": ssim_line}
+                "clocks": sampler.summary(), "tracking": track, "tracking_c2": track_c2,
+                "ssim_term": ssim_line}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
@@ -507,18 +486,29 @@ def bench_render_init(dev, iters=3):
             "ms_per_iteration": dt / iters * 1e3, "iterations": iters, "ok": bool(ok)}
 
 
-def bench_tracking(dev, iters=20, reps=5):
-    """Secondary metric: GN iterations/s of the fused GICP normal equations at
-    1200x680 (window fit of both frames, exact NN, host 6x6 solve)."""
+def bench_tracking(dev, which="c4size", iters=20, reps=5):
+    """Secondary metric: GN iterations/s of the fused GICP normal equations
+    (window fit of both frames, exact NN, host 6x6 solve), 20 GN iterations
+    with convergence_eps = 0, timed with CUDA events around ``reps`` runs
+    (the host solves are inside).  ``which``: "c4size" (1200x680 room scene,
+    816 k correspondences) or "c2" (BASELINE config 1: 320x240, 76.8 k).
+    Roofline: 84 B per correspondence for the linearisation (local centre +
+    covariance 36 B, target centre + covariance + normal 48 B) plus 84 B for
+    the candidate cost pass = 168 M bytes per GN iteration."""
+    import numpy as np
     import torch
     from paper_2603_21055_b200 import tracker as T
     from paper_2603_21055_b200 import scenes
     from paper_2603_21055_b200.geometry import Intrinsics, Pose
-    intr = Intrinsics(**scenes.C4_INTR)
-    prims = scenes.room_scene(0)
-    ref = scenes.render_frame(prims, Pose.identity(), intr, 0, depth_noise_rel=0.01, device=dev)
-    truth = scenes.se3_exp([0.01, -0.02, 0.015, 0.03, -0.01, 0.02])
-    qry = scenes.render_frame(prims, truth, intr, 1, depth_noise_rel=0.01, device=dev)
+    if which == "c2":
+        intr, ref, qry, truth = scenes.config_c2(device=dev)
+    else:
+        intr = Intrinsics(**scenes.C4_INTR)
+        prims = scenes.room_scene(0)
+        ref = scenes.render_frame(prims, Pose.identity(), intr, 0, depth_noise_rel=0.01,
+                                  device=dev)
+        truth = scenes.se3_exp([0.01, -0.02, 0.015, 0.03, -0.01, 0.02])
+        qry = scenes.render_frame(prims, truth, intr, 1, depth_noise_rel=0.01, device=dev)
     cfg = T.TrackerConfig(downsample_ratio=1, max_gicp_iters=iters, convergence_eps=0.0,
                           voxel_size=1e-4)
     g = T.GlobalGeomSet(cfg.voxel_size)
@@ -531,29 +521,68 @@ def bench_tracking(dev, iters=20, reps=5):
     local = T.build_local_set(qry, cfg)
     T.gicp_align(local, g, Pose.identity(), cfg)  # warm-up
     torch.cuda.synchronize()
-    t0 = time.perf_counter()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
     n_it = 0
     for _ in range(reps):
         pose, diag = T.gicp_align(local, g, Pose.identity(), cfg)
         n_it += diag.iterations + (0 if diag.iterations == iters else 1)
-    dt = time.perf_counter() - t0
-    t1 = time.perf_counter()
+    e1.record()
+    torch.cuda.synchronize()
+    dt = e0.elapsed_time(e1) / 1e3
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    f0.record()
     for _ in range(reps):
         T.build_local_set(qry, cfg)
+    f1.record()
     torch.cuda.synchronize()
-    fit_ms = (time.perf_counter() - t1) / reps * 1e3
-    return {"metric": "tracking GN iterations/s (1200x680, 5x5 window fit, exact NN, host solve)",
-            "value": n_it / dt, "unit": "GN iters/s", "correspondences": len(local),
-            "iterations_per_run": diag.iterations, "fit_ms_per_frame": fit_ms,
-            "global_insert_ms": insert_ms, "global_members": len(g)}
+    fit_ms = f0.elapsed_time(f1) / reps
+    m = len(local)
+    peak, peak_kind = load_peaks()
+    it_s = dt / n_it
+    achieved = 168.0 * m / it_s / 1e9
+    rot_err = float(np.linalg.norm(pose.rotation - np.asarray(truth.rotation)))
+    return {"metric": f"tracking GN iterations/s ({which}: {intr.width}x{intr.height}, 5x5 window "
+                      f"fit, exact NN, host solve)",
+            "value": n_it / dt, "unit": "GN iters/s", "correspondences": m,
+            "iterations_per_run": diag.iterations, "ms_per_iteration": it_s * 1e3,
+            "fit_ms_per_frame": fit_ms, "global_insert_ms": insert_ms, "global_members": len(g),
+            "pose_rot_err_vs_truth": rot_err,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak,
+                         "peak_source": peak_kind, "unit": "GB/s", "frac": achieved / peak,
+                         "bytes_per_iteration": 168 * m,
+                         "note": "whole GN iteration (NN search + normal equations + cost pass "
+                                 "+ 2 host round trips) against 168 B per correspondence"}}
+
+
+def free_port():
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def spawn_ranks(args):
+    """``--gpus N`` without a torchrun environment: re-exec this command under
+    torch.distributed.run with N ranks (one process per GPU, rendezvous on
+    127.0.0.1), the launch the driver uses for N > 1."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    print(f"bench.py: launching {args.gpus} ranks: {' '.join(cmd)}", file=sys.stderr, flush=True)
+    os.execv(sys.executable, cmd)
 
 
 def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
-    else:
-        run_ours(args)
+        return
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        spawn_ranks(args)
+    run_ours(args)
 
 
 if __name__ == "__main__":

@@ -203,9 +203,25 @@ def allreduce_window(grad: torch.Tensor, loss_acc: torch.Tensor, group=None) -> 
         return False
     if dist.get_world_size(group) == 1:
         return False
-    dist.all_reduce(grad, group=group)
-    dist.all_reduce(loss_acc, group=group)
+    _all_reduce(grad, group)
+    _all_reduce(loss_acc, group)
     return True
+
+
+def _host_staged(group, *tensors) -> bool:
+    """gloo moves host memory only: CUDA tensors are staged through the host
+    (tests run two ranks on one GPU with gloo; production uses NCCL)."""
+    dist = torch.distributed
+    return dist.get_backend(group) == "gloo" and any(t.is_cuda for t in tensors)
+
+
+def _all_reduce(t: torch.Tensor, group=None) -> None:
+    if _host_staged(group, t):
+        h = t.cpu()
+        torch.distributed.all_reduce(h, group=group)
+        t.copy_(h)
+    else:
+        torch.distributed.all_reduce(t, group=group)
 
 
 def frame_shard(n_frames: int, rank: int, world: int):
@@ -224,8 +240,13 @@ def reduce_scatter_window(grad: torch.Tensor, local: torch.Tensor, loss_acc: tor
     rows of this rank's frame block into ``local`` (reduce-scatter over the
     frame-major [N, 8] buffer) and the per-view loss sums everywhere."""
     dist = torch.distributed
-    dist.reduce_scatter_tensor(local, grad, group=group)
-    dist.all_reduce(loss_acc, group=group)
+    if _host_staged(group, grad, local):
+        h = local.cpu()
+        dist.reduce_scatter_tensor(h, grad.cpu(), group=group)
+        local.copy_(h)
+    else:
+        dist.reduce_scatter_tensor(local, grad, group=group)
+    _all_reduce(loss_acc, group)
 
 
 def allgather_planes(planes: torch.Tensor, stage: torch.Tensor, f0: int, f1: int,
@@ -233,7 +254,12 @@ def allgather_planes(planes: torch.Tensor, stage: torch.Tensor, f0: int, f1: int
     """Every rank's updated frame block back into everyone's [F, 7, H, W]
     parameter tensor (all-gather of contiguous frame blocks)."""
     stage.copy_(planes[f0:f1])
-    torch.distributed.all_gather_into_tensor(planes, stage, group=group)
+    if _host_staged(group, planes):
+        h = planes.cpu()
+        torch.distributed.all_gather_into_tensor(h, stage.cpu(), group=group)
+        planes.copy_(h)
+    else:
+        torch.distributed.all_gather_into_tensor(planes, stage, group=group)
 
 
 class WindowMapper:
@@ -242,9 +268,14 @@ class WindowMapper:
     ``frames``: per keyframe RGBD targets (``color`` HxWx3, ``depth`` HxW,
     ``valid_mask``); ``poses``: camera-to-world poses; ``params``: objects with
     ``base_depth, delta, log_radius, opacity_logit, color, active_mask``.
-    ``views``: the keyframes this process renders (default: all); under
-    torch.distributed the per-Gaussian gradient is summed over ranks with one
-    all-reduce before the (replicated) Adam step.
+    ``views``: the keyframes this process renders (default: all of them, or
+    under an initialised process group this rank's round-robin share,
+    ``shard_views``); under torch.distributed the per-Gaussian gradient is
+    summed over ranks (reduce-scatter by frame block + sharded Adam +
+    all-gather, or an all-reduce + replicated Adam).  ``frame_indices`` must
+    increase strictly: the Gaussian ids of frame i are rows [i HW, (i+1) HW)
+    of the gradient and parameter planes, and the rasterizer orders maps by
+    frame index.
     """
 
     def __init__(self, frames, poses, intr: Intrinsics, params, cfg: MapperConfig | None = None,
@@ -271,7 +302,10 @@ class WindowMapper:
             mask[i] = np.asarray(p.active_mask, dtype=bool)
         self.planes = torch.from_numpy(planes).to(dev)
         self.mask = torch.from_numpy(mask).to(dev)
-        idx = list(range(f)) if frame_indices is None else list(frame_indices)
+        idx = list(range(f)) if frame_indices is None else [int(i) for i in frame_indices]
+        if len(idx) != f or any(b <= a for a, b in zip(idx, idx[1:])):
+            raise ValueError("frame_indices must give one strictly increasing index per frame "
+                             "(sort the window's frames by index)")
         self.maps = [PixelGaussianMap.from_planes(idx[i], self.poses[i], intr, self.planes[i],
                                                   self.mask[i]) for i in range(f)]
         self.tcolor = torch.from_numpy(np.stack([np.asarray(fr.color, np.float32)
@@ -281,7 +315,14 @@ class WindowMapper:
         self.tmask = torch.from_numpy(np.stack([np.asarray(fr.valid_mask, bool)
                                                 for fr in frames]).astype(np.uint8)).to(dev)
         self.n_depth = [int(np.asarray(fr.valid_mask, bool).sum()) for fr in frames]
-        self.views = list(range(f)) if views is None else list(views)
+        if views is None:
+            dist = torch.distributed
+            if dist.is_available() and dist.is_initialized():
+                views = shard_views(f, dist.get_rank(process_group),
+                                    dist.get_world_size(process_group))
+            else:
+                views = range(f)
+        self.views = list(views)
         self.grad = torch.zeros((f * self.HW, 8), dtype=torch.float32, device=dev)
         self.m = torch.zeros((f, 6, h, w), dtype=torch.float32, device=dev)
         self.v = torch.zeros((f, 6, h, w), dtype=torch.float32, device=dev)
