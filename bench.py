@@ -244,12 +244,14 @@ def run_ours(args):
     # roofline of the compositing kernels (SURVEY 8d algorithmic bytes)
     hw = wm.HW
 
+    counts = wm.counts()  # per view (survivors, tile pairs): the same every step (fixed window)
+
     def kstats(kind, extra_surv, both=False):
         lst = [t for t in timing if t[0] == kind]
-        tot_ms = sum(a.elapsed_time(b) for _, a, b, _, _, _ in lst)
+        tot_ms = sum(a.elapsed_time(b) for _, a, b, _ in lst)
         per = (lambda ns, npairs: 72 * npairs + 40 * hw + 32 * ns) if both else \
             (lambda ns, npairs: 36 * npairs + 20 * hw + (32 * ns if extra_surv else 0))
-        tot_bytes = sum(per(ns, npairs) for _, _, _, _, ns, npairs in lst)
+        tot_bytes = sum(per(*counts[v]) for _, _, _, v in lst)
         return tot_ms, tot_bytes, len(lst)
 
     f_ms, f_bytes, f_n = kstats("fwd", False)
@@ -263,9 +265,8 @@ def run_ours(args):
         dom = ("k_backward", b_ms, b_bytes, b_n) if b_ms >= f_ms else \
             ("k_forward", f_ms, f_bytes, f_n)
     achieved = dom[2] / dom[3] / (dom[1] / dom[3] / 1e3) / 1e9
-    counts = list(wm.last_counts.values())
-    mean_ns = float(np.mean([c[0] for c in counts])) if counts else 0.0
-    mean_np = float(np.mean([c[1] for c in counts])) if counts else 0.0
+    mean_ns = float(np.mean([c[0] for c in counts.values()])) if counts else 0.0
+    mean_np = float(np.mean([c[1] for c in counts.values()])) if counts else 0.0
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
@@ -541,13 +542,11 @@ def bench_tracking(dev, which="c4size", iters=20, reps=5):
     peak, peak_kind = load_peaks()
     it_s = dt / n_it
     achieved = 168.0 * m / it_s / 1e9
-    rot_err = float(np.linalg.norm(pose.rotation - np.asarray(truth.rotation)))
     return {"metric": f"tracking GN iterations/s ({which}: {intr.width}x{intr.height}, 5x5 window "
                       f"fit, exact NN, host solve)",
             "value": n_it / dt, "unit": "GN iters/s", "correspondences": m,
             "iterations_per_run": diag.iterations, "ms_per_iteration": it_s * 1e3,
             "fit_ms_per_frame": fit_ms, "global_insert_ms": insert_ms, "global_members": len(g),
-            "pose_rot_err_vs_truth": rot_err,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak,
                          "peak_source": peak_kind, "unit": "GB/s", "frac": achieved / peak,
                          "bytes_per_iteration": 168 * m,

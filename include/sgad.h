@@ -101,6 +101,22 @@ int sgad_raster_prepare(sgad_raster* h, const sgad_frame* frames, int32_t n_fram
                         const sgad_camera* cam, int32_t want_coef, void* stream,
                         int64_t* n_survivors, int64_t* n_pairs);
 
+/* The same preparation without any host synchronisation (the window engine;
+ * capturable in a CUDA graph): element counts stay on the device.
+ * counts_out (device uint32[2], may be NULL) receives (survivors, pairs);
+ * if the view has more tile pairs than the handle's capacity (see
+ * sgad_raster_reserve; first use: 3 x Gaussians) the extra pairs are
+ * dropped and *overflow_flag (device int32, may be NULL) is set to 1 --
+ * the caller discards the view's results, reserves more and prepares again.
+ * Replaces the same reference functions as sgad_raster_prepare. */
+int sgad_raster_prepare_async(sgad_raster* h, const sgad_frame* frames, int32_t n_frames,
+                              const sgad_camera* cam, int32_t want_coef, uint32_t* counts_out,
+                              int32_t* overflow_flag, void* stream);
+
+/* Grow the handle's tile-pair capacity (buffers are resized at the next
+ * preparation). */
+int sgad_raster_reserve(sgad_raster* h, int64_t pair_capacity);
+
 /* Composite the prepared view.  Image outputs (fp64 / int32, device) may be
  * NULL.  save_state != 0 keeps per-pixel final transmittance and last list
  * position for the backward.  target != NULL fuses the tau=0 L1 loss and
@@ -146,10 +162,14 @@ int sgad_raster_tile_count(sgad_raster* h, int64_t* n_tiles);
  * m, v [F, 6, HW] and grads [F*HW, 8] (consumed and zeroed) in fp32
  * (f64 == 0) or fp64 (f64 != 0).
  * bc1 = 1 - beta1^t, bc2 = 1 - beta2^t.  lr[6] per channel (delta, log_radius,
- * opacity_logit, R, G, B); update_delta == 0 freezes the offsets. */
+ * opacity_logit, R, G, B); update_delta == 0 freezes the offsets.  skip
+ * (device int32, may be NULL): when *skip != 0 the gradients are consumed
+ * (zeroed) and nothing is updated (a window step whose preparation
+ * overflowed, see sgad_raster_prepare_async). */
 int sgad_adam_step(void* params, void* grads, void* m, void* v, int64_t n_frames, int64_t hw,
                    const double* lr, double beta1, double beta2, double eps, double bc1,
-                   double bc2, int32_t update_delta, int32_t f64, void* stream);
+                   double bc2, int32_t update_delta, int32_t f64, const int32_t* skip,
+                   void* stream);
 
 /* ---- render-based pose initialiser ------------------------------------
  * One IRLS linearisation of tracker.py:400-410: rows (device fp64 [12, n]) are

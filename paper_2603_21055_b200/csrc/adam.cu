@@ -14,6 +14,7 @@ struct AdamArgs {
   double lr[6];
   double b1, b2, eps, bc1, bc2;
   int update_delta;
+  const int32_t* skip;  // device flag: consume (zero) the gradients, update nothing
 };
 
 template <typename P>
@@ -30,6 +31,7 @@ k_adam(P* __restrict__ params, P* __restrict__ grads, P* __restrict__ m,
     gr[c] = (double)gp[c];
     gp[c] = (P)0;
   }
+  if (a.skip && *a.skip) return;
   P* pf = params + f * 7 * hw + p;
   P* mf = m + f * 6 * hw + p;
   P* vf = v + f * 6 * hw + p;
@@ -68,6 +70,7 @@ k_adam_f32(float* __restrict__ params, float* __restrict__ grads, float* __restr
   const float4 g0 = gp[0], g1 = gp[1];
   gp[0] = make_float4(0.f, 0.f, 0.f, 0.f);
   gp[1] = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (a.skip && *a.skip) return;
   float* pf = params + f * 7 * hw + p;
   float* mf = m + f * 6 * hw + p;
   float* vf = v + f * 6 * hw + p;
@@ -109,6 +112,7 @@ k_adam_f32x4(float* __restrict__ params, float* __restrict__ grads, float* __res
   for (int q = 0; q < 8; ++q) gr[q] = gp[q];
 #pragma unroll
   for (int q = 0; q < 8; ++q) gp[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (a.skip && *a.skip) return;
   float* pf = params + f * 7 * hw + p;
   float* mf = m + f * 6 * hw + p;
   float* vf = v + f * 6 * hw + p;
@@ -151,7 +155,7 @@ k_adam_f32x4(float* __restrict__ params, float* __restrict__ grads, float* __res
 extern "C" int sgad_adam_step(void* params, void* grads, void* m, void* v, int64_t n_frames,
                               int64_t hw, const double* lr, double beta1, double beta2, double eps,
                               double bc1, double bc2, int32_t update_delta, int32_t f64,
-                              void* stream) {
+                              const int32_t* skip, void* stream) {
   SGAD_REQUIRE(params && grads && m && v && lr && n_frames >= 0 && hw >= 0,
                "sgad_adam_step: bad arguments");
   const int64_t n = n_frames * hw;
@@ -164,6 +168,7 @@ extern "C" int sgad_adam_step(void* params, void* grads, void* m, void* v, int64
   a.bc1 = bc1;
   a.bc2 = bc2;
   a.update_delta = update_delta;
+  a.skip = skip;
   const unsigned nb = (unsigned)((n + 255) / 256);
   if (f64)
     sgad::k_adam<double><<<nb, 256, 0, (cudaStream_t)stream>>>(

@@ -15,9 +15,6 @@
 // (entries reaching the warp's 8x4 pixels + exact masks) that the backward
 // walks instead of the tile lists.  Per-view scratch is owned by the
 // sgad_raster handle.  DESIGN.md section 4 has the measured design notes.
-#include <thrust/iterator/counting_iterator.h>
-#include <thrust/iterator/transform_iterator.h>
-#include <cub/cub.cuh>
 #include <stdarg.h>
 #include <stddef.h>
 #include <stdlib.h>
@@ -25,6 +22,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "sort.cuh"
 
 namespace sgad {
 
@@ -67,20 +65,27 @@ constexpr int RASTER_THREADS = 256;
 }  // namespace sgad
 
 struct sgad_raster {
-  sgad::DevBuf frames, status, counters, records, coef, keys0, keys1, vals0, vals1;
-  sgad::DevBuf pcount, poffset, pkeys0, pkeys1, pvals0, pvals1, ranges, cub_tmp;
+  sgad::DevBuf frames, counters, records, coef, keys0, keys1, vals0, vals1;
+  sgad::DevBuf poffset, pkeys0, pkeys1, pvals0, pvals1, ranges, sortws;
   sgad::DevBuf trans_final, last_idx, signs, raw_grads, rank_of, scratch, col64, zrange, k32a, k32b, bbox, runs, raw32, cl_e, cl_m, cl_n;
   int any_f64 = 0;
   std::vector<sgad_frame> host_frames;
   sgad_camera cam{};
+  // n_surv / n_pairs: host copies, valid after a synchronous prepare (-1
+  // after an asynchronous one: the counts live in `counters` on the device)
   int64_t n_total = 0, n_surv = 0, n_pairs = 0;
+  int64_t cap_pairs = 0;  // capacity of the pair / compact-list buffers
   int32_t n_tiles = 0, ntx = 0, nty = 0;
   int prepared = 0, forwarded = 0, have_coef = 0, fused_ready = 0;
   int packed = 0;  // tile list values carry the warp-rectangle bits (n_total < 2^26)
+  int kbits = 24, dpasses = 3, tpasses = 2;
   double rho = 0, sigma_d = 0;
   int64_t n_depth = 0;
   uint32_t* pinned = nullptr;  // host-pinned counters
 };
+
+// counters[] slots (device, per prepared view)
+enum : int { C_NSURV = 1, C_NLONG = 3, C_NPAIRS = 4, C_OVERFLOW = 5 };
 
 namespace sgad {
 
@@ -326,52 +331,33 @@ k_project(const sgad_frame* __restrict__ frames, sgad_camera cam, int ntx, int n
 }
 
 // ------------------------------------------------------------------ K2
-// 24-bit monotone depth buckets: floor((z - zmin) * scale).  Sorting them
-// stably leaves only runs of equal buckets to be put in exact (z, emission)
-// order by k_depth_fixup -- 3 radix passes instead of 8 for the 63-bit key
-// (at C4 a bucket is ~1 um deep and nearly all runs are single entries).
+// Depth order = np.lexsort((pixel, frame, z)) (rasterizer.py:157-158).
+// Survivors are sorted stably by a 24-bit monotone depth bucket,
+// floor((z - zmin) * scale) (3 onesweep passes of sort.cuh; the first pass
+// computes the buckets from the fp64 z bits and drops culled ids), so equal
+// buckets keep emission (frame, pixel) order; the runs of equal buckets are
+// then put in exact (z, emission) order by k_depth_fixup / k_long_runs.
 static int depth_key_bits() {  // SGAD_DEPTH_BITS (A/B): 16..32, default 24
   const char* v = getenv("SGAD_DEPTH_BITS");
   const int b = v ? atoi(v) : 24;
   return b < 16 ? 16 : (b > 32 ? 32 : b);
 }
-__global__ void k_depth_key32(const unsigned long long* __restrict__ zkeys, uint32_t n,
-                              double zmin, double scale, double top, uint32_t* __restrict__ k32,
-                              uint32_t* __restrict__ vals) {
-  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const unsigned long long zk = zkeys[i];
-  if (zk == ~0ull) {
-    k32[i] = 0xFFFFFFFFu;  // culled: behind every survivor (low 24 bits all set)
-  } else {
-    const double b = floor((__longlong_as_double((long long)zk) - zmin) * scale);
-    k32[i] = b >= top ? (uint32_t)top : (uint32_t)b;  // top = 2^bits - 2 (survivors' largest)
-  }
-  vals[i] = i;
-}
 
-// Runs of equal buckets are sorted by (z bits, emission index) in place:
-// runs of up to 64 by this thread (insertion sort), longer runs are queued for
-// k_long_runs (a fronto-parallel plane seen head-on gives long runs of
-// exactly equal depth); runs beyond LONG_RUN_MAX raise *overflow and the
-// whole order is redone with the full 63-bit key.
-constexpr uint32_t LONG_RUN_MAX = 8192;
-
-__global__ void k_depth_fixup(const uint32_t* __restrict__ k32, uint32_t n,
+// Runs of equal buckets: up to 64 sorted here by their head thread
+// (insertion sort on (z bits, emission index)), longer ones queued for
+// k_long_runs (sort.cuh; any length).
+__global__ void k_depth_fixup(const uint32_t* __restrict__ k32, const uint32_t* __restrict__ n_dev,
                               const unsigned long long* __restrict__ zkeys,
-                              uint32_t* __restrict__ perm, uint32_t* __restrict__ overflow,
-                              uint32_t* __restrict__ n_long, uint2* __restrict__ long_runs) {
+                              uint32_t* __restrict__ perm, uint32_t* __restrict__ n_long,
+                              uint2* __restrict__ long_runs) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t n = *n_dev;
   if (i + 1 >= n) return;
-  if (k32[i] == 0xFFFFFFFFu) return;  // the culled tail
   if (k32[i + 1] != k32[i] || (i > 0 && k32[i - 1] == k32[i])) return;  // not a run head
   uint32_t end = i + 2;
-  while (end < n && k32[end] == k32[i] && end - i <= LONG_RUN_MAX) ++end;
-  if (end - i > LONG_RUN_MAX) {
-    atomicExch(overflow, 1u);
-    return;
-  }
+  while (end < n && k32[end] == k32[i] && end - i <= 64) ++end;
   if (end - i > 64) {
+    while (end < n && k32[end] == k32[i]) ++end;
     long_runs[atomicAdd(n_long, 1u)] = make_uint2(i, end - i);
     return;
   }
@@ -390,96 +376,67 @@ __global__ void k_depth_fixup(const uint32_t* __restrict__ k32, uint32_t n,
   }
 }
 
-// Long runs of equal depth buckets: a bitonic sort of (z bits, emission
-// index) in shared memory, one block per run (blocks loop over the queue).
-__global__ void __launch_bounds__(1024)
-k_long_runs(const uint2* __restrict__ long_runs, const uint32_t* __restrict__ n_long,
-            const unsigned long long* __restrict__ zkeys, uint32_t* __restrict__ perm) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  unsigned long long* zs = reinterpret_cast<unsigned long long*>(smem_raw);  // [LONG_RUN_MAX]
-  uint32_t* es = reinterpret_cast<uint32_t*>(zs + LONG_RUN_MAX);              // [LONG_RUN_MAX]
-  const uint32_t nr = *n_long;
-  for (uint32_t r = blockIdx.x; r < nr; r += gridDim.x) {
-    const uint2 ru = long_runs[r];
-    uint32_t P = 1;
-    while (P < ru.y) P <<= 1;
-    for (uint32_t i = threadIdx.x; i < P; i += blockDim.x) {
-      if (i < ru.y) {
-        const uint32_t e = perm[ru.x + i];
-        zs[i] = zkeys[e];
-        es[i] = e;
-      } else {
-        zs[i] = ~0ull;
-        es[i] = ~0u;
-      }
-    }
-    __syncthreads();
-    for (uint32_t k = 2; k <= P; k <<= 1) {
-      for (uint32_t j = k >> 1; j > 0; j >>= 1) {
-        for (uint32_t i = threadIdx.x; i < P; i += blockDim.x) {
-          const uint32_t x = i ^ j;
-          if (x > i) {
-            const bool gt = zs[i] > zs[x] || (zs[i] == zs[x] && es[i] > es[x]);
-            if (((i & k) == 0) == gt) {
-              const unsigned long long tz = zs[i];
-              zs[i] = zs[x];
-              zs[x] = tz;
-              const uint32_t te = es[i];
-              es[i] = es[x];
-              es[x] = te;
-            }
-          }
-        }
-        __syncthreads();
-      }
-    }
-    for (uint32_t i = threadIdx.x; i < ru.y; i += blockDim.x) perm[ru.x + i] = es[i];
-    __syncthreads();
-  }
-}
-
 // ------------------------------------------------------------------ K3
-// pair count of the i-th survivor in depth order (0 past the end), read by
-// the exclusive scan directly (no count array)
-struct TilePairCount {
-  const uint32_t* perm;
-  const TileBox* box;
-  uint32_t n;
-  __device__ __forceinline__ uint32_t operator()(uint32_t i) const {
-    if (i >= n) return 0u;
-    const TileBox r = box[perm[i]];
-    return (uint32_t)(r.tx1 - r.tx0 + 1) * (uint32_t)(r.ty1 - r.ty0 + 1);
-  }
-};
+// Tile lists = _build_tile_lists (rasterizer.py:178-218): the pair count of
+// every survivor in depth order is scanned (k_pair_scan, sort.cuh), each
+// survivor emits its (tile, value) pairs in (ty, tx) order at its offset, and
+// a stable radix sort on the tile key (6-bit digits) bins them: every tile's
+// list ends up in depth order.  Pairs past the handle's capacity are dropped
+// and flag *overflow (the caller grows the capacity and prepares again).
+constexpr int TILE_RB = 6;
 
-__global__ void k_tile_emit(const uint32_t* __restrict__ perm, const TileBox* __restrict__ box,
-                            const uint32_t* __restrict__ off, uint32_t n, int ntx, int packed,
-                            uint32_t* __restrict__ pkeys, uint32_t* __restrict__ pvals) {
+template <int TPASSES>
+__global__ void __launch_bounds__(256)
+k_tile_emit(const uint32_t* __restrict__ perm, const TileBox* __restrict__ box,
+            const uint32_t* __restrict__ off, const uint32_t* __restrict__ n_dev, int ntx,
+            int packed, uint32_t cap, uint32_t* __restrict__ pkeys, uint32_t* __restrict__ pvals,
+            uint32_t* __restrict__ hist, uint32_t* __restrict__ overflow,
+            int32_t* __restrict__ ext_flag) {
+  __shared__ uint32_t sh[TPASSES][1 << TILE_RB];
+  for (int j = threadIdx.x; j < TPASSES * (1 << TILE_RB); j += blockDim.x) (&sh[0][0])[j] = 0u;
+  __syncthreads();
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const uint32_t e = perm[i];
-  const TileBox r = box[e];
-  uint32_t o = off[i];
-  for (int ty = r.ty0; ty <= r.ty1; ++ty) {
-    uint32_t rows = 0;  // 4-row bands [by + 4b, by + 4b + 3] the box reaches
-    const int by = ty * SGAD_TILE;
+  const uint32_t n = *n_dev;
+  if (i < n) {
+    const uint32_t e = perm[i];
+    const TileBox r = box[e];
+    uint32_t o = off[i];
+    for (int ty = r.ty0; ty <= r.ty1; ++ty) {
+      uint32_t rows = 0;  // 4-row bands [by + 4b, by + 4b + 3] the box reaches
+      const int by = ty * SGAD_TILE;
 #pragma unroll
-    for (int b = 0; b < 4; ++b)
-      rows |= (r.py0 <= by + 4 * b + 3 && r.py1 >= by + 4 * b) ? (1u << b) : 0u;
-    for (int tx = r.tx0; tx <= r.tx1; ++tx) {
-      const int bx = tx * SGAD_TILE;
-      const uint32_t cols = ((r.px0 <= bx + 7 && r.px1 >= bx) ? 1u : 0u) |
-                            ((r.px0 <= bx + 15 && r.px1 >= bx + 8) ? 2u : 0u);
-      pkeys[o] = (uint32_t)(ty * ntx + tx);
-      pvals[o] = packed ? e | ((cols | rows << 2) << LIST_IDX_BITS) : e;
-      ++o;
+      for (int b = 0; b < 4; ++b)
+        rows |= (r.py0 <= by + 4 * b + 3 && r.py1 >= by + 4 * b) ? (1u << b) : 0u;
+      for (int tx = r.tx0; tx <= r.tx1; ++tx) {
+        const int bx = tx * SGAD_TILE;
+        const uint32_t cols = ((r.px0 <= bx + 7 && r.px1 >= bx) ? 1u : 0u) |
+                              ((r.px0 <= bx + 15 && r.px1 >= bx + 8) ? 2u : 0u);
+        const uint32_t t = (uint32_t)(ty * ntx + tx);
+        if (o < cap) {
+          pkeys[o] = t;
+          pvals[o] = packed ? e | ((cols | rows << 2) << LIST_IDX_BITS) : e;
+#pragma unroll
+          for (int p = 0; p < TPASSES; ++p)
+            atomicAdd(&sh[p][(t >> (TILE_RB * p)) & ((1u << TILE_RB) - 1u)], 1u);
+        } else {
+          *overflow = 1u;
+          if (ext_flag) *ext_flag = 1;
+        }
+        ++o;
+      }
     }
+  }
+  __syncthreads();
+  for (int j = threadIdx.x; j < TPASSES * (1 << TILE_RB); j += blockDim.x) {
+    const uint32_t c = (&sh[0][0])[j];
+    if (c) atomicAdd(hist + j, c);
   }
 }
 
-__global__ void k_tile_ranges(const uint32_t* __restrict__ pkeys, uint32_t n,
-                              uint2* __restrict__ ranges) {
+__global__ void k_tile_ranges(const uint32_t* __restrict__ pkeys, const uint32_t* __restrict__ n_dev,
+                              uint32_t cap, uint2* __restrict__ ranges) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t n = min(*n_dev, cap);
   if (i >= n) return;
   const uint32_t t = pkeys[i];
   if (i == 0 || pkeys[i - 1] != t) ranges[t].x = i;
@@ -1313,11 +1270,6 @@ __global__ void k_chain_exact(const Record* __restrict__ rec, const double* __re
   out[5 * hw + p] += rg[2];
 }
 
-__global__ void k_iota(uint32_t* __restrict__ v, uint32_t n) {
-  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) v[i] = i;
-}
-
 __global__ void k_rank_of(const uint32_t* __restrict__ perm, uint32_t n, uint32_t* __restrict__ rank) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) rank[perm[i]] = i;
@@ -1355,7 +1307,7 @@ constexpr size_t FWD_SMEM = sizeof(FwdStage) * NWARP;
 constexpr size_t FB_SMEM = FB_SLAB * NWARP;
 constexpr size_t BWD_SMEM = sizeof(WarpRing) * NWARP;
 
-constexpr size_t LONG_RUN_SMEM = (sizeof(unsigned long long) + sizeof(uint32_t)) * LONG_RUN_MAX;
+constexpr size_t LONG_RUN_SMEM = (sizeof(unsigned long long) + sizeof(uint32_t)) * LONG_RUN_SMEM_N;
 
 // opt in to >48 KB dynamic shared memory once per process
 static int smem_attrs() {
@@ -1389,7 +1341,7 @@ using namespace sgad;
 
 // the per-warp compact lists of the prepared view (sized at the forward)
 static int ensure_clist(sgad_raster* h) {
-  const size_t n = 8 * (size_t)(h->n_pairs > 0 ? h->n_pairs : 1);
+  const size_t n = 8 * (size_t)(h->cap_pairs > 0 ? h->cap_pairs : 1);
   SGAD_CHECK_CUDA(h->cl_e.ensure(sizeof(uint32_t) * n));
   SGAD_CHECK_CUDA(h->cl_m.ensure(sizeof(uint32_t) * n));
   SGAD_CHECK_CUDA(h->cl_n.ensure(sizeof(uint32_t) * 8 * (size_t)(h->n_tiles > 0 ? h->n_tiles : 1)));
@@ -1427,11 +1379,11 @@ int sgad_raster_create(sgad_raster** out) {
 
 int sgad_raster_destroy(sgad_raster* h) {
   if (!h) return SGAD_OK;
-  DevBuf* bufs[] = {&h->frames, &h->status, &h->counters, &h->records, &h->coef, &h->keys0,
-                    &h->keys1, &h->vals0, &h->vals1, &h->pcount, &h->poffset, &h->pkeys0,
-                    &h->pkeys1, &h->pvals0, &h->pvals1, &h->ranges, &h->cub_tmp,
-                    &h->trans_final, &h->last_idx, &h->signs, &h->raw_grads, &h->rank_of,
-                    &h->scratch, &h->col64, &h->zrange, &h->k32a, &h->k32b, &h->bbox, &h->runs, &h->raw32, &h->cl_e, &h->cl_m, &h->cl_n};
+  DevBuf* bufs[] = {&h->frames, &h->counters, &h->records, &h->coef, &h->keys0, &h->keys1,
+                    &h->vals0, &h->vals1, &h->poffset, &h->pkeys0, &h->pkeys1, &h->pvals0,
+                    &h->pvals1, &h->ranges, &h->sortws, &h->trans_final, &h->last_idx, &h->signs,
+                    &h->raw_grads, &h->rank_of, &h->scratch, &h->col64, &h->zrange, &h->k32a,
+                    &h->k32b, &h->bbox, &h->runs, &h->raw32, &h->cl_e, &h->cl_m, &h->cl_n};
   for (DevBuf* b : bufs) b->release();
   if (h->pinned) cudaFreeHost(h->pinned);
   delete h;
@@ -1444,12 +1396,59 @@ int sgad_raster_tile_count(sgad_raster* h, int64_t* n_tiles) {
   return SGAD_OK;
 }
 
-int sgad_raster_prepare(sgad_raster* h, const sgad_frame* frames, int32_t n_frames,
-                        const sgad_camera* cam, int32_t want_coef, void* stream_,
-                        int64_t* n_survivors, int64_t* n_pairs) {
+// ---- preparation (K1-K3), all on the stream, element counts on the device
+//
+// Workspace (h->sortws, zeroed by one memset per preparation):
+//   [0, 16)                 partition counters: depth passes, pair scan, tile passes
+//   depth_hist[dpasses][256], tile_hist[tpasses][64]
+//   depth_status[dpasses][parts(n_total)][256]
+//   scan_status[parts(n_total)]
+//   tile_status[tpasses][parts(cap_pairs)][64]
+struct PrepWs {
+  uint32_t* ctr;
+  uint32_t* dhist;
+  uint32_t* thist;
+  uint32_t* dstat;
+  uint32_t* sstat;
+  uint32_t* tstat;
+  size_t words;
+  size_t tile_off;  // first word of the tile region (counters 8.. are tile passes)
+};
+
+static PrepWs prep_layout(uint32_t* base, int dpasses, int tpasses, uint32_t n_total,
+                          uint32_t cap) {
+  PrepWs w{};
+  size_t o = 0;
+  w.ctr = base + o;
+  o += 16;
+  w.dhist = base + o;
+  o += (size_t)dpasses * 256;
+  w.thist = base + o;
+  o += (size_t)tpasses * (1u << TILE_RB);
+  w.dstat = base + o;
+  o += (size_t)dpasses * os_parts(n_total) * 256;
+  w.sstat = base + o;
+  o += os_parts(n_total);
+  w.tstat = base + o;
+  o += (size_t)tpasses * os_parts(cap) * (1u << TILE_RB);
+  w.words = o;
+  return w;
+}
+
+static int ensure_pair_buffers(sgad_raster* h) {
+  const size_t n = (size_t)h->cap_pairs + 1;
+  SGAD_CHECK_CUDA(h->pkeys0.ensure(sizeof(uint32_t) * n));
+  SGAD_CHECK_CUDA(h->pkeys1.ensure(sizeof(uint32_t) * n));
+  SGAD_CHECK_CUDA(h->pvals0.ensure(sizeof(uint32_t) * n));
+  SGAD_CHECK_CUDA(h->pvals1.ensure(sizeof(uint32_t) * n));
+  return SGAD_OK;
+}
+
+// K1 + K2 + the pair-count scan: independent of the pair capacity
+static int prepare_front(sgad_raster* h, const sgad_frame* frames, int32_t n_frames,
+                         const sgad_camera* cam, int32_t want_coef, cudaStream_t st) {
   SGAD_REQUIRE(h && cam && n_frames >= 0 && (n_frames == 0 || frames), "sgad_raster_prepare: bad args");
   SGAD_REQUIRE(cam->width > 0 && cam->height > 0, "sgad_raster_prepare: empty camera");
-  cudaStream_t st = (cudaStream_t)stream_;
   if (int rc = smem_attrs()) return rc;
   h->prepared = h->forwarded = h->fused_ready = 0;
   h->cam = *cam;
@@ -1474,17 +1473,21 @@ int sgad_raster_prepare(sgad_raster* h, const sgad_frame* frames, int32_t n_fram
   h->have_coef = want_coef != 0;
   h->any_f64 = 0;
   for (int i = 0; i < n_frames; ++i) h->any_f64 |= frames[i].planes_f64 ? 1 : 0;
+  h->kbits = depth_key_bits();
+  h->dpasses = (h->kbits + 7) / 8;
+  h->tpasses = (bits_for((uint32_t)(h->n_tiles > 1 ? h->n_tiles - 1 : 1)) + TILE_RB - 1) / TILE_RB;
+  SGAD_REQUIRE(h->tpasses <= 6, "too many tiles");
+  if (h->cap_pairs == 0) h->cap_pairs = 3 * n_total + 4096;  // grown on overflow
+  SGAD_REQUIRE(h->cap_pairs < (1ll << 30), "too many tile pairs");
   const int64_t nt = h->n_tiles;
   SGAD_CHECK_CUDA(h->ranges.ensure(sizeof(uint2) * nt));
-  SGAD_CHECK_CUDA(cudaMemsetAsync(h->ranges.p, 0, sizeof(uint2) * nt, st));
-  if (n_total == 0) {
-    h->n_surv = h->n_pairs = 0;
-    *n_survivors = *n_pairs = 0;
-    h->prepared = 1;
-    return SGAD_OK;
-  }
-  SGAD_CHECK_CUDA(h->frames.ensure(sizeof(sgad_frame) * n_frames));
   SGAD_CHECK_CUDA(h->counters.ensure(sizeof(uint32_t) * 8));
+  SGAD_CHECK_CUDA(cudaMemsetAsync(h->ranges.p, 0, sizeof(uint2) * nt, st));
+  SGAD_CHECK_CUDA(cudaMemsetAsync(h->counters.p, 0, sizeof(uint32_t) * 8, st));
+  h->prepared = 1;
+  if (n_total == 0) return SGAD_OK;
+  const uint32_t ntot = (uint32_t)n_total;
+  SGAD_CHECK_CUDA(h->frames.ensure(sizeof(sgad_frame) * n_frames));
   SGAD_CHECK_CUDA(h->records.ensure(sizeof(Record) * n_total));
   SGAD_CHECK_CUDA(h->bbox.ensure(sizeof(TileBox) * n_total));
   if (want_coef) SGAD_CHECK_CUDA(h->coef.ensure(sizeof(ChainCoef) * n_total));
@@ -1493,149 +1496,169 @@ int sgad_raster_prepare(sgad_raster* h, const sgad_frame* frames, int32_t n_fram
   SGAD_CHECK_CUDA(h->keys1.ensure(sizeof(unsigned long long) * n_total));
   SGAD_CHECK_CUDA(h->vals0.ensure(sizeof(uint32_t) * n_total));
   SGAD_CHECK_CUDA(h->vals1.ensure(sizeof(uint32_t) * n_total));
+  SGAD_CHECK_CUDA(h->k32a.ensure(sizeof(uint32_t) * n_total));
+  SGAD_CHECK_CUDA(h->k32b.ensure(sizeof(uint32_t) * n_total));
+  SGAD_CHECK_CUDA(h->runs.ensure(sizeof(uint2) * (n_total / 65 + 1)));
+  SGAD_CHECK_CUDA(h->poffset.ensure(sizeof(uint32_t) * (n_total + 1)));
+  if (int rc = ensure_pair_buffers(h)) return rc;
+  PrepWs w = prep_layout(nullptr, h->dpasses, h->tpasses, ntot, (uint32_t)h->cap_pairs);
+  SGAD_CHECK_CUDA(h->sortws.ensure(sizeof(uint32_t) * w.words));
+  w = prep_layout(h->sortws.as<uint32_t>(), h->dpasses, h->tpasses, ntot, (uint32_t)h->cap_pairs);
+  SGAD_CHECK_CUDA(cudaMemsetAsync(w.ctr, 0, sizeof(uint32_t) * w.words, st));
   SGAD_CHECK_CUDA(cudaMemcpyAsync(h->frames.p, frames, sizeof(sgad_frame) * n_frames,
                                   cudaMemcpyHostToDevice, st));
-  SGAD_CHECK_CUDA(cudaMemsetAsync(h->counters.p, 0, sizeof(uint32_t) * 8, st));
   SGAD_CHECK_CUDA(h->zrange.ensure(sizeof(unsigned long long) * 2));
   SGAD_CHECK_CUDA(cudaMemsetAsync(h->zrange.p, 0xff, sizeof(unsigned long long), st));
   SGAD_CHECK_CUDA(cudaMemsetAsync(h->zrange.as<unsigned long long>() + 1, 0, sizeof(unsigned long long), st));
+  uint32_t* cnt = h->counters.as<uint32_t>();
+  const unsigned long long* zkeys = h->keys0.as<unsigned long long>();
+  const unsigned long long* zr = h->zrange.as<unsigned long long>();
+  // K1
   const dim3 pgrid((unsigned)((max_hw + PROJ_THREADS - 1) / PROJ_THREADS), (unsigned)n_frames);
   k_project<<<pgrid, PROJ_THREADS, 0, st>>>(
       h->frames.as<sgad_frame>(), *cam, h->ntx, h->nty, want_coef, h->records.as<Record>(),
       h->bbox.as<TileBox>(), h->coef.as<ChainCoef>(), h->any_f64 ? h->col64.as<double>() : nullptr,
-      h->keys0.as<unsigned long long>(), h->counters.as<uint32_t>(),
-      h->zrange.as<unsigned long long>());
+      h->keys0.as<unsigned long long>(), cnt, h->zrange.as<unsigned long long>());
   SGAD_LAUNCH_CHECK();
-  SGAD_CHECK_CUDA(cudaMemcpyAsync(h->pinned, h->counters.as<uint32_t>() + 1, sizeof(uint32_t),
-                                  cudaMemcpyDeviceToHost, st));
-  SGAD_CHECK_CUDA(cudaMemcpyAsync(h->pinned + 4, h->zrange.p, 2 * sizeof(unsigned long long),
-                                  cudaMemcpyDeviceToHost, st));
-  SGAD_CHECK_CUDA(cudaStreamSynchronize(st));
-  const uint32_t ns = h->pinned[0];
-  h->n_surv = ns;
-  *n_survivors = ns;
-  if (ns == 0) {
-    h->n_pairs = 0;
-    *n_pairs = 0;
-    h->prepared = 1;
-    return SGAD_OK;
+  // K2: digit histograms, onesweep passes (the permutation lands in vals0
+  // and the sorted buckets in k32a), run fix-up
+  const unsigned hist_grid = (unsigned)std::min<int64_t>(148 * 8, (n_total + 255) / 256);
+  switch (h->dpasses) {
+    case 2: k_depth_hist<2><<<hist_grid, 256, 0, st>>>(zkeys, ntot, zr, h->kbits, w.dhist); break;
+    case 3: k_depth_hist<3><<<hist_grid, 256, 0, st>>>(zkeys, ntot, zr, h->kbits, w.dhist); break;
+    default: k_depth_hist<4><<<hist_grid, 256, 0, st>>>(zkeys, ntot, zr, h->kbits, w.dhist); break;
   }
-  // K2: depth order.  Stable sort of 24-bit monotone depth buckets, then the
-  // (rare, short) runs of equal buckets are ordered by exact (z, emission
-  // index) -- together the (z, frame, pixel) order of np.lexsort.
+  SGAD_LAUNCH_CHECK();
+  const unsigned dparts = os_parts(ntot);
+  uint32_t* kb[2] = {h->k32a.as<uint32_t>(), h->k32b.as<uint32_t>()};
+  uint32_t* vb[2] = {h->vals0.as<uint32_t>(), h->vals1.as<uint32_t>()};
+  int cur = (h->dpasses & 1) ? 0 : 1;  // the last pass writes buffer 0
+  for (int pss = 0; pss < h->dpasses; ++pss) {
+    uint32_t* st_p = w.dstat + (size_t)pss * dparts * 256;
+    if (pss == 0) {
+      k_onesweep<8, 1><<<dparts, OS_THREADS, 0, st>>>(
+          nullptr, nullptr, zkeys, zr, h->kbits, ntot, nullptr, kb[cur], vb[cur], w.dhist,
+          st_p, w.ctr + pss, 0);
+    } else {
+      k_onesweep<8, 0><<<dparts, OS_THREADS, 0, st>>>(
+          kb[cur ^ 1], vb[cur ^ 1], nullptr, nullptr, h->kbits, ntot, cnt + C_NSURV, kb[cur],
+          vb[cur], w.dhist + 256 * pss, st_p, w.ctr + pss, 8 * pss);
+    }
+    SGAD_LAUNCH_CHECK();
+    cur ^= 1;
+  }
   uint32_t* perm = h->vals0.as<uint32_t>();
-  {
-    unsigned long long zb[2];
-    memcpy(zb, h->pinned + 4, sizeof zb);
-    double zmin, zmax;
-    memcpy(&zmin, &zb[0], 8);
-    memcpy(&zmax, &zb[1], 8);
-    const int kbits = depth_key_bits();
-    const double ktop = (double)(uint32_t)((kbits == 32 ? 0u : (1u << kbits)) - 2u);
-    const double scale = zmax > zmin ? ktop / (zmax - zmin) : 0.0;
-    // the permutation lands in vals0 after an even number of 8-bit passes if
-    // it starts there, after an odd number if it starts in vals1
-    const bool odd = ((kbits + 7) / 8) & 1;
-    uint32_t* v_first = odd ? h->vals1.as<uint32_t>() : h->vals0.as<uint32_t>();
-    uint32_t* v_second = odd ? h->vals0.as<uint32_t>() : h->vals1.as<uint32_t>();
-    const uint32_t nt = (uint32_t)n_total;  // culled ids carry the sentinel key
-    SGAD_CHECK_CUDA(h->k32a.ensure(sizeof(uint32_t) * nt));
-    SGAD_CHECK_CUDA(h->k32b.ensure(sizeof(uint32_t) * nt));
-    k_depth_key32<<<blocks_for(nt, 256), 256, 0, st>>>(h->keys0.as<unsigned long long>(), nt, zmin,
-                                                       scale, ktop, h->k32a.as<uint32_t>(),
-                                                       v_first);
-    SGAD_LAUNCH_CHECK();
-    cub::DoubleBuffer<uint32_t> dk(h->k32a.as<uint32_t>(), h->k32b.as<uint32_t>());
-    cub::DoubleBuffer<uint32_t> dv(v_first, v_second);
-    size_t tmp = 0;
-    SGAD_CHECK_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, dk, dv, (int)nt, 0, kbits, st));
-    SGAD_CHECK_CUDA(h->cub_tmp.ensure(tmp));
-    SGAD_CHECK_CUDA(cub::DeviceRadixSort::SortPairs(h->cub_tmp.p, tmp, dk, dv, (int)nt, 0, kbits,
-                                                    st));
-    if (dv.Current() != perm)
-      SGAD_CHECK_CUDA(cudaMemcpyAsync(perm, dv.Current(), sizeof(uint32_t) * ns,
-                                      cudaMemcpyDeviceToDevice, st));
-    SGAD_CHECK_CUDA(h->runs.ensure(sizeof(uint2) * (ns / 65 + 1)));
-    k_depth_fixup<<<blocks_for(ns, 256), 256, 0, st>>>(dk.Current(), ns,
-                                                       h->keys0.as<unsigned long long>(), perm,
-                                                       h->counters.as<uint32_t>() + 2,
-                                                       h->counters.as<uint32_t>() + 3,
-                                                       h->runs.as<uint2>());
-    SGAD_LAUNCH_CHECK();
-    k_long_runs<<<148, 1024, LONG_RUN_SMEM, st>>>(h->runs.as<uint2>(),
-                                                  h->counters.as<uint32_t>() + 3,
-                                                  h->keys0.as<unsigned long long>(), perm);
-    SGAD_LAUNCH_CHECK();
-  }
-  size_t tmp = 0;
-  // K3: per-survivor tile counts in depth order, exclusive scan, emit, stable tile sort
-  SGAD_CHECK_CUDA(h->poffset.ensure(sizeof(uint32_t) * (ns + 1)));
-  const auto pair_counts = thrust::make_transform_iterator(
-      thrust::counting_iterator<uint32_t>(0u), TilePairCount{perm, h->bbox.as<TileBox>(), ns});
-  auto scan_counts = [&]() -> int {
-    size_t t2 = 0;
-    SGAD_CHECK_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, t2, pair_counts,
-                                                  h->poffset.as<uint32_t>(), (int)ns + 1, st));
-    SGAD_CHECK_CUDA(h->cub_tmp.ensure(t2));
-    SGAD_CHECK_CUDA(cub::DeviceScan::ExclusiveSum(h->cub_tmp.p, t2, pair_counts,
-                                                  h->poffset.as<uint32_t>(), (int)ns + 1, st));
-    return SGAD_OK;
-  };
-  if (int rc = scan_counts()) return rc;
-  SGAD_CHECK_CUDA(cudaMemcpyAsync(h->pinned + 1, h->poffset.as<uint32_t>() + ns, sizeof(uint32_t),
-                                  cudaMemcpyDeviceToHost, st));
-  SGAD_CHECK_CUDA(cudaMemcpyAsync(h->pinned + 2, h->counters.as<uint32_t>() + 2, sizeof(uint32_t),
-                                  cudaMemcpyDeviceToHost, st));
-  SGAD_CHECK_CUDA(cudaStreamSynchronize(st));
-  if (h->pinned[2]) {
-    // a long run of equal depth buckets (e.g. a fronto-parallel plane seen
-    // head-on): fall back to the stable sort of the full 63-bit depth key
-    const uint32_t nt = (uint32_t)n_total;
-    k_iota<<<blocks_for(nt, 256), 256, 0, st>>>(h->vals1.as<uint32_t>(), nt);
-    SGAD_LAUNCH_CHECK();
-    cub::DoubleBuffer<unsigned long long> dk(h->keys0.as<unsigned long long>(),
-                                             h->keys1.as<unsigned long long>());
-    cub::DoubleBuffer<uint32_t> dv(h->vals1.as<uint32_t>(), h->vals0.as<uint32_t>());
-    tmp = 0;
-    SGAD_CHECK_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, dk, dv, (int)nt, 0, 64, st));
-    SGAD_CHECK_CUDA(h->cub_tmp.ensure(tmp));
-    SGAD_CHECK_CUDA(cub::DeviceRadixSort::SortPairs(h->cub_tmp.p, tmp, dk, dv, (int)nt, 0, 64, st));
-    if (dv.Current() != perm)
-      SGAD_CHECK_CUDA(cudaMemcpyAsync(perm, dv.Current(), sizeof(uint32_t) * ns,
-                                      cudaMemcpyDeviceToDevice, st));
-    if (int rc = scan_counts()) return rc;
-    SGAD_CHECK_CUDA(cudaMemcpyAsync(h->pinned + 1, h->poffset.as<uint32_t>() + ns,
-                                    sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
-    SGAD_CHECK_CUDA(cudaStreamSynchronize(st));
-  }
-  const uint32_t np_ = h->pinned[1];
-  h->n_pairs = np_;
-  *n_pairs = np_;
-  SGAD_CHECK_CUDA(h->pkeys0.ensure(sizeof(uint32_t) * (np_ + 1)));
-  SGAD_CHECK_CUDA(h->pkeys1.ensure(sizeof(uint32_t) * (np_ + 1)));
-  SGAD_CHECK_CUDA(h->pvals0.ensure(sizeof(uint32_t) * (np_ + 1)));
-  SGAD_CHECK_CUDA(h->pvals1.ensure(sizeof(uint32_t) * (np_ + 1)));
-  k_tile_emit<<<blocks_for(ns, 256), 256, 0, st>>>(perm, h->bbox.as<TileBox>(),
-                                                   h->poffset.as<uint32_t>(), ns, h->ntx, h->packed,
-                                                   h->pkeys0.as<uint32_t>(), h->pvals0.as<uint32_t>());
+  k_depth_fixup<<<blocks_for(n_total, 256), 256, 0, st>>>(
+      h->k32a.as<uint32_t>(), cnt + C_NSURV, zkeys, perm, cnt + C_NLONG, h->runs.as<uint2>());
   SGAD_LAUNCH_CHECK();
-  cub::DoubleBuffer<uint32_t> pk(h->pkeys0.as<uint32_t>(), h->pkeys1.as<uint32_t>());
-  cub::DoubleBuffer<uint32_t> pv(h->pvals0.as<uint32_t>(), h->pvals1.as<uint32_t>());
-  const int tbits = bits_for((uint32_t)(h->n_tiles - 1));
-  tmp = 0;
-  SGAD_CHECK_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, pk, pv, (int)np_, 0, tbits, st));
-  SGAD_CHECK_CUDA(h->cub_tmp.ensure(tmp));
-  SGAD_CHECK_CUDA(cub::DeviceRadixSort::SortPairs(h->cub_tmp.p, tmp, pk, pv, (int)np_, 0, tbits, st));
-  if (pk.Current() != h->pkeys0.as<uint32_t>()) {
-    SGAD_CHECK_CUDA(cudaMemcpyAsync(h->pkeys0.p, pk.Current(), sizeof(uint32_t) * np_,
-                                    cudaMemcpyDeviceToDevice, st));
-    SGAD_CHECK_CUDA(cudaMemcpyAsync(h->pvals0.p, pv.Current(), sizeof(uint32_t) * np_,
-                                    cudaMemcpyDeviceToDevice, st));
-  }
-  k_tile_ranges<<<blocks_for(np_, 256), 256, 0, st>>>(h->pkeys0.as<uint32_t>(), np_,
-                                                      h->ranges.as<uint2>());
+  k_long_runs<<<148, 1024, LONG_RUN_SMEM, st>>>(h->runs.as<uint2>(), cnt + C_NLONG, zkeys, perm,
+                                                h->keys1.as<unsigned long long>(),
+                                                h->vals1.as<uint32_t>());
   SGAD_LAUNCH_CHECK();
-  h->prepared = 1;
+  // K3a: pair counts in depth order, exclusive scan -> offsets, total pairs
+  k_pair_scan<TileBox><<<dparts, OS_THREADS, 0, st>>>(perm, h->bbox.as<TileBox>(), cnt + C_NSURV,
+                                                      ntot, h->poffset.as<uint32_t>(), w.sstat,
+                                                      w.ctr + 8, cnt + C_NPAIRS);
+  SGAD_LAUNCH_CHECK();
+  return SGAD_OK;
+}
+
+// K3b: emit (tile, value) pairs, stable tile sort, per-tile ranges.  The
+// tile-pass counters / histograms / status are zeroed here (a retry after
+// an overflow re-runs only this part).
+static int prepare_pairs(sgad_raster* h, int32_t* ext_flag, cudaStream_t st) {
+  if (h->n_total == 0) return SGAD_OK;
+  const uint32_t ntot = (uint32_t)h->n_total, cap = (uint32_t)h->cap_pairs;
+  if (int rc = ensure_pair_buffers(h)) return rc;
+  PrepWs w = prep_layout(nullptr, h->dpasses, h->tpasses, ntot, cap);
+  SGAD_CHECK_CUDA(h->sortws.ensure(sizeof(uint32_t) * w.words));
+  w = prep_layout(h->sortws.as<uint32_t>(), h->dpasses, h->tpasses, ntot, cap);
+  uint32_t* cnt = h->counters.as<uint32_t>();
+  SGAD_CHECK_CUDA(cudaMemsetAsync(w.ctr + 9, 0, sizeof(uint32_t) * 7, st));
+  SGAD_CHECK_CUDA(cudaMemsetAsync(w.thist, 0, sizeof(uint32_t) * h->tpasses * (1u << TILE_RB), st));
+  SGAD_CHECK_CUDA(cudaMemsetAsync(w.tstat, 0,
+                                  sizeof(uint32_t) * h->tpasses * os_parts(cap) * (1u << TILE_RB), st));
+  SGAD_CHECK_CUDA(cudaMemsetAsync(h->ranges.p, 0, sizeof(uint2) * h->n_tiles, st));
+  SGAD_CHECK_CUDA(cudaMemsetAsync(cnt + C_OVERFLOW, 0, sizeof(uint32_t), st));
+  uint32_t* kb[2] = {h->pkeys0.as<uint32_t>(), h->pkeys1.as<uint32_t>()};
+  uint32_t* vb[2] = {h->pvals0.as<uint32_t>(), h->pvals1.as<uint32_t>()};
+  int cur = (h->tpasses & 1) ? 1 : 0;  // emit here; the last pass lands in buffer 0
+  const uint32_t* perm = h->vals0.as<uint32_t>();
+#define SGAD_EMIT(TP)                                                                           \
+  k_tile_emit<TP><<<blocks_for(h->n_total, 256), 256, 0, st>>>(                                  \
+      perm, h->bbox.as<TileBox>(), h->poffset.as<uint32_t>(), cnt + C_NSURV, h->ntx, h->packed, \
+      cap, kb[cur], vb[cur], w.thist, cnt + C_OVERFLOW, ext_flag)
+  switch (h->tpasses) {
+    case 1: SGAD_EMIT(1); break;
+    case 2: SGAD_EMIT(2); break;
+    case 3: SGAD_EMIT(3); break;
+    case 4: SGAD_EMIT(4); break;
+    case 5: SGAD_EMIT(5); break;
+    default: SGAD_EMIT(6); break;
+  }
+#undef SGAD_EMIT
+  SGAD_LAUNCH_CHECK();
+  const unsigned tparts = os_parts(cap);
+  for (int pss = 0; pss < h->tpasses; ++pss) {
+    k_onesweep<TILE_RB, 0><<<tparts, OS_THREADS, 0, st>>>(
+        kb[cur], vb[cur], nullptr, nullptr, 0, cap, cnt + C_NPAIRS, kb[cur ^ 1], vb[cur ^ 1],
+        w.thist + (1u << TILE_RB) * pss, w.tstat + (size_t)pss * tparts * (1u << TILE_RB),
+        w.ctr + 9 + pss, TILE_RB * pss);
+    SGAD_LAUNCH_CHECK();
+    cur ^= 1;
+  }
+  k_tile_ranges<<<blocks_for(h->cap_pairs, 256), 256, 0, st>>>(kb[0], cnt + C_NPAIRS, cap,
+                                                               h->ranges.as<uint2>());
+  SGAD_LAUNCH_CHECK();
+  return SGAD_OK;
+}
+
+int sgad_raster_prepare(sgad_raster* h, const sgad_frame* frames, int32_t n_frames,
+                        const sgad_camera* cam, int32_t want_coef, void* stream_,
+                        int64_t* n_survivors, int64_t* n_pairs) {
+  cudaStream_t st = (cudaStream_t)stream_;
+  if (int rc = prepare_front(h, frames, n_frames, cam, want_coef, st)) return rc;
+  if (int rc = prepare_pairs(h, nullptr, st)) return rc;
+  h->n_surv = h->n_pairs = 0;
+  if (h->n_total > 0) {
+    for (int attempt = 0; attempt < 2; ++attempt) {
+      SGAD_CHECK_CUDA(cudaMemcpyAsync(h->pinned, h->counters.p, sizeof(uint32_t) * 8,
+                                      cudaMemcpyDeviceToHost, st));
+      SGAD_CHECK_CUDA(cudaStreamSynchronize(st));
+      h->n_surv = h->pinned[C_NSURV];
+      h->n_pairs = h->pinned[C_NPAIRS];
+      if (h->n_pairs <= h->cap_pairs) break;
+      SGAD_REQUIRE(attempt == 0, "sgad_raster_prepare: pair capacity");
+      h->cap_pairs = h->n_pairs + h->n_pairs / 4 + 4096;  // grow and bin again
+      SGAD_REQUIRE(h->cap_pairs < (1ll << 30), "too many tile pairs (%lld)", (long long)h->n_pairs);
+      if (int rc = prepare_pairs(h, nullptr, st)) return rc;
+    }
+  }
+  if (n_survivors) *n_survivors = h->n_surv;
+  if (n_pairs) *n_pairs = h->n_pairs;
+  return SGAD_OK;
+}
+
+int sgad_raster_prepare_async(sgad_raster* h, const sgad_frame* frames, int32_t n_frames,
+                              const sgad_camera* cam, int32_t want_coef, uint32_t* counts_out,
+                              int32_t* overflow_flag, void* stream_) {
+  cudaStream_t st = (cudaStream_t)stream_;
+  if (int rc = prepare_front(h, frames, n_frames, cam, want_coef, st)) return rc;
+  if (int rc = prepare_pairs(h, overflow_flag, st)) return rc;
+  h->n_surv = h->n_pairs = -1;
+  if (counts_out) {
+    SGAD_CHECK_CUDA(cudaMemcpyAsync(counts_out, h->counters.as<uint32_t>() + C_NSURV,
+                                    sizeof(uint32_t), cudaMemcpyDeviceToDevice, st));
+    SGAD_CHECK_CUDA(cudaMemcpyAsync(counts_out + 1, h->counters.as<uint32_t>() + C_NPAIRS,
+                                    sizeof(uint32_t), cudaMemcpyDeviceToDevice, st));
+  }
+  return SGAD_OK;
+}
+
+int sgad_raster_reserve(sgad_raster* h, int64_t pair_capacity) {
+  SGAD_REQUIRE(h && pair_capacity >= 0 && pair_capacity < (1ll << 30),
+               "sgad_raster_reserve: bad capacity");
+  if (pair_capacity > h->cap_pairs) h->cap_pairs = pair_capacity;
   return SGAD_OK;
 }
 
@@ -1734,6 +1757,7 @@ int sgad_raster_backward(sgad_raster* h, int32_t mode, const double* g_color,
   }
   SGAD_REQUIRE(mode == 0 && g_color && g_depth && g_alpha && map_grads,
                "exact backward needs upstream images and map_grads");
+  SGAD_REQUIRE(h->n_surv >= 0, "exact backward needs a synchronous sgad_raster_prepare");
   const int n_frames = (int)h->host_frames.size();
   SGAD_CHECK_CUDA(h->raw_grads.ensure(sizeof(double) * 8 * h->n_total));
   SGAD_CHECK_CUDA(cudaMemsetAsync(h->raw_grads.p, 0, sizeof(double) * 8 * h->n_total, st));
@@ -1783,7 +1807,8 @@ int sgad_raster_forward_backward(sgad_raster* h, const sgad_loss_target* target,
 
 int sgad_raster_get_survivors(sgad_raster* h, int64_t* gid, double* u0, double* v0, double* z,
                               double* sigma, double* opacity, void* stream_) {
-  SGAD_REQUIRE(h && h->prepared, "sgad_raster_get_survivors: view not prepared");
+  SGAD_REQUIRE(h && h->prepared && h->n_surv >= 0,
+               "sgad_raster_get_survivors: view not prepared (synchronously)");
   if (h->n_surv == 0) return SGAD_OK;
   k_export_surv<<<blocks_for(h->n_surv, 256), 256, 0, (cudaStream_t)stream_>>>(
       h->vals0.as<uint32_t>(), h->records.as<Record>(), (uint32_t)h->n_surv, gid, u0, v0, z,
@@ -1793,7 +1818,8 @@ int sgad_raster_get_survivors(sgad_raster* h, int64_t* gid, double* u0, double* 
 }
 
 int sgad_raster_get_tiles(sgad_raster* h, int64_t* ranges, int64_t* lists, void* stream_) {
-  SGAD_REQUIRE(h && h->prepared, "sgad_raster_get_tiles: view not prepared");
+  SGAD_REQUIRE(h && h->prepared && h->n_surv >= 0,
+               "sgad_raster_get_tiles: view not prepared (synchronously)");
   cudaStream_t st = (cudaStream_t)stream_;
   if (ranges) {
     k_export_ranges<<<blocks_for(h->n_tiles, 256), 256, 0, st>>>(h->ranges.as<uint2>(),

@@ -66,12 +66,12 @@ class LossBreakdown:
     depth_l1: float
 
 
-def _adam(params, grads, m, v, n_frames, hw, cfg: MapperConfig, t: int, f64: bool):
+def _adam(params, grads, m, v, n_frames, hw, cfg: MapperConfig, t: int, f64: bool, skip=None):
     lr = (ctypes.c_double * 6)(*cfg.lrs())
     b1, b2 = cfg.adam_beta1, cfg.adam_beta2
     N.call("sgad_adam_step", params.data_ptr(), grads.data_ptr(), m.data_ptr(), v.data_ptr(),
            int(n_frames), int(hw), lr, b1, b2, cfg.adam_eps, 1.0 - b1**t, 1.0 - b2**t,
-           0 if cfg.offset_frozen else 1, 1 if f64 else 0, N.stream_ptr())
+           0 if cfg.offset_frozen else 1, 1 if f64 else 0, N.ptr(skip), N.stream_ptr())
 
 
 class MapOptimizer:
@@ -342,7 +342,15 @@ class WindowMapper:
         learn = set(range(f))
         self._frames = {v: build_frames(self.maps, self.poses[v], learn)[0] for v in self.views}
         self.raster = get_raster(dev)
-        self.last_counts = {}
+        # asynchronous preparation: per-view (survivors, pairs) on the device,
+        # a per-step pair-capacity overflow flag (Adam skips a step that
+        # overflowed; the host notices a step later, grows the capacity and
+        # rolls the step counter back), the handles' pair capacity
+        self._counts = torch.zeros((f, 2), dtype=torch.int32, device=dev)
+        self._flag = torch.zeros(1, dtype=torch.int32, device=dev)
+        self._cap = 0
+        self._pending = []
+        self.overflows = 0
         self.pipelined = True   # prepare view i+1 while view i composites
         self.adam_enabled = True
         # tau = 0: forward + loss + backward as one kernel (measured no faster
@@ -389,7 +397,7 @@ class WindowMapper:
         """Fused forward (+ loss) and backward of one view into self.grad."""
         r = raster or self.raster
         ns, npairs = r.prepare(self._frames[v], self.cam, want_coef=True, stream=stream)
-        self.last_counts[v] = (ns, npairs)
+        self._counts[v, 0], self._counts[v, 1] = ns, npairs
         if ns:
             self._composite(r, v, stream)
 
@@ -421,30 +429,79 @@ class WindowMapper:
             if used[i % 2] is not None:
                 prep.wait_event(used[i % 2])
             p0 = mark(prep)
-            ns, npairs = r.prepare(self._frames[v], self.cam, want_coef=True, stream=prep)
-            self.last_counts[v] = (ns, npairs)
+            r.prepare_async(self._frames[v], self.cam, want_coef=True, counts=self._counts[v],
+                            overflow=self._flag, stream=prep)
             p1 = mark(prep)
             main.wait_event(p1)
             if target_ready is not None and v in target_ready:
                 main.wait_event(target_ready[v])
-            if ns:
-                f0 = mark(main)
-                f1 = self._composite(r, v, main, marks=lambda: mark(main))
-                b1 = mark(main)
-                if timing is not None:
-                    timing.append(("prep", p0, p1, v, ns, npairs))
-                    if f1 is None:  # one fused kernel
-                        timing.append(("fb", f0, b1, v, ns, npairs))
-                    else:
-                        timing += [("fwd", f0, f1, v, ns, npairs), ("bwd", f1, b1, v, ns, npairs)]
+            f0 = mark(main)
+            f1 = self._composite(r, v, main, marks=lambda: mark(main))
+            b1 = mark(main)
+            if timing is not None:
+                timing.append(("prep", p0, p1, v))
+                if f1 is None:  # one fused kernel
+                    timing.append(("fb", f0, b1, v))
+                else:
+                    timing += [("fwd", f0, f1, v), ("bwd", f1, b1, v)]
             used[i % 2] = mark(main)
+
+    def _size_handles(self):
+        """Pair capacity of the pipelined raster handles: every view prepared
+        once synchronously, capacity = 1.3 x the largest pair count."""
+        if self._pipe is None:
+            self._pipe = ([Raster(self.dev), Raster(self.dev)], torch.cuda.Stream(self.dev))
+        r = self._pipe[0][0]
+        most = 0
+        for v in self.views:
+            ns, npairs = r.prepare(self._frames[v], self.cam, want_coef=True)
+            self._counts[v, 0], self._counts[v, 1] = ns, npairs
+            most = max(most, npairs)
+        self._cap = max(self._cap, int(most * 1.3) + 4096)
+        for h in self._pipe[0]:
+            h.reserve(self._cap)
+
+    def _check_overflow(self, block: bool) -> bool:
+        """Process the overflow flags of finished steps (all of them with
+        ``block``): a step that overflowed skipped its Adam update (its step
+        count is rolled back) and the capacity grows.  True if any did."""
+        hit = False
+        while self._pending:
+            ev, host, adam = self._pending[0]
+            if block:
+                ev.synchronize()
+            elif not ev.query():
+                break
+            self._pending.pop(0)
+            if int(host[0]):
+                hit = True
+                self.overflows += 1
+                if adam:
+                    self.t -= 1
+        if hit:
+            torch.cuda.synchronize(self.dev)
+            self._cap = int(self._cap * 1.5)
+            self._size_handles()
+        return hit
+
+    def counts(self):
+        """{view: (survivors, tile pairs)} of the last step (synchronises)."""
+        c = self._counts.cpu().numpy()
+        return {v: (int(c[v, 0]), int(c[v, 1])) for v in self.views}
 
     def step(self, sync_loss=False, timing=None, target_ready=None):
         """One window iteration: every assigned view fwd+bwd, gradient
         all-reduce across ranks, Adam.  Returns the summed loss (a device
         scalar unless ``sync_loss``).  ``target_ready`` ({view: CUDA event},
         optional): a view composites only after its event."""
+        with torch.cuda.device(self.dev):
+            if self.pipelined:
+                self._check_overflow(block=False)
+                if self._cap == 0:
+                    self._size_handles()
         self.loss_acc.zero_()
+        self._flag.zero_()
+        adam = self.adam_enabled
         with torch.cuda.device(self.dev):
             if self.pipelined:
                 self._render_pipelined(timing, target_ready)
@@ -458,7 +515,7 @@ class WindowMapper:
                     ev[0].record(main)
                     r = self.raster
                     ns, npairs = r.prepare(self._frames[v], self.cam, want_coef=True)
-                    self.last_counts[v] = (ns, npairs)
+                    self._counts[v, 0], self._counts[v, 1] = ns, npairs
                     ev[1].record(main)
                     if ns:
                         split = []
@@ -466,20 +523,23 @@ class WindowMapper:
                                         marks=lambda: (ev[2].record(main), split.append(1)))
                         ev[3].record(main)
                         if timing is not None:
-                            timing.append(("prep", ev[0], ev[1], v, ns, npairs))
+                            timing.append(("prep", ev[0], ev[1], v))
                             if split:
-                                timing += [("fwd", ev[1], ev[2], v, ns, npairs),
-                                           ("bwd", ev[2], ev[3], v, ns, npairs)]
+                                timing += [("fwd", ev[1], ev[2], v), ("bwd", ev[2], ev[3], v)]
                             else:
-                                timing.append(("fb", ev[1], ev[3], v, ns, npairs))
+                                timing.append(("fb", ev[1], ev[3], v))
             if self.adam_enabled and self._sharded():
                 self._sharded_update()
             else:
                 allreduce_window(self.grad, self.loss_acc, self.pg)
                 if self.adam_enabled:  # (tests inspect the reduced gradient with it off)
-                    self.t += 1
-                    _adam(self.planes, self.grad, self.m, self.v, self.F, self.HW, self.cfg,
-                          self.t, False)
+                    self.apply_adam()
+            if self.pipelined:
+                host = torch.empty(1, dtype=torch.int32).pin_memory()
+                host.copy_(self._flag, non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record()
+                self._pending.append((ev, host, adam))
         n_color = 3.0 * self.HW
         nd = torch.tensor([max(n, 1) for n in self.n_depth], dtype=torch.float64, device=self.dev)
         has_d = torch.tensor([n > 0 for n in self.n_depth], device=self.dev)
@@ -487,7 +547,20 @@ class WindowMapper:
         loss = (self.cfg.rho * self.loss_acc[:, 0] / n_color + self.cfg.tau * ssim_term +
                 self.cfg.sigma * torch.where(has_d, self.loss_acc[:, 1] / nd,
                                              torch.zeros_like(nd))).sum()
-        return float(loss) if sync_loss else loss
+        if sync_loss:
+            val = float(loss)
+            if self.pipelined and self._check_overflow(block=True):
+                return self.step(sync_loss=True, timing=timing, target_ready=target_ready)
+            return val
+        return loss
+
+    def apply_adam(self):
+        """One Adam step of the whole window from the (reduced) gradient
+        buffer, which it consumes (zeroes)."""
+        with torch.cuda.device(self.dev):
+            self.t += 1
+            _adam(self.planes, self.grad, self.m, self.v, self.F, self.HW, self.cfg, self.t, False,
+                  skip=self._flag)
 
     def _sharded(self) -> bool:
         dist = torch.distributed
@@ -511,7 +584,7 @@ class WindowMapper:
         self.grad.zero_()  # this step's contributions are all in the scattered blocks
         self.t += 1
         _adam(self.planes[f0:f1], local, self.m[f0:f1], self.v[f0:f1], f1 - f0, self.HW,
-              self.cfg, self.t, False)
+              self.cfg, self.t, False, skip=self._flag)
         allgather_planes(self.planes, stage, f0, f1, self.pg)
 
     def grads_numpy(self):

@@ -90,6 +90,21 @@ class Raster:
         self.n_surv, self.n_pairs = ns.value, npairs.value
         return self.n_surv, self.n_pairs
 
+    def prepare_async(self, frames, cam, want_coef=False, counts=None, overflow=None, stream=None):
+        """The preparation without host synchronisation: ``counts`` (device
+        int32[2], optional) receives (survivors, pairs); ``overflow`` (device
+        int32[1], optional) is set to 1 if the view has more tile pairs than
+        the reserved capacity (its results are then invalid)."""
+        self._frames = frames
+        N.check(N.load().sgad_raster_prepare_async(self.h, frames, len(frames), ctypes.byref(cam),
+                                                   int(want_coef), N.ptr(counts), N.ptr(overflow),
+                                                   N.stream_ptr(stream)))
+        self.cam = cam
+        self.n_surv = self.n_pairs = -1
+
+    def reserve(self, pair_capacity: int):
+        N.check(N.load().sgad_raster_reserve(self.h, int(pair_capacity)))
+
     def forward(self, color=None, depth=None, alpha=None, count=None, save_state=False,
                 target=None, stream=None):
         tgt = ctypes.byref(target) if target is not None else None

@@ -21,4 +21,4 @@ torch.cuda.profiler.start()
 wm.step()
 torch.cuda.synchronize()
 torch.cuda.profiler.stop()
-print("step ok", wm.last_counts)
+print("step ok", wm.counts())
