@@ -105,7 +105,7 @@ int sgad_raster_prepare(sgad_raster* h, const sgad_frame* frames, int32_t n_fram
  * capturable in a CUDA graph): element counts stay on the device.
  * counts_out (device uint32[2], may be NULL) receives (survivors, pairs);
  * if the view has more tile pairs than the handle's capacity (see
- * sgad_raster_reserve; first use: 3 x Gaussians) the extra pairs are
+ * sgad_raster_reserve; at least 2 x Gaussians) the extra pairs are
  * dropped and *overflow_flag (device int32, may be NULL) is set to 1 --
  * the caller discards the view's results, reserves more and prepares again.
  * Replaces the same reference functions as sgad_raster_prepare. */

@@ -12,7 +12,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libsgad.so")
 SOURCES = ["raster.cu", "adam.cu", "track.cu", "ssim.cu", "voxels.cu", "inpaint.cu", "irls.cu"]
-HEADERS = ["common.cuh"]
+HEADERS = ["common.cuh", "sort.cuh"]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",

@@ -34,10 +34,15 @@ extern std::atomic<long long> g_launches;
     }                                    \
   } while (0)
 
+// SGAD_DEBUG_SYNC=1 (debugging): synchronise after every launch so a fault is
+// reported at the kernel that caused it
+extern int g_debug_sync;
+
 #define SGAD_LAUNCH_CHECK()                                                                 \
   do {                                                                                      \
     ::sgad::g_launches.fetch_add(1, std::memory_order_relaxed);                             \
     cudaError_t e_ = cudaGetLastError();                                                    \
+    if (e_ == cudaSuccess && ::sgad::g_debug_sync) e_ = cudaDeviceSynchronize();            \
     if (e_ != cudaSuccess) {                                                                \
       ::sgad::set_error("%s:%d launch: %s", __FILE__, __LINE__, cudaGetErrorString(e_));    \
       return SGAD_E_CUDA;                                                                   \

@@ -66,7 +66,7 @@ constexpr int RASTER_THREADS = 256;
 
 struct sgad_raster {
   sgad::DevBuf frames, counters, records, coef, keys0, keys1, vals0, vals1;
-  sgad::DevBuf poffset, pkeys0, pkeys1, pvals0, pvals1, ranges, sortws;
+  sgad::DevBuf pkeys0, pkeys1, pvals0, pvals1, ranges, sortws, pairws;
   sgad::DevBuf trans_final, last_idx, signs, raw_grads, rank_of, scratch, col64, zrange, k32a, k32b, bbox, runs, raw32, cl_e, cl_m, cl_n;
   int any_f64 = 0;
   std::vector<sgad_frame> host_frames;
@@ -98,6 +98,10 @@ static int g_late_chain = [] {
   return e && e[0] == '0' ? 0 : 1;
 }();
 std::atomic<long long> g_launches{0};
+int g_debug_sync = [] {
+  const char* e = getenv("SGAD_DEBUG_SYNC");
+  return e && e[0] == '1' ? 1 : 0;
+}();
 
 void set_error(const char* fmt, ...) {
   va_list ap;
@@ -195,7 +199,7 @@ k_project(const sgad_frame* __restrict__ frames, sgad_camera cam, int ntx, int n
           int want_coef, Record* __restrict__ rec, TileBox* __restrict__ box,
           ChainCoef* __restrict__ coef, double* __restrict__ col64,
           unsigned long long* __restrict__ zkey, uint32_t* __restrict__ counters,
-          unsigned long long* __restrict__ zrange) {
+          unsigned long long* __restrict__ zrange, uint32_t* __restrict__ tile_count) {
   // one block = 256 consecutive pixels of frame blockIdx.y; the frame
   // descriptor is copied to shared memory (no per-thread frame search), and
   // the 64-byte records and 32-byte chain coefficients are staged in shared
@@ -220,6 +224,7 @@ k_project(const sgad_frame* __restrict__ frames, sgad_camera cam, int ntx, int n
 
   bool keep = false;
   Proj o;
+  TileBox bx{};
   if (p < hw) {
     const bool active = f.mask[p] != 0;
     const Params q = load_params(f, p, hw);
@@ -252,7 +257,6 @@ k_project(const sgad_frame* __restrict__ frames, sgad_camera cam, int ntx, int n
       y0 = y0 < 0 ? 0 : y0;
       x1 = x1 > ntx - 1 ? ntx - 1 : x1;
       y1 = y1 > nty - 1 ? nty - 1 : y1;
-      TileBox bx;
       bx.tx0 = (uint16_t)x0;
       bx.tx1 = (uint16_t)x1;
       bx.ty0 = (uint16_t)y0;
@@ -279,6 +283,25 @@ k_project(const sgad_frame* __restrict__ frames, sgad_camera cam, int ntx, int n
         c.pad_[0] = (float)(1.0 / o.sig);  // 1 / sigma for the late chain
         c.pad_[1] = 0.0f;
         cs[threadIdx.x] = c;
+      }
+    }
+  }
+  // pairs per tile (the tile lists' sizes): the lanes of a warp hold
+  // neighbouring pixels whose boxes share tiles, so each round of tiles is
+  // aggregated over the lanes naming the same tile (one atomic per tile)
+  {
+    const int bw = keep ? bx.tx1 - bx.tx0 + 1 : 0, bh = keep ? bx.ty1 - bx.ty0 + 1 : 0;
+    const int cnt_t = bw * bh;
+    int most = cnt_t;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) most = max(most, __shfl_xor_sync(0xffffffffu, most, off));
+    for (int j = 0; j < most; ++j) {
+      const bool has = j < cnt_t;
+      const uint32_t t = has ? (uint32_t)((bx.ty0 + j / bw) * ntx + bx.tx0 + j % bw) : ~0u;
+      const uint32_t act = __ballot_sync(0xffffffffu, has);
+      if (has) {
+        const uint32_t peers = __match_any_sync(act, t);
+        if ((peers & ((1u << lane) - 1u)) == 0u) atomicAdd(tile_count + t, (uint32_t)__popc(peers));
       }
     }
   }
@@ -343,32 +366,72 @@ static int depth_key_bits() {  // SGAD_DEPTH_BITS (A/B): 16..32, default 24
   return b < 16 ? 16 : (b > 32 ? 32 : b);
 }
 
-// Runs of equal buckets: up to 64 sorted here by their head thread
-// (insertion sort on (z bits, emission index)), longer ones queued for
-// k_long_runs (sort.cuh; any length).
+// Runs of equal buckets whose exact (z bits, emission index) order differs
+// from the stable bucket order: every adjacent pair of equal buckets is
+// checked in parallel (runs of exactly equal z -- a plane seen head-on -- are
+// already in order: the sort is stable); an out-of-order pair claims its
+// run's head in a bitmap, and the claiming thread sorts a run of up to 64 by
+// insertion or queues it for k_long_runs (sort.cuh; any length).
 __global__ void k_depth_fixup(const uint32_t* __restrict__ k32, const uint32_t* __restrict__ n_dev,
                               const unsigned long long* __restrict__ zkeys,
-                              uint32_t* __restrict__ perm, uint32_t* __restrict__ n_long,
-                              uint2* __restrict__ long_runs) {
+                              uint32_t* __restrict__ perm, uint32_t* __restrict__ claim,
+                              uint32_t* __restrict__ n_long, uint2* __restrict__ long_runs) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   const uint32_t n = *n_dev;
   if (i + 1 >= n) return;
-  if (k32[i + 1] != k32[i] || (i > 0 && k32[i - 1] == k32[i])) return;  // not a run head
-  uint32_t end = i + 2;
-  while (end < n && k32[end] == k32[i] && end - i <= 64) ++end;
-  if (end - i > 64) {
-    while (end < n && k32[end] == k32[i]) ++end;
-    long_runs[atomicAdd(n_long, 1u)] = make_uint2(i, end - i);
+  const uint32_t kk = k32[i];
+  if (k32[i + 1] != kk) return;
+  {
+    const uint32_t e0 = perm[i], e1 = perm[i + 1];
+    if (zlt(zkeys[e0], e0, zkeys[e1], e1)) return;  // in order
+  }
+  // the run [h, end) of bucket kk: galloping searches in the sorted buckets
+  uint32_t h = i, step = 1;
+  while (h > 0 && k32[h - 1] == kk) {  // k32[h] == kk; find lo with k32[lo] < kk
+    const uint32_t lo = h > step ? h - step : 0;
+    if (k32[lo] == kk) {
+      h = lo;
+      step <<= 1;
+    } else {
+      uint32_t a = lo, b = h;  // k32[a] < kk == k32[b]
+      while (b - a > 1) {
+        const uint32_t m = (a + b) >> 1;
+        if (k32[m] == kk) b = m; else a = m;
+      }
+      h = b;
+      break;
+    }
+  }
+  if (atomicOr(claim + (h >> 5), 1u << (h & 31)) & (1u << (h & 31))) return;  // claimed
+  uint32_t end = i + 1;
+  step = 1;
+  while (end + 1 < n && k32[end + 1] == kk) {  // k32[end] == kk
+    const uint32_t hi = end + step < n - 1 ? end + step : n - 1;
+    if (k32[hi] == kk) {
+      end = hi;
+      step <<= 1;
+    } else {
+      uint32_t a = end, b = hi;  // k32[a] == kk < k32[b]
+      while (b - a > 1) {
+        const uint32_t m = (a + b) >> 1;
+        if (k32[m] == kk) a = m; else b = m;
+      }
+      end = a;
+      break;
+    }
+  }
+  ++end;
+  if (end - h > 64) {
+    long_runs[atomicAdd(n_long, 1u)] = make_uint2(h, end - h);
     return;
   }
-  for (uint32_t a = i + 1; a < end; ++a) {  // insertion sort, stable on (z, e)
+  for (uint32_t a = h + 1; a < end; ++a) {  // insertion sort on (z, e)
     const uint32_t e = perm[a];
     const unsigned long long z = zkeys[e];
     uint32_t b = a;
-    while (b > i) {
+    while (b > h) {
       const uint32_t pe = perm[b - 1];
-      const unsigned long long pz = zkeys[pe];
-      if (pz < z || (pz == z && pe < e)) break;
+      if (zlt(zkeys[pe], pe, z, e)) break;
       perm[b] = pe;
       --b;
     }
@@ -378,29 +441,22 @@ __global__ void k_depth_fixup(const uint32_t* __restrict__ k32, const uint32_t* 
 
 // ------------------------------------------------------------------ K3
 // Tile lists = _build_tile_lists (rasterizer.py:178-218): the pair count of
-// every survivor in depth order is scanned (k_pair_scan, sort.cuh), each
+// every survivor in depth order is scanned (k_pair_emit, sort.cuh), each
 // survivor emits its (tile, value) pairs in (ty, tx) order at its offset, and
 // a stable radix sort on the tile key (6-bit digits) bins them: every tile's
 // list ends up in depth order.  Pairs past the handle's capacity are dropped
 // and flag *overflow (the caller grows the capacity and prepares again).
 constexpr int TILE_RB = 6;
 
-template <int TPASSES>
-__global__ void __launch_bounds__(256)
-k_tile_emit(const uint32_t* __restrict__ perm, const TileBox* __restrict__ box,
-            const uint32_t* __restrict__ off, const uint32_t* __restrict__ n_dev, int ntx,
-            int packed, uint32_t cap, uint32_t* __restrict__ pkeys, uint32_t* __restrict__ pvals,
-            uint32_t* __restrict__ hist, uint32_t* __restrict__ overflow,
-            int32_t* __restrict__ ext_flag) {
-  __shared__ uint32_t sh[TPASSES][1 << TILE_RB];
-  for (int j = threadIdx.x; j < TPASSES * (1 << TILE_RB); j += blockDim.x) (&sh[0][0])[j] = 0u;
-  __syncthreads();
-  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  const uint32_t n = *n_dev;
-  if (i < n) {
-    const uint32_t e = perm[i];
-    const TileBox r = box[e];
-    uint32_t o = off[i];
+struct TileEmit {
+  int ntx, packed;
+  uint32_t cap;
+  uint32_t* pkeys;
+  uint32_t* pvals;
+  uint32_t* overflow;
+  int32_t* ext_flag;
+  // the (tile, value) pairs of survivor e from offset o, in (ty, tx) order
+  __device__ __forceinline__ void operator()(uint32_t e, const TileBox& r, uint32_t o) const {
     for (int ty = r.ty0; ty <= r.ty1; ++ty) {
       uint32_t rows = 0;  // 4-row bands [by + 4b, by + 4b + 3] the box reaches
       const int by = ty * SGAD_TILE;
@@ -411,13 +467,9 @@ k_tile_emit(const uint32_t* __restrict__ perm, const TileBox* __restrict__ box,
         const int bx = tx * SGAD_TILE;
         const uint32_t cols = ((r.px0 <= bx + 7 && r.px1 >= bx) ? 1u : 0u) |
                               ((r.px0 <= bx + 15 && r.px1 >= bx + 8) ? 2u : 0u);
-        const uint32_t t = (uint32_t)(ty * ntx + tx);
         if (o < cap) {
-          pkeys[o] = t;
+          pkeys[o] = (uint32_t)(ty * ntx + tx);
           pvals[o] = packed ? e | ((cols | rows << 2) << LIST_IDX_BITS) : e;
-#pragma unroll
-          for (int p = 0; p < TPASSES; ++p)
-            atomicAdd(&sh[p][(t >> (TILE_RB * p)) & ((1u << TILE_RB) - 1u)], 1u);
         } else {
           *overflow = 1u;
           if (ext_flag) *ext_flag = 1;
@@ -426,21 +478,45 @@ k_tile_emit(const uint32_t* __restrict__ perm, const TileBox* __restrict__ box,
       }
     }
   }
-  __syncthreads();
-  for (int j = threadIdx.x; j < TPASSES * (1 << TILE_RB); j += blockDim.x) {
-    const uint32_t c = (&sh[0][0])[j];
-    if (c) atomicAdd(hist + j, c);
-  }
-}
+};
 
-__global__ void k_tile_ranges(const uint32_t* __restrict__ pkeys, const uint32_t* __restrict__ n_dev,
-                              uint32_t cap, uint2* __restrict__ ranges) {
-  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  const uint32_t n = min(*n_dev, cap);
-  if (i >= n) return;
-  const uint32_t t = pkeys[i];
-  if (i == 0 || pkeys[i - 1] != t) ranges[t].x = i;
-  if (i == n - 1 || pkeys[i + 1] != t) ranges[t].y = i + 1;
+// Per-tile list ranges (exclusive scan of K1's per-tile pair counts) and the
+// digit histograms of the tile sort's passes -- one block.
+__global__ void __launch_bounds__(1024)
+k_tile_scan(const uint32_t* __restrict__ tile_count, int n_tiles, int tpasses, uint32_t cap,
+            uint2* __restrict__ ranges, uint32_t* __restrict__ hist) {
+  __shared__ uint32_t s_wt[32];
+  __shared__ uint32_t s_carry;
+  __shared__ uint32_t sh[6 << TILE_RB];
+  for (int j = threadIdx.x; j < (6 << TILE_RB); j += blockDim.x) sh[j] = 0u;
+  if (threadIdx.x == 0) s_carry = 0u;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int b0 = 0; b0 < n_tiles; b0 += 1024) {
+    const int t = b0 + (int)threadIdx.x;
+    const uint32_t c = t < n_tiles ? tile_count[t] : 0u;
+    uint32_t x = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) s_wt[w] = x;
+    __syncthreads();
+    uint32_t before = s_carry;
+    for (int i = 0; i < w; ++i) before += s_wt[i];
+    const uint32_t start = before + x - c;
+    if (t < n_tiles) {
+      // (clamped to the capacity: an overflowed view is discarded, never read out of bounds)
+      ranges[t] = make_uint2(min(start, cap), min(start + c, cap));
+      for (int p = 0; p < tpasses; ++p)
+        atomicAdd(&sh[(p << TILE_RB) + (((uint32_t)t >> (TILE_RB * p)) & ((1u << TILE_RB) - 1u))], c);
+    }
+    __syncthreads();
+    if (threadIdx.x == 1023) s_carry = start + c;
+    __syncthreads();
+  }
+  for (int j = threadIdx.x; j < (tpasses << TILE_RB); j += blockDim.x) hist[j] = sh[j];
 }
 
 // ------------------------------------------------------------------ K4 / K5 shared
@@ -1380,8 +1456,8 @@ int sgad_raster_create(sgad_raster** out) {
 int sgad_raster_destroy(sgad_raster* h) {
   if (!h) return SGAD_OK;
   DevBuf* bufs[] = {&h->frames, &h->counters, &h->records, &h->coef, &h->keys0, &h->keys1,
-                    &h->vals0, &h->vals1, &h->poffset, &h->pkeys0, &h->pkeys1, &h->pvals0,
-                    &h->pvals1, &h->ranges, &h->sortws, &h->trans_final, &h->last_idx, &h->signs,
+                    &h->vals0, &h->vals1, &h->pkeys0, &h->pkeys1, &h->pvals0,
+                    &h->pvals1, &h->ranges, &h->sortws, &h->pairws, &h->trans_final, &h->last_idx, &h->signs,
                     &h->raw_grads, &h->rank_of, &h->scratch, &h->col64, &h->zrange, &h->k32a,
                     &h->k32b, &h->bbox, &h->runs, &h->raw32, &h->cl_e, &h->cl_m, &h->cl_n};
   for (DevBuf* b : bufs) b->release();
@@ -1398,35 +1474,51 @@ int sgad_raster_tile_count(sgad_raster* h, int64_t* n_tiles) {
 
 // ---- preparation (K1-K3), all on the stream, element counts on the device
 //
-// Workspace (h->sortws, zeroed by one memset per preparation):
-//   [0, 16)                 partition counters: depth passes, pair scan, tile passes
-//   depth_hist[dpasses][256], tile_hist[tpasses][64]
-//   depth_status[dpasses][parts(n_total)][256]
-//   scan_status[parts(n_total)]
-//   tile_status[tpasses][parts(cap_pairs)][64]
+// Workspaces: h->sortws (zeroed once per preparation) and h->pairws (zeroed
+// before every binning attempt; resized when the pair capacity grows).
+//   sortws: [0, 16) partition counters (depth passes 0..7, pair emit 8, tile
+//           passes 9..15), depth_hist[dpasses][256], tile_count[n_tiles],
+//           claim bitmap[n_total / 32 + 1], depth_status[dpasses][parts(n_total)][256]
+//   pairws: tile_hist[tpasses][64], emit_status[parts(n_total)],
+//           tile_status[tpasses][parts(cap_pairs)][64]
 struct PrepWs {
   uint32_t* ctr;
   uint32_t* dhist;
-  uint32_t* thist;
+  uint32_t* tcount;
+  uint32_t* claim;
   uint32_t* dstat;
+  size_t words;
+};
+
+struct PairWs {
+  uint32_t* thist;
   uint32_t* sstat;
   uint32_t* tstat;
   size_t words;
-  size_t tile_off;  // first word of the tile region (counters 8.. are tile passes)
 };
 
-static PrepWs prep_layout(uint32_t* base, int dpasses, int tpasses, uint32_t n_total,
-                          uint32_t cap) {
+static PrepWs prep_layout(uint32_t* base, int dpasses, uint32_t n_total, uint32_t n_tiles) {
   PrepWs w{};
   size_t o = 0;
   w.ctr = base + o;
   o += 16;
   w.dhist = base + o;
   o += (size_t)dpasses * 256;
-  w.thist = base + o;
-  o += (size_t)tpasses * (1u << TILE_RB);
+  w.tcount = base + o;
+  o += n_tiles;
+  w.claim = base + o;
+  o += n_total / 32 + 1;
   w.dstat = base + o;
   o += (size_t)dpasses * os_parts(n_total) * 256;
+  w.words = o;
+  return w;
+}
+
+static PairWs pair_layout(uint32_t* base, int tpasses, uint32_t n_total, uint32_t cap) {
+  PairWs w{};
+  size_t o = 0;
+  w.thist = base + o;
+  o += (size_t)tpasses * (1u << TILE_RB);
   w.sstat = base + o;
   o += os_parts(n_total);
   w.tstat = base + o;
@@ -1477,7 +1569,9 @@ static int prepare_front(sgad_raster* h, const sgad_frame* frames, int32_t n_fra
   h->dpasses = (h->kbits + 7) / 8;
   h->tpasses = (bits_for((uint32_t)(h->n_tiles > 1 ? h->n_tiles - 1 : 1)) + TILE_RB - 1) / TILE_RB;
   SGAD_REQUIRE(h->tpasses <= 6, "too many tiles");
-  if (h->cap_pairs == 0) h->cap_pairs = 3 * n_total + 4096;  // grown on overflow
+  // pair capacity: at least 2 x Gaussians (C4: 1.6 pairs per survivor); a
+  // synchronous prepare grows it on overflow, the window engine reserves it
+  if (h->cap_pairs < 2 * n_total + 4096) h->cap_pairs = 2 * n_total + 4096;
   SGAD_REQUIRE(h->cap_pairs < (1ll << 30), "too many tile pairs");
   const int64_t nt = h->n_tiles;
   SGAD_CHECK_CUDA(h->ranges.ensure(sizeof(uint2) * nt));
@@ -1499,11 +1593,10 @@ static int prepare_front(sgad_raster* h, const sgad_frame* frames, int32_t n_fra
   SGAD_CHECK_CUDA(h->k32a.ensure(sizeof(uint32_t) * n_total));
   SGAD_CHECK_CUDA(h->k32b.ensure(sizeof(uint32_t) * n_total));
   SGAD_CHECK_CUDA(h->runs.ensure(sizeof(uint2) * (n_total / 65 + 1)));
-  SGAD_CHECK_CUDA(h->poffset.ensure(sizeof(uint32_t) * (n_total + 1)));
   if (int rc = ensure_pair_buffers(h)) return rc;
-  PrepWs w = prep_layout(nullptr, h->dpasses, h->tpasses, ntot, (uint32_t)h->cap_pairs);
+  PrepWs w = prep_layout(nullptr, h->dpasses, ntot, (uint32_t)h->n_tiles);
   SGAD_CHECK_CUDA(h->sortws.ensure(sizeof(uint32_t) * w.words));
-  w = prep_layout(h->sortws.as<uint32_t>(), h->dpasses, h->tpasses, ntot, (uint32_t)h->cap_pairs);
+  w = prep_layout(h->sortws.as<uint32_t>(), h->dpasses, ntot, (uint32_t)h->n_tiles);
   SGAD_CHECK_CUDA(cudaMemsetAsync(w.ctr, 0, sizeof(uint32_t) * w.words, st));
   SGAD_CHECK_CUDA(cudaMemcpyAsync(h->frames.p, frames, sizeof(sgad_frame) * n_frames,
                                   cudaMemcpyHostToDevice, st));
@@ -1518,7 +1611,7 @@ static int prepare_front(sgad_raster* h, const sgad_frame* frames, int32_t n_fra
   k_project<<<pgrid, PROJ_THREADS, 0, st>>>(
       h->frames.as<sgad_frame>(), *cam, h->ntx, h->nty, want_coef, h->records.as<Record>(),
       h->bbox.as<TileBox>(), h->coef.as<ChainCoef>(), h->any_f64 ? h->col64.as<double>() : nullptr,
-      h->keys0.as<unsigned long long>(), cnt, h->zrange.as<unsigned long long>());
+      h->keys0.as<unsigned long long>(), cnt, h->zrange.as<unsigned long long>(), w.tcount);
   SGAD_LAUNCH_CHECK();
   // K2: digit histograms, onesweep passes (the permutation lands in vals0
   // and the sorted buckets in k32a), run fix-up
@@ -1549,67 +1642,53 @@ static int prepare_front(sgad_raster* h, const sgad_frame* frames, int32_t n_fra
   }
   uint32_t* perm = h->vals0.as<uint32_t>();
   k_depth_fixup<<<blocks_for(n_total, 256), 256, 0, st>>>(
-      h->k32a.as<uint32_t>(), cnt + C_NSURV, zkeys, perm, cnt + C_NLONG, h->runs.as<uint2>());
+      h->k32a.as<uint32_t>(), cnt + C_NSURV, zkeys, perm, w.claim, cnt + C_NLONG,
+      h->runs.as<uint2>());
   SGAD_LAUNCH_CHECK();
   k_long_runs<<<148, 1024, LONG_RUN_SMEM, st>>>(h->runs.as<uint2>(), cnt + C_NLONG, zkeys, perm,
                                                 h->keys1.as<unsigned long long>(),
                                                 h->vals1.as<uint32_t>());
   SGAD_LAUNCH_CHECK();
-  // K3a: pair counts in depth order, exclusive scan -> offsets, total pairs
-  k_pair_scan<TileBox><<<dparts, OS_THREADS, 0, st>>>(perm, h->bbox.as<TileBox>(), cnt + C_NSURV,
-                                                      ntot, h->poffset.as<uint32_t>(), w.sstat,
-                                                      w.ctr + 8, cnt + C_NPAIRS);
-  SGAD_LAUNCH_CHECK();
   return SGAD_OK;
 }
 
-// K3b: emit (tile, value) pairs, stable tile sort, per-tile ranges.  The
-// tile-pass counters / histograms / status are zeroed here (a retry after
-// an overflow re-runs only this part).
+// K3: pair counts in depth order -> offsets (look-back scan) and the
+// (tile, value) pairs at their offsets, stable tile sort, per-tile ranges.
+// The pair region of the workspace is zeroed here (a retry after an
+// overflow re-runs only this part).
 static int prepare_pairs(sgad_raster* h, int32_t* ext_flag, cudaStream_t st) {
   if (h->n_total == 0) return SGAD_OK;
   const uint32_t ntot = (uint32_t)h->n_total, cap = (uint32_t)h->cap_pairs;
   if (int rc = ensure_pair_buffers(h)) return rc;
-  PrepWs w = prep_layout(nullptr, h->dpasses, h->tpasses, ntot, cap);
-  SGAD_CHECK_CUDA(h->sortws.ensure(sizeof(uint32_t) * w.words));
-  w = prep_layout(h->sortws.as<uint32_t>(), h->dpasses, h->tpasses, ntot, cap);
+  const PrepWs w = prep_layout(h->sortws.as<uint32_t>(), h->dpasses, ntot, (uint32_t)h->n_tiles);
+  PairWs pw = pair_layout(nullptr, h->tpasses, ntot, cap);
+  SGAD_CHECK_CUDA(h->pairws.ensure(sizeof(uint32_t) * pw.words));
+  pw = pair_layout(h->pairws.as<uint32_t>(), h->tpasses, ntot, cap);
   uint32_t* cnt = h->counters.as<uint32_t>();
-  SGAD_CHECK_CUDA(cudaMemsetAsync(w.ctr + 9, 0, sizeof(uint32_t) * 7, st));
-  SGAD_CHECK_CUDA(cudaMemsetAsync(w.thist, 0, sizeof(uint32_t) * h->tpasses * (1u << TILE_RB), st));
-  SGAD_CHECK_CUDA(cudaMemsetAsync(w.tstat, 0,
-                                  sizeof(uint32_t) * h->tpasses * os_parts(cap) * (1u << TILE_RB), st));
-  SGAD_CHECK_CUDA(cudaMemsetAsync(h->ranges.p, 0, sizeof(uint2) * h->n_tiles, st));
+  SGAD_CHECK_CUDA(cudaMemsetAsync(w.ctr + 8, 0, sizeof(uint32_t) * 8, st));
+  SGAD_CHECK_CUDA(cudaMemsetAsync(pw.thist, 0, sizeof(uint32_t) * pw.words, st));
   SGAD_CHECK_CUDA(cudaMemsetAsync(cnt + C_OVERFLOW, 0, sizeof(uint32_t), st));
+  k_tile_scan<<<1, 1024, 0, st>>>(w.tcount, h->n_tiles, h->tpasses, cap, h->ranges.as<uint2>(),
+                                  pw.thist);
+  SGAD_LAUNCH_CHECK();
   uint32_t* kb[2] = {h->pkeys0.as<uint32_t>(), h->pkeys1.as<uint32_t>()};
   uint32_t* vb[2] = {h->pvals0.as<uint32_t>(), h->pvals1.as<uint32_t>()};
   int cur = (h->tpasses & 1) ? 1 : 0;  // emit here; the last pass lands in buffer 0
   const uint32_t* perm = h->vals0.as<uint32_t>();
-#define SGAD_EMIT(TP)                                                                           \
-  k_tile_emit<TP><<<blocks_for(h->n_total, 256), 256, 0, st>>>(                                  \
-      perm, h->bbox.as<TileBox>(), h->poffset.as<uint32_t>(), cnt + C_NSURV, h->ntx, h->packed, \
-      cap, kb[cur], vb[cur], w.thist, cnt + C_OVERFLOW, ext_flag)
-  switch (h->tpasses) {
-    case 1: SGAD_EMIT(1); break;
-    case 2: SGAD_EMIT(2); break;
-    case 3: SGAD_EMIT(3); break;
-    case 4: SGAD_EMIT(4); break;
-    case 5: SGAD_EMIT(5); break;
-    default: SGAD_EMIT(6); break;
-  }
-#undef SGAD_EMIT
+  const unsigned dparts = os_parts(ntot);
+  k_pair_emit<TileBox, TileEmit><<<dparts, OS_THREADS, 0, st>>>(
+      perm, h->bbox.as<TileBox>(), cnt + C_NSURV, ntot, pw.sstat, w.ctr + 8, cnt + C_NPAIRS,
+      TileEmit{h->ntx, h->packed, cap, kb[cur], vb[cur], cnt + C_OVERFLOW, ext_flag});
   SGAD_LAUNCH_CHECK();
   const unsigned tparts = os_parts(cap);
   for (int pss = 0; pss < h->tpasses; ++pss) {
     k_onesweep<TILE_RB, 0><<<tparts, OS_THREADS, 0, st>>>(
         kb[cur], vb[cur], nullptr, nullptr, 0, cap, cnt + C_NPAIRS, kb[cur ^ 1], vb[cur ^ 1],
-        w.thist + (1u << TILE_RB) * pss, w.tstat + (size_t)pss * tparts * (1u << TILE_RB),
+        pw.thist + (1u << TILE_RB) * pss, pw.tstat + (size_t)pss * tparts * (1u << TILE_RB),
         w.ctr + 9 + pss, TILE_RB * pss);
     SGAD_LAUNCH_CHECK();
     cur ^= 1;
   }
-  k_tile_ranges<<<blocks_for(h->cap_pairs, 256), 256, 0, st>>>(kb[0], cnt + C_NPAIRS, cap,
-                                                               h->ranges.as<uint2>());
-  SGAD_LAUNCH_CHECK();
   return SGAD_OK;
 }
 

@@ -109,8 +109,16 @@ k_depth_hist(const unsigned long long* __restrict__ zkeys, uint32_t n,
 // MODE 0: keys/values from kin/vin; MODE 1: the depth sort's first pass --
 // keys are the depth buckets of zkeys[i], values the emission index i,
 // culled ids (zkeys == ~0) are dropped.
+//
+// Order of work inside a partition ("early counts"): the partition's digit
+// counts (shared-memory atomics) are published before the warps rank their
+// keys, so a successor's look-back rarely waits; the stable warp ranks come
+// from RB ballots per round of 32 keys (the lanes sharing a digit).
+#ifndef SGAD_OS_MINB
+#define SGAD_OS_MINB 4
+#endif
 template <int RB, int MODE>
-__global__ void __launch_bounds__(OS_THREADS)
+__global__ void __launch_bounds__(OS_THREADS, SGAD_OS_MINB)
 k_onesweep(const uint32_t* __restrict__ kin, const uint32_t* __restrict__ vin,
            const unsigned long long* __restrict__ zkeys,
            const unsigned long long* __restrict__ zrange, int kbits, uint32_t n_static,
@@ -123,6 +131,7 @@ k_onesweep(const uint32_t* __restrict__ kin, const uint32_t* __restrict__ vin,
   __shared__ uint32_t s_keys[OS_PART];
   __shared__ uint32_t s_vals[OS_PART];
   __shared__ uint32_t whist[OS_WARPS][R];
+  __shared__ uint32_t s_cnt[R];      // the partition's digit counts
   __shared__ uint32_t s_bstart[R];   // first smem slot of each digit
   __shared__ int32_t s_goff[R];      // global position of smem slot 0 of each digit's run
   __shared__ uint32_t s_wt[OS_WARPS];
@@ -130,12 +139,18 @@ k_onesweep(const uint32_t* __restrict__ kin, const uint32_t* __restrict__ vin,
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   if (tid == 0) s_part = atomicAdd(ctr, 1u);
   for (int i = tid; i < OS_WARPS * R; i += OS_THREADS) (&whist[0][0])[i] = 0u;
+  if (tid < R) s_cnt[tid] = 0u;
+  // n_dev above n_static: the pairs overflowed their capacity (the view is
+  // discarded); the digit histograms count every pair, so nothing is moved
+  const uint32_t nd = n_dev ? *n_dev : n_static;
+  const uint32_t n = nd > n_static ? 0u : nd;
   __syncthreads();
   const uint32_t p = s_part;
-  const uint32_t n = n_dev ? min(*n_dev, n_static) : n_static;
   if (p >= os_parts(n)) return;  // block-uniform
 
-  uint32_t key[OS_ITEMS], val[OS_ITEMS];
+  // keys in registers; values are read (MODE 0) or formed (MODE 1: the
+  // index) when they are placed, so they do not hold registers meanwhile
+  uint32_t key[OS_ITEMS];
   uint32_t vbits = 0;  // valid items of this lane
   const uint32_t base = p * OS_PART + (uint32_t)w * (OS_ITEMS * 32) + (uint32_t)lane;
   if (MODE == 1) {
@@ -147,7 +162,6 @@ k_onesweep(const uint32_t* __restrict__ kin, const uint32_t* __restrict__ vin,
       const unsigned long long zk = i < n ? zkeys[i] : ~0ull;
       const bool ok = zk != ~0ull;
       key[k] = ok ? bk(zk) : 0u;
-      val[k] = i;
       vbits |= ok ? (1u << k) : 0u;
     }
   } else {
@@ -156,39 +170,50 @@ k_onesweep(const uint32_t* __restrict__ kin, const uint32_t* __restrict__ vin,
       const uint32_t i = base + 32u * k;
       const bool ok = i < n;
       key[k] = ok ? kin[i] : 0u;
-      val[k] = ok ? vin[i] : 0u;
       vbits |= ok ? (1u << k) : 0u;
     }
   }
-  // warp-local stable ranks
+  // early counts, published as the partition's aggregate
+#pragma unroll
+  for (int k = 0; k < OS_ITEMS; ++k)
+    if ((vbits >> k) & 1u) atomicAdd(&s_cnt[(key[k] >> shift) & DMASK], 1u);
+  __syncthreads();
+  uint32_t cnt = 0;
+  if (tid < R) {
+    cnt = s_cnt[tid];
+    st_volatile_u32(status + (size_t)p * R + tid, (p == 0 ? LB_FLAG_P : LB_FLAG_A) | cnt);
+  }
+  // warp-local stable ranks (16-bit, two per register)
   const uint32_t lt = (1u << lane) - 1u;
-  uint32_t rank[OS_ITEMS];
+  uint32_t rank2[OS_ITEMS / 2];
 #pragma unroll
   for (int k = 0; k < OS_ITEMS; ++k) {
     const bool ok = (vbits >> k) & 1u;
-    const uint32_t vm = __ballot_sync(0xffffffffu, ok);
     const uint32_t d = (key[k] >> shift) & DMASK;
-    uint32_t old = 0, peers = 0;
-    if (ok) {
-      peers = __match_any_sync(vm, d);
-      old = whist[w][d];
+    uint32_t peers = __ballot_sync(0xffffffffu, ok);
+#pragma unroll
+    for (int b = 0; b < RB; ++b) {
+      const uint32_t bal = __ballot_sync(0xffffffffu, (d >> b) & 1u);
+      peers &= ((d >> b) & 1u) ? bal : ~bal;
     }
+    const uint32_t old = ok ? whist[w][d] : 0u;
     __syncwarp();
     if (ok && (peers & lt) == 0u) whist[w][d] = old + __popc(peers);
     __syncwarp();
-    rank[k] = old + __popc(peers & lt);
+    const uint32_t rk = old + __popc(peers & lt);
+    if (k & 1) rank2[k >> 1] |= rk << 16;
+    else rank2[k >> 1] = rk;
   }
   __syncthreads();
-  // per digit: exclusive over warps, partition count, publish the aggregate
-  uint32_t cnt = 0;
+  // per digit: exclusive over warps
   if (tid < R) {
+    uint32_t c = 0;
 #pragma unroll
     for (int i = 0; i < OS_WARPS; ++i) {
       const uint32_t x = whist[i][tid];
-      whist[i][tid] = cnt;
-      cnt += x;
+      whist[i][tid] = c;
+      c += x;
     }
-    st_volatile_u32(status + (size_t)p * R + tid, (p == 0 ? LB_FLAG_P : LB_FLAG_A) | cnt);
   }
   uint32_t nvalid;
   const uint32_t bstart = block_excl_scan<R>(cnt, s_wt, &nvalid);
@@ -218,9 +243,11 @@ k_onesweep(const uint32_t* __restrict__ kin, const uint32_t* __restrict__ vin,
   for (int k = 0; k < OS_ITEMS; ++k) {
     if ((vbits >> k) & 1u) {
       const uint32_t d = (key[k] >> shift) & DMASK;
-      const uint32_t pos = s_bstart[d] + whist[w][d] + rank[k];
+      const uint32_t rk = (rank2[k >> 1] >> (16 * (k & 1))) & 0xFFFFu;
+      const uint32_t pos = s_bstart[d] + whist[w][d] + rk;
+      const uint32_t i = base + 32u * k;
       s_keys[pos] = key[k];
-      s_vals[pos] = val[k];
+      s_vals[pos] = MODE == 1 ? i : vin[i];
     }
   }
   __syncthreads();
@@ -233,49 +260,63 @@ k_onesweep(const uint32_t* __restrict__ kin, const uint32_t* __restrict__ vin,
   }
 }
 
-// ---------------------------------------------------------------- pair-count scan
-// poff[i] = sum of tile counts of survivors 0..i-1 in depth order (exclusive
-// scan, decoupled look-back over 4096-item partitions); poff[ns] = total
-// pairs, also stored at *n_pairs.
-struct TileBoxView {  // the fields of TileBox the scan reads
-  uint16_t tx0, tx1, ty0, ty1;
-};
-
-template <class Box>
-__global__ void __launch_bounds__(OS_THREADS)
-k_pair_scan(const uint32_t* __restrict__ perm, const Box* __restrict__ box,
-            const uint32_t* __restrict__ n_dev, uint32_t n_static, uint32_t* __restrict__ poff,
+// ---------------------------------------------------------------- pair scan + emit
+// The tile pairs of the survivors in depth order (rasterizer.py:187-217):
+// each partition of 4096 survivors counts its pairs (tile boxes), takes its
+// exclusive offset from the decoupled look-back, and emits its (tile, value)
+// pairs at their final positions in emission order, accumulating the digit
+// histograms of the tile sort.  *n_pairs receives the total; pairs at or past
+// cap are dropped and flag *overflow (and *ext_flag).
+template <class Box, class Emit>
+__global__ void __launch_bounds__(OS_THREADS, 4)
+k_pair_emit(const uint32_t* __restrict__ perm, const Box* __restrict__ box,
+            const uint32_t* __restrict__ n_dev, uint32_t n_static,
             uint32_t* __restrict__ status, uint32_t* __restrict__ ctr,
-            uint32_t* __restrict__ n_pairs) {
+            uint32_t* __restrict__ n_pairs, Emit emit) {
   __shared__ uint32_t s_wt[OS_WARPS];
   __shared__ uint32_t s_part, s_excl;
-  const int tid = threadIdx.x, lane = tid & 31;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   if (tid == 0) s_part = atomicAdd(ctr, 1u);
+  const uint32_t n = min(*n_dev, n_static);
   __syncthreads();
   const uint32_t p = s_part;
-  const uint32_t n = min(*n_dev, n_static);
   if (p >= os_parts(n)) return;
-  const uint32_t i0 = p * OS_PART + (uint32_t)tid * OS_ITEMS;
-  uint32_t c[OS_ITEMS];
-  uint32_t sum = 0;
+  const uint32_t base = p * OS_PART + (uint32_t)w * (OS_ITEMS * 32) + (uint32_t)lane;
+  uint32_t off[OS_ITEMS];  // this item's offset within the warp's pairs
+  uint32_t ee[OS_ITEMS];   // its survivor id
+  uint32_t run = 0;
 #pragma unroll
   for (int k = 0; k < OS_ITEMS; ++k) {
-    const uint32_t i = i0 + k;
-    uint32_t v = 0;
+    const uint32_t i = base + 32u * k;
+    uint32_t c = 0;
+    ee[k] = i < n ? perm[i] : 0u;
     if (i < n) {
-      const Box b = box[perm[i]];
-      v = (uint32_t)(b.tx1 - b.tx0 + 1) * (uint32_t)(b.ty1 - b.ty0 + 1);
+      const Box b = box[ee[k]];
+      c = (uint32_t)(b.tx1 - b.tx0 + 1) * (uint32_t)(b.ty1 - b.ty0 + 1);
     }
-    c[k] = v;
-    sum += v;
+    uint32_t x = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    off[k] = run + x - c;
+    run += __shfl_sync(0xffffffffu, x, 31);
   }
-  uint32_t total;
-  const uint32_t mine = block_excl_scan<OS_THREADS>(sum, s_wt, &total);
+  if (lane == 0) s_wt[w] = run;
+  __syncthreads();
+  uint32_t wbefore = 0, total = 0;
+#pragma unroll
+  for (int i = 0; i < OS_WARPS; ++i) {
+    const uint32_t t = s_wt[i];
+    wbefore += i < w ? t : 0u;
+    total += t;
+  }
   if (tid == 0) {
     if (p == 0) st_volatile_u32(status, LB_FLAG_P | total);
     else st_volatile_u32(status + p, LB_FLAG_A | total);
   }
-  if (tid < 32) {
+  if (w == 0) {
     uint32_t excl = 0;
     if (p > 0) {
       excl = lookback_exclusive(status, (int)p);
@@ -284,16 +325,18 @@ k_pair_scan(const uint32_t* __restrict__ perm, const Box* __restrict__ box,
     if (lane == 0) s_excl = excl;
   }
   __syncthreads();
-  uint32_t run = s_excl + mine;
+  const uint32_t o0 = s_excl + wbefore;
+  if (p + 1 == os_parts(n) && w == OS_WARPS - 1 && lane == 31) *n_pairs = s_excl + total;
+  // emit, four items at a time with their boxes loaded together
+#pragma unroll 1
+  for (int k0 = 0; k0 < OS_ITEMS; k0 += 4) {
+    Box bb[4];
 #pragma unroll
-  for (int k = 0; k < OS_ITEMS; ++k) {
-    const uint32_t i = i0 + k;
-    if (i < n) poff[i] = run;
-    run += c[k];
-    if (i + 1 == n) {
-      poff[n] = run;
-      *n_pairs = run;
-    }
+    for (int k = 0; k < 4; ++k)
+      if (base + 32u * (k0 + k) < n) bb[k] = box[ee[k0 + k]];
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (base + 32u * (k0 + k) < n) emit(ee[k0 + k], bb[k], o0 + off[k0 + k]);
   }
 }
 

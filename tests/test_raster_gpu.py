@@ -274,6 +274,31 @@ def test_fronto_parallel_runs_bit_exact(size):
     check_view(maps_np, wc.poses[1], wc.intr)
 
 
+@pytest.mark.parametrize("bits", [16, 24, 32])
+def test_unsorted_bucket_runs_bit_exact(monkeypatch, bits):
+    """Runs of equal depth buckets holding distinct depths, from a few to one
+    of ~50 k (a plane at 2 m with 1e-7 m of jitter, a few pixels at 8 m so the
+    bucket width is far above the jitter): the fix-up's insertion sort, the
+    shared-memory bitonic and the global merge sort of k_long_runs must all
+    leave the exact (z, frame, pixel) order, at every depth-key width."""
+    from types import SimpleNamespace
+    from paper_2603_21055_b200.geometry import Pose
+    monkeypatch.setenv("SGAD_DEPTH_BITS", str(bits))
+    wc = _window_np(n_frames=3, seed=4, w=160, h=120, fx=140.0)
+    rng = np.random.default_rng(11)
+    maps_np = []
+    for i, p in enumerate(wc.params):
+        p.base_depth = np.full_like(p.base_depth, 2.0)
+        p.delta = rng.normal(0.0, 1e-7, p.delta.shape).astype(np.float32).astype(np.float64)
+        p.base_depth[:2, :4] = 8.0
+        p.active_mask = np.ones_like(p.active_mask)
+        maps_np.append(SimpleNamespace(frame_index=i, pose=Pose.identity(), intrinsics=wc.intr,
+                                       base_depth=p.base_depth, delta=p.delta,
+                                       log_radius=p.log_radius, opacity_logit=p.opacity_logit,
+                                       color=p.color, active_mask=p.active_mask))
+    check_view(maps_np, Pose.identity(), wc.intr)
+
+
 def test_random_footprints_backward_exact():
     """The exact drop-in backward (compact per-warp lists from the forward, the
     ring of windows) against the oracle on footprints from ~0.05 px to ~40 px:
