@@ -26,7 +26,13 @@ namespace sgad {
 
 constexpr int OS_THREADS = 256;
 constexpr int OS_WARPS = OS_THREADS / 32;
-constexpr int OS_ITEMS = 16;
+#ifndef SGAD_OS_ITEMS
+#define SGAD_OS_ITEMS 16
+#endif
+#ifndef SGAD_OS_MATCH
+#define SGAD_OS_MATCH 0  // warp ranks: 0 = RB ballots per round, 1 = __match_any_sync
+#endif
+constexpr int OS_ITEMS = SGAD_OS_ITEMS;
 constexpr int OS_PART = OS_THREADS * OS_ITEMS;  // 4096 keys per partition
 
 // partitions needed for n keys
@@ -114,11 +120,10 @@ k_depth_hist(const unsigned long long* __restrict__ zkeys, uint32_t n,
 // counts (shared-memory atomics) are published before the warps rank their
 // keys, so a successor's look-back rarely waits; the stable warp ranks come
 // from RB ballots per round of 32 keys (the lanes sharing a digit).
-#ifndef SGAD_OS_MINB
-#define SGAD_OS_MINB 4
-#endif
+// blocks per SM: 4 for the 6-bit passes (64 registers), 3 for the 8-bit ones
+// (their 64-register build spills)
 template <int RB, int MODE>
-__global__ void __launch_bounds__(OS_THREADS, SGAD_OS_MINB)
+__global__ void __launch_bounds__(OS_THREADS, RB <= 6 ? 4 : 3)
 k_onesweep(const uint32_t* __restrict__ kin, const uint32_t* __restrict__ vin,
            const unsigned long long* __restrict__ zkeys,
            const unsigned long long* __restrict__ zrange, int kbits, uint32_t n_static,
@@ -142,6 +147,7 @@ k_onesweep(const uint32_t* __restrict__ kin, const uint32_t* __restrict__ vin,
   if (tid < R) s_cnt[tid] = 0u;
   // n_dev above n_static: the pairs overflowed their capacity (the view is
   // discarded); the digit histograms count every pair, so nothing is moved
+  const uint32_t gh = tid < R ? hist[tid] : 0u;  // (this pass's global digit counts)
   const uint32_t nd = n_dev ? *n_dev : n_static;
   const uint32_t n = nd > n_static ? 0u : nd;
   __syncthreads();
@@ -178,24 +184,47 @@ k_onesweep(const uint32_t* __restrict__ kin, const uint32_t* __restrict__ vin,
   for (int k = 0; k < OS_ITEMS; ++k)
     if ((vbits >> k) & 1u) atomicAdd(&s_cnt[(key[k] >> shift) & DMASK], 1u);
   __syncthreads();
-  uint32_t cnt = 0;
+  // publish the aggregate; with fewer digits than threads the look-back runs
+  // right away on the digit warps (the inclusive prefix is out early, so
+  // successors' look-backs stay short) while the other warps rank their keys;
+  // with a digit per thread it runs after the ranking, which hides its wait
+  constexpr bool EARLY_LB = R < OS_THREADS;
+  uint32_t cnt = 0, excl = 0;
   if (tid < R) {
     cnt = s_cnt[tid];
     st_volatile_u32(status + (size_t)p * R + tid, (p == 0 ? LB_FLAG_P : LB_FLAG_A) | cnt);
   }
+  auto lookback = [&]() {
+    if (tid < R && p > 0) {
+      for (int q = (int)p - 1; q >= 0; --q) {
+        uint32_t s;
+        do {
+          s = ld_volatile_u32(status + (size_t)q * R + tid);
+        } while ((s >> 30) == 0u);
+        excl += s & LB_VALUE;
+        if ((s >> 30) == 2u) break;
+      }
+      st_volatile_u32(status + (size_t)p * R + tid, LB_FLAG_P | (excl + cnt));
+    }
+  };
+  if (EARLY_LB) lookback();
   // warp-local stable ranks (16-bit, two per register)
   const uint32_t lt = (1u << lane) - 1u;
-  uint32_t rank2[OS_ITEMS / 2];
+  uint32_t rank2[(OS_ITEMS + 1) / 2];
 #pragma unroll
   for (int k = 0; k < OS_ITEMS; ++k) {
     const bool ok = (vbits >> k) & 1u;
     const uint32_t d = (key[k] >> shift) & DMASK;
     uint32_t peers = __ballot_sync(0xffffffffu, ok);
+#if SGAD_OS_MATCH
+    if (ok) peers = __match_any_sync(peers, d);
+#else
 #pragma unroll
     for (int b = 0; b < RB; ++b) {
       const uint32_t bal = __ballot_sync(0xffffffffu, (d >> b) & 1u);
       peers &= ((d >> b) & 1u) ? bal : ~bal;
     }
+#endif
     const uint32_t old = ok ? whist[w][d] : 0u;
     __syncwarp();
     if (ok && (peers & lt) == 0u) whist[w][d] = old + __popc(peers);
@@ -215,25 +244,12 @@ k_onesweep(const uint32_t* __restrict__ kin, const uint32_t* __restrict__ vin,
       c += x;
     }
   }
+  if (!EARLY_LB) lookback();
   uint32_t nvalid;
   const uint32_t bstart = block_excl_scan<R>(cnt, s_wt, &nvalid);
-  uint32_t gh = 0;
-  if (tid < R) gh = hist[tid];
   uint32_t gtot;
   const uint32_t gstart = block_excl_scan<R>(gh, s_wt, &gtot);
   if (tid < R) {
-    uint32_t excl = 0;
-    if (p > 0) {
-      for (int q = (int)p - 1; q >= 0; --q) {
-        uint32_t s;
-        do {
-          s = ld_volatile_u32(status + (size_t)q * R + tid);
-        } while ((s >> 30) == 0u);
-        excl += s & LB_VALUE;
-        if ((s >> 30) == 2u) break;
-      }
-      st_volatile_u32(status + (size_t)p * R + tid, LB_FLAG_P | (excl + cnt));
-    }
     s_bstart[tid] = bstart;
     s_goff[tid] = (int32_t)(gstart + excl) - (int32_t)bstart;
   }
@@ -328,6 +344,7 @@ k_pair_emit(const uint32_t* __restrict__ perm, const Box* __restrict__ box,
   const uint32_t o0 = s_excl + wbefore;
   if (p + 1 == os_parts(n) && w == OS_WARPS - 1 && lane == 31) *n_pairs = s_excl + total;
   // emit, four items at a time with their boxes loaded together
+  static_assert(OS_ITEMS % 4 == 0, "items per thread");
 #pragma unroll 1
   for (int k0 = 0; k0 < OS_ITEMS; k0 += 4) {
     Box bb[4];

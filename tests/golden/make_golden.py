@@ -396,11 +396,70 @@ def golden_frame_driver(G, GEO, M, RgbdFrame):
     return d
 
 
+BENCH_VIEWS = {"c3": 3, "c4": 5}
+
+
+def golden_bench(cfg_name, state, ref_path):
+    """One target view of a benched window (C3 640x480 / C4 1200x680, 8
+    keyframes, the bench's init_params or the teacher-forced state
+    helpers.forced_params) through the REAL reference (oracle/refwindow.py:
+    its _prepare / _build_tile_lists / _forward_kernel / _backward_kernel,
+    loss upstream and chain rule, all maps learnable -- delta D1), stored as
+    compact exact digests: tile offsets and per-tile list hashes, loss terms,
+    sampled pixels and Gaussians, per-frame gradient sums."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import time
+    from helpers import forced_params, sample_indices, tile_digest
+    from oracle import refwindow as RW
+    from paper_2603_21055_b200 import scenes
+    ref = RW.import_reference(ref_path)
+    wc = scenes.config_c3() if cfg_name == "c3" else scenes.config_c4()
+    params = wc.params if state == "init" else forced_params(wc.params)
+    v = BENCH_VIEWS[cfg_name]
+    ri, maps = RW.ref_maps(ref, wc.intr, wc.poses, params)
+    fr = wc.frames[v]
+    t0 = time.time()
+    r = RW.window_view(ref, maps, wc.poses[v], ri, fr.color, fr.depth, fr.valid_mask,
+                       keep_lists=True)
+    print(f"{cfg_name}/{state}: reference view {v} in {time.time() - t0:.1f} s", flush=True)
+    h, w = ri.height, ri.width
+    ent = r.lists
+    d = {"view": np.array(v), "n_surv": np.array(len(r.frame)),
+         "offsets": np.asarray(r.offsets, dtype=np.int64),
+         "tile_hash": tile_digest(r.offsets, r.frame[ent], r.pixel[ent]),
+         "loss": np.array([r.color_l1, r.depth_l1])}
+    px = sample_indices(h * w, 8000, 5)
+    d["px"] = px
+    d["px_color"] = r.color.reshape(-1, 3)[px]
+    d["px_depth"] = r.depth.reshape(-1)[px]
+    d["px_alpha"] = r.alpha.reshape(-1)[px]
+    d["px_count"] = r.count.reshape(-1)[px]
+    d["img_sums"] = np.array([r.color.sum(), r.depth.sum(), r.alpha.sum(), r.count.sum()])
+    n_g = len(maps) * h * w
+    gs = sample_indices(n_g, 20000, 6)
+    d["gs"] = gs
+    planes = np.zeros((len(maps), 6, h * w))
+    for f, m in enumerate(maps):
+        gc, gr, gl, gd = r.grads[m.frame_index]
+        planes[f] = np.stack([gd.reshape(-1), gr.reshape(-1), gl.reshape(-1),
+                              *gc.reshape(-1, 3).T])
+    flat = planes.transpose(0, 2, 1).reshape(n_g, 6)
+    d["g_sample"] = flat[gs]
+    d["g_frame_sums"] = planes.sum(axis=2)
+    d["g_frame_abs"] = np.abs(planes).sum(axis=2)
+    return d
+
+
 def main():
     sys.path.insert(0, ROOT)
     want = set(sys.argv[1:]) or {"c1", "window", "eig", "track", "ssim", "render_init", "voxels",
-                                    "frame_driver"}
+                                    "frame_driver", "bench"}
     tmp, G, GEO, M, R, T, RgbdFrame = import_reference()
+    for cfg_name in ("c3", "c4"):
+        for state in ("init", "forced"):
+            if f"bench_{cfg_name}_{state}" in want or f"bench_{cfg_name}" in want or "bench" in want:
+                np.savez_compressed(os.path.join(HERE, f"bench_{cfg_name}_{state}.npz"),
+                                    **golden_bench(cfg_name, state, tmp))
     try:
         if "c1" in want:
             np.savez_compressed(os.path.join(HERE, "c1.npz"), **golden_c1(G, GEO, M, R, RgbdFrame))
