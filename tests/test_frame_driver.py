@@ -127,10 +127,13 @@ def test_gpu_map_frame(golden):
                               truth.translation, 1, intr, gmap.base_depth.cpu().numpy(),
                               [(fa.color, fa.depth, fa.valid_mask, np.eye(3), np.zeros(3),
                                 map_a.to_numpy())], 4)
-    for ref in (olosses, g["mf_losses"]):
-        np.testing.assert_allclose(losses, ref, rtol=1e-3)
+    # vs the oracle replay (same fp64 exp, same knife-edge decisions): tight
+    np.testing.assert_allclose(losses, olosses, rtol=1e-10)
+    for k in ("delta", "log_radius", "opacity_logit", "color"):
+        d = np.abs(getattr(gmap, k).cpu().numpy() - getattr(om, k))
+        assert d.max() < 1e-9, (k, d.max())
+    # vs the reference's own run: the knife-edge inclusions differ (D7), the
+    # loss moves by ~1e-4 relative
+    np.testing.assert_allclose(losses, g["mf_losses"], rtol=1e-3)
     np.testing.assert_array_equal(gmap.active_mask.cpu().numpy(), g["mf_active_mask"])
     np.testing.assert_allclose(gmap.base_depth.cpu().numpy(), g["mf_base_depth"], atol=1e-9)
-    for k in ("delta", "log_radius", "color"):
-        d = np.abs(getattr(gmap, k).cpu().numpy() - getattr(om, k))
-        assert (d < 1e-4).mean() > 0.9, k
