@@ -51,12 +51,23 @@ static_assert(offsetof(Record, sigma) == 16 && offsetof(Record, z) == 32 &&
               offsetof(Record, nh) == 40 && offsetof(Record, r) == 48 && offsetof(Record, gid) == 60,
               "record field offsets");
 
-struct __align__(16) ChainCoef {  // fused backward: d(param)/d(image quantity), fp32
-  float k_r;        // d sigma -> radius: fx / z
-  float a_u, a_v, a_z, a_s;  // delta <- (u0, v0, z, sigma)
-  float k_op;       // opacity -> logit: op (1 - op)
-  float pad_[2];    // [0]: 1 / sigma (late chain); one 32-byte sector per Gaussian
+// The window backward's record (one 64-byte line, two 32-byte loads): the
+// fields a contribution needs and the view-dependent chain-rule coefficients
+// of rasterizer.py:462-483, so K5 adds parameter gradients directly.  The
+// compositing fields stay fp64: the backward reconstructs T and the suffix
+// sums from the forward's fp64 state, and c T_b - S / (1 - a) cancels
+// heavily (neighbouring Gaussians share colour and depth), so fp32 opacity
+// or exponent scale cost 1e-3 of a gradient (measured).  The remaining
+// coefficients follow from these: d delta / d(sigma g_sigma) = -a_z / z,
+// d radius / d(sigma g_sigma) = fx sqrt(-2 nh) / z, d logit / d op =
+// op (1 - op).
+struct __align__(16) BwdRecord {
+  double u0, v0, op, nh;       // nh = -0.5 / sigma^2
+  double z;
+  float r, g, b;
+  float a_u, a_v, a_z;         // d delta / d (u0, v0, z)
 };
+static_assert(sizeof(BwdRecord) == 64, "backward record must be one 64-byte line");
 
 constexpr uint32_t GID_LEARN = 0x80000000u;
 constexpr int PROJ_THREADS = 256;
@@ -67,7 +78,7 @@ constexpr int RASTER_THREADS = 256;
 struct sgad_raster {
   sgad::DevBuf frames, counters, records, coef, keys0, keys1, vals0, vals1;
   sgad::DevBuf pkeys0, pkeys1, pvals0, pvals1, ranges, sortws, pairws;
-  sgad::DevBuf trans_final, last_idx, signs, raw_grads, rank_of, scratch, col64, zrange, k32a, k32b, bbox, runs, raw32, cl_e, cl_m, cl_n;
+  sgad::DevBuf trans_final, last_idx, signs, raw_grads, rank_of, scratch, col64, zrange, k32a, k32b, bbox, runs, cl_e, cl_m, cl_n;
   int any_f64 = 0;
   std::vector<sgad_frame> host_frames;
   sgad_camera cam{};
@@ -90,13 +101,6 @@ enum : int { C_NSURV = 1, C_NLONG = 3, C_NPAIRS = 4, C_OVERFLOW = 5 };
 namespace sgad {
 
 static thread_local char g_err[1024] = "";
-// fused backward variant: chain rule per Gaussian after the sweep (1, the
-// default: 2.20 vs 2.36 ms per C4 view) or per contribution (0); the
-// environment variable SGAD_LATE_CHAIN=0 selects the latter (A/B)
-static int g_late_chain = [] {
-  const char* e = getenv("SGAD_LATE_CHAIN");
-  return e && e[0] == '0' ? 0 : 1;
-}();
 std::atomic<long long> g_launches{0};
 int g_debug_sync = [] {
   const char* e = getenv("SGAD_DEBUG_SYNC");
@@ -197,7 +201,7 @@ __device__ __forceinline__ bool project_point(const sgad_frame& f, int64_t p, co
 __global__ void __launch_bounds__(PROJ_THREADS, SGAD_PROJ_MINB)
 k_project(const sgad_frame* __restrict__ frames, sgad_camera cam, int ntx, int nty,
           int want_coef, Record* __restrict__ rec, TileBox* __restrict__ box,
-          ChainCoef* __restrict__ coef, double* __restrict__ col64,
+          BwdRecord* __restrict__ coef, double* __restrict__ col64,
           unsigned long long* __restrict__ zkey, uint32_t* __restrict__ counters,
           unsigned long long* __restrict__ zrange, uint32_t* __restrict__ tile_count) {
   // one block = 256 consecutive pixels of frame blockIdx.y; the frame
@@ -206,7 +210,7 @@ k_project(const sgad_frame* __restrict__ frames, sgad_camera cam, int ntx, int n
   // memory so the global stores are whole contiguous lines
   __shared__ sgad_frame fsh;
   __shared__ __align__(16) Record rs[PROJ_THREADS];
-  __shared__ __align__(16) ChainCoef cs[PROJ_THREADS];
+  __shared__ __align__(16) BwdRecord cs[PROJ_THREADS];
   __shared__ unsigned long long red_z[2][PROJ_THREADS / 32];
   __shared__ uint32_t red_n[PROJ_THREADS / 32];
   constexpr int FW = (int)(sizeof(sgad_frame) / 4);
@@ -271,17 +275,20 @@ k_project(const sgad_frame* __restrict__ frames, sgad_camera cam, int ntx, int n
       }
       box[gid] = bx;
       if (want_coef) {
-        ChainCoef c;
+        BwdRecord c;
         const double sgn = o.bd >= 0.0 ? 1.0 : -1.0;
         const double iz = 1.0 / o.z;
-        c.k_r = (float)(cam.fx * iz);
+        c.u0 = o.u0;
+        c.v0 = o.v0;
+        c.op = o.op;
+        c.nh = r.nh;
+        c.z = o.z;
+        c.r = r.r;
+        c.g = r.g;
+        c.b = r.b;
         c.a_u = (float)(sgn * cam.fx * iz * (o.dir[0] - o.dir[2] * o.y[0] * iz));
         c.a_v = (float)(sgn * cam.fy * iz * (o.dir[1] - o.dir[2] * o.y[1] * iz));
         c.a_z = (float)(sgn * o.dir[2]);
-        c.a_s = (float)(-sgn * o.dir[2] * o.sig * iz);
-        c.k_op = (float)(o.op * (1.0 - o.op));
-        c.pad_[0] = (float)(1.0 / o.sig);  // 1 / sigma for the late chain
-        c.pad_[1] = 0.0f;
         cs[threadIdx.x] = c;
       }
     }
@@ -349,7 +356,7 @@ k_project(const sgad_frame* __restrict__ frames, sgad_camera cam, int ntx, int n
   if (want_coef) {
     const uint4* src = reinterpret_cast<const uint4*>(cs);
     uint4* dst = reinterpret_cast<uint4*>(coef + gid0);
-    for (int i = threadIdx.x; i < nvalid * 2; i += PROJ_THREADS) dst[i] = src[i];
+    for (int i = threadIdx.x; i < nvalid * 4; i += PROJ_THREADS) dst[i] = src[i];
   }
 }
 
@@ -772,7 +779,27 @@ struct Contrib {
   double u0, v0, sig, op, z, nh;
   float r, g, b;
   uint32_t gid, e;
+  float a_u, a_v, a_z;  // chain coefficients (window backward)
 };
+
+// the window backward's 64-byte record (BwdRecord) as two 256-bit loads
+__device__ __forceinline__ void load_contrib_bwd(Contrib& q, const WarpRing& rg, int slot, int j,
+                                                 const BwdRecord* __restrict__ brec) {
+  q.e = rg.e[slot][j];
+  const double* rp = reinterpret_cast<const double*>(brec + q.e);
+  double r_g, b_au, av_az;
+  ld256(rp, q.u0, q.v0, q.op, q.nh);
+  ld256(rp + 4, q.z, r_g, b_au, av_az);
+  const float2 c = *reinterpret_cast<const float2*>(&r_g);
+  const float2 d = *reinterpret_cast<const float2*>(&b_au);
+  const float2 e = *reinterpret_cast<const float2*>(&av_az);
+  q.r = c.x;
+  q.g = c.y;
+  q.b = d.x;
+  q.a_u = d.y;
+  q.a_v = e.x;
+  q.a_z = e.y;
+}
 
 __device__ __forceinline__ void load_contrib(Contrib& q, const WarpRing& rg, int slot, int j,
                                              const Record* __restrict__ rec) {
@@ -1005,8 +1032,9 @@ k_forward(const uint2* __restrict__ ranges, const uint32_t* __restrict__ lists, 
 }
 
 // ------------------------------------------------------------------ K5
-struct Upstream {  // fused-loss upstream scales: rho / (3HW), sigma / |U|
+struct Upstream {  // fused-loss upstream scales: rho / (3HW), sigma / |U|; camera fx
   double kc, kd;
+  float fx;
 };
 
 __device__ __forceinline__ double sign_of(uint32_t code) {
@@ -1037,16 +1065,17 @@ __device__ __forceinline__ void red_add_v2(float* addr, float a, float b) {
 
 struct PixUpstream {
   double gc0, gc1, gc2, gd, ga;
+  float fx;  // target camera fx (the window backward's radius coefficient)
 };
 
 // rasterizer.py:272-363 (+ the fused chain of :462-483) for the warp's
 // pixels: reverse sweep from each pixel's last contributor with transmittance
 // T_final, walking a ring of windows per warp (K5)
-template <bool FUSED, bool LATE = false>
+template <bool FUSED>
 __device__ __forceinline__ void bwd_sweep(WarpRing& ring, const TileGeom& g, const SweepGeom& q,
                                           uint2 rg, const CList& cl,
                                           const Record* __restrict__ rec,
-                                          const ChainCoef* __restrict__ coef,
+                                          const BwdRecord* __restrict__ brec,
                                           const double* __restrict__ col64, const double* tab,
                                           const PixUpstream& u, double T, int mylast,
                                           double* __restrict__ raw,
@@ -1106,7 +1135,8 @@ __device__ __forceinline__ void bwd_sweep(WarpRing& ring, const TileGeom& g, con
     {
       const int j = __ffsll((long long)c.cur) - 1;
       c.cur &= c.cur - 1;
-      load_contrib(cc, ring, c.slot, j, rec);
+      if (FUSED) load_contrib_bwd(cc, ring, c.slot, j, brec);
+      else load_contrib(cc, ring, c.slot, j, rec);
     }
     {
       const uint32_t e = cc.e;
@@ -1126,7 +1156,7 @@ __device__ __forceinline__ void bwd_sweep(WarpRing& ring, const TileGeom& g, con
         c1 = __ldg(col64 + 3 * (size_t)e + 1);
         c2 = __ldg(col64 + 3 * (size_t)e + 2);
       }
-      if (cc.gid & GID_LEARN) {
+      if (FUSED || (cc.gid & GID_LEARN)) {  // (the window: every Gaussian learnable)
         // (the fused loss has no alpha upstream: its term is compiled out)
         double d_alpha = u.gc0 * (c0 * tb - sc0 * iom) + u.gc1 * (c1 * tb - sc1 * iom) +
                          u.gc2 * (c2 * tb - sc2 * iom) + u.gd * (z * tb - sd * iom);
@@ -1136,26 +1166,24 @@ __device__ __forceinline__ void bwd_sweep(WarpRing& ring, const TileGeom& g, con
         if (!clamped) {
           const double gw = d_alpha * op;
           gop = d_alpha * w;
-          // gw w d2 / (s2 sigma) = gw w d2 (-2 nh) / sigma; the late chain
-          // divides by sigma once per Gaussian (k_chain_late)
+          // gw w d2 / (s2 sigma) = gw w d2 (-2 nh) / sigma: the fused path
+          // keeps sigma g_sigma (its coefficients carry the 1 / sigma)
           gsig = gw * w * d2 * (-2.0 * nh);
-          if (!LATE) gsig *= fast_rcp(cc.sig);
+          if (!FUSED) gsig *= fast_rcp(cc.sig);
           const double gd2 = gw * w * nh;  // gw (-0.5 w / s2)
           gu = 2.0 * gd2 * dx;
           gv = 2.0 * gd2 * dy;
         }
-        if (FUSED && LATE) {
-          // image-space gradients; k_chain_late applies the chain rule per
-          // Gaussian after the sweep (grad_accum is the view's raw buffer)
+        if (FUSED) {
+          // rasterizer.py:462-483 with this view's coefficients: window
+          // gradients (delta, radius, logit, R, G, B) straight into grad_accum
+          // (gsig holds sigma g_sigma)
+          const float gs = (float)gsig, iz = (float)(1.0 / z);
+          const float g_delta = cc.a_u * (float)gu + cc.a_v * (float)gv + cc.a_z * (float)gz -
+                                cc.a_z * iz * gs;
+          const float g_radius = u.fx * sqrtf(-2.0f * (float)nh) * iz * gs;
           float* dst = grad_accum + (size_t)e * 8;
-          red_add_v4(dst, (float)gu, (float)gv, (float)gz, (float)gsig);
-          red_add_v4(dst + 4, (float)gop, (float)gcol0, (float)gcol1, (float)gcol2);
-        } else if (FUSED) {
-          const float4* cp = reinterpret_cast<const float4*>(coef + e);
-          const float4 k0 = __ldg(cp), k1 = __ldg(cp + 1);
-          float* dst = grad_accum + (size_t)(cc.gid & ~GID_LEARN) * 8;
-          red_add_v4(dst, (float)(k0.y * gu + k0.z * gv + k0.w * gz + k1.x * gsig),
-                     (float)(k0.x * gsig), (float)(k1.y * gop), (float)gcol0);
+          red_add_v4(dst, g_delta, g_radius, (float)(op * (1.0 - op) * gop), (float)gcol0);
           red_add_v2(dst + 4, (float)gcol1, (float)gcol2);
         } else {
           double* dst = raw + (size_t)e * 8;
@@ -1194,6 +1222,7 @@ __device__ __forceinline__ PixUpstream fused_upstream(uint32_t code, const doubl
   }
   u.gd = SG_MUL(up.kd, sign_of((code >> 6) & 3u));
   u.ga = 0.0;
+  u.fx = up.fx;
   return u;
 }
 
@@ -1201,10 +1230,10 @@ __device__ __forceinline__ bool any_upstream(const PixUpstream& u) {
   return !(u.gc0 == 0.0 && u.gc1 == 0.0 && u.gc2 == 0.0 && u.gd == 0.0 && u.ga == 0.0);
 }
 
-template <bool FUSED, bool LATE = false>
+template <bool FUSED>
 __global__ void __launch_bounds__(RASTER_THREADS)
 k_backward(const uint2* __restrict__ ranges, const uint32_t* __restrict__ lists,
-           const Record* __restrict__ rec, const ChainCoef* __restrict__ coef,
+           const Record* __restrict__ rec, const BwdRecord* __restrict__ coef,
            const double* __restrict__ col64, int ntx, int width, int height,
            const double* __restrict__ t_final, const int32_t* __restrict__ last_idx,
            const uint8_t* __restrict__ signs, Upstream up, const double* __restrict__ g_color,
@@ -1217,7 +1246,7 @@ k_backward(const uint2* __restrict__ ranges, const uint32_t* __restrict__ lists,
   const TileGeom g = tile_geom(ntx, width, height);
   const SweepGeom q = sweep_geom(g);
   const int64_t p = (int64_t)g.py * width + g.px;
-  PixUpstream u{0.0, 0.0, 0.0, 0.0, 0.0};
+  PixUpstream u{0.0, 0.0, 0.0, 0.0, 0.0, 0.0f};
   double T = 0.0;
   int mylast = -1;
   if (g.valid) {
@@ -1235,41 +1264,8 @@ k_backward(const uint2* __restrict__ ranges, const uint32_t* __restrict__ lists,
       T = t_final[p];
     }
   }
-  bwd_sweep<FUSED, LATE>(ring, g, q, ranges[g.tile], cl, rec, coef, col64, tab, u, T, mylast,
+  bwd_sweep<FUSED>(ring, g, q, ranges[g.tile], cl, rec, coef, col64, tab, u, T, mylast,
                          raw, grad_accum);
-}
-
-// Chain rule (rasterizer.py:462-483) per Gaussian for the late-chain fused
-// backward: raw image-space gradients (g_u0, g_v0, g_z, g_sigma, g_op,
-// g_rgb) -> window parameter gradients, added into grad_accum; the raw slot
-// is cleared for the next view.  One thread per Gaussian id, no atomics.
-__global__ void k_chain_late(float* __restrict__ raw, const ChainCoef* __restrict__ coef,
-                             const Record* __restrict__ rec, uint32_t n,
-                             float* __restrict__ grad_accum) {
-  const uint32_t e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= n) return;
-  float4* rp = reinterpret_cast<float4*>(raw + (size_t)e * 8);
-  const float4 r0 = rp[0], r1 = rp[1];
-  if (r0.x == 0.f && r0.y == 0.f && r0.z == 0.f && r0.w == 0.f && r1.x == 0.f && r1.y == 0.f &&
-      r1.z == 0.f && r1.w == 0.f)
-    return;  // not reached by this view (or culled)
-  const float4* cp = reinterpret_cast<const float4*>(coef + e);
-  const float4 k0 = __ldg(cp), k1 = __ldg(cp + 1);
-  const uint32_t gid = e;  // records and gradients are indexed by Gaussian id
-  const float gsig = r0.w * k1.z;  // the raw slot holds gsig * sigma; k1.z = 1 / sigma
-  float4* dst = reinterpret_cast<float4*>(grad_accum + (size_t)gid * 8);
-  float4 a = dst[0];
-  float2 b = *reinterpret_cast<float2*>(grad_accum + (size_t)gid * 8 + 4);
-  a.x += k0.y * r0.x + k0.z * r0.y + k0.w * r0.z + k1.x * gsig;  // delta
-  a.y += k0.x * gsig;                                             // radius
-  a.z += k1.y * r1.x;                                             // opacity logit
-  a.w += r1.y;
-  b.x += r1.z;
-  b.y += r1.w;
-  dst[0] = a;
-  *reinterpret_cast<float2*>(grad_accum + (size_t)gid * 8 + 4) = b;
-  rp[0] = make_float4(0.f, 0.f, 0.f, 0.f);
-  rp[1] = make_float4(0.f, 0.f, 0.f, 0.f);
 }
 
 // K4+K5 fused (tau = 0 window step): the tile's forward sweep, the L1 loss
@@ -1282,7 +1278,7 @@ constexpr size_t FB_SLAB = sizeof(WarpRing) > sizeof(FwdStage) ? sizeof(WarpRing
 
 __global__ void __launch_bounds__(RASTER_THREADS)
 k_forward_backward(const uint2* __restrict__ ranges, const uint32_t* __restrict__ lists,
-                   int packed, const Record* __restrict__ rec, const ChainCoef* __restrict__ coef, int ntx,
+                   int packed, const Record* __restrict__ rec, const BwdRecord* __restrict__ coef, int ntx,
                    int width, int height, sgad_loss_target tgt, Upstream up,
                    float* __restrict__ grad_accum, CList cl) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -1297,7 +1293,7 @@ k_forward_backward(const uint2* __restrict__ ranges, const uint32_t* __restrict_
   const int64_t p = (int64_t)g.py * width + g.px;
   const uint8_t code = loss_epilogue(st, g, p, tgt);
   __syncwarp();
-  PixUpstream u{0.0, 0.0, 0.0, 0.0, 0.0};
+  PixUpstream u{0.0, 0.0, 0.0, 0.0, 0.0, 0.0f};
   int mylast = -1;
   if (g.valid) {
     u = fused_upstream(code, nullptr, p, up);
@@ -1396,7 +1392,6 @@ static int smem_attrs() {
   SGAD_CHECK_CUDA(cudaFuncSetAttribute(k_forward<false, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FWD_SMEM));
   SGAD_CHECK_CUDA(cudaFuncSetAttribute(k_backward<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)BWD_SMEM));
   SGAD_CHECK_CUDA(cudaFuncSetAttribute(k_backward<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)BWD_SMEM));
-  SGAD_CHECK_CUDA(cudaFuncSetAttribute(k_backward<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)BWD_SMEM));
   SGAD_CHECK_CUDA(cudaFuncSetAttribute(k_forward_backward, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FB_SMEM));
   SGAD_CHECK_CUDA(cudaFuncSetAttribute(k_long_runs, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LONG_RUN_SMEM));
   done = 1;
@@ -1459,7 +1454,7 @@ int sgad_raster_destroy(sgad_raster* h) {
                     &h->vals0, &h->vals1, &h->pkeys0, &h->pkeys1, &h->pvals0,
                     &h->pvals1, &h->ranges, &h->sortws, &h->pairws, &h->trans_final, &h->last_idx, &h->signs,
                     &h->raw_grads, &h->rank_of, &h->scratch, &h->col64, &h->zrange, &h->k32a,
-                    &h->k32b, &h->bbox, &h->runs, &h->raw32, &h->cl_e, &h->cl_m, &h->cl_n};
+                    &h->k32b, &h->bbox, &h->runs, &h->cl_e, &h->cl_m, &h->cl_n};
   for (DevBuf* b : bufs) b->release();
   if (h->pinned) cudaFreeHost(h->pinned);
   delete h;
@@ -1584,7 +1579,7 @@ static int prepare_front(sgad_raster* h, const sgad_frame* frames, int32_t n_fra
   SGAD_CHECK_CUDA(h->frames.ensure(sizeof(sgad_frame) * n_frames));
   SGAD_CHECK_CUDA(h->records.ensure(sizeof(Record) * n_total));
   SGAD_CHECK_CUDA(h->bbox.ensure(sizeof(TileBox) * n_total));
-  if (want_coef) SGAD_CHECK_CUDA(h->coef.ensure(sizeof(ChainCoef) * n_total));
+  if (want_coef) SGAD_CHECK_CUDA(h->coef.ensure(sizeof(BwdRecord) * n_total));
   if (h->any_f64) SGAD_CHECK_CUDA(h->col64.ensure(sizeof(double) * 3 * n_total));
   SGAD_CHECK_CUDA(h->keys0.ensure(sizeof(unsigned long long) * n_total));
   SGAD_CHECK_CUDA(h->keys1.ensure(sizeof(unsigned long long) * n_total));
@@ -1610,7 +1605,7 @@ static int prepare_front(sgad_raster* h, const sgad_frame* frames, int32_t n_fra
   const dim3 pgrid((unsigned)((max_hw + PROJ_THREADS - 1) / PROJ_THREADS), (unsigned)n_frames);
   k_project<<<pgrid, PROJ_THREADS, 0, st>>>(
       h->frames.as<sgad_frame>(), *cam, h->ntx, h->nty, want_coef, h->records.as<Record>(),
-      h->bbox.as<TileBox>(), h->coef.as<ChainCoef>(), h->any_f64 ? h->col64.as<double>() : nullptr,
+      h->bbox.as<TileBox>(), h->coef.as<BwdRecord>(), h->any_f64 ? h->col64.as<double>() : nullptr,
       h->keys0.as<unsigned long long>(), cnt, h->zrange.as<unsigned long long>(), w.tcount);
   SGAD_LAUNCH_CHECK();
   // K2: digit histograms, onesweep passes (the permutation lands in vals0
@@ -1804,30 +1799,10 @@ int sgad_raster_backward(sgad_raster* h, int32_t mode, const double* g_color,
     Upstream up;
     up.kc = h->rho / (double)(3 * npx);
     up.kd = h->n_depth > 0 ? h->sigma_d / (double)h->n_depth : 0.0;
-    if (g_late_chain) {
-      // image-space gradients into the handle's raw buffer, then the chain
-      // rule per Gaussian (k_chain_late); the raw buffer is kept zeroed
-      const size_t bytes = sizeof(float) * 8 * (size_t)h->n_total;
-      if (h->raw32.cap < bytes || !h->raw32.p) {
-        SGAD_CHECK_CUDA(h->raw32.ensure(bytes));
-        SGAD_CHECK_CUDA(cudaMemsetAsync(h->raw32.p, 0, h->raw32.cap, st));
-      }
-      k_backward<true, true><<<grid, block, BWD_SMEM, st>>>(
-          h->ranges.as<uint2>(), h->pvals0.as<uint32_t>(), h->records.as<Record>(),
-          h->coef.as<ChainCoef>(), h->any_f64 ? h->col64.as<double>() : nullptr, h->ntx,
-          h->cam.width, h->cam.height, h->trans_final.as<double>(), h->last_idx.as<int32_t>(),
-          h->signs.as<uint8_t>(), up, g_color, nullptr, nullptr, nullptr, h->raw32.as<float>(),
-          clist_of(h));
-      SGAD_LAUNCH_CHECK();
-      k_chain_late<<<blocks_for(h->n_total, 256), 256, 0, st>>>(
-          h->raw32.as<float>(), h->coef.as<ChainCoef>(), h->records.as<Record>(),
-          (uint32_t)h->n_total, grad_accum);
-      SGAD_LAUNCH_CHECK();
-      return SGAD_OK;
-    }
+    up.fx = (float)h->cam.fx;
     k_backward<true><<<grid, block, BWD_SMEM, st>>>(
         h->ranges.as<uint2>(), h->pvals0.as<uint32_t>(), h->records.as<Record>(),
-        h->coef.as<ChainCoef>(), h->any_f64 ? h->col64.as<double>() : nullptr, h->ntx,
+        h->coef.as<BwdRecord>(), h->any_f64 ? h->col64.as<double>() : nullptr, h->ntx,
         h->cam.width, h->cam.height,
         h->trans_final.as<double>(), h->last_idx.as<int32_t>(), h->signs.as<uint8_t>(), up,
         g_color, nullptr, nullptr, nullptr, grad_accum, clist_of(h));
@@ -1843,7 +1818,7 @@ int sgad_raster_backward(sgad_raster* h, int32_t mode, const double* g_color,
   SGAD_CHECK_CUDA(h->scratch.ensure(sizeof(double*) * n_frames));
   SGAD_CHECK_CUDA(cudaMemcpyAsync(h->scratch.p, map_grads, sizeof(double*) * n_frames,
                                   cudaMemcpyHostToDevice, st));
-  Upstream up{0.0, 0.0};
+  Upstream up{0.0, 0.0, 0.0f};
   k_backward<false><<<grid, block, BWD_SMEM, st>>>(
       h->ranges.as<uint2>(), h->pvals0.as<uint32_t>(), h->records.as<Record>(), nullptr,
       h->any_f64 ? h->col64.as<double>() : nullptr, h->ntx, h->cam.width, h->cam.height, h->trans_final.as<double>(), h->last_idx.as<int32_t>(),
@@ -1874,9 +1849,10 @@ int sgad_raster_forward_backward(sgad_raster* h, const sgad_loss_target* target,
   Upstream up;
   up.kc = target->rho / (double)(3 * npx);
   up.kd = target->n_depth > 0 ? target->sigma / (double)target->n_depth : 0.0;
+  up.fx = (float)h->cam.fx;
   k_forward_backward<<<dim3((unsigned)h->n_tiles), dim3(RASTER_THREADS), FB_SMEM, st>>>(
       h->ranges.as<uint2>(), h->pvals0.as<uint32_t>(), h->packed, h->records.as<Record>(),
-      h->coef.as<ChainCoef>(), h->ntx, h->cam.width, h->cam.height, *target, up, grad_accum,
+      h->coef.as<BwdRecord>(), h->ntx, h->cam.width, h->cam.height, *target, up, grad_accum,
       clist_of(h));
   SGAD_LAUNCH_CHECK();
   h->forwarded = 0;
