@@ -108,9 +108,12 @@ int sgad_raster_prepare(sgad_raster* h, const sgad_frame* frames, int32_t n_fram
  * sgad_raster_reserve; at least 2 x Gaussians) the extra pairs are
  * dropped and *overflow_flag (device int32, may be NULL) is set to 1 --
  * the caller discards the view's results, reserves more and prepares again.
+ * frames_dev (device, may be NULL): a resident device copy of frames[] to
+ * use instead of uploading it (nothing is then read from host memory). 
  * Replaces the same reference functions as sgad_raster_prepare. */
 int sgad_raster_prepare_async(sgad_raster* h, const sgad_frame* frames, int32_t n_frames,
-                              const sgad_camera* cam, int32_t want_coef, uint32_t* counts_out,
+                              const sgad_camera* cam, int32_t want_coef,
+                              const sgad_frame* frames_dev, uint32_t* counts_out,
                               int32_t* overflow_flag, void* stream);
 
 /* Grow the handle's tile-pair capacity (buffers are resized at the next
@@ -165,11 +168,13 @@ int sgad_raster_tile_count(sgad_raster* h, int64_t* n_tiles);
  * opacity_logit, R, G, B); update_delta == 0 freezes the offsets.  skip
  * (device int32, may be NULL): when *skip != 0 the gradients are consumed
  * (zeroed) and nothing is updated (a window step whose preparation
- * overflowed, see sgad_raster_prepare_async). */
+ * overflowed, see sgad_raster_prepare_async).  step_dev (device int32, may
+ * be NULL; fp32 only): the step count t is read from device memory and bc1,
+ * bc2 are formed from it (a step captured in a CUDA graph). */
 int sgad_adam_step(void* params, void* grads, void* m, void* v, int64_t n_frames, int64_t hw,
                    const double* lr, double beta1, double beta2, double eps, double bc1,
                    double bc2, int32_t update_delta, int32_t f64, const int32_t* skip,
-                   void* stream);
+                   const int32_t* step_dev, void* stream);
 
 /* ---- render-based pose initialiser ------------------------------------
  * One IRLS linearisation of tracker.py:400-410: rows (device fp64 [12, n]) are

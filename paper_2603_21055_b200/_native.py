@@ -62,7 +62,7 @@ _SIGNATURES = {
     "sgad_raster_prepare": (_i32, [_vp, ctypes.POINTER(Frame), _i32, ctypes.POINTER(Camera), _i32,
                                    _vp, ctypes.POINTER(_i64), ctypes.POINTER(_i64)]),
     "sgad_raster_prepare_async": (_i32, [_vp, ctypes.POINTER(Frame), _i32, ctypes.POINTER(Camera),
-                                         _i32, _vp, _vp, _vp]),
+                                         _i32, _vp, _vp, _vp, _vp]),
     "sgad_raster_reserve": (_i32, [_vp, _i64]),
     "sgad_raster_forward": (_i32, [_vp, _vp, _vp, _vp, _vp, _i32, ctypes.POINTER(LossTarget), _vp]),
     "sgad_raster_backward": (_i32, [_vp, _i32, _vp, _vp, _vp, ctypes.POINTER(_vp), _vp, _vp]),
@@ -71,7 +71,7 @@ _SIGNATURES = {
     "sgad_raster_get_tiles": (_i32, [_vp, _vp, _vp, _vp]),
     "sgad_raster_tile_count": (_i32, [_vp, ctypes.POINTER(_i64)]),
     "sgad_adam_step": (_i32, [_vp, _vp, _vp, _vp, _i64, _i64, ctypes.POINTER(_f64), _f64, _f64,
-                              _f64, _f64, _f64, _i32, _i32, _vp, _vp]),
+                              _f64, _f64, _f64, _i32, _i32, _vp, _vp, _vp]),
     "sgad_sym_eigh3": (_i32, [_vp, _i64, _vp, _vp, _vp]),
     "sgad_track_fit": (_i32, [_vp, _vp, _i32, _i32, _f64, _f64, _f64, _f64, _i32, _i32, _i32, _i32,
                               _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),

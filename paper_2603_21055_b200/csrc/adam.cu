@@ -15,7 +15,20 @@ struct AdamArgs {
   double b1, b2, eps, bc1, bc2;
   int update_delta;
   const int32_t* skip;  // device flag: consume (zero) the gradients, update nothing
+  const int32_t* t_dev;  // device step count (fp32 window): bc1, bc2 from it, not from the host
 };
+
+// bias corrections 1 / (1 - beta^t) of the fp32 window update
+__device__ __forceinline__ void inv_bias(const AdamArgs& a, float& ib1, float& ib2) {
+  if (a.t_dev) {
+    const double t = (double)*a.t_dev;
+    ib1 = (float)(1.0 / (1.0 - pow(a.b1, t)));
+    ib2 = (float)(1.0 / (1.0 - pow(a.b2, t)));
+  } else {
+    ib1 = (float)(1.0 / a.bc1);
+    ib2 = (float)(1.0 / a.bc2);
+  }
+}
 
 template <typename P>
 __global__ void __launch_bounds__(256)
@@ -75,7 +88,8 @@ k_adam_f32(float* __restrict__ params, float* __restrict__ grads, float* __restr
   float* mf = m + f * 6 * hw + p;
   float* vf = v + f * 6 * hw + p;
   const float b1 = (float)a.b1, b2 = (float)a.b2, eps = (float)a.eps;
-  const float ib1 = (float)(1.0 / a.bc1), ib2 = (float)(1.0 / a.bc2);
+  float ib1, ib2;
+  inv_bias(a, ib1, ib2);
   // every load issued before any store (18 independent streams in flight)
   float m0[6], v0[6], p0[6];
 #pragma unroll
@@ -117,7 +131,8 @@ k_adam_f32x4(float* __restrict__ params, float* __restrict__ grads, float* __res
   float* mf = m + f * 6 * hw + p;
   float* vf = v + f * 6 * hw + p;
   const float b1 = (float)a.b1, b2 = (float)a.b2, eps = (float)a.eps;
-  const float ib1 = (float)(1.0 / a.bc1), ib2 = (float)(1.0 / a.bc2);
+  float ib1, ib2;
+  inv_bias(a, ib1, ib2);
   float4 m0[6], v0[6], p0[6];
 #pragma unroll
   for (int c = 0; c < 6; ++c) {
@@ -155,7 +170,7 @@ k_adam_f32x4(float* __restrict__ params, float* __restrict__ grads, float* __res
 extern "C" int sgad_adam_step(void* params, void* grads, void* m, void* v, int64_t n_frames,
                               int64_t hw, const double* lr, double beta1, double beta2, double eps,
                               double bc1, double bc2, int32_t update_delta, int32_t f64,
-                              const int32_t* skip, void* stream) {
+                              const int32_t* skip, const int32_t* step_dev, void* stream) {
   SGAD_REQUIRE(params && grads && m && v && lr && n_frames >= 0 && hw >= 0,
                "sgad_adam_step: bad arguments");
   const int64_t n = n_frames * hw;
@@ -169,6 +184,7 @@ extern "C" int sgad_adam_step(void* params, void* grads, void* m, void* v, int64
   a.bc2 = bc2;
   a.update_delta = update_delta;
   a.skip = skip;
+  a.t_dev = f64 ? nullptr : step_dev;
   const unsigned nb = (unsigned)((n + 255) / 256);
   if (f64)
     sgad::k_adam<double><<<nb, 256, 0, (cudaStream_t)stream>>>(

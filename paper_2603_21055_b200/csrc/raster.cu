@@ -1533,7 +1533,8 @@ static int ensure_pair_buffers(sgad_raster* h) {
 
 // K1 + K2 + the pair-count scan: independent of the pair capacity
 static int prepare_front(sgad_raster* h, const sgad_frame* frames, int32_t n_frames,
-                         const sgad_camera* cam, int32_t want_coef, cudaStream_t st) {
+                         const sgad_camera* cam, int32_t want_coef, const sgad_frame* frames_dev,
+                         cudaStream_t st) {
   SGAD_REQUIRE(h && cam && n_frames >= 0 && (n_frames == 0 || frames), "sgad_raster_prepare: bad args");
   SGAD_REQUIRE(cam->width > 0 && cam->height > 0, "sgad_raster_prepare: empty camera");
   if (int rc = smem_attrs()) return rc;
@@ -1576,7 +1577,7 @@ static int prepare_front(sgad_raster* h, const sgad_frame* frames, int32_t n_fra
   h->prepared = 1;
   if (n_total == 0) return SGAD_OK;
   const uint32_t ntot = (uint32_t)n_total;
-  SGAD_CHECK_CUDA(h->frames.ensure(sizeof(sgad_frame) * n_frames));
+  if (!frames_dev) SGAD_CHECK_CUDA(h->frames.ensure(sizeof(sgad_frame) * n_frames));
   SGAD_CHECK_CUDA(h->records.ensure(sizeof(Record) * n_total));
   SGAD_CHECK_CUDA(h->bbox.ensure(sizeof(TileBox) * n_total));
   if (want_coef) SGAD_CHECK_CUDA(h->coef.ensure(sizeof(BwdRecord) * n_total));
@@ -1593,8 +1594,14 @@ static int prepare_front(sgad_raster* h, const sgad_frame* frames, int32_t n_fra
   SGAD_CHECK_CUDA(h->sortws.ensure(sizeof(uint32_t) * w.words));
   w = prep_layout(h->sortws.as<uint32_t>(), h->dpasses, ntot, (uint32_t)h->n_tiles);
   SGAD_CHECK_CUDA(cudaMemsetAsync(w.ctr, 0, sizeof(uint32_t) * w.words, st));
-  SGAD_CHECK_CUDA(cudaMemcpyAsync(h->frames.p, frames, sizeof(sgad_frame) * n_frames,
-                                  cudaMemcpyHostToDevice, st));
+  // the frame table: the caller's device copy (resident: a step captured in a
+  // CUDA graph), or uploaded here
+  const sgad_frame* dframes = frames_dev;
+  if (!dframes) {
+    SGAD_CHECK_CUDA(cudaMemcpyAsync(h->frames.p, frames, sizeof(sgad_frame) * n_frames,
+                                    cudaMemcpyHostToDevice, st));
+    dframes = h->frames.as<sgad_frame>();
+  }
   SGAD_CHECK_CUDA(h->zrange.ensure(sizeof(unsigned long long) * 2));
   SGAD_CHECK_CUDA(cudaMemsetAsync(h->zrange.p, 0xff, sizeof(unsigned long long), st));
   SGAD_CHECK_CUDA(cudaMemsetAsync(h->zrange.as<unsigned long long>() + 1, 0, sizeof(unsigned long long), st));
@@ -1604,7 +1611,7 @@ static int prepare_front(sgad_raster* h, const sgad_frame* frames, int32_t n_fra
   // K1
   const dim3 pgrid((unsigned)((max_hw + PROJ_THREADS - 1) / PROJ_THREADS), (unsigned)n_frames);
   k_project<<<pgrid, PROJ_THREADS, 0, st>>>(
-      h->frames.as<sgad_frame>(), *cam, h->ntx, h->nty, want_coef, h->records.as<Record>(),
+      dframes, *cam, h->ntx, h->nty, want_coef, h->records.as<Record>(),
       h->bbox.as<TileBox>(), h->coef.as<BwdRecord>(), h->any_f64 ? h->col64.as<double>() : nullptr,
       h->keys0.as<unsigned long long>(), cnt, h->zrange.as<unsigned long long>(), w.tcount);
   SGAD_LAUNCH_CHECK();
@@ -1691,7 +1698,7 @@ int sgad_raster_prepare(sgad_raster* h, const sgad_frame* frames, int32_t n_fram
                         const sgad_camera* cam, int32_t want_coef, void* stream_,
                         int64_t* n_survivors, int64_t* n_pairs) {
   cudaStream_t st = (cudaStream_t)stream_;
-  if (int rc = prepare_front(h, frames, n_frames, cam, want_coef, st)) return rc;
+  if (int rc = prepare_front(h, frames, n_frames, cam, want_coef, nullptr, st)) return rc;
   if (int rc = prepare_pairs(h, nullptr, st)) return rc;
   h->n_surv = h->n_pairs = 0;
   if (h->n_total > 0) {
@@ -1714,10 +1721,11 @@ int sgad_raster_prepare(sgad_raster* h, const sgad_frame* frames, int32_t n_fram
 }
 
 int sgad_raster_prepare_async(sgad_raster* h, const sgad_frame* frames, int32_t n_frames,
-                              const sgad_camera* cam, int32_t want_coef, uint32_t* counts_out,
+                              const sgad_camera* cam, int32_t want_coef,
+                              const sgad_frame* frames_dev, uint32_t* counts_out,
                               int32_t* overflow_flag, void* stream_) {
   cudaStream_t st = (cudaStream_t)stream_;
-  if (int rc = prepare_front(h, frames, n_frames, cam, want_coef, st)) return rc;
+  if (int rc = prepare_front(h, frames, n_frames, cam, want_coef, frames_dev, st)) return rc;
   if (int rc = prepare_pairs(h, overflow_flag, st)) return rc;
   h->n_surv = h->n_pairs = -1;
   if (counts_out) {

@@ -66,12 +66,14 @@ class LossBreakdown:
     depth_l1: float
 
 
-def _adam(params, grads, m, v, n_frames, hw, cfg: MapperConfig, t: int, f64: bool, skip=None):
+def _adam(params, grads, m, v, n_frames, hw, cfg: MapperConfig, t: int, f64: bool, skip=None,
+          t_dev=None):
     lr = (ctypes.c_double * 6)(*cfg.lrs())
     b1, b2 = cfg.adam_beta1, cfg.adam_beta2
     N.call("sgad_adam_step", params.data_ptr(), grads.data_ptr(), m.data_ptr(), v.data_ptr(),
            int(n_frames), int(hw), lr, b1, b2, cfg.adam_eps, 1.0 - b1**t, 1.0 - b2**t,
-           0 if cfg.offset_frozen else 1, 1 if f64 else 0, N.ptr(skip), N.stream_ptr())
+           0 if cfg.offset_frozen else 1, 1 if f64 else 0, N.ptr(skip), N.ptr(t_dev),
+           N.stream_ptr())
 
 
 class MapOptimizer:
@@ -315,6 +317,8 @@ class WindowMapper:
         self.tmask = torch.from_numpy(np.stack([np.asarray(fr.valid_mask, bool)
                                                 for fr in frames]).astype(np.uint8)).to(dev)
         self.n_depth = [int(np.asarray(fr.valid_mask, bool).sum()) for fr in frames]
+        self._nd = (torch.tensor([max(n, 1) for n in self.n_depth], dtype=torch.float64, device=dev),
+                    torch.tensor([n > 0 for n in self.n_depth], device=dev))
         if views is None:
             dist = torch.distributed
             if dist.is_available() and dist.is_initialized():
@@ -336,7 +340,9 @@ class WindowMapper:
             self._gcol = torch.empty((h, w, 3), dtype=torch.float64, device=dev)
             self._ws = torch.empty(max(S.workspace_bytes(h, w, 3) // 8, 1), dtype=torch.float64,
                                    device=dev)
-        self.t = 0
+        # Adam's step count lives on the device (the bias corrections are
+        # formed there, so a step can be replayed from a CUDA graph)
+        self._t_dev = torch.zeros(1, dtype=torch.int32, device=dev)
         self.pg = process_group
         self.cam = camera_of(intr)
         learn = set(range(f))
@@ -351,6 +357,13 @@ class WindowMapper:
         self._cap = 0
         self._pending = []
         self.overflows = 0
+        # resident copies of every view's frame table (no host reads in a step)
+        self._frames_dev = {v: torch.frombuffer(bytearray(bytes(fr)), dtype=torch.uint8).to(dev)
+                            for v, fr in self._frames.items()}
+        # CUDA graph of the whole window step (use_graph: captured at the first
+        # step, replayed after; the per-view timing path stays eager)
+        self.use_graph = False
+        self._graph = None
         self.pipelined = True   # prepare view i+1 while view i composites
         self.adam_enabled = True
         # tau = 0: forward + loss + backward as one kernel (measured no faster
@@ -363,6 +376,15 @@ class WindowMapper:
         # the frames do not split evenly over the ranks
         self.shard_adam = True
         self._shard = None
+
+    @property
+    def t(self) -> int:
+        """Adam step count (device-resident; reading it synchronises)."""
+        return int(self._t_dev.item())
+
+    @t.setter
+    def t(self, value: int):
+        self._t_dev.fill_(int(value))
 
     @property
     def n_gaussians(self) -> int:
@@ -430,7 +452,7 @@ class WindowMapper:
                 prep.wait_event(used[i % 2])
             p0 = mark(prep)
             r.prepare_async(self._frames[v], self.cam, want_coef=True, counts=self._counts[v],
-                            overflow=self._flag, stream=prep)
+                            overflow=self._flag, stream=prep, frames_dev=self._frames_dev[v])
             p1 = mark(prep)
             main.wait_event(p1)
             if target_ready is not None and v in target_ready:
@@ -463,8 +485,8 @@ class WindowMapper:
 
     def _check_overflow(self, block: bool) -> bool:
         """Process the overflow flags of finished steps (all of them with
-        ``block``): a step that overflowed skipped its Adam update (its step
-        count is rolled back) and the capacity grows.  True if any did."""
+        ``block``): a step that overflowed skipped its Adam update on the
+        device (its step count too); the capacity grows.  True if any did."""
         hit = False
         while self._pending:
             ev, host, adam = self._pending[0]
@@ -476,12 +498,11 @@ class WindowMapper:
             if int(host[0]):
                 hit = True
                 self.overflows += 1
-                if adam:
-                    self.t -= 1
         if hit:
             torch.cuda.synchronize(self.dev)
             self._cap = int(self._cap * 1.5)
             self._size_handles()
+            self._graph = None  # buffers were resized: capture again
         return hit
 
     def counts(self):
@@ -493,12 +514,43 @@ class WindowMapper:
         """One window iteration: every assigned view fwd+bwd, gradient
         all-reduce across ranks, Adam.  Returns the summed loss (a device
         scalar unless ``sync_loss``).  ``target_ready`` ({view: CUDA event},
-        optional): a view composites only after its event."""
+        optional): a view composites only after its event.  With
+        ``use_graph`` the step is captured once in a CUDA graph and replayed
+        (not with ``timing`` / ``target_ready``, which stay eager)."""
         with torch.cuda.device(self.dev):
             if self.pipelined:
                 self._check_overflow(block=False)
                 if self._cap == 0:
                     self._size_handles()
+            if self.use_graph and self.pipelined and timing is None and target_ready is None:
+                loss = self._step_graphed()
+            else:
+                loss = self._step_body(timing, target_ready)
+        if sync_loss:
+            val = float(loss)
+            if self.pipelined and self._check_overflow(block=True):
+                return self.step(sync_loss=True, timing=timing, target_ready=target_ready)
+            return val
+        return loss
+
+    def _step_graphed(self):
+        """Replay the captured step (the first call runs the step eagerly --
+        sizes and allocations settle -- and captures it for the next calls)."""
+        if self._graph is None:
+            loss = self._step_body(None, None)
+            self._graph_host = torch.empty(1, dtype=torch.int32).pin_memory()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                self._graph_loss = self._step_body(None, None, host_flag=self._graph_host)
+            self._graph = g
+            return loss
+        self._graph.replay()
+        ev = torch.cuda.Event()
+        ev.record()
+        self._pending.append((ev, self._graph_host, self.adam_enabled))
+        return self._graph_loss
+
+    def _step_body(self, timing=None, target_ready=None, host_flag=None):
         self.loss_acc.zero_()
         self._flag.zero_()
         adam = self.adam_enabled
@@ -535,32 +587,27 @@ class WindowMapper:
                 if self.adam_enabled:  # (tests inspect the reduced gradient with it off)
                     self.apply_adam()
             if self.pipelined:
-                host = torch.empty(1, dtype=torch.int32).pin_memory()
+                capturing = host_flag is not None
+                host = host_flag if capturing else torch.empty(1, dtype=torch.int32).pin_memory()
                 host.copy_(self._flag, non_blocking=True)
-                ev = torch.cuda.Event()
-                ev.record()
-                self._pending.append((ev, host, adam))
+                if not capturing:
+                    ev = torch.cuda.Event()
+                    ev.record()
+                    self._pending.append((ev, host, adam))
         n_color = 3.0 * self.HW
-        nd = torch.tensor([max(n, 1) for n in self.n_depth], dtype=torch.float64, device=self.dev)
-        has_d = torch.tensor([n > 0 for n in self.n_depth], device=self.dev)
+        nd, has_d = self._nd
         ssim_term = (1.0 - self.loss_acc[:, 2] / n_color) if self.cfg.tau != 0.0 else 0.0
-        loss = (self.cfg.rho * self.loss_acc[:, 0] / n_color + self.cfg.tau * ssim_term +
+        return (self.cfg.rho * self.loss_acc[:, 0] / n_color + self.cfg.tau * ssim_term +
                 self.cfg.sigma * torch.where(has_d, self.loss_acc[:, 1] / nd,
                                              torch.zeros_like(nd))).sum()
-        if sync_loss:
-            val = float(loss)
-            if self.pipelined and self._check_overflow(block=True):
-                return self.step(sync_loss=True, timing=timing, target_ready=target_ready)
-            return val
-        return loss
 
     def apply_adam(self):
         """One Adam step of the whole window from the (reduced) gradient
         buffer, which it consumes (zeroes)."""
         with torch.cuda.device(self.dev):
-            self.t += 1
-            _adam(self.planes, self.grad, self.m, self.v, self.F, self.HW, self.cfg, self.t, False,
-                  skip=self._flag)
+            self._t_dev.add_(1 - self._flag)  # (a step that overflowed does not count)
+            _adam(self.planes, self.grad, self.m, self.v, self.F, self.HW, self.cfg, 1, False,
+                  skip=self._flag, t_dev=self._t_dev)
 
     def _sharded(self) -> bool:
         dist = torch.distributed
@@ -582,9 +629,9 @@ class WindowMapper:
         f0, f1, local, stage = self._shard
         reduce_scatter_window(self.grad, local, self.loss_acc, self.pg)
         self.grad.zero_()  # this step's contributions are all in the scattered blocks
-        self.t += 1
+        self._t_dev.add_(1 - self._flag)
         _adam(self.planes[f0:f1], local, self.m[f0:f1], self.v[f0:f1], f1 - f0, self.HW,
-              self.cfg, self.t, False, skip=self._flag)
+              self.cfg, 1, False, skip=self._flag, t_dev=self._t_dev)
         allgather_planes(self.planes, stage, f0, f1, self.pg)
 
     def grads_numpy(self):

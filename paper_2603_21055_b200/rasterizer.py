@@ -90,14 +90,18 @@ class Raster:
         self.n_surv, self.n_pairs = ns.value, npairs.value
         return self.n_surv, self.n_pairs
 
-    def prepare_async(self, frames, cam, want_coef=False, counts=None, overflow=None, stream=None):
+    def prepare_async(self, frames, cam, want_coef=False, counts=None, overflow=None, stream=None,
+                      frames_dev=None):
         """The preparation without host synchronisation: ``counts`` (device
         int32[2], optional) receives (survivors, pairs); ``overflow`` (device
         int32[1], optional) is set to 1 if the view has more tile pairs than
-        the reserved capacity (its results are then invalid)."""
+        the reserved capacity (its results are then invalid); ``frames_dev``
+        (optional device tensor holding ``frames``' bytes) is used instead of
+        uploading the frame table (CUDA-graph capture)."""
         self._frames = frames
         N.check(N.load().sgad_raster_prepare_async(self.h, frames, len(frames), ctypes.byref(cam),
-                                                   int(want_coef), N.ptr(counts), N.ptr(overflow),
+                                                   int(want_coef), N.ptr(frames_dev),
+                                                   N.ptr(counts), N.ptr(overflow),
                                                    N.stream_ptr(stream)))
         self.cam = cam
         self.n_surv = self.n_pairs = -1

@@ -466,3 +466,21 @@ def test_c4_full_size_images_vs_oracle():
     np.testing.assert_array_equal(out.color.cpu().numpy(), ref.color)
     np.testing.assert_array_equal(out.depth.cpu().numpy(), ref.depth)
     np.testing.assert_array_equal(out.alpha.cpu().numpy(), ref.alpha)
+
+
+def test_window_step_cuda_graph_matches_eager():
+    """The window step captured in a CUDA graph (use_graph) and replayed:
+    the same losses, step count and parameters as eager steps (fp32
+    gradient sums in another order: 1e-5)."""
+    from paper_2603_21055_b200.mapper import MapperConfig, WindowMapper
+    wc = _window_np(n_frames=4, seed=12)
+    runs = {}
+    for graph in (False, True):
+        wm = WindowMapper(wc.frames, wc.poses, wc.intr, wc.params, MapperConfig(tau=0.0))
+        wm.use_graph = graph
+        losses = [wm.step(sync_loss=True) for _ in range(4)]
+        runs[graph] = (np.array(losses), wm.t, wm.planes.cpu().numpy(), wm._graph is not None)
+    assert runs[True][3] and not runs[False][3]
+    assert runs[True][1] == runs[False][1] == 4
+    np.testing.assert_allclose(runs[True][0], runs[False][0], rtol=1e-5)
+    np.testing.assert_allclose(runs[True][2], runs[False][2], rtol=0, atol=2e-3)
