@@ -1032,6 +1032,36 @@ k_forward(const uint2* __restrict__ ranges, const uint32_t* __restrict__ lists, 
 }
 
 // ------------------------------------------------------------------ K5
+// The exact drop-in backward sums its per-Gaussian fp64 gradients in 128-bit
+// fixed point (resolution 2^-100, |sum| < 2^27): integer addition is
+// associative, so the sums -- and the map gradients, map_frame's
+// trajectories and map files -- are bit-identical run to run whatever order
+// the atomics land in (the reference's gradients are deterministic,
+// reference tests/test_pipeline.py:76-85).  Each contribution loses at most
+// 2^-100 absolute (8e-31: the chain rule multiplies the image-space sums by
+// up to fx y / z^2 and subtracts them, so the sums need resolution far below
+// the gradients' own ulp); the window engine's fp32 path keeps fp32 atomics.
+struct Fx128 {
+  unsigned long long lo;
+  long long hi;  // value = (hi 2^64 + lo) 2^-100
+};
+
+__device__ __forceinline__ void fx_add(Fx128* dst, double x) {
+  const double t = x * 0x1p36;  // x 2^36 (exact)
+  const double hf = floor(t);
+  long long hi = (long long)hf;
+  const unsigned long long lo = (unsigned long long)((t - hf) * 18446744073709551616.0);
+  if (lo) {
+    const unsigned long long old = atomicAdd(&dst->lo, lo);
+    if (old + lo < old) ++hi;  // the low word wrapped: carry
+  }
+  if (hi) atomicAdd(reinterpret_cast<unsigned long long*>(&dst->hi), (unsigned long long)hi);
+}
+
+__device__ __forceinline__ double fx_value(const Fx128& v) {
+  return (double)v.hi * 0x1p-36 + (double)v.lo * 0x1p-100;
+}
+
 struct Upstream {  // fused-loss upstream scales: rho / (3HW), sigma / |U|; camera fx
   double kc, kd;
   float fx;
@@ -1078,7 +1108,7 @@ __device__ __forceinline__ void bwd_sweep(WarpRing& ring, const TileGeom& g, con
                                           const BwdRecord* __restrict__ brec,
                                           const double* __restrict__ col64, const double* tab,
                                           const PixUpstream& u, double T, int mylast,
-                                          double* __restrict__ raw,
+                                          Fx128* __restrict__ raw,
                                           float* __restrict__ grad_accum) {
   int wend = mylast + 1;
 #pragma unroll
@@ -1186,15 +1216,15 @@ __device__ __forceinline__ void bwd_sweep(WarpRing& ring, const TileGeom& g, con
           red_add_v4(dst, g_delta, g_radius, (float)(op * (1.0 - op) * gop), (float)gcol0);
           red_add_v2(dst + 4, (float)gcol1, (float)gcol2);
         } else {
-          double* dst = raw + (size_t)e * 8;
-          atomicAdd(dst + 0, gcol0);
-          atomicAdd(dst + 1, gcol1);
-          atomicAdd(dst + 2, gcol2);
-          atomicAdd(dst + 3, gop);
-          atomicAdd(dst + 4, gu);
-          atomicAdd(dst + 5, gv);
-          atomicAdd(dst + 6, gsig);
-          atomicAdd(dst + 7, gz);
+          Fx128* dst = raw + (size_t)e * 8;
+          fx_add(dst + 0, gcol0);
+          fx_add(dst + 1, gcol1);
+          fx_add(dst + 2, gcol2);
+          fx_add(dst + 3, gop);
+          fx_add(dst + 4, gu);
+          fx_add(dst + 5, gv);
+          fx_add(dst + 6, gsig);
+          fx_add(dst + 7, gz);
         }
       }
       sc0 = fma(c0, at, sc0);
@@ -1238,7 +1268,7 @@ k_backward(const uint2* __restrict__ ranges, const uint32_t* __restrict__ lists,
            const double* __restrict__ t_final, const int32_t* __restrict__ last_idx,
            const uint8_t* __restrict__ signs, Upstream up, const double* __restrict__ g_color,
            const double* __restrict__ g_depth, const double* __restrict__ g_alpha,
-           double* __restrict__ raw, float* __restrict__ grad_accum, CList cl) {
+           Fx128* __restrict__ raw, float* __restrict__ grad_accum, CList cl) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   WarpRing& ring = reinterpret_cast<WarpRing*>(smem_raw)[threadIdx.x >> 5];
   __shared__ double tab[SGAD_EXP2_TABLE_N];
@@ -1304,7 +1334,7 @@ k_forward_backward(const uint2* __restrict__ ranges, const uint32_t* __restrict_
 }
 
 // Exact-mode chain rule (rasterizer.py:462-483) from per-survivor fp64 sums.
-__global__ void k_chain_exact(const Record* __restrict__ rec, const double* __restrict__ raw,
+__global__ void k_chain_exact(const Record* __restrict__ rec, const Fx128* __restrict__ raw,
                               const uint32_t* __restrict__ perm, uint32_t n_surv,
                               const sgad_frame* __restrict__ frames, int n_frames,
                               sgad_camera cam, double* const* __restrict__ map_grads) {
@@ -1322,7 +1352,10 @@ __global__ void k_chain_exact(const Record* __restrict__ rec, const double* __re
   const int64_t p = (int64_t)gid - f.gauss_offset;
   Proj o;
   project_point(f, p, load_params(f, p, hw), cam, o);
-  const double* rg = raw + (size_t)e * 8;
+  const Fx128* rf = raw + (size_t)e * 8;
+  double rg[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) rg[k] = fx_value(rf[k]);
   const double g_op = rg[3], g_u0 = rg[4], g_v0 = rg[5], g_sig = rg[6], g_z = rg[7];
   const double z = o.z, z2 = SG_MUL(z, z);
   const double g_radius = SG_DIV(SG_MUL(g_sig, cam.fx), z);
@@ -1821,8 +1854,8 @@ int sgad_raster_backward(sgad_raster* h, int32_t mode, const double* g_color,
                "exact backward needs upstream images and map_grads");
   SGAD_REQUIRE(h->n_surv >= 0, "exact backward needs a synchronous sgad_raster_prepare");
   const int n_frames = (int)h->host_frames.size();
-  SGAD_CHECK_CUDA(h->raw_grads.ensure(sizeof(double) * 8 * h->n_total));
-  SGAD_CHECK_CUDA(cudaMemsetAsync(h->raw_grads.p, 0, sizeof(double) * 8 * h->n_total, st));
+  SGAD_CHECK_CUDA(h->raw_grads.ensure(sizeof(Fx128) * 8 * h->n_total));
+  SGAD_CHECK_CUDA(cudaMemsetAsync(h->raw_grads.p, 0, sizeof(Fx128) * 8 * h->n_total, st));
   SGAD_CHECK_CUDA(h->scratch.ensure(sizeof(double*) * n_frames));
   SGAD_CHECK_CUDA(cudaMemcpyAsync(h->scratch.p, map_grads, sizeof(double*) * n_frames,
                                   cudaMemcpyHostToDevice, st));
@@ -1830,10 +1863,10 @@ int sgad_raster_backward(sgad_raster* h, int32_t mode, const double* g_color,
   k_backward<false><<<grid, block, BWD_SMEM, st>>>(
       h->ranges.as<uint2>(), h->pvals0.as<uint32_t>(), h->records.as<Record>(), nullptr,
       h->any_f64 ? h->col64.as<double>() : nullptr, h->ntx, h->cam.width, h->cam.height, h->trans_final.as<double>(), h->last_idx.as<int32_t>(),
-      nullptr, up, g_color, g_depth, g_alpha, h->raw_grads.as<double>(), nullptr, clist_of(h));
+      nullptr, up, g_color, g_depth, g_alpha, h->raw_grads.as<Fx128>(), nullptr, clist_of(h));
   SGAD_LAUNCH_CHECK();
   k_chain_exact<<<blocks_for(h->n_surv, 256), 256, 0, st>>>(
-      h->records.as<Record>(), h->raw_grads.as<double>(), h->vals0.as<uint32_t>(),
+      h->records.as<Record>(), h->raw_grads.as<Fx128>(), h->vals0.as<uint32_t>(),
       (uint32_t)h->n_surv, h->frames.as<sgad_frame>(), n_frames, h->cam, h->scratch.as<double*>());
   SGAD_LAUNCH_CHECK();
   // the pointer table is read by the kernel; keep the host copy alive until done

@@ -137,3 +137,29 @@ def test_gpu_map_frame(golden):
     np.testing.assert_allclose(losses, g["mf_losses"], rtol=1e-3)
     np.testing.assert_array_equal(gmap.active_mask.cpu().numpy(), g["mf_active_mask"])
     np.testing.assert_allclose(gmap.base_depth.cpu().numpy(), g["mf_base_depth"], atol=1e-9)
+
+
+@pytest.mark.gpu
+def test_gpu_map_frame_deterministic(golden, tmp_path):
+    """Run twice, map_frame gives byte-identical maps and map files (the
+    reference's pipeline is bit-reproducible across runs and worker counts,
+    reference tests/test_pipeline.py:76-85): the exact backward sums in
+    integer fixed point, so atomic ordering cannot change a bit."""
+    from paper_2603_21055_b200.gaussians import save_gaussian_map
+    from paper_2603_21055_b200.geometry import Pose
+    from paper_2603_21055_b200.mapper import MapperConfig, map_frame
+    from paper_2603_21055_b200.scenes import Frame
+    g = golden("frame_driver")
+    intr, fa, fb, map_a, truth = _gpu_case()
+    fr_b = Frame(fb.color, g["target_depth"], g["target_valid"], intr, index=1)
+    fr_a = Frame(fa.color, fa.depth, fa.valid_mask, intr, index=0)
+    outs = []
+    for k in range(2):
+        gmap, losses = map_frame(fr_b, truth, [(fr_a, Pose.identity(), map_a)],
+                                 MapperConfig(mapping_iters=6), seed=0)
+        path = tmp_path / f"m{k}.bin"
+        save_gaussian_map(str(path), gmap)
+        outs.append((gmap.planes.cpu().numpy().tobytes(), path.read_bytes(), losses))
+    assert outs[0][0] == outs[1][0]
+    assert outs[0][1] == outs[1][1]
+    np.testing.assert_allclose(outs[0][2], outs[1][2], rtol=1e-14)
