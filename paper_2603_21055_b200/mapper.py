@@ -433,13 +433,14 @@ class WindowMapper:
         compositing until its target has arrived (targets uploaded while
         earlier views composite)."""
         if self._pipe is None:
-            self._pipe = ([Raster(self.dev), Raster(self.dev)], torch.cuda.Stream(self.dev))
+            self._new_pipe()
         rasters, prep = self._pipe
+        nh = len(rasters)
         main = torch.cuda.current_stream(self.dev)
         ev = torch.cuda.Event()
         ev.record(main)           # parameters / loss accumulators are ready
         prep.wait_event(ev)
-        used = [None, None]       # compositing done on each handle
+        used = [None] * nh        # compositing done on each handle
 
         def mark(stream):
             e = torch.cuda.Event(enable_timing=timing is not None)
@@ -448,8 +449,8 @@ class WindowMapper:
 
         for i, v in enumerate(self.views):
             r = rasters[i % 2]
-            if used[i % 2] is not None:
-                prep.wait_event(used[i % 2])
+            if used[i % nh] is not None:
+                prep.wait_event(used[i % nh])
             p0 = mark(prep)
             r.prepare_async(self._frames[v], self.cam, want_coef=True, counts=self._counts[v],
                             overflow=self._flag, stream=prep, frames_dev=self._frames_dev[v])
@@ -466,13 +467,18 @@ class WindowMapper:
                     timing.append(("fb", f0, b1, v))
                 else:
                     timing += [("fwd", f0, f1, v), ("bwd", f1, b1, v)]
-            used[i % 2] = mark(main)
+            used[i % nh] = mark(main)
+
+    def _new_pipe(self):
+        import os
+        n = max(2, int(os.environ.get("SGAD_HANDLES", "2")))  # (A/B: views prepared ahead + 1)
+        self._pipe = ([Raster(self.dev) for _ in range(n)], torch.cuda.Stream(self.dev))
 
     def _size_handles(self):
         """Pair capacity of the pipelined raster handles: every view prepared
         once synchronously, capacity = 1.3 x the largest pair count."""
         if self._pipe is None:
-            self._pipe = ([Raster(self.dev), Raster(self.dev)], torch.cuda.Stream(self.dev))
+            self._new_pipe()
         r = self._pipe[0][0]
         most = 0
         for v in self.views:
