@@ -260,6 +260,13 @@ int sgad_track_normal_eqs(sgad_geomset* g, const double* local_centers, const do
  * sgad_track_normal_eqs call (device uint8 [m]). */
 int sgad_track_accepted(sgad_geomset* g, uint8_t* out, int64_t m, void* stream);
 
+/* The last sgad_track_normal_eqs call's exact nearest neighbours (device
+ * int64 [m]; tracker.py:288 j).  Across GICP iterations a query whose old
+ * neighbour is provably still the unique nearest (it moved by delta, every
+ * other point was >= d2 away at its last full search, and the old neighbour
+ * is now closer than d2 - delta) skips the search. */
+int sgad_track_correspondences(sgad_geomset* g, int64_t* idx, int64_t m, void* stream);
+
 /* Frozen-weight cost sum_i (b_i - T a_i)^T W_i (b_i - T a_i) for n_cand poses
  * (poses: host array [n_cand, 12], rot row-major then trans) -> out[n_cand]
  * (device). */

@@ -82,6 +82,7 @@ _SIGNATURES = {
     "sgad_track_normal_eqs": (_i32, [_vp, _vp, _vp, _i64, ctypes.POINTER(_f64),
                                      ctypes.POINTER(_f64), _i32, _f64, _i32, _vp, _vp]),
     "sgad_track_accepted": (_i32, [_vp, _vp, _i64, _vp]),
+    "sgad_track_correspondences": (_i32, [_vp, _vp, _i64, _vp]),
     "sgad_track_cost": (_i32, [_vp, _vp, _i64, ctypes.POINTER(_f64), _i32, _vp, _vp]),
 }
 

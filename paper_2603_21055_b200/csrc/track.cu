@@ -468,9 +468,12 @@ __device__ __forceinline__ int hash_find(const LevelView& v, unsigned long long 
 }
 
 // Bounded ring search on one level, refining (best_j, best_d2); returns
-// false if MAX_RINGS rings did not settle it.
+// false if MAX_RINGS rings did not settle it.  `second` accumulates a lower
+// bound on the squared distance of every point other than best_j: exact
+// distances of the points scanned, the cell bound of every pruned cell and,
+// once settled, the distance to the unvisited region.
 __device__ bool grid_nearest(const LevelView& v, const double* pts, const double* q,
-                             int64_t& best_j, double& best_d2) {
+                             int64_t& best_j, double& best_d2, double& second) {
   const Grid& g = v.g;
   int c0[3];
   for (int k = 0; k < 3; ++k) c0[k] = cell_coord(q[k], g.lo[k], g.h, g.dim[k]);
@@ -489,17 +492,25 @@ __device__ bool grid_nearest(const LevelView& v, const double* pts, const double
             continue;
           }
           const double bz0 = g.lo[2] + z * g.h, bz = fmax(fmax(bz0 - q[2], q[2] - (bz0 + g.h)), 0.0);
-          if (bx * bx + by * by + bz * bz > best_d2) continue;
+          const double bmin = bx * bx + by * by + bz * bz;
+          if (bmin > best_d2) {
+            second = fmin(second, bmin);  // (a non-empty pruned cell: all its points beyond bmin)
+            continue;
+          }
           const int c = hash_find(v, cell_key(x, y, z));
           if (c < 0) continue;
           for (uint32_t t = v.start[c]; t < v.start[c + 1]; ++t) {
             const uint32_t j = v.items[t];
+            if ((int64_t)j == best_j) continue;
             const double dx = q[0] - pts[3 * j], dy = q[1] - pts[3 * j + 1],
                          dz = q[2] - pts[3 * j + 2];
             const double d2 = dx * dx + dy * dy + dz * dz;
             if (d2 < best_d2 || (d2 == best_d2 && (int64_t)j < best_j)) {
+              second = fmin(second, best_d2);
               best_d2 = d2;
               best_j = j;
+            } else {
+              second = fmin(second, d2);
             }
           }
         }
@@ -521,7 +532,10 @@ __device__ bool grid_nearest(const LevelView& v, const double* pts, const double
       }
     }
     if (all_sat) return true;
-    if (best_j >= 0 && best_d2 < lb * lb) return true;
+    if (best_j >= 0 && best_d2 < lb * lb) {
+      second = fmin(second, lb * lb);
+      return true;
+    }
   }
   return false;
 }
@@ -536,6 +550,10 @@ struct NNArgs {
   double* d2;
   uint32_t* unresolved;   // [m] list, count in *n_unres
   uint32_t* n_unres;
+  // persistence test (GICP iterations): the query position of the last full
+  // search and a lower bound on its second-nearest squared distance
+  double* q_prev;         // [m, 3] or null
+  double* second;         // [m]
 };
 
 __device__ __forceinline__ void query_point(const NNArgs& a, int64_t i, double* p) {
@@ -567,16 +585,44 @@ __global__ void k_nearest(GridView v, NNArgs a) {
     j = a.idx[i];
     const double dx = q[0] - v.pts[3 * j], dy = q[1] - v.pts[3 * j + 1], dz = q[2] - v.pts[3 * j + 2];
     d2 = dx * dx + dy * dy + dz * dz;
+    if (a.q_prev) {
+      // persistence: the query moved by delta since its last full search,
+      // where every other point was at least sqrt(second) away; so they are
+      // now at least sqrt(second) - delta away, and if the old neighbour is
+      // strictly closer than that it is still the unique nearest (exact)
+      const double* qp = a.q_prev + 3 * i;
+      const double ex = q[0] - qp[0], ey = q[1] - qp[1], ez = q[2] - qp[2];
+      const double low = sqrt(a.second[i]) - sqrt(ex * ex + ey * ey + ez * ez);
+      if (low > 0.0 && sqrt(d2) < low * (1.0 - 1e-12)) {
+        a.idx[i] = j;
+        a.d2[i] = d2;
+        a.second[i] = low * low * (1.0 - 1e-12);
+        double* qw = a.q_prev + 3 * i;
+        qw[0] = q[0];
+        qw[1] = q[1];
+        qw[2] = q[2];
+        return;
+      }
+    }
     const double reach = sqrt(d2);
     while (l0 < NLEV - 1 && MAX_RINGS * v.lv[l0].g.h < reach) ++l0;
   }
+  double second = INFINITY;
   for (int l = l0; l < NLEV; ++l) {
-    if (grid_nearest(v.lv[l], v.pts, q, j, d2)) {
+    if (grid_nearest(v.lv[l], v.pts, q, j, d2, second)) {
       a.idx[i] = j;
       a.d2[i] = d2;
+      if (a.q_prev) {
+        double* qw = a.q_prev + 3 * i;
+        qw[0] = q[0];
+        qw[1] = q[1];
+        qw[2] = q[2];
+        a.second[i] = second;
+      }
       return;
     }
   }
+  if (a.q_prev) a.second[i] = 0.0;  // (resolved by the brute force: no bound kept)
   a.unresolved[atomicAdd(a.n_unres, 1u)] = (uint32_t)i;
 }
 
@@ -822,7 +868,7 @@ __global__ void k_sqrt(const double* __restrict__ x, int64_t n, double* __restri
 struct sgad_geomset {
   sgad::DevBuf pts, cov, nrm, bbox, keys0, keys1, idx0, idx1, head, headscan, start, hkeys, hvals,
       cub_tmp;
-  sgad::DevBuf w, b, acc, partial, poses, nn_j, nn_d2, unres, counter;
+  sgad::DevBuf w, b, acc, partial, poses, nn_j, nn_d2, unres, counter, nn_qprev, nn_second;
   sgad::Grid grid[sgad::NLEV]{};
   sgad::DevBuf lhkeys[sgad::NLEV], lhvals[sgad::NLEV], lstart[sgad::NLEV], litems[sgad::NLEV];
   int64_t n = 0;
@@ -886,7 +932,7 @@ int sgad_geomset_destroy(sgad_geomset* g) {
   DevBuf* bufs[] = {&g->pts, &g->cov, &g->nrm, &g->bbox, &g->keys0, &g->keys1, &g->idx0,
                     &g->idx1, &g->head, &g->headscan, &g->start, &g->hkeys, &g->hvals,
                     &g->cub_tmp, &g->w, &g->b, &g->acc, &g->partial, &g->poses, &g->nn_j,
-                    &g->nn_d2, &g->unres, &g->counter};
+                    &g->nn_d2, &g->unres, &g->counter, &g->nn_qprev, &g->nn_second};
   for (DevBuf* b : bufs) b->release();
   for (int l = 0; l < NLEV; ++l) {
     g->lhkeys[l].release();
@@ -1043,9 +1089,19 @@ static GridView view_of(sgad_geomset* g) {
   return v;
 }
 
+// SGAD_NN_PERSIST=0 (A/B): every GICP iteration searches every query afresh
+static bool nn_persist() {
+  static const bool on = [] {
+    const char* e = getenv("SGAD_NN_PERSIST");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 // exact 1-NN for m queries (optionally transformed by rot/trans) into idx/d2
 static int run_nearest(sgad_geomset* g, const double* queries, int64_t m, const double* rot,
-                       const double* trans, int64_t* idx, double* d2, int warm, cudaStream_t st) {
+                       const double* trans, int64_t* idx, double* d2, int warm, cudaStream_t st,
+                       bool persist = false) {
   SGAD_CHECK_CUDA(g->unres.ensure(sizeof(uint32_t) * m));
   SGAD_CHECK_CUDA(g->counter.ensure(sizeof(uint32_t) * 4));
   SGAD_CHECK_CUDA(cudaMemsetAsync(g->counter.p, 0, sizeof(uint32_t), st));
@@ -1060,6 +1116,14 @@ static int run_nearest(sgad_geomset* g, const double* queries, int64_t m, const 
   a.d2 = d2;
   a.unresolved = g->unres.as<uint32_t>();
   a.n_unres = g->counter.as<uint32_t>();
+  a.q_prev = nullptr;
+  a.second = nullptr;
+  if (persist) {
+    SGAD_CHECK_CUDA(g->nn_qprev.ensure(sizeof(double) * 3 * m));
+    SGAD_CHECK_CUDA(g->nn_second.ensure(sizeof(double) * m));
+    a.q_prev = g->nn_qprev.as<double>();
+    a.second = g->nn_second.as<double>();
+  }
   const GridView v = view_of(g);
   k_nearest<<<nblk(m, 128), 128, 0, st>>>(v, a);
   SGAD_LAUNCH_CHECK();
@@ -1101,7 +1165,7 @@ int sgad_track_normal_eqs(sgad_geomset* g, const double* local_centers, const do
   SGAD_CHECK_CUDA(g->nn_d2.ensure(sizeof(double) * m));
   g->nn_m = m;
   int rc = run_nearest(g, local_centers, m, rot, trans, g->nn_j.as<int64_t>(), g->nn_d2.as<double>(),
-                       warm ? 1 : 0, st);
+                       warm ? 1 : 0, st, nn_persist());
   if (rc) return rc;
   PoseArg P;
   for (int k = 0; k < 9; ++k) P.r[k] = rot[k];
@@ -1114,6 +1178,14 @@ int sgad_track_normal_eqs(sgad_geomset* g, const double* local_centers, const do
   SGAD_LAUNCH_CHECK();
   k_reduce_partials<<<NE_VALS, 256, 0, st>>>(g->partial.as<double>(), (int)nb, NE_VALS, out);
   SGAD_LAUNCH_CHECK();
+  return SGAD_OK;
+}
+
+int sgad_track_correspondences(sgad_geomset* g, int64_t* idx, int64_t m, void* stream_) {
+  SGAD_REQUIRE(g && idx && m >= 0 && g->nn_m == m, "sgad_track_correspondences: bad arguments");
+  if (m == 0) return SGAD_OK;
+  SGAD_CHECK_CUDA(cudaMemcpyAsync(idx, g->nn_j.p, sizeof(int64_t) * m, cudaMemcpyDeviceToDevice,
+                                  (cudaStream_t)stream_));
   return SGAD_OK;
 }
 

@@ -342,6 +342,12 @@ class GicpSolver:
         h.copy_(self.costs[:len(poses)])
         return h.numpy().copy()
 
+    def correspondences(self):
+        """The last linearisation's exact nearest neighbours (tracker.py:288 j)."""
+        idx = torch.empty(self.m, dtype=torch.int64, device=self.local.centers.device)
+        N.call("sgad_track_correspondences", self.g._h, idx.data_ptr(), self.m, N.stream_ptr())
+        return idx.cpu().numpy()
+
     def accepted(self):
         acc = torch.empty(self.m, dtype=torch.uint8, device=self.local.centers.device)
         N.call("sgad_track_accepted", self.g._h, acc.data_ptr(), self.m, N.stream_ptr())

@@ -151,3 +151,39 @@ def test_c2_tracking_vs_oracle():
     # and the registration recovers the seeded perturbation (1 % depth noise)
     r_true, t_true = pose_difference(pose, truth)
     assert r_true < np.deg2rad(0.3) and t_true < 5e-3
+
+
+def test_nearest_neighbours_exact_along_gicp_iterations():
+    """The correspondences of every GN linearisation (warm-started search and
+    the persistence test that skips queries whose old neighbour is provably
+    still the unique nearest) equal cKDTree's exact 1-NN at that pose -- along
+    a real gicp_align trajectory (large first steps, then tiny ones) and at
+    a repeated pose."""
+    from scipy.spatial import cKDTree
+    from paper_2603_21055_b200 import scenes
+    from paper_2603_21055_b200.geometry import Pose
+    from paper_2603_21055_b200.tracker import (GicpSolver, GlobalGeomSet, TrackerConfig,
+                                               build_local_set, gicp_align, update_global_set)
+    intr, ref, qry, truth = scenes.config_c2()
+    cfg = TrackerConfig(downsample_ratio=1, max_gicp_iters=20, convergence_eps=0.0,
+                        voxel_size=1e-4)
+    gs = GlobalGeomSet(cfg.voxel_size)
+    update_global_set(gs, build_local_set(ref, cfg), Pose.identity())
+    local = build_local_set(qry, cfg)
+    _, _, systems = gicp_align(local, gs, Pose.identity(), cfg, return_systems=True)
+    assert len(systems) >= 5
+    # replay the trajectory's poses through one solver (warm, persistent)
+    from paper_2603_21055_b200.geometry import se3_exp
+    poses = [Pose.identity()]
+    for h, g, _, _ in systems:
+        xi = np.linalg.solve(h, -g)
+        poses.append(se3_exp(xi).compose(poses[-1]))
+    poses.append(poses[-1])
+    tree = cKDTree(gs.centers.cpu().numpy())
+    lc = local.centers.cpu().numpy()
+    s = GicpSolver(local, gs, cfg)
+    for k, p in enumerate(poses):
+        s.linearize(p)
+        q = lc @ np.asarray(p.rotation).T + np.asarray(p.translation)
+        _, jk = tree.query(q)
+        np.testing.assert_array_equal(s.correspondences(), jk, err_msg=f"pose {k}")
