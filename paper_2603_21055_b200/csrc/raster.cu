@@ -1208,7 +1208,7 @@ __device__ __forceinline__ void bwd_sweep(WarpRing& ring, const TileGeom& g, con
           // rasterizer.py:462-483 with this view's coefficients: window
           // gradients (delta, radius, logit, R, G, B) straight into grad_accum
           // (gsig holds sigma g_sigma)
-          const float gs = (float)gsig, iz = (float)(1.0 / z);
+          const float gs = (float)gsig, iz = __frcp_rn((float)z);
           const float g_delta = cc.a_u * (float)gu + cc.a_v * (float)gv + cc.a_z * (float)gz -
                                 cc.a_z * iz * gs;
           const float g_radius = u.fx * sqrtf(-2.0f * (float)nh) * iz * gs;
