@@ -51,7 +51,28 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-track", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--launch-check", action="store_true",
+                    help="only start the ranks, join a process group (gloo without GPUs) and "
+                         "report them (tests the --gpus N launch)")
     return ap.parse_args()
+
+
+def launch_check(args):
+    """--launch-check: the rank launch of --gpus N without any GPU work."""
+    import torch
+    import torch.distributed as dist
+    rank, world, _ = dist_env()
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+    if world > 1:
+        dist.init_process_group("nccl" if torch.cuda.is_available() else "gloo")
+        t = torch.tensor([rank + 1.0])
+        dist.all_reduce(t)
+        assert dist.get_world_size() == args.gpus and int(t.item()) == world * (world + 1) // 2
+    if rank == 0:
+        print(json.dumps({"launch_check": True, "world_size": world}), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
 
 
 def dist_env():
@@ -318,6 +339,10 @@ def run_ours(args):
         except Exception as exc:
             track_c2 = {"error": repr(exc)}
         try:
+            track["rendered_geometry"] = bench_tracking_rendered(dev, wc)
+        except Exception as exc:
+            track["rendered_geometry"] = {"error": repr(exc)}
+        try:
             track["render_init"] = bench_render_init(dev)
         except Exception as exc:
             track["render_init"] = {"error": repr(exc)}
@@ -567,6 +592,58 @@ def bench_tracking(dev, which="c4size", iters=20, reps=5):
                                  "+ 2 host round trips) against 168 B per correspondence"}}
 
 
+def bench_tracking_rendered(dev, wc, key=3, iters=20, reps=3):
+    """BASELINE config 4's tracking: a frame tracked (20 GN iterations)
+    against geometry Gaussians fitted to the window's RENDERED depth, as the
+    reference pipeline builds its global set (mapper.py:208-210,
+    pipeline.py:346-349: D / A where the accumulated alpha A > 0.5).  The
+    window maps (fp64 drop-in maps of the bench's window) render keyframe
+    ``key``'s view with normalize_depth; the next keyframe's sensor depth is
+    registered against it from keyframe ``key``'s pose."""
+    import numpy as np
+    import torch
+    from paper_2603_21055_b200 import tracker as T
+    from paper_2603_21055_b200.gaussians import PixelGaussianMap
+    from paper_2603_21055_b200.geometry import pose_difference
+    from paper_2603_21055_b200.rasterizer import splat
+    from paper_2603_21055_b200.scenes import Frame
+    maps = [PixelGaussianMap(i, wc.poses[i], wc.intr, p.base_depth, p.delta, p.color,
+                             p.log_radius, p.opacity_logit, p.active_mask, dtype=torch.float64,
+                             device=dev) for i, p in enumerate(wc.params)]
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    out = splat(maps, wc.poses[key], wc.intr, normalize_depth=True)
+    geo = out.alpha > 0.5
+    depth = torch.where(geo, out.depth, torch.zeros_like(out.depth)).float()
+    cfg = T.TrackerConfig(downsample_ratio=1, max_gicp_iters=iters, convergence_eps=0.0,
+                          voxel_size=1e-4)
+    g = T.GlobalGeomSet(cfg.voxel_size)
+    T.update_global_set(g, T.build_local_set(Frame(None, depth, geo, wc.intr, index=key), cfg),
+                        wc.poses[key])
+    torch.cuda.synchronize()
+    build_ms = (time.perf_counter() - t0) * 1e3
+    fr = wc.frames[key + 1]
+    local = T.build_local_set(fr, cfg)
+    T.gicp_align(local, g, wc.poses[key], cfg)  # warm-up
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    n_it = 0
+    for _ in range(reps):
+        pose, diag = T.gicp_align(local, g, wc.poses[key], cfg)
+        n_it += max(diag.iterations, 1)
+    e1.record()
+    torch.cuda.synchronize()
+    dt = e0.elapsed_time(e1) / 1e3
+    rot_err, t_err = pose_difference(pose, wc.poses[key + 1])
+    return {"metric": "tracking GN iterations/s against rendered-geometry Gaussians "
+                      f"(keyframe {key + 1} of the window vs keyframe {key}'s render, "
+                      f"{wc.intr.width}x{wc.intr.height})",
+            "value": n_it / dt, "unit": "GN iters/s", "correspondences": len(local),
+            "global_members": len(g), "iterations_per_run": diag.iterations,
+            "render_fit_insert_ms": build_ms, "pose_error_rad_m": [rot_err, t_err]}
+
+
 def free_port():
     import socket
     s = socket.socket()
@@ -594,6 +671,9 @@ def main():
         return
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         spawn_ranks(args)
+    if args.launch_check:
+        launch_check(args)
+        return
     run_ours(args)
 
 
