@@ -448,7 +448,7 @@ class WindowMapper:
             return e
 
         for i, v in enumerate(self.views):
-            r = rasters[i % 2]
+            r = rasters[i % nh]
             if used[i % nh] is not None:
                 prep.wait_event(used[i % nh])
             p0 = mark(prep)
