@@ -315,6 +315,11 @@ def run_ours(args):
                 "prepare_ms_per_view": p_ms / max(p_n, 1),
                 "prepare_overlapped": bool(wm.pipelined),
                 "mean_survivors_per_view": mean_ns, "mean_pairs_per_view": mean_np}
+    # the whole window iteration against the same peak (per view
+    # 52 N + 80 P + 57 HW bytes, N = the window's Gaussians; + 168 N for Adam)
+    b_iter = sum(52 * n_g + 80 * counts[v][1] + 57 * hw for v in counts) + 168 * n_g
+    roofline["step"] = {"bytes": b_iter, "achieved_gbs": b_iter / (ms_step / 1e3) / 1e9,
+                        "frac": b_iter / (ms_step / 1e3) / 1e9 / peak}
 
     # e2e through the public API with host buffers (params + targets up, params down)
     e2e = None

@@ -484,3 +484,25 @@ def test_window_step_cuda_graph_matches_eager():
     assert runs[True][1] == runs[False][1] == 4
     np.testing.assert_allclose(runs[True][0], runs[False][0], rtol=1e-5)
     np.testing.assert_allclose(runs[True][2], runs[False][2], rtol=0, atol=2e-3)
+
+
+def test_window_pair_capacity_overflow_recovers():
+    """The asynchronous preparation outgrowing its pair capacity (the radii
+    grow after the handles were sized): the view sets the device overflow
+    flag, Adam skips that step on the device (no update, step count
+    unchanged), the host grows the capacity and the synchronous step runs
+    again -- the same trajectory as a window re-sized before the growth."""
+    from paper_2603_21055_b200.mapper import MapperConfig, WindowMapper
+    wc = _window_np(n_frames=3, seed=21)
+    runs = []
+    for resize in (True, False):
+        wm = WindowMapper(wc.frames, wc.poses, wc.intr, wc.params, MapperConfig(tau=0.0))
+        wm.step(sync_loss=True)           # sizes the handles for these radii
+        wm.planes[:, 2] += 1.5            # radii x4.5: far more tile pairs
+        if resize:
+            wm._cap = 0                   # (re-sized at the next step: no overflow)
+        losses = [wm.step(sync_loss=True) for _ in range(3)]
+        runs.append((np.array(losses), wm.t, wm.overflows))
+    assert runs[0][2] == 0 and runs[1][2] >= 1
+    np.testing.assert_allclose(runs[1][0], runs[0][0], rtol=1e-5)
+    assert runs[1][1] == runs[0][1] == 4
