@@ -317,7 +317,9 @@ def run_ours(args):
                 "mean_survivors_per_view": mean_ns, "mean_pairs_per_view": mean_np}
     # the whole window iteration against the same peak (per view
     # 52 N + 80 P + 57 HW bytes, N = the window's Gaussians; + 168 N for Adam)
-    b_iter = sum(52 * n_g + 80 * counts[v][1] + 57 * hw for v in counts) + 168 * n_g
+    # (this rank's views, scaled to the window's: all ranks' views per step)
+    b_iter = (n_views_total / max(len(counts), 1) *
+              sum(52 * n_g + 80 * counts[v][1] + 57 * hw for v in counts) + 168 * n_g)
     roofline["step"] = {"bytes": b_iter, "achieved_gbs": b_iter / (ms_step / 1e3) / 1e9,
                         "frac": b_iter / (ms_step / 1e3) / 1e9 / peak}
 
