@@ -1217,8 +1217,8 @@ int sgad_track_cost(sgad_geomset* g, const double* local_centers, int64_t m, con
   SGAD_LAUNCH_CHECK();
   k_reduce_partials<<<MAX_CAND, 256, 0, st>>>(g->partial.as<double>(), (int)nb, MAX_CAND, out);
   SGAD_LAUNCH_CHECK();
-  // hp lives on this stack frame: make sure the copy has been consumed
-  SGAD_CHECK_CUDA(cudaStreamSynchronize(st));
+  // (hp may go: an asynchronous copy from pageable memory returns once the
+  // source is staged)
   return SGAD_OK;
 }
 

@@ -319,17 +319,47 @@ class GicpSolver:
 
     def linearize(self, pose: Pose):
         """K8 at ``pose``: returns (H 6x6, g 6, cost, inliers)."""
+        # (later linearisations seed the exact NN search with these neighbours)
+        self._eqs_launch(pose)
+        h = self.host[:29]
+        h.copy_(self.out)  # synchronising copy into pinned memory
+        v = h.numpy()
+        return _sym6(v[:21]), v[21:27].copy(), float(v[27]), int(round(v[28]))
+
+    def _eqs_launch(self, pose: Pose):
         rot = (ctypes.c_double * 9)(*np.asarray(pose.rotation, dtype=np.float64).reshape(9))
         tr = (ctypes.c_double * 3)(*np.asarray(pose.translation, dtype=np.float64).reshape(3))
         N.call("sgad_track_normal_eqs", self.g._h, self.local.centers.data_ptr(),
                self.local.cov6.data_ptr(), self.m, rot, tr, self.metric,
                float(self.cfg.correspondence_dist_max), self._warm, self.out.data_ptr(),
                N.stream_ptr())
-        self._warm = 1  # later iterations seed the exact NN search with these neighbours
-        h = self.host[:29]
-        h.copy_(self.out)  # synchronising copy into pinned memory
-        v = h.numpy()
-        return _sym6(v[:21]), v[21:27].copy(), float(v[27]), int(round(v[28]))
+        self._warm = 1
+
+    def _cost_launch(self, poses):
+        arr = np.concatenate([np.concatenate([np.asarray(p.rotation).reshape(9),
+                                              np.asarray(p.translation).reshape(3)])
+                              for p in poses])
+        buf = (ctypes.c_double * len(arr))(*arr)
+        N.call("sgad_track_cost", self.g._h, self.local.centers.data_ptr(), self.m, buf,
+               len(poses), self.costs.data_ptr(), N.stream_ptr())
+
+    def costs_and_linearize(self, poses, next_pose: Pose):
+        """The frozen-weight costs of the candidate poses, then (speculatively)
+        the linearisation at ``next_pose``, read back with one synchronisation:
+        a GN iteration whose full step is accepted needs one host round trip."""
+        self._cost_launch(poses)
+        if next_pose is not None:
+            self._eqs_launch(next_pose)
+        n = len(poses)
+        self.host[29:29 + n].copy_(self.costs[:n], non_blocking=True)
+        if next_pose is not None:
+            self.host[:29].copy_(self.out, non_blocking=True)
+        torch.cuda.current_stream(self.local.centers.device).synchronize()
+        v = self.host.numpy()
+        if next_pose is None:
+            return v[29:29 + n].copy(), None
+        return (v[29:29 + n].copy(),
+                (_sym6(v[:21]), v[21:27].copy(), float(v[27]), int(round(v[28]))))
 
     def costs_at(self, poses):
         arr = np.concatenate([np.concatenate([np.asarray(p.rotation).reshape(9),
@@ -364,8 +394,9 @@ def gicp_align(local: LocalGeomSet, global_set: GlobalGeomSet, init: Pose, cfg: 
     systems = []
     pose = init
     solver = GicpSolver(local, global_set, cfg)
+    nxt = solver.linearize(pose) if cfg.max_gicp_iters > 0 else None
     for it in range(cfg.max_gicp_iters):
-        h, g, cost_before, n_acc = solver.linearize(pose)
+        h, g, cost_before, n_acc = nxt
         diag.inlier_count = n_acc
         if it == 0:
             diag.accepted_first = solver.accepted()
@@ -382,7 +413,10 @@ def gicp_align(local: LocalGeomSet, global_set: GlobalGeomSet, init: Pose, cfg: 
             xis.append(xi)
             cands.append(se3_exp(xi).compose(pose))
             xi = 0.5 * xi
-        costs = solver.costs_at(cands)
+        # the candidates' costs and, speculatively, the next linearisation at
+        # the full step (usually accepted): one host round trip per iteration
+        last = it + 1 == cfg.max_gicp_iters
+        costs, spec = solver.costs_and_linearize(cands, None if last else cands[0])
         k = 0
         while costs[k] > cost_before and k < MAX_STEP_HALVINGS:
             k += 1
@@ -397,6 +431,8 @@ def gicp_align(local: LocalGeomSet, global_set: GlobalGeomSet, init: Pose, cfg: 
         if np.linalg.norm(xi) < cfg.convergence_eps:
             diag.converged = True
             break
+        if it + 1 < cfg.max_gicp_iters:
+            nxt = spec if k == 0 else solver.linearize(pose)
     return (pose, diag, systems) if return_systems else (pose, diag)
 
 
