@@ -226,8 +226,9 @@ def run_ours(args):
     if os.environ.get("SGAD_FUSE") == "1":  # A/B: forward + backward as one kernel
         wm.fuse_fwd_bwd = True
     # the window step as one CUDA graph (captured at the first warm-up step);
-    # SGAD_GRAPH=0: launched eagerly (A/B)
-    wm.use_graph = os.environ.get("SGAD_GRAPH", "1") != "0"
+    # SGAD_GRAPH=0: launched eagerly (A/B).  Multi-rank runs stay eager: the
+    # NCCL exchange is not captured (no multi-GPU box to validate it here)
+    wm.use_graph = world == 1 and os.environ.get("SGAD_GRAPH", "1") != "0"
     n_g = wm.n_gaussians
     n_views_total = len(wc.poses)
 
