@@ -523,6 +523,10 @@ k_tile_scan(const uint32_t* __restrict__ tile_count, int n_tiles, int tpasses, u
     if (threadIdx.x == 1023) s_carry = start + c;
     __syncthreads();
   }
+  // more pairs than the capacity: the tile sort is skipped (sort.cuh), so the
+  // lists hold stale entries -- every tile renders empty and the view is discarded
+  if (s_carry > cap)
+    for (int t = threadIdx.x; t < n_tiles; t += blockDim.x) ranges[t] = make_uint2(0u, 0u);
   for (int j = threadIdx.x; j < (tpasses << TILE_RB); j += blockDim.x) hist[j] = sh[j];
 }
 
