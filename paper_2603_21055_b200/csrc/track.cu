@@ -12,6 +12,7 @@
 // latency-bound, so fp64 costs nothing measurable and keeps H within the
 // 1e-3 parity bar with margin.  Reductions are two-stage and deterministic.
 #include <cub/cub.cuh>
+#include <stdlib.h>
 
 #include "common.cuh"
 
@@ -420,35 +421,56 @@ __global__ void k_cell_heads(const unsigned long long* __restrict__ keys, int64_
 }
 
 // head_scan = inclusive scan of head: cell id of point i is head_scan[i] - 1
-__global__ void k_cell_table(const unsigned long long* __restrict__ keys, int64_t n,
-                             const uint32_t* __restrict__ head_scan, uint32_t* __restrict__ start,
-                             unsigned long long* __restrict__ hkeys, uint32_t* __restrict__ hvals,
-                             unsigned long long hmask) {
+__global__ void k_cell_starts(const unsigned long long* __restrict__ keys, int64_t n,
+                              const uint32_t* __restrict__ head_scan, uint32_t* __restrict__ start) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  if (i == 0 || keys[i] != keys[i - 1]) {
-    const uint32_t c = head_scan[i] - 1;
-    start[c] = (uint32_t)i;
-    const unsigned long long k = keys[i];
-    unsigned long long s = hash64(k) & hmask;
-    while (true) {
-      const unsigned long long prev = atomicCAS(hkeys + s, HASH_EMPTY, k);
-      if (prev == HASH_EMPTY) {
-        hvals[s] = c;
-        break;
-      }
-      s = (s + 1) & hmask;
-    }
-  }
+  if (i == 0 || keys[i] != keys[i - 1]) start[head_scan[i] - 1] = (uint32_t)i;
   if (i == n - 1) start[head_scan[i]] = (uint32_t)n;
+}
+
+// One 16-byte hash slot per occupied cell: the key and the cell's range in
+// the cell-ordered point array, so a probe that hits yields the range in the
+// same load.
+struct __align__(16) CellSlot {
+  unsigned long long key;
+  uint32_t start, count;
+};
+
+__global__ void k_cell_slots(const unsigned long long* __restrict__ keys,
+                             const uint32_t* __restrict__ start, int64_t n_cells,
+                             CellSlot* __restrict__ slots, unsigned long long hmask) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= n_cells) return;
+  const uint32_t s0 = start[c], s1 = start[c + 1];
+  const unsigned long long k = keys[s0];
+  unsigned long long s = hash64(k) & hmask;
+  while (true) {
+    const unsigned long long prev = atomicCAS(&slots[s].key, HASH_EMPTY, k);
+    if (prev == HASH_EMPTY) {
+      slots[s].start = s0;
+      slots[s].count = s1 - s0;
+      break;
+    }
+    s = (s + 1) & hmask;
+  }
+}
+
+// the points of each level in cell order, one 32-byte record each: x, y, z
+// and the point's index (as the bits of the 4th double)
+__global__ void k_cell_points(const uint32_t* __restrict__ order, const double* __restrict__ pts,
+                              int64_t n, double4* __restrict__ out) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  const uint32_t j = order[t];
+  out[t] = make_double4(pts[3 * (int64_t)j], pts[3 * (int64_t)j + 1], pts[3 * (int64_t)j + 2],
+                        __longlong_as_double((long long)j));
 }
 
 struct LevelView {
   Grid g;
-  const unsigned long long* hkeys;
-  const uint32_t* hvals;
-  const uint32_t* start;
-  const uint32_t* items;
+  const CellSlot* slots;
+  const double4* cpts;
 };
 
 struct GridView {
@@ -457,12 +479,14 @@ struct GridView {
   int64_t n;
 };
 
-__device__ __forceinline__ int hash_find(const LevelView& v, unsigned long long k) {
+// the cell's (start, count) in the cell-ordered points, or count 0 if empty
+__device__ __forceinline__ uint2 hash_find(const LevelView& v, unsigned long long k) {
   unsigned long long s = hash64(k) & v.g.hmask;
   while (true) {
-    const unsigned long long hk = v.hkeys[s];
-    if (hk == k) return (int)v.hvals[s];
-    if (hk == HASH_EMPTY) return -1;
+    ulonglong2 sl;
+    asm("ld.global.nc.v2.u64 {%0, %1}, [%2];" : "=l"(sl.x), "=l"(sl.y) : "l"(v.slots + s));
+    if (sl.x == k) return make_uint2((uint32_t)sl.y, (uint32_t)(sl.y >> 32));
+    if (sl.x == HASH_EMPTY) return make_uint2(0u, 0u);
     s = (s + 1) & v.g.hmask;
   }
 }
@@ -497,15 +521,16 @@ __device__ bool grid_nearest(const LevelView& v, const double* pts, const double
             second = fmin(second, bmin);  // (a non-empty pruned cell: all its points beyond bmin)
             continue;
           }
-          const int c = hash_find(v, cell_key(x, y, z));
-          if (c < 0) continue;
-          for (uint32_t t = v.start[c]; t < v.start[c + 1]; ++t) {
-            const uint32_t j = v.items[t];
-            if ((int64_t)j == best_j) continue;
-            const double dx = q[0] - pts[3 * j], dy = q[1] - pts[3 * j + 1],
-                         dz = q[2] - pts[3 * j + 2];
+          const uint2 rg = hash_find(v, cell_key(x, y, z));
+          for (uint32_t t = rg.x; t < rg.x + rg.y; ++t) {
+            double px, py, pz, pj;
+            asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];"
+                : "=d"(px), "=d"(py), "=d"(pz), "=d"(pj) : "l"(v.cpts + t));
+            const int64_t j = (int64_t)__double_as_longlong(pj);
+            if (j == best_j) continue;
+            const double dx = q[0] - px, dy = q[1] - py, dz = q[2] - pz;
             const double d2 = dx * dx + dy * dy + dz * dz;
-            if (d2 < best_d2 || (d2 == best_d2 && (int64_t)j < best_j)) {
+            if (d2 < best_d2 || (d2 == best_d2 && j < best_j)) {
               second = fmin(second, best_d2);
               best_d2 = d2;
               best_j = j;
@@ -554,6 +579,8 @@ struct NNArgs {
   // search and a lower bound on its second-nearest squared distance
   double* q_prev;         // [m, 3] or null
   double* second;         // [m]
+  uint32_t* level_count;  // [NLEV] queries left to search per starting level
+  uint32_t* level_list;   // [NLEV, m]
 };
 
 __device__ __forceinline__ void query_point(const NNArgs& a, int64_t i, double* p) {
@@ -571,7 +598,111 @@ __device__ __forceinline__ void query_point(const NNArgs& a, int64_t i, double* 
   }
 }
 
-__global__ void k_nearest(GridView v, NNArgs a) {
+// Two passes so that the searching queries fill whole warps (a warp of
+// queries that mostly pass the persistence test used to wait on its few
+// searching lanes: 6.4 of 32 threads per instruction).
+//   k_nn_triage: transform, warm distance and persistence test per query;
+//     the queries left to search are appended, warp-aggregated, to the list
+//     of the grid level their warm reach selects (level 0 when cold);
+//   k_nn_search: threads walk the concatenated level lists (grid-stride,
+//     counts read on the device), so a warp searches queries that start at
+//     the same level and were neighbours in the query order.
+__device__ __forceinline__ void nn_commit(const NNArgs& a, int64_t i, int64_t j, double d2,
+                                          const double* q, double second) {
+  a.idx[i] = j;
+  a.d2[i] = d2;
+  if (a.q_prev) {
+    double* qw = a.q_prev + 3 * i;
+    qw[0] = q[0];
+    qw[1] = q[1];
+    qw[2] = q[2];
+    a.second[i] = second;
+  }
+}
+
+__device__ __forceinline__ double warm_d2(const GridView& v, const double* q, int64_t j) {
+  const double dx = q[0] - v.pts[3 * j], dy = q[1] - v.pts[3 * j + 1], dz = q[2] - v.pts[3 * j + 2];
+  return dx * dx + dy * dy + dz * dz;
+}
+
+__global__ void __launch_bounds__(128) k_nn_triage(GridView v, NNArgs a) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int key = -1;  // level list to join (-1: settled or past the end)
+  if (i < a.m) {
+    key = 0;
+    if (a.warm) {
+      double q[3];
+      query_point(a, i, q);
+      const int64_t j = a.idx[i];
+      const double d2 = warm_d2(v, q, j);
+      bool settled = false;
+      if (a.q_prev) {
+        // persistence: the query moved by delta since its last full search,
+        // where every other point was at least sqrt(second) away; so they are
+        // now at least sqrt(second) - delta away, and if the old neighbour is
+        // strictly closer than that it is still the unique nearest (exact)
+        const double* qp = a.q_prev + 3 * i;
+        const double ex = q[0] - qp[0], ey = q[1] - qp[1], ez = q[2] - qp[2];
+        const double low = sqrt(a.second[i]) - sqrt(ex * ex + ey * ey + ez * ez);
+        if (low > 0.0 && sqrt(d2) < low * (1.0 - 1e-12)) {
+          nn_commit(a, i, j, d2, q, low * low * (1.0 - 1e-12));
+          settled = true;
+        }
+      }
+      if (settled) {
+        key = -1;
+      } else {
+        // the old neighbour's distance bounds the answer: start at the finest
+        // level whose ring reach covers it
+        const double reach = sqrt(d2);
+        while (key < NLEV - 1 && MAX_RINGS * v.lv[key].g.h < reach) ++key;
+      }
+    }
+  }
+  const unsigned same = __match_any_sync(0xffffffffu, key);
+  const int lane = threadIdx.x & 31, leader = __ffs(same) - 1;
+  uint32_t base = 0;
+  if (lane == leader && key >= 0) base = atomicAdd(a.level_count + key, (uint32_t)__popc(same));
+  base = __shfl_sync(0xffffffffu, base, leader);
+  if (key >= 0)
+    a.level_list[(int64_t)key * a.m + base + __popc(same & ((1u << lane) - 1u))] = (uint32_t)i;
+}
+
+__global__ void __launch_bounds__(128) k_nn_search(GridView v, NNArgs a) {
+  uint32_t cnt[NLEV];
+  uint32_t total = 0;
+#pragma unroll
+  for (int l = 0; l < NLEV; ++l) {
+    cnt[l] = a.level_count[l];
+    total += cnt[l];
+  }
+  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
+    int l0 = 0;
+    uint32_t pos = t;
+    while (pos >= cnt[l0]) pos -= cnt[l0++];
+    const int64_t i = a.level_list[(int64_t)l0 * a.m + pos];
+    double q[3];
+    query_point(a, i, q);
+    int64_t j = -1;
+    double d2 = INFINITY;
+    if (a.warm) {
+      j = a.idx[i];
+      d2 = warm_d2(v, q, j);
+    }
+    double second = INFINITY;
+    bool ok = false;
+    for (int l = l0; l < NLEV && !ok; ++l) ok = grid_nearest(v.lv[l], v.pts, q, j, d2, second);
+    if (ok) {
+      nn_commit(a, i, j, d2, q, second);
+    } else {
+      if (a.q_prev) a.second[i] = 0.0;  // (resolved by the brute force: no bound kept)
+      a.unresolved[atomicAdd(a.n_unres, 1u)] = (uint32_t)i;
+    }
+  }
+}
+
+// Single-pass variant (SGAD_NN_SPLIT=0): one thread per query in query order.
+__global__ void __launch_bounds__(128) k_nearest(GridView v, NNArgs a) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= a.m) return;
   double q[3];
@@ -580,27 +711,14 @@ __global__ void k_nearest(GridView v, NNArgs a) {
   double d2 = INFINITY;
   int l0 = 0;
   if (a.warm) {
-    // warm start from the previous iteration's neighbour: its distance bounds
-    // the answer, so start at the finest level whose ring reach covers it
     j = a.idx[i];
-    const double dx = q[0] - v.pts[3 * j], dy = q[1] - v.pts[3 * j + 1], dz = q[2] - v.pts[3 * j + 2];
-    d2 = dx * dx + dy * dy + dz * dz;
+    d2 = warm_d2(v, q, j);
     if (a.q_prev) {
-      // persistence: the query moved by delta since its last full search,
-      // where every other point was at least sqrt(second) away; so they are
-      // now at least sqrt(second) - delta away, and if the old neighbour is
-      // strictly closer than that it is still the unique nearest (exact)
       const double* qp = a.q_prev + 3 * i;
       const double ex = q[0] - qp[0], ey = q[1] - qp[1], ez = q[2] - qp[2];
       const double low = sqrt(a.second[i]) - sqrt(ex * ex + ey * ey + ez * ez);
       if (low > 0.0 && sqrt(d2) < low * (1.0 - 1e-12)) {
-        a.idx[i] = j;
-        a.d2[i] = d2;
-        a.second[i] = low * low * (1.0 - 1e-12);
-        double* qw = a.q_prev + 3 * i;
-        qw[0] = q[0];
-        qw[1] = q[1];
-        qw[2] = q[2];
+        nn_commit(a, i, j, d2, q, low * low * (1.0 - 1e-12));
         return;
       }
     }
@@ -610,15 +728,7 @@ __global__ void k_nearest(GridView v, NNArgs a) {
   double second = INFINITY;
   for (int l = l0; l < NLEV; ++l) {
     if (grid_nearest(v.lv[l], v.pts, q, j, d2, second)) {
-      a.idx[i] = j;
-      a.d2[i] = d2;
-      if (a.q_prev) {
-        double* qw = a.q_prev + 3 * i;
-        qw[0] = q[0];
-        qw[1] = q[1];
-        qw[2] = q[2];
-        a.second[i] = second;
-      }
+      nn_commit(a, i, j, d2, q, second);
       return;
     }
   }
@@ -868,9 +978,9 @@ __global__ void k_sqrt(const double* __restrict__ x, int64_t n, double* __restri
 struct sgad_geomset {
   sgad::DevBuf pts, cov, nrm, bbox, keys0, keys1, idx0, idx1, head, headscan, start, hkeys, hvals,
       cub_tmp;
-  sgad::DevBuf w, b, acc, partial, poses, nn_j, nn_d2, unres, counter, nn_qprev, nn_second;
+  sgad::DevBuf w, b, acc, partial, poses, nn_j, nn_d2, unres, counter, nn_qprev, nn_second, nn_lists;
   sgad::Grid grid[sgad::NLEV]{};
-  sgad::DevBuf lhkeys[sgad::NLEV], lhvals[sgad::NLEV], lstart[sgad::NLEV], litems[sgad::NLEV];
+  sgad::DevBuf lslots[sgad::NLEV], lpts[sgad::NLEV];
   int64_t n = 0;
   int64_t nn_m = -1;  // queries whose neighbours nn_j holds (warm start)
   unsigned long long* pinned = nullptr;
@@ -932,13 +1042,12 @@ int sgad_geomset_destroy(sgad_geomset* g) {
   DevBuf* bufs[] = {&g->pts, &g->cov, &g->nrm, &g->bbox, &g->keys0, &g->keys1, &g->idx0,
                     &g->idx1, &g->head, &g->headscan, &g->start, &g->hkeys, &g->hvals,
                     &g->cub_tmp, &g->w, &g->b, &g->acc, &g->partial, &g->poses, &g->nn_j,
-                    &g->nn_d2, &g->unres, &g->counter, &g->nn_qprev, &g->nn_second};
+                    &g->nn_d2, &g->unres, &g->counter, &g->nn_qprev, &g->nn_second,
+                    &g->nn_lists};
   for (DevBuf* b : bufs) b->release();
   for (int l = 0; l < NLEV; ++l) {
-    g->lhkeys[l].release();
-    g->lhvals[l].release();
-    g->lstart[l].release();
-    g->litems[l].release();
+    g->lslots[l].release();
+    g->lpts[l].release();
   }
   if (g->pinned) cudaFreeHost(g->pinned);
   delete g;
@@ -1059,18 +1168,19 @@ int sgad_geomset_set(sgad_geomset* g, const double* centers, const double* cov,
     while (hsize < 2ull * (unsigned long long)n_cells) hsize <<= 1;
     gr.hmask = hsize - 1;
     g->grid[l] = gr;
-    SGAD_CHECK_CUDA(g->lstart[l].ensure(sizeof(uint32_t) * (n_cells + 1)));
-    SGAD_CHECK_CUDA(g->lhkeys[l].ensure(sizeof(unsigned long long) * hsize));
-    SGAD_CHECK_CUDA(g->lhvals[l].ensure(sizeof(uint32_t) * hsize));
-    SGAD_CHECK_CUDA(g->litems[l].ensure(sizeof(uint32_t) * n));
-    SGAD_CHECK_CUDA(cudaMemsetAsync(g->lhkeys[l].p, 0xff, sizeof(unsigned long long) * hsize, st));
-    k_cell_table<<<nblk(n, 256), 256, 0, st>>>(ks, n, g->headscan.as<uint32_t>(),
-                                               g->lstart[l].as<uint32_t>(),
-                                               g->lhkeys[l].as<unsigned long long>(),
-                                               g->lhvals[l].as<uint32_t>(), gr.hmask);
+    SGAD_CHECK_CUDA(g->start.ensure(sizeof(uint32_t) * (n_cells + 1)));
+    SGAD_CHECK_CUDA(g->lslots[l].ensure(sizeof(CellSlot) * hsize));
+    SGAD_CHECK_CUDA(g->lpts[l].ensure(sizeof(double4) * n));
+    SGAD_CHECK_CUDA(cudaMemsetAsync(g->lslots[l].p, 0xff, sizeof(CellSlot) * hsize, st));
+    k_cell_starts<<<nblk(n, 256), 256, 0, st>>>(ks, n, g->headscan.as<uint32_t>(),
+                                                g->start.as<uint32_t>());
     SGAD_LAUNCH_CHECK();
-    SGAD_CHECK_CUDA(cudaMemcpyAsync(g->litems[l].p, is, sizeof(uint32_t) * n,
-                                    cudaMemcpyDeviceToDevice, st));
+    k_cell_slots<<<nblk(n_cells, 256), 256, 0, st>>>(ks, g->start.as<uint32_t>(), n_cells,
+                                                     g->lslots[l].as<CellSlot>(), gr.hmask);
+    SGAD_LAUNCH_CHECK();
+    k_cell_points<<<nblk(n, 256), 256, 0, st>>>(is, g->pts.as<double>(), n,
+                                                g->lpts[l].as<double4>());
+    SGAD_LAUNCH_CHECK();
   }
   return SGAD_OK;
 }
@@ -1079,10 +1189,8 @@ static GridView view_of(sgad_geomset* g) {
   GridView v;
   for (int l = 0; l < NLEV; ++l) {
     v.lv[l].g = g->grid[l];
-    v.lv[l].hkeys = g->lhkeys[l].as<unsigned long long>();
-    v.lv[l].hvals = g->lhvals[l].as<uint32_t>();
-    v.lv[l].start = g->lstart[l].as<uint32_t>();
-    v.lv[l].items = g->litems[l].as<uint32_t>();
+    v.lv[l].slots = g->lslots[l].as<CellSlot>();
+    v.lv[l].cpts = g->lpts[l].as<double4>();
   }
   v.pts = g->pts.as<double>();
   v.n = g->n;
@@ -1103,8 +1211,9 @@ static int run_nearest(sgad_geomset* g, const double* queries, int64_t m, const 
                        const double* trans, int64_t* idx, double* d2, int warm, cudaStream_t st,
                        bool persist = false) {
   SGAD_CHECK_CUDA(g->unres.ensure(sizeof(uint32_t) * m));
-  SGAD_CHECK_CUDA(g->counter.ensure(sizeof(uint32_t) * 4));
-  SGAD_CHECK_CUDA(cudaMemsetAsync(g->counter.p, 0, sizeof(uint32_t), st));
+  SGAD_CHECK_CUDA(g->counter.ensure(sizeof(uint32_t) * (NLEV + 1)));
+  SGAD_CHECK_CUDA(g->nn_lists.ensure(sizeof(uint32_t) * NLEV * m));
+  SGAD_CHECK_CUDA(cudaMemsetAsync(g->counter.p, 0, sizeof(uint32_t) * (NLEV + 1), st));
   NNArgs a;
   a.queries = queries;
   a.m = m;
@@ -1116,6 +1225,8 @@ static int run_nearest(sgad_geomset* g, const double* queries, int64_t m, const 
   a.d2 = d2;
   a.unresolved = g->unres.as<uint32_t>();
   a.n_unres = g->counter.as<uint32_t>();
+  a.level_count = g->counter.as<uint32_t>() + 1;
+  a.level_list = g->nn_lists.as<uint32_t>();
   a.q_prev = nullptr;
   a.second = nullptr;
   if (persist) {
@@ -1125,10 +1236,28 @@ static int run_nearest(sgad_geomset* g, const double* queries, int64_t m, const 
     a.second = g->nn_second.as<double>();
   }
   const GridView v = view_of(g);
-  k_nearest<<<nblk(m, 128), 128, 0, st>>>(v, a);
+  static const bool split = [] {
+    const char* e = getenv("SGAD_NN_SPLIT");
+    return e && e[0] == '1';
+  }();
+  if (split) {
+    k_nn_triage<<<nblk(m, 128), 128, 0, st>>>(v, a);
+    SGAD_LAUNCH_CHECK();
+    k_nn_search<<<nblk(m, 128) < 148u * 16u ? nblk(m, 128) : 148u * 16u, 128, 0, st>>>(v, a);
+  } else {
+    k_nearest<<<nblk(m, 128), 128, 0, st>>>(v, a);
+  }
   SGAD_LAUNCH_CHECK();
   k_nearest_brute<<<256, 256, 0, st>>>(v, a);
   SGAD_LAUNCH_CHECK();
+  if (getenv("SGAD_NN_STATS")) {  // (diagnostics: queries searched per starting level)
+    uint32_t c[NLEV + 1];
+    SGAD_CHECK_CUDA(cudaMemcpyAsync(c, g->counter.p, sizeof c, cudaMemcpyDeviceToHost, st));
+    SGAD_CHECK_CUDA(cudaStreamSynchronize(st));
+    fprintf(stderr, "nn m=%lld unres=%u levels:", (long long)m, c[0]);
+    for (int l = 0; l < NLEV; ++l) fprintf(stderr, " %u", c[l + 1]);
+    fprintf(stderr, "\n");
+  }
   return SGAD_OK;
 }
 
