@@ -31,6 +31,8 @@
  *   sgad_track_normal_eqs <- tracker.py:286-321 (one GICP iteration's
  *                            correspondences, gate, combined covariance,
  *                            H = sum J^T W J, g = sum J^T W d, cost)
+ *   sgad_track_gicp       <- tracker.py:265-346 (the whole Gauss-Newton loop on
+ *                            the device, one host round trip per registration)
  *   sgad_track_cost       <- tracker.py:312-314,329-333 (frozen-weight cost at
  *                            candidate poses for step halving)
  */
@@ -272,6 +274,25 @@ int sgad_track_correspondences(sgad_geomset* g, int64_t* idx, int64_t m, void* s
  * (device). */
 int sgad_track_cost(sgad_geomset* g, const double* local_centers, int64_t m, const double* poses,
                     int32_t n_cand, double* out, void* stream);
+
+/* A whole gicp_align (tracker.py:265-346) enqueued at once and read back once:
+ * per iteration the 6x6 solve (np.linalg.solve's partial-pivot LU), the step
+ * and its 5 halvings (se3_exp(xi).compose(pose)), their frozen-weight costs,
+ * the acceptance test and the next linearisation at the accepted pose all
+ * run on the device.  init_pose: host [12] (rot row-major, trans).  Outputs
+ * (host): result[19] = final pose (12), final cost, iterations, inlier count,
+ * converged, failed, singular iteration (-1: none; at an exactly singular
+ * system -- where numpy falls back to lstsq -- the loop stops with `pose` the
+ * pose reached and the caller continues on the host), systems logged;
+ * systems (optional) [max_iters, 29] as sgad_track_normal_eqs' out per
+ * iteration; cost_pairs (optional) [max_iters, 2] (cost before, after) per
+ * accepted iteration; accepted_first (optional, device or host uint8 [m]):
+ * the first linearisation's acceptance flags. */
+int sgad_track_gicp(sgad_geomset* g, const double* local_centers, const double* local_cov,
+                    int64_t m, const double* init_pose, int32_t metric_mode, double dist_max,
+                    int32_t max_iters, double convergence_eps, int32_t warm_start,
+                    int32_t min_inliers, double* result, double* systems, double* cost_pairs,
+                    uint8_t* accepted_first, void* stream);
 
 /* ---- voxel occupancy of the global geometry set -----------------------
  * Replaces the cell gating of GlobalGeomSet.insert (tracker.py:105-122): a

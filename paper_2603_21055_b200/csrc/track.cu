@@ -479,11 +479,20 @@ struct GridView {
   int64_t n;
 };
 
+#ifdef SGAD_NN_COUNT
+// (diagnostics) [searches, level calls, cells tested, cells probed, empty cells, points, probes]
+__device__ unsigned long long g_nn_count[8];
+#define NN_COUNT(k, x) atomicAdd(&g_nn_count[k], (unsigned long long)(x))
+#else
+#define NN_COUNT(k, x) ((void)0)
+#endif
+
 // the cell's (start, count) in the cell-ordered points, or count 0 if empty
 __device__ __forceinline__ uint2 hash_find(const LevelView& v, unsigned long long k) {
   unsigned long long s = hash64(k) & v.g.hmask;
   while (true) {
     ulonglong2 sl;
+    NN_COUNT(6, 1);
     asm("ld.global.nc.v2.u64 {%0, %1}, [%2];" : "=l"(sl.x), "=l"(sl.y) : "l"(v.slots + s));
     if (sl.x == k) return make_uint2((uint32_t)sl.y, (uint32_t)(sl.y >> 32));
     if (sl.x == HASH_EMPTY) return make_uint2(0u, 0u);
@@ -499,6 +508,7 @@ __device__ __forceinline__ uint2 hash_find(const LevelView& v, unsigned long lon
 __device__ bool grid_nearest(const LevelView& v, const double* pts, const double* q,
                              int64_t& best_j, double& best_d2, double& second) {
   const Grid& g = v.g;
+  NN_COUNT(1, 1);
   int c0[3];
   for (int k = 0; k < 3; ++k) c0[k] = cell_coord(q[k], g.lo[k], g.h, g.dim[k]);
   for (int r = 0; r <= MAX_RINGS; ++r) {
@@ -517,11 +527,15 @@ __device__ bool grid_nearest(const LevelView& v, const double* pts, const double
           }
           const double bz0 = g.lo[2] + z * g.h, bz = fmax(fmax(bz0 - q[2], q[2] - (bz0 + g.h)), 0.0);
           const double bmin = bx * bx + by * by + bz * bz;
+          NN_COUNT(2, 1);
           if (bmin > best_d2) {
             second = fmin(second, bmin);  // (a non-empty pruned cell: all its points beyond bmin)
             continue;
           }
           const uint2 rg = hash_find(v, cell_key(x, y, z));
+          NN_COUNT(3, 1);
+          NN_COUNT(4, rg.y == 0);
+          NN_COUNT(5, rg.y);
           for (uint32_t t = rg.x; t < rg.x + rg.y; ++t) {
             double px, py, pz, pj;
             asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];"
@@ -571,6 +585,8 @@ struct NNArgs {
   int warm;               // idx[] holds a previous nearest neighbour per query
   int transform;          // apply pose P to the queries first
   double r[9], t[3];
+  const double* pose_dev; // [12] device pose (R row-major, t) overriding r, t, or null
+  const int32_t* skip;    // nonzero: nothing to do (a finished device GN loop), or null
   int64_t* idx;
   double* d2;
   uint32_t* unresolved;   // [m] list, count in *n_unres
@@ -579,18 +595,18 @@ struct NNArgs {
   // search and a lower bound on its second-nearest squared distance
   double* q_prev;         // [m, 3] or null
   double* second;         // [m]
-  uint32_t* level_count;  // [NLEV] queries left to search per starting level
-  uint32_t* level_list;   // [NLEV, m]
 };
 
 __device__ __forceinline__ void query_point(const NNArgs& a, int64_t i, double* p) {
   const double* s = a.queries + 3 * i;
   if (a.transform) {
     // pts @ R.T + t in OpenBLAS dgemm order: fma(a2, R[j,2], fma(a1, R[j,1], a0 * R[j,0])) + t[j]
+    const double* r = a.pose_dev ? a.pose_dev : a.r;
+    const double* t = a.pose_dev ? a.pose_dev + 9 : a.t;
 #pragma unroll
     for (int j = 0; j < 3; ++j)
-      p[j] = SG_ADD(SG_FMA(s[2], a.r[3 * j + 2], SG_FMA(s[1], a.r[3 * j + 1], SG_MUL(s[0], a.r[3 * j]))),
-                    a.t[j]);
+      p[j] = SG_ADD(SG_FMA(s[2], r[3 * j + 2], SG_FMA(s[1], r[3 * j + 1], SG_MUL(s[0], r[3 * j]))),
+                    t[j]);
   } else {
     p[0] = s[0];
     p[1] = s[1];
@@ -598,15 +614,6 @@ __device__ __forceinline__ void query_point(const NNArgs& a, int64_t i, double* 
   }
 }
 
-// Two passes so that the searching queries fill whole warps (a warp of
-// queries that mostly pass the persistence test used to wait on its few
-// searching lanes: 6.4 of 32 threads per instruction).
-//   k_nn_triage: transform, warm distance and persistence test per query;
-//     the queries left to search are appended, warp-aggregated, to the list
-//     of the grid level their warm reach selects (level 0 when cold);
-//   k_nn_search: threads walk the concatenated level lists (grid-stride,
-//     counts read on the device), so a warp searches queries that start at
-//     the same level and were neighbours in the query order.
 __device__ __forceinline__ void nn_commit(const NNArgs& a, int64_t i, int64_t j, double d2,
                                           const double* q, double second) {
   a.idx[i] = j;
@@ -625,86 +632,15 @@ __device__ __forceinline__ double warm_d2(const GridView& v, const double* q, in
   return dx * dx + dy * dy + dz * dz;
 }
 
-__global__ void __launch_bounds__(128) k_nn_triage(GridView v, NNArgs a) {
+// One thread per query, in query order (neighbouring queries search
+// neighbouring cells: measured faster than compacting the queries that fail
+// the persistence test into per-level lists, which loses that coherence).
+#ifndef SGAD_NN_MINB
+#define SGAD_NN_MINB 1
+#endif
+__global__ void __launch_bounds__(128, SGAD_NN_MINB) k_nearest(GridView v, NNArgs a) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  int key = -1;  // level list to join (-1: settled or past the end)
-  if (i < a.m) {
-    key = 0;
-    if (a.warm) {
-      double q[3];
-      query_point(a, i, q);
-      const int64_t j = a.idx[i];
-      const double d2 = warm_d2(v, q, j);
-      bool settled = false;
-      if (a.q_prev) {
-        // persistence: the query moved by delta since its last full search,
-        // where every other point was at least sqrt(second) away; so they are
-        // now at least sqrt(second) - delta away, and if the old neighbour is
-        // strictly closer than that it is still the unique nearest (exact)
-        const double* qp = a.q_prev + 3 * i;
-        const double ex = q[0] - qp[0], ey = q[1] - qp[1], ez = q[2] - qp[2];
-        const double low = sqrt(a.second[i]) - sqrt(ex * ex + ey * ey + ez * ez);
-        if (low > 0.0 && sqrt(d2) < low * (1.0 - 1e-12)) {
-          nn_commit(a, i, j, d2, q, low * low * (1.0 - 1e-12));
-          settled = true;
-        }
-      }
-      if (settled) {
-        key = -1;
-      } else {
-        // the old neighbour's distance bounds the answer: start at the finest
-        // level whose ring reach covers it
-        const double reach = sqrt(d2);
-        while (key < NLEV - 1 && MAX_RINGS * v.lv[key].g.h < reach) ++key;
-      }
-    }
-  }
-  const unsigned same = __match_any_sync(0xffffffffu, key);
-  const int lane = threadIdx.x & 31, leader = __ffs(same) - 1;
-  uint32_t base = 0;
-  if (lane == leader && key >= 0) base = atomicAdd(a.level_count + key, (uint32_t)__popc(same));
-  base = __shfl_sync(0xffffffffu, base, leader);
-  if (key >= 0)
-    a.level_list[(int64_t)key * a.m + base + __popc(same & ((1u << lane) - 1u))] = (uint32_t)i;
-}
-
-__global__ void __launch_bounds__(128) k_nn_search(GridView v, NNArgs a) {
-  uint32_t cnt[NLEV];
-  uint32_t total = 0;
-#pragma unroll
-  for (int l = 0; l < NLEV; ++l) {
-    cnt[l] = a.level_count[l];
-    total += cnt[l];
-  }
-  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
-    int l0 = 0;
-    uint32_t pos = t;
-    while (pos >= cnt[l0]) pos -= cnt[l0++];
-    const int64_t i = a.level_list[(int64_t)l0 * a.m + pos];
-    double q[3];
-    query_point(a, i, q);
-    int64_t j = -1;
-    double d2 = INFINITY;
-    if (a.warm) {
-      j = a.idx[i];
-      d2 = warm_d2(v, q, j);
-    }
-    double second = INFINITY;
-    bool ok = false;
-    for (int l = l0; l < NLEV && !ok; ++l) ok = grid_nearest(v.lv[l], v.pts, q, j, d2, second);
-    if (ok) {
-      nn_commit(a, i, j, d2, q, second);
-    } else {
-      if (a.q_prev) a.second[i] = 0.0;  // (resolved by the brute force: no bound kept)
-      a.unresolved[atomicAdd(a.n_unres, 1u)] = (uint32_t)i;
-    }
-  }
-}
-
-// Single-pass variant (SGAD_NN_SPLIT=0): one thread per query in query order.
-__global__ void __launch_bounds__(128) k_nearest(GridView v, NNArgs a) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= a.m) return;
+  if (i >= a.m || (a.skip && *a.skip)) return;
   double q[3];
   query_point(a, i, q);
   int64_t j = -1;
@@ -714,6 +650,10 @@ __global__ void __launch_bounds__(128) k_nearest(GridView v, NNArgs a) {
     j = a.idx[i];
     d2 = warm_d2(v, q, j);
     if (a.q_prev) {
+      // persistence: the query moved by delta since its last full search,
+      // where every other point was at least sqrt(second) away; so they are
+      // now at least sqrt(second) - delta away, and if the old neighbour is
+      // strictly closer than that it is still the unique nearest (exact)
       const double* qp = a.q_prev + 3 * i;
       const double ex = q[0] - qp[0], ey = q[1] - qp[1], ez = q[2] - qp[2];
       const double low = sqrt(a.second[i]) - sqrt(ex * ex + ey * ey + ez * ez);
@@ -722,10 +662,13 @@ __global__ void __launch_bounds__(128) k_nearest(GridView v, NNArgs a) {
         return;
       }
     }
+    // the old neighbour's distance bounds the answer: start at the finest
+    // level whose ring reach covers it
     const double reach = sqrt(d2);
     while (l0 < NLEV - 1 && MAX_RINGS * v.lv[l0].g.h < reach) ++l0;
   }
   double second = INFINITY;
+  NN_COUNT(0, 1);
   for (int l = l0; l < NLEV; ++l) {
     if (grid_nearest(v.lv[l], v.pts, q, j, d2, second)) {
       nn_commit(a, i, j, d2, q, second);
@@ -740,6 +683,7 @@ __global__ void __launch_bounds__(128) k_nearest(GridView v, NNArgs a) {
 __global__ void __launch_bounds__(256) k_nearest_brute(GridView v, NNArgs a) {
   __shared__ double s_d[8];
   __shared__ int64_t s_j[8];
+  if (a.skip && *a.skip) return;
   const uint32_t nu = *a.n_unres;
   for (uint32_t u = blockIdx.x; u < nu; u += gridDim.x) {
     const int64_t i = a.unresolved[u];
@@ -801,10 +745,13 @@ __global__ void __launch_bounds__(TRK_THREADS)
 k_normal_eqs(GridView v, const int64_t* __restrict__ nn_j, const double* __restrict__ nn_d2,
              const double* __restrict__ cov_b, const double* __restrict__ nrm_b,
              const double* __restrict__ a_c, const double* __restrict__ a_cov, int64_t m,
-             PoseArg P, int metric_mode, double dist_max, double* __restrict__ w_out,
+             PoseArg P, const PoseArg* __restrict__ P_dev, const int32_t* __restrict__ skip,
+             int metric_mode, double dist_max, double* __restrict__ w_out,
              double* __restrict__ b_out, uint8_t* __restrict__ acc_out,
              double* __restrict__ partial) {
   __shared__ double s_part[TRK_THREADS / 32][NE_VALS];
+  if (skip && *skip) return;
+  if (P_dev) P = *P_dev;
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   double acc[NE_VALS];
 #pragma unroll
@@ -914,8 +861,9 @@ k_normal_eqs(GridView v, const int64_t* __restrict__ nn_j, const double* __restr
 // 3188 partials at 1200x680).
 __global__ void __launch_bounds__(256)
 k_reduce_partials(const double* __restrict__ partial, int nblocks, int nvals,
-                  double* __restrict__ out) {
+                  double* __restrict__ out, const int32_t* __restrict__ skip = nullptr) {
   __shared__ double red[256];
+  if (skip && *skip) return;
   const int k = blockIdx.x;
   double x = 0.0;
   for (int b = threadIdx.x; b < nblocks; b += 256) x += partial[(size_t)b * nvals + k];
@@ -933,9 +881,10 @@ constexpr int MAX_CAND = 8;
 __global__ void __launch_bounds__(TRK_THREADS)
 k_cost(const double* __restrict__ a_c, const double* __restrict__ w, const double* __restrict__ bb,
        const uint8_t* __restrict__ acc_in, int64_t m, int n_cand, const PoseArg* __restrict__ poses,
-       double* __restrict__ partial) {
+       double* __restrict__ partial, const int32_t* __restrict__ skip = nullptr) {
   __shared__ PoseArg s_pose[MAX_CAND];
   __shared__ double s_part[TRK_THREADS / 32][MAX_CAND];
+  if (skip && *skip) return;
   if (threadIdx.x < n_cand) s_pose[threadIdx.x] = poses[threadIdx.x];
   __syncthreads();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -973,12 +922,168 @@ __global__ void k_sqrt(const double* __restrict__ x, int64_t n, double* __restri
   if (i < n) y[i] = sqrt(x[i]);
 }
 
+// ---------------------------------------------------------------- GN loop on the device
+// gicp_align (tracker.py:265-346) with the host steps as one-thread kernels
+// between the launches, so a whole registration is enqueued at once and read
+// back once: per iteration the 6x6 solve and the halving candidates
+// (k_gn_solve), their frozen-weight costs (K9), the acceptance test
+// (k_gn_accept) and the next linearisation (K10 + K8) at the accepted pose.
+// Once the loop has stopped (failure, cost increase, convergence, last
+// iteration) `done` turns every later launch into a no-op.
+constexpr int GN_HALVINGS = 5;  // tracker.py MAX_STEP_HALVINGS
+
+struct GnState {
+  PoseArg pose, init;
+  PoseArg cand[MAX_CAND];
+  double xi_norm[MAX_CAND];
+  double lin[NE_VALS];   // linearisation at `pose`: H upper 21, g 6, cost, inliers
+  double costs[MAX_CAND];
+  double final_cost;
+  int32_t done, failed, converged, iterations, inliers, singular_it, n_systems, pad;
+};
+
+// geometry.py so3_exp / _left_jacobian (restated from the reference's
+// geometry.py:72-82,144-169): R = I + a [w]x + b [w]x^2, J = I + b [w]x + c [w]x^2
+__device__ void se3_exp_dev(const double* xi, double* R, double* t) {
+  const double w0 = xi[0], w1 = xi[1], w2 = xi[2];
+  const double theta = sqrt(w0 * w0 + w1 * w1 + w2 * w2);
+  const double K[9] = {0.0, -w2, w1, w2, 0.0, -w0, -w1, w0, 0.0};
+  double K2[9];
+  for (int r = 0; r < 3; ++r)
+    for (int c = 0; c < 3; ++c)
+      K2[3 * r + c] = K[3 * r] * K[c] + K[3 * r + 1] * K[3 + c] + K[3 * r + 2] * K[6 + c];
+  double a, b, c;
+  if (theta < 1e-8) {
+    a = 1.0;
+    b = 0.5;
+    c = 1.0 / 6.0;
+  } else {
+    const double sn = sin(theta), cs = cos(theta), t2 = theta * theta;
+    a = sn / theta;
+    b = (1.0 - cs) / t2;
+    c = (theta - sn) / (t2 * theta);
+  }
+  double J[9];
+  for (int k = 0; k < 9; ++k) {
+    const double id = (k % 4 == 0) ? 1.0 : 0.0;
+    R[k] = id + a * K[k] + b * K2[k];
+    J[k] = id + (theta < 1e-8 ? 0.5 : b) * K[k] + c * K2[k];
+  }
+  for (int r = 0; r < 3; ++r) t[r] = J[3 * r] * xi[3] + J[3 * r + 1] * xi[4] + J[3 * r + 2] * xi[5];
+}
+
+// np.linalg.solve(h, -g): LU with partial pivoting (LAPACK dgesv's pivot
+// choice); false on an exactly singular system (numpy raises LinAlgError)
+__device__ bool solve6(double A[6][6], double* x) {
+  int piv[6];
+  for (int k = 0; k < 6; ++k) piv[k] = k;
+  for (int k = 0; k < 6; ++k) {
+    int p = k;
+    double best = fabs(A[k][k]);
+    for (int r = k + 1; r < 6; ++r)
+      if (fabs(A[r][k]) > best) {
+        best = fabs(A[r][k]);
+        p = r;
+      }
+    if (best == 0.0) return false;
+    if (p != k) {
+      for (int c = 0; c < 6; ++c) {
+        const double tmp = A[k][c];
+        A[k][c] = A[p][c];
+        A[p][c] = tmp;
+      }
+      const double tx = x[k];
+      x[k] = x[p];
+      x[p] = tx;
+    }
+    for (int r = k + 1; r < 6; ++r) {
+      const double f = A[r][k] / A[k][k];
+      A[r][k] = f;
+      for (int c = k + 1; c < 6; ++c) A[r][c] -= f * A[k][c];
+      x[r] -= f * x[k];
+    }
+  }
+  for (int k = 5; k >= 0; --k) {
+    double v = x[k];
+    for (int c = k + 1; c < 6; ++c) v -= A[k][c] * x[c];
+    x[k] = v / A[k][k];
+  }
+  return true;
+}
+
+__global__ void k_gn_solve(GnState* __restrict__ s, double* __restrict__ systems, int it,
+                           int min_inliers) {
+  if (threadIdx.x != 0 || s->done) return;
+  const int n_acc = (int)llround(s->lin[28]);
+  s->inliers = n_acc;
+  if (n_acc < min_inliers) {  // tracker.py: failure returns the initial pose
+    s->failed = 1;
+    s->done = 1;
+    s->pose = s->init;
+    return;
+  }
+  for (int k = 0; k < NE_VALS; ++k) systems[(size_t)it * NE_VALS + k] = s->lin[k];
+  s->n_systems = it + 1;
+  double A[6][6], xi[6];
+  int q = 0;
+  for (int r = 0; r < 6; ++r)
+    for (int c = r; c < 6; ++c) A[r][c] = A[c][r] = s->lin[q++];
+  for (int k = 0; k < 6; ++k) xi[k] = -s->lin[21 + k];
+  if (!solve6(A, xi)) {  // numpy falls back to lstsq: the host finishes the loop
+    s->singular_it = it;
+    s->done = 1;
+    return;
+  }
+  const PoseArg P = s->pose;
+  for (int h = 0; h <= GN_HALVINGS; ++h) {
+    double R[9], t[3];
+    se3_exp_dev(xi, R, t);
+    PoseArg c;  // se3_exp(xi).compose(pose)
+    for (int r = 0; r < 3; ++r) {
+      for (int k = 0; k < 3; ++k)
+        c.r[3 * r + k] = R[3 * r] * P.r[k] + R[3 * r + 1] * P.r[3 + k] + R[3 * r + 2] * P.r[6 + k];
+      c.t[r] = R[3 * r] * P.t[0] + R[3 * r + 1] * P.t[1] + R[3 * r + 2] * P.t[2] + t[r];
+    }
+    s->cand[h] = c;
+    double nn = 0.0;
+    for (int k = 0; k < 6; ++k) nn += xi[k] * xi[k];
+    s->xi_norm[h] = sqrt(nn);
+    for (int k = 0; k < 6; ++k) xi[k] *= 0.5;
+  }
+}
+
+__global__ void k_gn_accept(GnState* __restrict__ s, double* __restrict__ pairs, int it,
+                            int max_iters, double eps) {
+  if (threadIdx.x != 0 || s->done) return;
+  const double before = s->lin[27];
+  int k = 0;
+  while (s->costs[k] > before && k < GN_HALVINGS) ++k;
+  const double after = s->costs[k];
+  if (after > before) {
+    s->final_cost = before;
+    s->done = 1;
+    return;
+  }
+  s->pose = s->cand[k];
+  s->iterations += 1;
+  s->final_cost = after;
+  pairs[2 * it] = before;
+  pairs[2 * it + 1] = after;
+  if (s->xi_norm[k] < eps) {
+    s->converged = 1;
+    s->done = 1;
+  } else if (it + 1 == max_iters) {
+    s->done = 1;
+  }
+}
+
 }  // namespace sgad
 
 struct sgad_geomset {
   sgad::DevBuf pts, cov, nrm, bbox, keys0, keys1, idx0, idx1, head, headscan, start, hkeys, hvals,
       cub_tmp;
-  sgad::DevBuf w, b, acc, partial, poses, nn_j, nn_d2, unres, counter, nn_qprev, nn_second, nn_lists;
+  sgad::DevBuf w, b, acc, partial, poses, nn_j, nn_d2, unres, counter, nn_qprev, nn_second;
+  sgad::DevBuf gn_state, gn_log;
   sgad::Grid grid[sgad::NLEV]{};
   sgad::DevBuf lslots[sgad::NLEV], lpts[sgad::NLEV];
   int64_t n = 0;
@@ -1043,7 +1148,7 @@ int sgad_geomset_destroy(sgad_geomset* g) {
                     &g->idx1, &g->head, &g->headscan, &g->start, &g->hkeys, &g->hvals,
                     &g->cub_tmp, &g->w, &g->b, &g->acc, &g->partial, &g->poses, &g->nn_j,
                     &g->nn_d2, &g->unres, &g->counter, &g->nn_qprev, &g->nn_second,
-                    &g->nn_lists};
+                    &g->gn_state, &g->gn_log};
   for (DevBuf* b : bufs) b->release();
   for (int l = 0; l < NLEV; ++l) {
     g->lslots[l].release();
@@ -1209,24 +1314,24 @@ static bool nn_persist() {
 // exact 1-NN for m queries (optionally transformed by rot/trans) into idx/d2
 static int run_nearest(sgad_geomset* g, const double* queries, int64_t m, const double* rot,
                        const double* trans, int64_t* idx, double* d2, int warm, cudaStream_t st,
-                       bool persist = false) {
+                       bool persist = false, const double* pose_dev = nullptr,
+                       const int32_t* skip = nullptr) {
   SGAD_CHECK_CUDA(g->unres.ensure(sizeof(uint32_t) * m));
-  SGAD_CHECK_CUDA(g->counter.ensure(sizeof(uint32_t) * (NLEV + 1)));
-  SGAD_CHECK_CUDA(g->nn_lists.ensure(sizeof(uint32_t) * NLEV * m));
-  SGAD_CHECK_CUDA(cudaMemsetAsync(g->counter.p, 0, sizeof(uint32_t) * (NLEV + 1), st));
+  SGAD_CHECK_CUDA(g->counter.ensure(sizeof(uint32_t) * 4));
+  SGAD_CHECK_CUDA(cudaMemsetAsync(g->counter.p, 0, sizeof(uint32_t), st));
   NNArgs a;
   a.queries = queries;
   a.m = m;
   a.warm = warm;
-  a.transform = rot != nullptr;
+  a.transform = rot != nullptr || pose_dev != nullptr;
+  a.pose_dev = pose_dev;
+  a.skip = skip;
   for (int k = 0; k < 9; ++k) a.r[k] = rot ? rot[k] : 0.0;
   for (int k = 0; k < 3; ++k) a.t[k] = trans ? trans[k] : 0.0;
   a.idx = idx;
   a.d2 = d2;
   a.unresolved = g->unres.as<uint32_t>();
   a.n_unres = g->counter.as<uint32_t>();
-  a.level_count = g->counter.as<uint32_t>() + 1;
-  a.level_list = g->nn_lists.as<uint32_t>();
   a.q_prev = nullptr;
   a.second = nullptr;
   if (persist) {
@@ -1236,28 +1341,21 @@ static int run_nearest(sgad_geomset* g, const double* queries, int64_t m, const 
     a.second = g->nn_second.as<double>();
   }
   const GridView v = view_of(g);
-  static const bool split = [] {
-    const char* e = getenv("SGAD_NN_SPLIT");
-    return e && e[0] == '1';
-  }();
-  if (split) {
-    k_nn_triage<<<nblk(m, 128), 128, 0, st>>>(v, a);
-    SGAD_LAUNCH_CHECK();
-    k_nn_search<<<nblk(m, 128) < 148u * 16u ? nblk(m, 128) : 148u * 16u, 128, 0, st>>>(v, a);
-  } else {
-    k_nearest<<<nblk(m, 128), 128, 0, st>>>(v, a);
-  }
+  k_nearest<<<nblk(m, 128), 128, 0, st>>>(v, a);
   SGAD_LAUNCH_CHECK();
   k_nearest_brute<<<256, 256, 0, st>>>(v, a);
   SGAD_LAUNCH_CHECK();
-  if (getenv("SGAD_NN_STATS")) {  // (diagnostics: queries searched per starting level)
-    uint32_t c[NLEV + 1];
-    SGAD_CHECK_CUDA(cudaMemcpyAsync(c, g->counter.p, sizeof c, cudaMemcpyDeviceToHost, st));
+#ifdef SGAD_NN_COUNT
+  {
+    unsigned long long c[8];
     SGAD_CHECK_CUDA(cudaStreamSynchronize(st));
-    fprintf(stderr, "nn m=%lld unres=%u levels:", (long long)m, c[0]);
-    for (int l = 0; l < NLEV; ++l) fprintf(stderr, " %u", c[l + 1]);
-    fprintf(stderr, "\n");
+    SGAD_CHECK_CUDA(cudaMemcpyFromSymbol(c, g_nn_count, sizeof c));
+    fprintf(stderr, "nn m=%lld searches=%llu levels=%llu cells=%llu probed=%llu empty=%llu "
+            "points=%llu probes=%llu\n", (long long)m, c[0], c[1], c[2], c[3], c[4], c[5], c[6]);
+    memset(c, 0, sizeof c);
+    SGAD_CHECK_CUDA(cudaMemcpyToSymbol(g_nn_count, c, sizeof c));
   }
+#endif
   return SGAD_OK;
 }
 
@@ -1277,13 +1375,14 @@ int sgad_geomset_nearest(sgad_geomset* g, const double* queries, int64_t m, int6
   return SGAD_OK;
 }
 
-int sgad_track_normal_eqs(sgad_geomset* g, const double* local_centers, const double* local_cov,
-                          int64_t m, const double* rot, const double* trans, int32_t metric_mode,
-                          double dist_max, int32_t warm_start, double* out, void* stream_) {
-  SGAD_REQUIRE(g && g->n > 0, "global set is empty");
-  SGAD_REQUIRE(local_centers && local_cov && rot && trans && out && m > 0,
-               "sgad_track_normal_eqs: bad arguments");
-  cudaStream_t st = (cudaStream_t)stream_;
+}  // extern "C"
+
+// One linearisation (NN + K8 + reduce into out[NE_VALS]) at a host pose
+// (rot/trans) or at a device pose (P_dev), skipped on the device when *skip.
+static int linearize(sgad_geomset* g, const double* local_centers, const double* local_cov,
+                     int64_t m, const double* rot, const double* trans, const PoseArg* P_dev,
+                     const int32_t* skip, int32_t metric_mode, double dist_max, int32_t warm_start,
+                     double* out, cudaStream_t st) {
   const unsigned nb = nblk(m, TRK_THREADS);
   SGAD_CHECK_CUDA(g->w.ensure(sizeof(double) * 6 * m));
   SGAD_CHECK_CUDA(g->b.ensure(sizeof(double) * 3 * m));
@@ -1294,20 +1393,34 @@ int sgad_track_normal_eqs(sgad_geomset* g, const double* local_centers, const do
   SGAD_CHECK_CUDA(g->nn_d2.ensure(sizeof(double) * m));
   g->nn_m = m;
   int rc = run_nearest(g, local_centers, m, rot, trans, g->nn_j.as<int64_t>(), g->nn_d2.as<double>(),
-                       warm ? 1 : 0, st, nn_persist());
+                       warm ? 1 : 0, st, nn_persist(), reinterpret_cast<const double*>(P_dev), skip);
   if (rc) return rc;
-  PoseArg P;
-  for (int k = 0; k < 9; ++k) P.r[k] = rot[k];
-  for (int k = 0; k < 3; ++k) P.t[k] = trans[k];
+  PoseArg P{};
+  if (rot)
+    for (int k = 0; k < 9; ++k) P.r[k] = rot[k];
+  if (trans)
+    for (int k = 0; k < 3; ++k) P.t[k] = trans[k];
   k_normal_eqs<<<nb, TRK_THREADS, 0, st>>>(view_of(g), g->nn_j.as<int64_t>(), g->nn_d2.as<double>(),
                                            g->cov.as<double>(), g->nrm.as<double>(),
-                                           local_centers, local_cov, m, P, metric_mode, dist_max,
-                                           g->w.as<double>(), g->b.as<double>(),
+                                           local_centers, local_cov, m, P, P_dev, skip, metric_mode,
+                                           dist_max, g->w.as<double>(), g->b.as<double>(),
                                            g->acc.as<uint8_t>(), g->partial.as<double>());
   SGAD_LAUNCH_CHECK();
-  k_reduce_partials<<<NE_VALS, 256, 0, st>>>(g->partial.as<double>(), (int)nb, NE_VALS, out);
+  k_reduce_partials<<<NE_VALS, 256, 0, st>>>(g->partial.as<double>(), (int)nb, NE_VALS, out, skip);
   SGAD_LAUNCH_CHECK();
   return SGAD_OK;
+}
+
+extern "C" {
+
+int sgad_track_normal_eqs(sgad_geomset* g, const double* local_centers, const double* local_cov,
+                          int64_t m, const double* rot, const double* trans, int32_t metric_mode,
+                          double dist_max, int32_t warm_start, double* out, void* stream_) {
+  SGAD_REQUIRE(g && g->n > 0, "global set is empty");
+  SGAD_REQUIRE(local_centers && local_cov && rot && trans && out && m > 0,
+               "sgad_track_normal_eqs: bad arguments");
+  return linearize(g, local_centers, local_cov, m, rot, trans, nullptr, nullptr, metric_mode,
+                   dist_max, warm_start, out, (cudaStream_t)stream_);
 }
 
 int sgad_track_correspondences(sgad_geomset* g, int64_t* idx, int64_t m, void* stream_) {
@@ -1348,6 +1461,74 @@ int sgad_track_cost(sgad_geomset* g, const double* local_centers, int64_t m, con
   SGAD_LAUNCH_CHECK();
   // (hp may go: an asynchronous copy from pageable memory returns once the
   // source is staged)
+  return SGAD_OK;
+}
+
+int sgad_track_gicp(sgad_geomset* g, const double* local_centers, const double* local_cov,
+                    int64_t m, const double* init_pose, int32_t metric_mode, double dist_max,
+                    int32_t max_iters, double convergence_eps, int32_t warm_start,
+                    int32_t min_inliers, double* result, double* systems, double* cost_pairs,
+                    uint8_t* accepted_first, void* stream_) {
+  SGAD_REQUIRE(g && g->n > 0, "global set is empty");
+  SGAD_REQUIRE(local_centers && local_cov && init_pose && result && m > 0 && max_iters > 0,
+               "sgad_track_gicp: bad arguments");
+  cudaStream_t st = (cudaStream_t)stream_;
+  const unsigned nb = nblk(m, TRK_THREADS);
+  SGAD_CHECK_CUDA(g->gn_state.ensure(sizeof(GnState)));
+  SGAD_CHECK_CUDA(g->gn_log.ensure(sizeof(double) * (size_t)max_iters * (NE_VALS + 2)));
+  SGAD_CHECK_CUDA(g->partial.ensure(sizeof(double) * (NE_VALS > MAX_CAND ? NE_VALS : MAX_CAND) * nb));
+  GnState h{};
+  for (int k = 0; k < 9; ++k) h.pose.r[k] = h.init.r[k] = init_pose[k];
+  for (int k = 0; k < 3; ++k) h.pose.t[k] = h.init.t[k] = init_pose[9 + k];
+  h.final_cost = NAN;
+  h.singular_it = -1;
+  GnState* s = g->gn_state.as<GnState>();
+  double* sys = g->gn_log.as<double>();
+  double* pairs = sys + (size_t)max_iters * NE_VALS;
+  SGAD_CHECK_CUDA(cudaMemcpyAsync(s, &h, sizeof h, cudaMemcpyHostToDevice, st));
+  const int32_t* done = &s->done;
+  if (int rc = linearize(g, local_centers, local_cov, m, nullptr, nullptr, &s->pose, done,
+                         metric_mode, dist_max, warm_start, s->lin, st))
+    return rc;
+  if (accepted_first)
+    SGAD_CHECK_CUDA(cudaMemcpyAsync(accepted_first, g->acc.p, m, cudaMemcpyDefault, st));
+  for (int it = 0; it < max_iters; ++it) {
+    k_gn_solve<<<1, 32, 0, st>>>(s, sys, it, min_inliers);
+    SGAD_LAUNCH_CHECK();
+    k_cost<<<nb, TRK_THREADS, 0, st>>>(local_centers, g->w.as<double>(), g->b.as<double>(),
+                                       g->acc.as<uint8_t>(), m, GN_HALVINGS + 1, s->cand,
+                                       g->partial.as<double>(), done);
+    SGAD_LAUNCH_CHECK();
+    k_reduce_partials<<<MAX_CAND, 256, 0, st>>>(g->partial.as<double>(), (int)nb, MAX_CAND,
+                                                s->costs, done);
+    SGAD_LAUNCH_CHECK();
+    k_gn_accept<<<1, 32, 0, st>>>(s, pairs, it, max_iters, convergence_eps);
+    SGAD_LAUNCH_CHECK();
+    if (it + 1 < max_iters) {
+      if (int rc = linearize(g, local_centers, local_cov, m, nullptr, nullptr, &s->pose, done,
+                             metric_mode, dist_max, 1, s->lin, st))
+        return rc;
+    }
+  }
+  SGAD_CHECK_CUDA(cudaMemcpyAsync(&h, s, sizeof h, cudaMemcpyDeviceToHost, st));
+  if (systems)
+    SGAD_CHECK_CUDA(cudaMemcpyAsync(systems, sys, sizeof(double) * (size_t)max_iters * NE_VALS,
+                                    cudaMemcpyDeviceToHost, st));
+  if (cost_pairs)
+    SGAD_CHECK_CUDA(cudaMemcpyAsync(cost_pairs, pairs, sizeof(double) * 2 * (size_t)max_iters,
+                                    cudaMemcpyDeviceToHost, st));
+  SGAD_CHECK_CUDA(cudaStreamSynchronize(st));
+  // result: pose (12), final cost, iterations, inliers, converged, failed,
+  // singular iteration (-1: none), systems logged
+  for (int k = 0; k < 9; ++k) result[k] = h.pose.r[k];
+  for (int k = 0; k < 3; ++k) result[9 + k] = h.pose.t[k];
+  result[12] = h.final_cost;
+  result[13] = h.iterations;
+  result[14] = h.inliers;
+  result[15] = h.converged;
+  result[16] = h.failed;
+  result[17] = h.singular_it;
+  result[18] = h.n_systems;
   return SGAD_OK;
 }
 

@@ -372,6 +372,24 @@ class GicpSolver:
         h.copy_(self.costs[:len(poses)])
         return h.numpy().copy()
 
+    def run_device_loop(self, init: Pose):
+        """The whole Gauss-Newton loop on the device (sgad_track_gicp) from
+        ``init``: (result[19], systems [iters, 29], cost pairs [iters, 2],
+        first acceptance flags [m] bool)."""
+        it = int(self.cfg.max_gicp_iters)
+        p = (ctypes.c_double * 12)(*np.concatenate([np.asarray(init.rotation, np.float64).reshape(9),
+                                                    np.asarray(init.translation, np.float64).reshape(3)]))
+        res = np.empty(19)
+        sys_rows = np.empty((it, 29))
+        pairs = np.empty((it, 2))
+        acc = torch.empty(self.m, dtype=torch.uint8, device=self.local.centers.device)
+        N.call("sgad_track_gicp", self.g._h, self.local.centers.data_ptr(), self.local.cov6.data_ptr(),
+               self.m, p, self.metric, float(self.cfg.correspondence_dist_max), it,
+               float(self.cfg.convergence_eps), self._warm, MIN_INLIERS, res.ctypes.data,
+               sys_rows.ctypes.data, pairs.ctypes.data, acc.data_ptr(), N.stream_ptr())
+        self._warm = 1
+        return res, sys_rows, pairs, acc.bool().cpu().numpy()
+
     def correspondences(self):
         """The last linearisation's exact nearest neighbours (tracker.py:288 j)."""
         idx = torch.empty(self.m, dtype=torch.int64, device=self.local.centers.device)
@@ -384,6 +402,13 @@ class GicpSolver:
         return acc.bool().cpu().numpy()
 
 
+# gicp_align runs its Gauss-Newton loop on the device (sgad_track_gicp: one
+# host round trip per registration); False selects the host loop (one round
+# trip per iteration), which also finishes a device loop stopped by an
+# exactly singular system (numpy's lstsq fallback).
+GICP_DEVICE_LOOP = True
+
+
 def gicp_align(local: LocalGeomSet, global_set: GlobalGeomSet, init: Pose, cfg: TrackerConfig,
                return_systems: bool = False):
     """tracker.py:265-346: Gauss-Newton on the combined-covariance cost with
@@ -392,17 +417,45 @@ def gicp_align(local: LocalGeomSet, global_set: GlobalGeomSet, init: Pose, cfg: 
         raise TrackerError("global set is empty")
     diag = GicpDiagnostics()
     systems = []
-    pose = init
+    if cfg.max_gicp_iters <= 0:
+        return (init, diag, systems) if return_systems else (init, diag)
     solver = GicpSolver(local, global_set, cfg)
-    nxt = solver.linearize(pose) if cfg.max_gicp_iters > 0 else None
-    for it in range(cfg.max_gicp_iters):
+    if not GICP_DEVICE_LOOP:
+        pose = _gicp_host_loop(solver, init, init, cfg, diag, systems, 0)
+        return (pose, diag, systems) if return_systems else (pose, diag)
+    res, sys_rows, pairs, acc = solver.run_device_loop(init)
+    diag.accepted_first = acc
+    diag.iterations = int(res[13])
+    diag.inlier_count = int(res[14])
+    diag.converged = bool(res[15])
+    diag.failed = bool(res[16])
+    diag.final_cost = float(res[12])
+    diag.cost_pairs = [(float(a), float(b)) for a, b in pairs[:diag.iterations]]
+    systems = [(_sym6(r[:21]), r[21:27].copy(), float(r[27]), int(round(r[28])))
+               for r in sys_rows[:int(res[18])]]
+    pose = Pose(res[:9].reshape(3, 3).copy(), res[9:12].copy())
+    singular = int(res[17])
+    if singular >= 0:
+        # numpy's lstsq fallback for an exactly singular system: the host
+        # continues from the pose reached, re-linearising it
+        systems = systems[:singular]
+        pose = _gicp_host_loop(solver, pose, init, cfg, diag, systems, singular)
+    return (pose, diag, systems) if return_systems else (pose, diag)
+
+
+def _gicp_host_loop(solver, pose, init, cfg, diag, systems, it0):
+    """The Gauss-Newton loop with the solve on the host from iteration it0 at
+    ``pose`` (one host round trip per iteration: the candidate costs and,
+    speculatively, the next linearisation at the full step)."""
+    nxt = solver.linearize(pose)
+    for it in range(it0, cfg.max_gicp_iters):
         h, g, cost_before, n_acc = nxt
         diag.inlier_count = n_acc
         if it == 0:
             diag.accepted_first = solver.accepted()
         if n_acc < MIN_INLIERS:
             diag.failed = True
-            return (init, diag, systems) if return_systems else (init, diag)
+            return init
         systems.append((h, g, cost_before, n_acc))
         try:
             xi = np.linalg.solve(h, -g)
@@ -413,8 +466,6 @@ def gicp_align(local: LocalGeomSet, global_set: GlobalGeomSet, init: Pose, cfg: 
             xis.append(xi)
             cands.append(se3_exp(xi).compose(pose))
             xi = 0.5 * xi
-        # the candidates' costs and, speculatively, the next linearisation at
-        # the full step (usually accepted): one host round trip per iteration
         last = it + 1 == cfg.max_gicp_iters
         costs, spec = solver.costs_and_linearize(cands, None if last else cands[0])
         k = 0
@@ -431,9 +482,9 @@ def gicp_align(local: LocalGeomSet, global_set: GlobalGeomSet, init: Pose, cfg: 
         if np.linalg.norm(xi) < cfg.convergence_eps:
             diag.converged = True
             break
-        if it + 1 < cfg.max_gicp_iters:
+        if not last:
             nxt = spec if k == 0 else solver.linearize(pose)
-    return (pose, diag, systems) if return_systems else (pose, diag)
+    return pose
 
 
 def init_pose_constant_speed(prev: Pose, prev_prev: Pose) -> Pose:

@@ -187,3 +187,56 @@ def test_nearest_neighbours_exact_along_gicp_iterations():
         q = lc @ np.asarray(p.rotation).T + np.asarray(p.translation)
         _, jk = tree.query(q)
         np.testing.assert_array_equal(s.correspondences(), jk, err_msg=f"pose {k}")
+
+
+def test_device_gn_loop_matches_host_loop():
+    """gicp_align's device-resident Gauss-Newton loop (sgad_track_gicp: solve,
+    halvings, costs and acceptance on the device) against the host loop
+    (np.linalg.solve, se3_exp on the host) on C2: same iteration count, poses
+    within 1e-9, the logged systems within 1e-6 of their largest entry (the
+    two solves round differently in the last bits, and g sums terms that
+    cancel to ~1e-3 of their magnitude), cost pairs within 1e-8."""
+    from paper_2603_21055_b200 import scenes, tracker as T
+    from paper_2603_21055_b200.geometry import Pose, pose_difference
+    intr, ref, qry, truth = scenes.config_c2()
+    cfg = T.TrackerConfig(downsample_ratio=1, max_gicp_iters=12, convergence_eps=0.0,
+                          voxel_size=1e-4)
+    gs = T.GlobalGeomSet(cfg.voxel_size)
+    T.update_global_set(gs, T.build_local_set(ref, cfg), Pose.identity())
+    local = T.build_local_set(qry, cfg)
+    out = {}
+    for dev_loop in (True, False):
+        T.GICP_DEVICE_LOOP = dev_loop
+        try:
+            out[dev_loop] = T.gicp_align(local, gs, Pose.identity(), cfg, return_systems=True)
+        finally:
+            T.GICP_DEVICE_LOOP = True
+    (pd, dd, sd), (ph, dh, sh) = out[True], out[False]
+    assert dd.iterations == dh.iterations and len(sd) == len(sh)
+    assert dd.inlier_count == dh.inlier_count and dd.failed == dh.failed
+    np.testing.assert_array_equal(dd.accepted_first, dh.accepted_first)
+    for (h1, g1, c1, n1), (h2, g2, c2, n2) in zip(sd, sh):
+        assert n1 == n2
+        np.testing.assert_allclose(h1, h2, rtol=0, atol=1e-6 * np.abs(h2).max())
+        np.testing.assert_allclose(g1, g2, rtol=0, atol=1e-6 * np.abs(g2).max())
+        assert abs(c1 - c2) <= 1e-8 * abs(c2)
+    np.testing.assert_allclose(np.array(dd.cost_pairs), np.array(dh.cost_pairs), rtol=1e-8)
+    rot_err, t_err = pose_difference(pd, ph)
+    assert rot_err < 1e-9 and t_err < 1e-9
+
+
+def test_device_gn_loop_failure_returns_init():
+    """Fewer than 10 accepted correspondences on the device loop: the initial
+    pose back, failed set, no iteration counted (tracker.py:291-295)."""
+    from paper_2603_21055_b200 import scenes, tracker as T
+    from paper_2603_21055_b200.geometry import Pose
+    intr, ref, qry, truth = scenes.config_c2()
+    cfg = T.TrackerConfig(downsample_ratio=1, max_gicp_iters=5, voxel_size=1e-4,
+                          correspondence_dist_max=1e-9)
+    gs = T.GlobalGeomSet(cfg.voxel_size)
+    T.update_global_set(gs, T.build_local_set(ref, cfg), Pose.identity())
+    init = Pose(np.eye(3), np.array([0.3, -0.2, 0.1]))
+    pose, diag = T.gicp_align(T.build_local_set(qry, cfg), gs, init, cfg)
+    assert diag.failed and diag.iterations == 0
+    np.testing.assert_array_equal(pose.translation, init.translation)
+    np.testing.assert_array_equal(pose.rotation, init.rotation)
