@@ -1684,7 +1684,7 @@ static int prepare_front(sgad_raster* h, const sgad_frame* frames, int32_t n_fra
       h->k32a.as<uint32_t>(), cnt + C_NSURV, zkeys, perm, w.claim, cnt + C_NLONG,
       h->runs.as<uint2>());
   SGAD_LAUNCH_CHECK();
-  k_long_runs<<<148, 1024, LONG_RUN_SMEM, st>>>(h->runs.as<uint2>(), cnt + C_NLONG, zkeys, perm,
+  k_long_runs<<<2 * 148, 1024, LONG_RUN_SMEM, st>>>(h->runs.as<uint2>(), cnt + C_NLONG, zkeys, perm,
                                                 h->keys1.as<unsigned long long>(),
                                                 h->vals1.as<uint32_t>());
   SGAD_LAUNCH_CHECK();
@@ -1751,6 +1751,16 @@ int sgad_raster_prepare(sgad_raster* h, const sgad_frame* frames, int32_t n_fram
       SGAD_REQUIRE(h->cap_pairs < (1ll << 30), "too many tile pairs (%lld)", (long long)h->n_pairs);
       if (int rc = prepare_pairs(h, nullptr, st)) return rc;
     }
+  }
+  if (getenv("SGAD_DEBUG_RUNS") && h->n_total > 0) {  // (diagnostics: the depth fix-up's long runs)
+    uint32_t nl = 0;
+    SGAD_CHECK_CUDA(cudaMemcpy(&nl, h->counters.as<uint32_t>() + C_NLONG, 4, cudaMemcpyDeviceToHost));
+    std::vector<uint2> runs(nl);
+    if (nl) SGAD_CHECK_CUDA(cudaMemcpy(runs.data(), h->runs.p, sizeof(uint2) * nl, cudaMemcpyDeviceToHost));
+    unsigned long long tot = 0, mx = 0;
+    for (auto& r : runs) { tot += r.y; mx = std::max<unsigned long long>(mx, r.y); }
+    fprintf(stderr, "depth runs: survivors %lld long runs %u elements %llu longest %llu\n",
+            (long long)h->n_surv, nl, tot, mx);
   }
   if (n_survivors) *n_survivors = h->n_surv;
   if (n_pairs) *n_pairs = h->n_pairs;

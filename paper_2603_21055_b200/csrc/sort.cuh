@@ -359,9 +359,9 @@ k_pair_emit(const uint32_t* __restrict__ perm, const Box* __restrict__ box,
 
 // ---------------------------------------------------------------- long runs
 // Runs of equal depth buckets longer than 64 (queued by k_depth_fixup) are
-// put in exact (z bits, emission index) order here, one block per run:
-// already-ordered runs (a plane seen head-on: equal z, emission order kept by
-// the stable sort) are skipped, runs of up to LONG_RUN_SMEM_N are sorted
+// put in exact (z bits, emission index) order here, one block per run (two
+// blocks per SM: ~300 runs per C4 view; already-ordered runs, e.g. a plane
+// seen head-on, are never queued): runs of up to LONG_RUN_SMEM_N are sorted
 // bitonically in shared memory, longer ones by a block merge sort through a
 // global scratch (each element finds its place in the other half by binary
 // search; the keys are unique).
@@ -379,18 +379,10 @@ k_long_runs(const uint2* __restrict__ long_runs, const uint32_t* __restrict__ n_
   extern __shared__ __align__(16) unsigned char smem_raw[];
   unsigned long long* zs = reinterpret_cast<unsigned long long*>(smem_raw);  // [LONG_RUN_SMEM_N]
   uint32_t* es = reinterpret_cast<uint32_t*>(zs + LONG_RUN_SMEM_N);           // [LONG_RUN_SMEM_N]
-  __shared__ int s_unsorted;
   const uint32_t nr = *n_long;
   for (uint32_t r = blockIdx.x; r < nr; r += gridDim.x) {
+    // (queued by k_depth_fixup only after an out-of-order pair: never sorted)
     const uint2 ru = long_runs[r];
-    if (threadIdx.x == 0) s_unsorted = 0;
-    __syncthreads();
-    for (uint32_t i = threadIdx.x; i + 1 < ru.y; i += blockDim.x) {
-      const uint32_t ea = perm[ru.x + i], eb = perm[ru.x + i + 1];
-      if (!zlt(zkeys[ea], ea, zkeys[eb], eb)) s_unsorted = 1;
-    }
-    __syncthreads();
-    if (!s_unsorted) continue;
     if (ru.y <= LONG_RUN_SMEM_N) {
       uint32_t P = 1;
       while (P < ru.y) P <<= 1;
