@@ -1013,43 +1013,56 @@ __device__ bool solve6(double A[6][6], double* x) {
 
 __global__ void k_gn_solve(GnState* __restrict__ s, double* __restrict__ systems, int it,
                            int min_inliers) {
-  if (threadIdx.x != 0 || s->done) return;
-  const int n_acc = (int)llround(s->lin[28]);
-  s->inliers = n_acc;
-  if (n_acc < min_inliers) {  // tracker.py: failure returns the initial pose
-    s->failed = 1;
-    s->done = 1;
-    s->pose = s->init;
-    return;
-  }
-  for (int k = 0; k < NE_VALS; ++k) systems[(size_t)it * NE_VALS + k] = s->lin[k];
-  s->n_systems = it + 1;
-  double A[6][6], xi[6];
-  int q = 0;
-  for (int r = 0; r < 6; ++r)
-    for (int c = r; c < 6; ++c) A[r][c] = A[c][r] = s->lin[q++];
-  for (int k = 0; k < 6; ++k) xi[k] = -s->lin[21 + k];
-  if (!solve6(A, xi)) {  // numpy falls back to lstsq: the host finishes the loop
-    s->singular_it = it;
-    s->done = 1;
-    return;
-  }
-  const PoseArg P = s->pose;
-  for (int h = 0; h <= GN_HALVINGS; ++h) {
-    double R[9], t[3];
-    se3_exp_dev(xi, R, t);
-    PoseArg c;  // se3_exp(xi).compose(pose)
-    for (int r = 0; r < 3; ++r) {
-      for (int k = 0; k < 3; ++k)
-        c.r[3 * r + k] = R[3 * r] * P.r[k] + R[3 * r + 1] * P.r[3 + k] + R[3 * r + 2] * P.r[6 + k];
-      c.t[r] = R[3 * r] * P.t[0] + R[3 * r + 1] * P.t[1] + R[3 * r + 2] * P.t[2] + t[r];
+  // thread 0: the gate and the solve; threads 0-5: one halving candidate each
+  __shared__ double s_xi[6];
+  __shared__ int s_go;
+  if (threadIdx.x == 0) {
+    s_go = 0;
+    if (!s->done) {
+      const int n_acc = (int)llround(s->lin[28]);
+      s->inliers = n_acc;
+      if (n_acc < min_inliers) {  // tracker.py: failure returns the initial pose
+        s->failed = 1;
+        s->done = 1;
+        s->pose = s->init;
+      } else {
+        for (int k = 0; k < NE_VALS; ++k) systems[(size_t)it * NE_VALS + k] = s->lin[k];
+        s->n_systems = it + 1;
+        double A[6][6], xi[6];
+        int q = 0;
+        for (int r = 0; r < 6; ++r)
+          for (int c = r; c < 6; ++c) A[r][c] = A[c][r] = s->lin[q++];
+        for (int k = 0; k < 6; ++k) xi[k] = -s->lin[21 + k];
+        if (!solve6(A, xi)) {  // numpy falls back to lstsq: the host finishes the loop
+          s->singular_it = it;
+          s->done = 1;
+        } else {
+          for (int k = 0; k < 6; ++k) s_xi[k] = xi[k];
+          s_go = 1;
+        }
+      }
     }
-    s->cand[h] = c;
-    double nn = 0.0;
-    for (int k = 0; k < 6; ++k) nn += xi[k] * xi[k];
-    s->xi_norm[h] = sqrt(nn);
-    for (int k = 0; k < 6; ++k) xi[k] *= 0.5;
   }
+  __syncthreads();
+  const int h = threadIdx.x;
+  if (!s_go || h > GN_HALVINGS) return;
+  // candidate h: se3_exp(xi / 2^h).compose(pose) (the halvings scale exactly)
+  double xi[6];
+  const double f = ldexp(1.0, -h);
+  for (int k = 0; k < 6; ++k) xi[k] = s_xi[k] * f;
+  double R[9], t[3];
+  se3_exp_dev(xi, R, t);
+  const PoseArg P = s->pose;
+  PoseArg c;
+  for (int r = 0; r < 3; ++r) {
+    for (int k = 0; k < 3; ++k)
+      c.r[3 * r + k] = R[3 * r] * P.r[k] + R[3 * r + 1] * P.r[3 + k] + R[3 * r + 2] * P.r[6 + k];
+    c.t[r] = R[3 * r] * P.t[0] + R[3 * r + 1] * P.t[1] + R[3 * r + 2] * P.t[2] + t[r];
+  }
+  s->cand[h] = c;
+  double nn = 0.0;
+  for (int k = 0; k < 6; ++k) nn += xi[k] * xi[k];
+  s->xi_norm[h] = sqrt(nn);
 }
 
 __global__ void k_gn_accept(GnState* __restrict__ s, double* __restrict__ pairs, int it,
@@ -1075,6 +1088,7 @@ __global__ void k_gn_accept(GnState* __restrict__ s, double* __restrict__ pairs,
   } else if (it + 1 == max_iters) {
     s->done = 1;
   }
+
 }
 
 }  // namespace sgad
@@ -1155,6 +1169,7 @@ int sgad_geomset_destroy(sgad_geomset* g) {
     g->lpts[l].release();
   }
   if (g->pinned) cudaFreeHost(g->pinned);
+
   delete g;
   return SGAD_OK;
 }
@@ -1377,24 +1392,29 @@ int sgad_geomset_nearest(sgad_geomset* g, const double* queries, int64_t m, int6
 
 }  // extern "C"
 
-// One linearisation (NN + K8 + reduce into out[NE_VALS]) at a host pose
-// (rot/trans) or at a device pose (P_dev), skipped on the device when *skip.
-static int linearize(sgad_geomset* g, const double* local_centers, const double* local_cov,
-                     int64_t m, const double* rot, const double* trans, const PoseArg* P_dev,
-                     const int32_t* skip, int32_t metric_mode, double dist_max, int32_t warm_start,
-                     double* out, cudaStream_t st) {
+// The exact nearest neighbours of the local centres at a host pose
+// (rot/trans) or a device pose (P_dev), skipped on the device when *skip.
+static int nearest_at(sgad_geomset* g, const double* local_centers, int64_t m, const double* rot,
+                      const double* trans, const PoseArg* P_dev, const int32_t* skip,
+                      int32_t warm_start, cudaStream_t st) {
+  const bool warm = warm_start && g->nn_m == m && g->nn_j.cap >= sizeof(int64_t) * m;
+  SGAD_CHECK_CUDA(g->nn_j.ensure(sizeof(int64_t) * m));
+  SGAD_CHECK_CUDA(g->nn_d2.ensure(sizeof(double) * m));
+  g->nn_m = m;
+  return run_nearest(g, local_centers, m, rot, trans, g->nn_j.as<int64_t>(), g->nn_d2.as<double>(),
+                     warm ? 1 : 0, st, nn_persist(), reinterpret_cast<const double*>(P_dev), skip);
+}
+
+// K8 + reduce into out[NE_VALS] at the pose the last nearest_at used.
+static int eqs_at(sgad_geomset* g, const double* local_centers, const double* local_cov, int64_t m,
+                  const double* rot, const double* trans, const PoseArg* P_dev,
+                  const int32_t* skip, int32_t metric_mode, double dist_max, double* out,
+                  cudaStream_t st) {
   const unsigned nb = nblk(m, TRK_THREADS);
   SGAD_CHECK_CUDA(g->w.ensure(sizeof(double) * 6 * m));
   SGAD_CHECK_CUDA(g->b.ensure(sizeof(double) * 3 * m));
   SGAD_CHECK_CUDA(g->acc.ensure(m));
   SGAD_CHECK_CUDA(g->partial.ensure(sizeof(double) * NE_VALS * nb));
-  const bool warm = warm_start && g->nn_m == m && g->nn_j.cap >= sizeof(int64_t) * m;
-  SGAD_CHECK_CUDA(g->nn_j.ensure(sizeof(int64_t) * m));
-  SGAD_CHECK_CUDA(g->nn_d2.ensure(sizeof(double) * m));
-  g->nn_m = m;
-  int rc = run_nearest(g, local_centers, m, rot, trans, g->nn_j.as<int64_t>(), g->nn_d2.as<double>(),
-                       warm ? 1 : 0, st, nn_persist(), reinterpret_cast<const double*>(P_dev), skip);
-  if (rc) return rc;
   PoseArg P{};
   if (rot)
     for (int k = 0; k < 9; ++k) P.r[k] = rot[k];
@@ -1409,6 +1429,17 @@ static int linearize(sgad_geomset* g, const double* local_centers, const double*
   k_reduce_partials<<<NE_VALS, 256, 0, st>>>(g->partial.as<double>(), (int)nb, NE_VALS, out, skip);
   SGAD_LAUNCH_CHECK();
   return SGAD_OK;
+}
+
+// One linearisation (NN + K8 + reduce into out[NE_VALS]) at a host pose
+// (rot/trans) or at a device pose (P_dev), skipped on the device when *skip.
+static int linearize(sgad_geomset* g, const double* local_centers, const double* local_cov,
+                     int64_t m, const double* rot, const double* trans, const PoseArg* P_dev,
+                     const int32_t* skip, int32_t metric_mode, double dist_max, int32_t warm_start,
+                     double* out, cudaStream_t st) {
+  if (int rc = nearest_at(g, local_centers, m, rot, trans, P_dev, skip, warm_start, st)) return rc;
+  return eqs_at(g, local_centers, local_cov, m, rot, trans, P_dev, skip, metric_mode, dist_max, out,
+                st);
 }
 
 extern "C" {
