@@ -70,6 +70,9 @@ struct __align__(16) BwdRecord {
 static_assert(sizeof(BwdRecord) == 64, "backward record must be one 64-byte line");
 
 constexpr uint32_t GID_LEARN = 0x80000000u;
+#ifdef SGAD_K5_COUNT
+__device__ unsigned long long g_k5_count[2];
+#endif
 constexpr int PROJ_THREADS = 256;
 constexpr int RASTER_THREADS = 256;
 
@@ -1217,6 +1220,14 @@ __device__ __forceinline__ void bwd_sweep(WarpRing& ring, const TileGeom& g, con
                                 cc.a_z * iz * gs;
           const float g_radius = u.fx * sqrtf(-2.0f * (float)nh) * iz * gs;
           float* dst = grad_accum + (size_t)e * 8;
+#ifdef SGAD_K5_COUNT
+          {  // (diagnostics) contributions and distinct entries per warp iteration
+            const unsigned act = __activemask(), grp = __match_any_sync(act, e);
+            const int ln = threadIdx.x & 31;
+            if (ln == __ffs(act) - 1) atomicAdd(&g_k5_count[0], (unsigned long long)__popc(act));
+            if (ln == __ffs(grp) - 1) atomicAdd(&g_k5_count[1], 1ull);
+          }
+#endif
           red_add_v4(dst, g_delta, g_radius, (float)(op * (1.0 - op) * gop), (float)gcol0);
           red_add_v2(dst + 4, (float)gcol1, (float)gcol2);
         } else {
@@ -1862,6 +1873,17 @@ int sgad_raster_backward(sgad_raster* h, int32_t mode, const double* g_color,
         h->trans_final.as<double>(), h->last_idx.as<int32_t>(), h->signs.as<uint8_t>(), up,
         g_color, nullptr, nullptr, nullptr, grad_accum, clist_of(h));
     SGAD_LAUNCH_CHECK();
+#ifdef SGAD_K5_COUNT
+    {
+      unsigned long long c[2];
+      SGAD_CHECK_CUDA(cudaStreamSynchronize(st));
+      SGAD_CHECK_CUDA(cudaMemcpyFromSymbol(c, g_k5_count, sizeof c));
+      fprintf(stderr, "k5 contributions %llu distinct (entry, iteration) %llu ratio %.3f\n", c[0],
+              c[1], c[1] ? (double)c[0] / (double)c[1] : 0.0);
+      memset(c, 0, sizeof c);
+      SGAD_CHECK_CUDA(cudaMemcpyToSymbol(g_k5_count, c, sizeof c));
+    }
+#endif
     return SGAD_OK;
   }
   SGAD_REQUIRE(mode == 0 && g_color && g_depth && g_alpha && map_grads,
