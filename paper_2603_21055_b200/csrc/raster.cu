@@ -71,7 +71,7 @@ static_assert(sizeof(BwdRecord) == 64, "backward record must be one 64-byte line
 
 constexpr uint32_t GID_LEARN = 0x80000000u;
 #ifdef SGAD_K5_COUNT
-__device__ unsigned long long g_k5_count[2];
+__device__ unsigned long long g_k5_count[4];
 #endif
 constexpr int PROJ_THREADS = 256;
 constexpr int RASTER_THREADS = 256;
@@ -744,6 +744,12 @@ __device__ __forceinline__ int stage_from_queue(FwdStage& s, int qh, int take,
   }
   const uint32_t keep = __ballot_sync(0xffffffffu, m != 0);
   const int c = __popc(keep);
+#ifdef SGAD_K5_COUNT
+  if (EXACT && lane == 0) {  // (diagnostics) queued entries vs entries with pixels
+    atomicAdd(&g_k5_count[2], (unsigned long long)take);
+    atomicAdd(&g_k5_count[3], (unsigned long long)c);
+  }
+#endif
   if (m) {
     const int j = n + __popc(keep & ((1u << lane) - 1u));
     if (EXACT) {  // the backward's compact list (cbase = this batch's first slot - n)
@@ -1875,11 +1881,12 @@ int sgad_raster_backward(sgad_raster* h, int32_t mode, const double* g_color,
     SGAD_LAUNCH_CHECK();
 #ifdef SGAD_K5_COUNT
     {
-      unsigned long long c[2];
+      unsigned long long c[4];
       SGAD_CHECK_CUDA(cudaStreamSynchronize(st));
       SGAD_CHECK_CUDA(cudaMemcpyFromSymbol(c, g_k5_count, sizeof c));
-      fprintf(stderr, "k5 contributions %llu distinct (entry, iteration) %llu ratio %.3f\n", c[0],
-              c[1], c[1] ? (double)c[0] / (double)c[1] : 0.0);
+      fprintf(stderr, "k5 contributions %llu distinct (entry, iteration) %llu ratio %.3f; "
+              "k4 queued %llu with pixels %llu\n", c[0], c[1],
+              c[1] ? (double)c[0] / (double)c[1] : 0.0, c[2], c[3]);
       memset(c, 0, sizeof c);
       SGAD_CHECK_CUDA(cudaMemcpyToSymbol(g_k5_count, c, sizeof c));
     }
