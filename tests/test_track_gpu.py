@@ -240,3 +240,33 @@ def test_device_gn_loop_failure_returns_init():
     assert diag.failed and diag.iterations == 0
     np.testing.assert_array_equal(pose.translation, init.translation)
     np.testing.assert_array_equal(pose.rotation, init.rotation)
+
+
+@pytest.mark.parametrize("iters,eps", [(1, 0.0), (3, 1e3), (7, 1e-4)])
+def test_device_gn_loop_stops_like_host_loop(iters, eps):
+    """The device loop's stopping rules against the host loop's on C2: the
+    last iteration (no linearisation after it), convergence (|xi| < eps
+    stops right after the step that reached it) -- same iteration count,
+    converged flag, final cost and pose."""
+    from paper_2603_21055_b200 import scenes, tracker as T
+    from paper_2603_21055_b200.geometry import Pose, pose_difference
+    intr, ref, qry, truth = scenes.config_c2()
+    cfg = T.TrackerConfig(downsample_ratio=1, max_gicp_iters=iters, convergence_eps=eps,
+                          voxel_size=1e-4)
+    gs = T.GlobalGeomSet(cfg.voxel_size)
+    T.update_global_set(gs, T.build_local_set(ref, cfg), Pose.identity())
+    local = T.build_local_set(qry, cfg)
+    out = {}
+    for dev_loop in (True, False):
+        T.GICP_DEVICE_LOOP = dev_loop
+        try:
+            out[dev_loop] = T.gicp_align(local, gs, Pose.identity(), cfg)
+        finally:
+            T.GICP_DEVICE_LOOP = True
+    (pd, dd), (ph, dh) = out[True], out[False]
+    assert (dd.iterations, dd.converged, dd.failed) == (dh.iterations, dh.converged, dh.failed)
+    assert abs(dd.final_cost - dh.final_cost) <= 1e-8 * abs(dh.final_cost)
+    rot_err, t_err = pose_difference(pd, ph)
+    assert rot_err < 1e-9 and t_err < 1e-9
+    if eps == 1e3:
+        assert dd.converged and dd.iterations == 1
