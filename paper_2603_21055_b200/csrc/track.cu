@@ -362,18 +362,37 @@ __device__ __forceinline__ unsigned long long dkey(double x) {
   return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
 }
 
-__global__ void k_bbox(const double* __restrict__ pts, int64_t n, unsigned long long* __restrict__ bb) {
-  unsigned long long lo[3] = {~0ull, ~0ull, ~0ull}, hi[3] = {0, 0, 0};
+// bounding box of the centres as order-preserving keys: per-thread, then warp
+// (shuffles) and block (shared memory) reductions, one atomic per block and
+// value (a per-thread atomic on six addresses serialised: ~1 ms at 816 k)
+__global__ void __launch_bounds__(256) k_bbox(const double* __restrict__ pts, int64_t n,
+                                             unsigned long long* __restrict__ bb) {
+  __shared__ unsigned long long s_v[8][6];
+  unsigned long long v[6] = {~0ull, ~0ull, ~0ull, 0, 0, 0};
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
     for (int k = 0; k < 3; ++k) {
       const unsigned long long key = dkey(pts[3 * i + k]);
-      lo[k] = key < lo[k] ? key : lo[k];
-      hi[k] = key > hi[k] ? key : hi[k];
+      v[k] = key < v[k] ? key : v[k];
+      v[3 + k] = key > v[3 + k] ? key : v[3 + k];
     }
-  for (int k = 0; k < 3; ++k) {
-    atomicMin(bb + k, lo[k]);
-    atomicMax(bb + 3 + k, hi[k]);
+#pragma unroll
+  for (int k = 0; k < 6; ++k)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const unsigned long long y = __shfl_xor_sync(0xffffffffu, v[k], o);
+      v[k] = k < 3 ? (y < v[k] ? y : v[k]) : (y > v[k] ? y : v[k]);
+    }
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0)
+    for (int k = 0; k < 6; ++k) s_v[w][k] = v[k];
+  __syncthreads();
+  if (threadIdx.x < 6) {
+    const int k = threadIdx.x;
+    unsigned long long r = s_v[0][k];
+    for (int i = 1; i < (int)(blockDim.x >> 5); ++i) r = k < 3 ? min(r, s_v[i][k]) : max(r, s_v[i][k]);
+    if (k < 3) atomicMin(bb + k, r);
+    else atomicMax(bb + k, r);
   }
 }
 
@@ -1234,7 +1253,7 @@ int sgad_geomset_set(sgad_geomset* g, const double* centers, const double* cov,
   unsigned long long init[6] = {~0ull, ~0ull, ~0ull, 0, 0, 0};
   memcpy(g->pinned, init, sizeof init);
   SGAD_CHECK_CUDA(cudaMemcpyAsync(g->bbox.p, g->pinned, sizeof init, cudaMemcpyHostToDevice, st));
-  k_bbox<<<min(nblk(n, 256), 1024u), 256, 0, st>>>(g->pts.as<double>(), n,
+  k_bbox<<<min(nblk(n, 256), 148u * 4u), 256, 0, st>>>(g->pts.as<double>(), n,
                                                    g->bbox.as<unsigned long long>());
   SGAD_LAUNCH_CHECK();
   SGAD_CHECK_CUDA(cudaMemcpyAsync(g->pinned, g->bbox.p, sizeof init, cudaMemcpyDeviceToHost, st));
