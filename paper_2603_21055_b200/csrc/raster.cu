@@ -69,6 +69,10 @@ struct __align__(16) BwdRecord {
 };
 static_assert(sizeof(BwdRecord) == 64, "backward record must be one 64-byte line");
 
+#ifndef SGAD_K1_TMA
+#define SGAD_K1_TMA 1  // K1 writes its staged records with bulk copies (TMA)
+#endif
+
 constexpr uint32_t GID_LEARN = 0x80000000u;
 #ifdef SGAD_K5_COUNT
 __device__ unsigned long long g_k5_count[4];
@@ -351,6 +355,23 @@ k_project(const sgad_frame* __restrict__ frames, sgad_camera cam, int ntx, int n
   // nothing reads a record whose depth key is the sentinel)
   const int nvalid = (int)min((int64_t)PROJ_THREADS, hw - p0);
   const uint32_t gid0 = (uint32_t)(f.gauss_offset + p0);
+#if SGAD_K1_TMA
+  // one thread hands both staged arrays to the bulk-copy engine (TMA,
+  // cp.async.bulk shared -> global) and waits until they have been read
+  if (threadIdx.x == 0) {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    const uint32_t bytes = (uint32_t)nvalid * (uint32_t)sizeof(Record);
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+                 ::"l"(rec + gid0), "r"((uint32_t)__cvta_generic_to_shared(rs)), "r"(bytes)
+                 : "memory");
+    if (want_coef)
+      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+                   ::"l"(coef + gid0), "r"((uint32_t)__cvta_generic_to_shared(cs)), "r"(bytes)
+                   : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+  }
+#else
   {
     const uint4* src = reinterpret_cast<const uint4*>(rs);
     uint4* dst = reinterpret_cast<uint4*>(rec + gid0);
@@ -361,6 +382,7 @@ k_project(const sgad_frame* __restrict__ frames, sgad_camera cam, int ntx, int n
     uint4* dst = reinterpret_cast<uint4*>(coef + gid0);
     for (int i = threadIdx.x; i < nvalid * 4; i += PROJ_THREADS) dst[i] = src[i];
   }
+#endif
 }
 
 // ------------------------------------------------------------------ K2
