@@ -364,6 +364,9 @@ class WindowMapper:
         # step, replayed after; the per-view timing path stays eager)
         self.use_graph = False
         self._graph = None
+        self._hgraph = None   # step_with_targets' capture (for one set of host buffers)
+        self._hgraph_key = None
+        self._copy = None     # upload stream of step_with_targets
         self.pipelined = True   # prepare view i+1 while view i composites
         self.adam_enabled = True
         # tau = 0: forward + loss + backward as one kernel (measured no faster
@@ -509,6 +512,7 @@ class WindowMapper:
             self._cap = int(self._cap * 1.5)
             self._size_handles()
             self._graph = None  # buffers were resized: capture again
+            self._hgraph = None
         return hit
 
     def counts(self):
@@ -538,6 +542,67 @@ class WindowMapper:
                 return self.step(sync_loss=True, timing=timing, target_ready=target_ready)
             return val
         return loss
+
+    def step_with_targets(self, color, depth, mask, sync_loss=False):
+        """One window iteration whose targets -- colour ``[n, H, W, 3]``, depth
+        and valid mask ``[n, H, W]`` of this rank's views in ``views`` order,
+        in pinned host memory, dtypes as ``tcolor`` / ``tdepth`` / ``tmask`` --
+        are uploaded on a copy stream as part of the step: each view
+        composites once its own target has arrived (no view's preparation
+        waits for them).  Returns the loss like :meth:`step`.  With
+        ``use_graph`` the uploads and the step are captured once for these
+        host buffers and replayed."""
+        with torch.cuda.device(self.dev):
+            if self.pipelined:
+                self._check_overflow(block=False)
+                if self._cap == 0:
+                    self._size_handles()
+            if self.use_graph and self.pipelined:
+                loss = self._host_step_graphed(color, depth, mask)
+            else:
+                loss = self._host_step_body(color, depth, mask)
+        if sync_loss:
+            val = float(loss)
+            if self.pipelined and self._check_overflow(block=True):
+                return self.step_with_targets(color, depth, mask, sync_loss=True)
+            return val
+        return loss
+
+    def _host_step_body(self, color, depth, mask, host_flag=None):
+        main = torch.cuda.current_stream(self.dev)
+        if self._copy is None:
+            self._copy = torch.cuda.Stream(self.dev)
+        start = torch.cuda.Event()
+        start.record(main)  # the previous step no longer reads the targets
+        self._copy.wait_event(start)
+        ready = {}
+        with torch.cuda.stream(self._copy):
+            for j, v in enumerate(self.views):
+                self.tcolor[v].copy_(color[j], non_blocking=True)
+                self.tdepth[v].copy_(depth[j], non_blocking=True)
+                self.tmask[v].copy_(mask[j], non_blocking=True)
+                ready[v] = torch.cuda.Event()
+                ready[v].record(self._copy)
+        loss = self._step_body(None, ready, host_flag=host_flag)
+        main.wait_stream(self._copy)
+        return loss
+
+    def _host_step_graphed(self, color, depth, mask):
+        key = (color.data_ptr(), depth.data_ptr(), mask.data_ptr())
+        if self._hgraph is None or self._hgraph_key != key:
+            loss = self._host_step_body(color, depth, mask)  # sizes and allocations settle
+            self._hgraph_host = torch.empty(1, dtype=torch.int32).pin_memory()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                self._hgraph_loss = self._host_step_body(color, depth, mask,
+                                                         host_flag=self._hgraph_host)
+            self._hgraph, self._hgraph_key = g, key
+            return loss
+        self._hgraph.replay()
+        ev = torch.cuda.Event()
+        ev.record()
+        self._pending.append((ev, self._hgraph_host, self.adam_enabled))
+        return self._hgraph_loss
 
     def _step_graphed(self):
         """Replay the captured step (the first call runs the step eagerly --

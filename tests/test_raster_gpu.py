@@ -486,6 +486,36 @@ def test_window_step_cuda_graph_matches_eager():
     np.testing.assert_allclose(runs[True][2], runs[False][2], rtol=0, atol=2e-3)
 
 
+def test_window_step_with_host_targets():
+    """step_with_targets (targets uploaded from pinned host buffers inside the
+    step, eager and replayed from a CUDA graph) against step() with the same
+    targets resident: the same losses, step count and parameters (fp32
+    gradient sums in another order: 1e-5), and the uploaded targets land."""
+    from paper_2603_21055_b200.mapper import MapperConfig, WindowMapper
+    wc = _window_np(n_frames=4, seed=13)
+    runs = {}
+    for mode in ("resident", "host", "host_graph"):
+        wm = WindowMapper(wc.frames, wc.poses, wc.intr, wc.params, MapperConfig(tau=0.0))
+        wm.use_graph = mode == "host_graph"
+        vs = list(wm.views)
+        tc = wm.tcolor[vs].cpu().pin_memory()
+        td = wm.tdepth[vs].cpu().pin_memory()
+        tm = wm.tmask[vs].cpu().pin_memory()
+        if mode != "resident":  # the device copies must come from the uploads
+            wm.tcolor.zero_()
+            wm.tdepth.zero_()
+            wm.tmask.zero_()
+        losses = [wm.step(sync_loss=True) if mode == "resident" else
+                  wm.step_with_targets(tc, td, tm, sync_loss=True) for _ in range(4)]
+        runs[mode] = (np.array(losses), wm.t, wm.planes.cpu().numpy())
+        if mode == "host_graph":
+            assert wm._hgraph is not None
+    for mode in ("host", "host_graph"):
+        assert runs[mode][1] == runs["resident"][1] == 4
+        np.testing.assert_allclose(runs[mode][0], runs["resident"][0], rtol=1e-5)
+        np.testing.assert_allclose(runs[mode][2], runs["resident"][2], rtol=0, atol=2e-3)
+
+
 def test_window_pair_capacity_overflow_recovers():
     """The asynchronous preparation outgrowing its pair capacity (the radii
     grow after the handles were sized): the view sets the device overflow
