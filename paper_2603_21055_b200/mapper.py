@@ -552,6 +552,15 @@ class WindowMapper:
         waits for them).  Returns the loss like :meth:`step`.  With
         ``use_graph`` the uploads and the step are captured once for these
         host buffers and replayed."""
+        n = len(self.views)
+        for name, t, ref in (("color", color, self.tcolor), ("depth", depth, self.tdepth),
+                             ("mask", mask, self.tmask)):
+            if t.is_cuda or tuple(t.shape) != (n,) + tuple(ref.shape[1:]) or t.dtype != ref.dtype:
+                raise ValueError(f"step_with_targets: {name} must be a host tensor "
+                                 f"{(n,) + tuple(ref.shape[1:])} {ref.dtype}")
+            if self.use_graph and not t.is_pinned():
+                raise ValueError(f"step_with_targets: {name} must be in pinned memory "
+                                 "(the copies are captured in a CUDA graph)")
         with torch.cuda.device(self.dev):
             if self.pipelined:
                 self._check_overflow(block=False)

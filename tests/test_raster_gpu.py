@@ -510,6 +510,8 @@ def test_window_step_with_host_targets():
         runs[mode] = (np.array(losses), wm.t, wm.planes.cpu().numpy())
         if mode == "host_graph":
             assert wm._hgraph is not None
+    with pytest.raises(ValueError):  # pageable buffers cannot be captured
+        wm.step_with_targets(tc.clone(), td, tm)
     for mode in ("host", "host_graph"):
         assert runs[mode][1] == runs["resident"][1] == 4
         np.testing.assert_allclose(runs[mode][0], runs["resident"][0], rtol=1e-5)
