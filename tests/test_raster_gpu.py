@@ -518,6 +518,33 @@ def test_window_step_with_host_targets():
         np.testing.assert_allclose(runs[mode][2], runs["resident"][2], rtol=0, atol=2e-3)
 
 
+@pytest.mark.parametrize("graph", [False, True])
+def test_window_view_without_survivors(graph):
+    """A window view that sees no Gaussian (its own frame has no active
+    pixel and it faces away from the others): the step runs through the
+    asynchronous preparation (zero survivors, empty tile lists), the view's
+    loss is its bare target, it adds no gradient -- the parameters move as
+    in a window that renders only the other view."""
+    from paper_2603_21055_b200.geometry import Pose
+    from paper_2603_21055_b200.mapper import MapperConfig, WindowMapper
+    wc = _window_np(n_frames=2, seed=5)
+    wc.params[1].active_mask[:] = False
+    flip = np.diag([-1.0, 1.0, -1.0])  # 180 degrees about y: looking away
+    wc.poses[1] = Pose(wc.poses[0].rotation @ flip, wc.poses[0].translation)
+    runs = {}
+    for views in ([0, 1], [0]):
+        wm = WindowMapper(wc.frames, wc.poses, wc.intr, wc.params, MapperConfig(tau=0.0),
+                          views=views)
+        wm.use_graph = graph
+        losses = [wm.step(sync_loss=True) for _ in range(3)]
+        runs[tuple(views)] = (np.array(losses), wm.planes.cpu().numpy(), wm.counts())
+    (l2, p2, c2), (l1, p1, c1) = runs[(0, 1)], runs[(0,)]
+    assert c2[1] == (0, 0) and c2[0][0] > 0
+    assert np.all(np.isfinite(l2)) and np.all(l2 > l1)
+    # (the fp32 gradient atomics sum in run-dependent order: an ulp apart)
+    np.testing.assert_allclose(p2, p1, rtol=0, atol=1e-5)
+
+
 def test_window_pair_capacity_overflow_recovers():
     """The asynchronous preparation outgrowing its pair capacity (the radii
     grow after the handles were sized): the view sets the device overflow
