@@ -609,6 +609,14 @@ def bench_tracking(dev, which="c4size", iters=20, reps=5):
     f1.record()
     torch.cuda.synchronize()
     fit_ms = f0.elapsed_time(f1) / reps
+    # the next keyframe's insertion into the existing set (voxel gating +
+    # grid rebuild over all members), as the tracking loop does per keyframe
+    members = len(g)
+    torch.cuda.synchronize()
+    t_ins = time.perf_counter()
+    added = T.update_global_set(g, local, pose)
+    torch.cuda.synchronize()
+    insert_next_ms = (time.perf_counter() - t_ins) * 1e3
     m = len(local)
     peak, peak_kind = load_peaks()
     it_s = dt / n_it
@@ -617,7 +625,9 @@ def bench_tracking(dev, which="c4size", iters=20, reps=5):
                       f"fit, exact NN, host solve)",
             "value": n_it / dt, "unit": "GN iters/s", "correspondences": m,
             "iterations_per_run": diag.iterations, "ms_per_iteration": it_s * 1e3,
-            "fit_ms_per_frame": fit_ms, "global_insert_ms": insert_ms, "global_members": len(g),
+            "fit_ms_per_frame": fit_ms, "global_insert_ms": insert_ms,
+            "global_insert_next_ms": insert_next_ms, "global_insert_next_added": int(added),
+            "global_members": members,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak,
                          "peak_source": peak_kind, "unit": "GB/s", "frac": achieved / peak,
                          "bytes_per_iteration": 168 * m,
