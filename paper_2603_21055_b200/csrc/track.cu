@@ -598,6 +598,97 @@ __device__ bool grid_nearest(const LevelView& v, const double* pts, const double
   return false;
 }
 
+// Warp-cooperative version of grid_nearest for one query (every lane of the
+// warp calls it with the same q, best and second): each ring's cells are
+// dealt round robin to the lanes, each lane keeps its own best and bound,
+// and the warp merges them (lexicographic (d2, index) minimum; a lane's best
+// that lost is another point's exact distance, so it bounds `second`) before
+// the ring's termination test.  Same result and bound as grid_nearest: the
+// lanes prune with their own (at least as good) best, the termination test
+// is the same.  Used when few queries search, so that a search's chain of
+// dependent slot and point loads is split over 32 lanes.
+__device__ bool grid_nearest_warp(const LevelView& v, const double* q, int64_t& best_j,
+                                  double& best_d2, double& second) {
+  const Grid& g = v.g;
+  const int lane = threadIdx.x & 31;
+  int c0[3];
+  for (int k = 0; k < 3; ++k) c0[k] = cell_coord(q[k], g.lo[k], g.h, g.dim[k]);
+  for (int r = 0; r <= MAX_RINGS; ++r) {
+    const int x0 = max(c0[0] - r, 0), x1 = min(c0[0] + r, g.dim[0] - 1);
+    const int y0 = max(c0[1] - r, 0), y1 = min(c0[1] + r, g.dim[1] - 1);
+    const int z0 = max(c0[2] - r, 0), z1 = min(c0[2] + r, g.dim[2] - 1);
+    const int ny = y1 - y0 + 1, nz = z1 - z0 + 1, total = (x1 - x0 + 1) * ny * nz;
+    double lb2 = best_d2, lsec = INFINITY;
+    int64_t lj = best_j;
+    for (int ci = lane; ci < total; ci += 32) {
+      const int x = x0 + ci / (ny * nz), rem = ci % (ny * nz), y = y0 + rem / nz, z = z0 + rem % nz;
+      if (abs(x - c0[0]) != r && abs(y - c0[1]) != r && abs(z - c0[2]) != r) continue;  // interior
+      const double bx0 = g.lo[0] + x * g.h, bx = fmax(fmax(bx0 - q[0], q[0] - (bx0 + g.h)), 0.0);
+      const double by0 = g.lo[1] + y * g.h, by = fmax(fmax(by0 - q[1], q[1] - (by0 + g.h)), 0.0);
+      const double bz0 = g.lo[2] + z * g.h, bz = fmax(fmax(bz0 - q[2], q[2] - (bz0 + g.h)), 0.0);
+      const double bmin = bx * bx + by * by + bz * bz;
+      if (bmin > lb2) {
+        lsec = fmin(lsec, bmin);
+        continue;
+      }
+      const uint2 rg = hash_find(v, cell_key(x, y, z));
+      for (uint32_t t = rg.x; t < rg.x + rg.y; ++t) {
+        double px, py, pz, pj;
+        asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];"
+            : "=d"(px), "=d"(py), "=d"(pz), "=d"(pj) : "l"(v.cpts + t));
+        const int64_t j = (int64_t)__double_as_longlong(pj);
+        if (j == lj) continue;
+        const double dx = q[0] - px, dy = q[1] - py, dz = q[2] - pz;
+        const double d2 = dx * dx + dy * dy + dz * dz;
+        if (d2 < lb2 || (d2 == lb2 && j < lj)) {
+          lsec = fmin(lsec, lb2);
+          lb2 = d2;
+          lj = j;
+        } else {
+          lsec = fmin(lsec, d2);
+        }
+      }
+    }
+    // merge the lanes' bests (ties -> lower index) and bounds
+    double wb = lb2;
+    int64_t wj = lj;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, wb, o);
+      const int64_t oj = __shfl_xor_sync(0xffffffffu, wj, o);
+      if (ob < wb || (ob == wb && oj < wj)) {
+        wb = ob;
+        wj = oj;
+      }
+    }
+    double sc = (lj != wj) ? fmin(lsec, lb2) : lsec;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sc = fmin(sc, __shfl_xor_sync(0xffffffffu, sc, o));
+    second = fmin(second, sc);
+    best_d2 = wb;
+    best_j = wj;
+    double lb = INFINITY;
+    bool all_sat = true;
+    const int lo_c[3] = {x0, y0, z0}, hi_c[3] = {x1, y1, z1};
+    for (int k = 0; k < 3; ++k) {
+      if (lo_c[k] > 0) {
+        all_sat = false;
+        lb = fmin(lb, fmax(q[k] - (g.lo[k] + lo_c[k] * g.h), 0.0));
+      }
+      if (hi_c[k] < g.dim[k] - 1) {
+        all_sat = false;
+        lb = fmin(lb, fmax((g.lo[k] + (hi_c[k] + 1) * g.h) - q[k], 0.0));
+      }
+    }
+    if (all_sat) return true;
+    if (best_j >= 0 && best_d2 < lb * lb) {
+      second = fmin(second, lb * lb);
+      return true;
+    }
+  }
+  return false;
+}
+
 struct NNArgs {
   const double* queries;  // [m, 3]
   int64_t m;
@@ -614,6 +705,11 @@ struct NNArgs {
   // search and a lower bound on its second-nearest squared distance
   double* q_prev;         // [m, 3] or null
   double* second;         // [m]
+  // few searching queries (late GN iterations): warp-cooperative searches
+  uint32_t* mode;         // [1] 1: k_nearest only triages, k_nn_warp searches
+  uint32_t* list;         // [m] queries left to search (warp mode)
+  uint32_t* n_list;       // [1]
+  uint32_t* n_search;     // [1] queries searched in thread mode (the next call's mode)
 };
 
 __device__ __forceinline__ void query_point(const NNArgs& a, int64_t i, double* p) {
@@ -654,6 +750,9 @@ __device__ __forceinline__ double warm_d2(const GridView& v, const double* q, in
 // One thread per query, in query order (neighbouring queries search
 // neighbouring cells: measured faster than compacting the queries that fail
 // the persistence test into per-level lists, which loses that coherence).
+#ifndef SGAD_NN_WARP_BELOW
+#define SGAD_NN_WARP_BELOW 150000  // warp-cooperative searches when fewer queries searched (the call before)
+#endif
 #ifndef SGAD_NN_MINB
 #define SGAD_NN_MINB 10  // 48 registers: +11 % GN iterations/s over the unbounded 56 (816 k queries)
 #endif
@@ -665,6 +764,7 @@ __global__ void __launch_bounds__(128, SGAD_NN_MINB) k_nearest(GridView v, NNArg
   int64_t j = -1;
   double d2 = INFINITY;
   int l0 = 0;
+  bool search = true;
   if (a.warm) {
     j = a.idx[i];
     d2 = warm_d2(v, q, j);
@@ -678,7 +778,7 @@ __global__ void __launch_bounds__(128, SGAD_NN_MINB) k_nearest(GridView v, NNArg
       const double low = sqrt(a.second[i]) - sqrt(ex * ex + ey * ey + ez * ez);
       if (low > 0.0 && sqrt(d2) < low * (1.0 - 1e-12)) {
         nn_commit(a, i, j, d2, q, low * low * (1.0 - 1e-12));
-        return;
+        search = false;
       }
     }
     // the old neighbour's distance bounds the answer: start at the finest
@@ -686,6 +786,17 @@ __global__ void __launch_bounds__(128, SGAD_NN_MINB) k_nearest(GridView v, NNArg
     const double reach = sqrt(d2);
     while (l0 < NLEV - 1 && MAX_RINGS * v.lv[l0].g.h < reach) ++l0;
   }
+  const bool warp_mode = a.warm && a.mode && *a.mode == 1u;
+  if (a.mode) {  // count (thread mode) or list (warp mode) the searching queries
+    const unsigned act = __activemask(), sm = __ballot_sync(act, search);
+    const int lane = threadIdx.x & 31, leader = __ffs(act) - 1;
+    uint32_t base = 0;
+    if (lane == leader && sm)
+      base = atomicAdd(warp_mode ? a.n_list : a.n_search, (uint32_t)__popc(sm));
+    base = __shfl_sync(act, base, leader);
+    if (warp_mode && search) a.list[base + __popc(sm & ((1u << lane) - 1u))] = (uint32_t)i;
+  }
+  if (!search || warp_mode) return;
   double second = INFINITY;
   NN_COUNT(0, 1);
   for (int l = l0; l < NLEV; ++l) {
@@ -698,11 +809,49 @@ __global__ void __launch_bounds__(128, SGAD_NN_MINB) k_nearest(GridView v, NNArg
   a.unresolved[atomicAdd(a.n_unres, 1u)] = (uint32_t)i;
 }
 
+// Warp mode: one warp per listed query (grid-stride over the list).
+__global__ void __launch_bounds__(128) k_nn_warp(GridView v, NNArgs a) {
+  if ((a.skip && *a.skip) || *a.mode != 1u) return;
+  const uint32_t n = *a.n_list;
+  const int lane = threadIdx.x & 31;
+  const uint32_t nw = gridDim.x * (blockDim.x >> 5);
+  for (uint32_t w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); w < n; w += nw) {
+    const int64_t i = a.list[w];
+    double q[3];
+    query_point(a, i, q);
+    int64_t j = a.idx[i];
+    double d2 = warm_d2(v, q, j);
+    int l0 = 0;
+    const double reach = sqrt(d2);
+    while (l0 < NLEV - 1 && MAX_RINGS * v.lv[l0].g.h < reach) ++l0;
+    double second = INFINITY;
+    bool ok = false;
+    for (int l = l0; l < NLEV && !ok; ++l) ok = grid_nearest_warp(v.lv[l], q, j, d2, second);
+    if (lane == 0) {
+      if (ok) {
+        nn_commit(a, i, j, d2, q, second);
+      } else {
+        if (a.q_prev) a.second[i] = 0.0;
+        a.unresolved[atomicAdd(a.n_unres, 1u)] = (uint32_t)i;
+      }
+    }
+  }
+}
+
 // Exact fallback: one block per unresolved query scans every centre.
 __global__ void __launch_bounds__(256) k_nearest_brute(GridView v, NNArgs a) {
   __shared__ double s_d[8];
   __shared__ int64_t s_j[8];
   if (a.skip && *a.skip) return;
+  if (a.mode && blockIdx.x == 0 && threadIdx.x == 0) {
+    // the next call's mode from this call's searching queries; counts reset
+    // (a cold call counts in thread mode whatever the mode says: one of the
+    // two counts is zero)
+    const uint32_t searched = *a.n_list + *a.n_search;
+    *a.mode = searched < (uint32_t)SGAD_NN_WARP_BELOW ? 1u : 0u;
+    *a.n_list = 0u;
+    *a.n_search = 0u;
+  }
   const uint32_t nu = *a.n_unres;
   for (uint32_t u = blockIdx.x; u < nu; u += gridDim.x) {
     const int64_t i = a.unresolved[u];
@@ -1115,7 +1264,7 @@ __global__ void k_gn_accept(GnState* __restrict__ s, double* __restrict__ pairs,
 struct sgad_geomset {
   sgad::DevBuf pts, cov, nrm, bbox, keys0, keys1, idx0, idx1, head, headscan, start, hkeys, hvals,
       cub_tmp;
-  sgad::DevBuf w, b, acc, partial, poses, nn_j, nn_d2, unres, counter, nn_qprev, nn_second;
+  sgad::DevBuf w, b, acc, partial, poses, nn_j, nn_d2, unres, counter, nn_qprev, nn_second, nn_list;
   sgad::DevBuf gn_state, gn_log;
   sgad::Grid grid[sgad::NLEV]{};
   sgad::DevBuf lslots[sgad::NLEV], lpts[sgad::NLEV];
@@ -1181,7 +1330,7 @@ int sgad_geomset_destroy(sgad_geomset* g) {
                     &g->idx1, &g->head, &g->headscan, &g->start, &g->hkeys, &g->hvals,
                     &g->cub_tmp, &g->w, &g->b, &g->acc, &g->partial, &g->poses, &g->nn_j,
                     &g->nn_d2, &g->unres, &g->counter, &g->nn_qprev, &g->nn_second,
-                    &g->gn_state, &g->gn_log};
+                    &g->gn_state, &g->gn_log, &g->nn_list};
   for (DevBuf* b : bufs) b->release();
   for (int l = 0; l < NLEV; ++l) {
     g->lslots[l].release();
@@ -1351,8 +1500,12 @@ static int run_nearest(sgad_geomset* g, const double* queries, int64_t m, const 
                        bool persist = false, const double* pose_dev = nullptr,
                        const int32_t* skip = nullptr) {
   SGAD_CHECK_CUDA(g->unres.ensure(sizeof(uint32_t) * m));
+  SGAD_CHECK_CUDA(g->nn_list.ensure(sizeof(uint32_t) * m));
+  // counter: [0] unresolved (per call), [1] mode, [2] listed, [3] searched
+  // (the last three carried from call to call, reset by k_nearest_brute)
+  const bool fresh = g->counter.p == nullptr;
   SGAD_CHECK_CUDA(g->counter.ensure(sizeof(uint32_t) * 4));
-  SGAD_CHECK_CUDA(cudaMemsetAsync(g->counter.p, 0, sizeof(uint32_t), st));
+  SGAD_CHECK_CUDA(cudaMemsetAsync(g->counter.p, 0, sizeof(uint32_t) * (fresh ? 4 : 1), st));
   NNArgs a;
   a.queries = queries;
   a.m = m;
@@ -1366,6 +1519,10 @@ static int run_nearest(sgad_geomset* g, const double* queries, int64_t m, const 
   a.d2 = d2;
   a.unresolved = g->unres.as<uint32_t>();
   a.n_unres = g->counter.as<uint32_t>();
+  a.mode = SGAD_NN_WARP_BELOW > 0 ? g->counter.as<uint32_t>() + 1 : nullptr;
+  a.n_list = g->counter.as<uint32_t>() + 2;
+  a.n_search = g->counter.as<uint32_t>() + 3;
+  a.list = g->nn_list.as<uint32_t>();
   a.q_prev = nullptr;
   a.second = nullptr;
   if (persist) {
@@ -1377,6 +1534,10 @@ static int run_nearest(sgad_geomset* g, const double* queries, int64_t m, const 
   const GridView v = view_of(g);
   k_nearest<<<nblk(m, 128), 128, 0, st>>>(v, a);
   SGAD_LAUNCH_CHECK();
+  if (a.mode) {
+    k_nn_warp<<<148 * 16, 128, 0, st>>>(v, a);
+    SGAD_LAUNCH_CHECK();
+  }
   k_nearest_brute<<<256, 256, 0, st>>>(v, a);
   SGAD_LAUNCH_CHECK();
 #ifdef SGAD_NN_COUNT
