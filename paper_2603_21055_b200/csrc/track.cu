@@ -613,7 +613,9 @@ __device__ bool grid_nearest_warp(const LevelView& v, const double* q, int64_t& 
   const int lane = threadIdx.x & 31;
   int c0[3];
   for (int k = 0; k < 3; ++k) c0[k] = cell_coord(q[k], g.lo[k], g.h, g.dim[k]);
-  for (int r = 0; r <= MAX_RINGS; ++r) {
+  // the query's cell and its first ring together (27 cells: one round for
+  // the warp; ring 0 alone almost never settles a query), then ring by ring
+  for (int r = 1; r <= MAX_RINGS; ++r) {
     const int x0 = max(c0[0] - r, 0), x1 = min(c0[0] + r, g.dim[0] - 1);
     const int y0 = max(c0[1] - r, 0), y1 = min(c0[1] + r, g.dim[1] - 1);
     const int z0 = max(c0[2] - r, 0), z1 = min(c0[2] + r, g.dim[2] - 1);
@@ -622,7 +624,8 @@ __device__ bool grid_nearest_warp(const LevelView& v, const double* q, int64_t& 
     int64_t lj = best_j;
     for (int ci = lane; ci < total; ci += 32) {
       const int x = x0 + ci / (ny * nz), rem = ci % (ny * nz), y = y0 + rem / nz, z = z0 + rem % nz;
-      if (abs(x - c0[0]) != r && abs(y - c0[1]) != r && abs(z - c0[2]) != r) continue;  // interior
+      if (r > 1 && abs(x - c0[0]) != r && abs(y - c0[1]) != r && abs(z - c0[2]) != r)
+        continue;  // interior: visited
       const double bx0 = g.lo[0] + x * g.h, bx = fmax(fmax(bx0 - q[0], q[0] - (bx0 + g.h)), 0.0);
       const double by0 = g.lo[1] + y * g.h, by = fmax(fmax(by0 - q[1], q[1] - (by0 + g.h)), 0.0);
       const double bz0 = g.lo[2] + z * g.h, bz = fmax(fmax(bz0 - q[2], q[2] - (bz0 + g.h)), 0.0);
