@@ -622,33 +622,61 @@ __device__ bool grid_nearest_warp(const LevelView& v, const double* q, int64_t& 
     const int ny = y1 - y0 + 1, nz = z1 - z0 + 1, total = (x1 - x0 + 1) * ny * nz;
     double lb2 = best_d2, lsec = INFINITY;
     int64_t lj = best_j;
-    for (int ci = lane; ci < total; ci += 32) {
-      const int x = x0 + ci / (ny * nz), rem = ci % (ny * nz), y = y0 + rem / nz, z = z0 + rem % nz;
-      if (r > 1 && abs(x - c0[0]) != r && abs(y - c0[1]) != r && abs(z - c0[2]) != r)
-        continue;  // interior: visited
-      const double bx0 = g.lo[0] + x * g.h, bx = fmax(fmax(bx0 - q[0], q[0] - (bx0 + g.h)), 0.0);
-      const double by0 = g.lo[1] + y * g.h, by = fmax(fmax(by0 - q[1], q[1] - (by0 + g.h)), 0.0);
-      const double bz0 = g.lo[2] + z * g.h, bz = fmax(fmax(bz0 - q[2], q[2] - (bz0 + g.h)), 0.0);
-      const double bmin = bx * bx + by * by + bz * bz;
-      if (bmin > lb2) {
-        lsec = fmin(lsec, bmin);
-        continue;
+    for (int cb = 0; cb < total; cb += 32) {  // (uniform trip count: shuffles below)
+      // each lane probes one cell of the round ...
+      const int ci = cb + lane;
+      uint32_t cstart = 0, ccount = 0;
+      if (ci < total) {
+        const int x = x0 + ci / (ny * nz), rem = ci % (ny * nz), y = y0 + rem / nz,
+                  z = z0 + rem % nz;
+        if (r == 1 || abs(x - c0[0]) == r || abs(y - c0[1]) == r || abs(z - c0[2]) == r) {
+          const double bx0 = g.lo[0] + x * g.h, bx = fmax(fmax(bx0 - q[0], q[0] - (bx0 + g.h)), 0.0);
+          const double by0 = g.lo[1] + y * g.h, by = fmax(fmax(by0 - q[1], q[1] - (by0 + g.h)), 0.0);
+          const double bz0 = g.lo[2] + z * g.h, bz = fmax(fmax(bz0 - q[2], q[2] - (bz0 + g.h)), 0.0);
+          const double bmin = bx * bx + by * by + bz * bz;
+          if (bmin > lb2) {
+            lsec = fmin(lsec, bmin);
+          } else {
+            const uint2 rg = hash_find(v, cell_key(x, y, z));
+            cstart = rg.x;
+            ccount = rg.y;
+          }
+        }
       }
-      const uint2 rg = hash_find(v, cell_key(x, y, z));
-      for (uint32_t t = rg.x; t < rg.x + rg.y; ++t) {
-        double px, py, pz, pj;
-        asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];"
-            : "=d"(px), "=d"(py), "=d"(pz), "=d"(pj) : "l"(v.cpts + t));
-        const int64_t j = (int64_t)__double_as_longlong(pj);
-        if (j == lj) continue;
-        const double dx = q[0] - px, dy = q[1] - py, dz = q[2] - pz;
-        const double d2 = dx * dx + dy * dy + dz * dz;
-        if (d2 < lb2 || (d2 == lb2 && j < lj)) {
-          lsec = fmin(lsec, lb2);
-          lb2 = d2;
-          lj = j;
-        } else {
-          lsec = fmin(lsec, d2);
+      // ... then the round's points are dealt to the lanes (one load each)
+      uint32_t incl = ccount;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      const uint32_t excl = incl - ccount, npts = __shfl_sync(0xffffffffu, incl, 31);
+      for (uint32_t pb = 0; pb < npts; pb += 32) {
+        const uint32_t pi = pb + lane;
+        int own = 0;  // the lane whose cell holds point pi: last lane with excl <= pi
+#pragma unroll
+        for (int bit = 16; bit > 0; bit >>= 1) {
+          const uint32_t e = __shfl_sync(0xffffffffu, excl, own | bit);
+          if (e <= pi) own |= bit;
+        }
+        const uint32_t t = __shfl_sync(0xffffffffu, cstart, own) +
+                           (pi - __shfl_sync(0xffffffffu, excl, own));
+        if (pi < npts) {
+          double px, py, pz, pj;
+          asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];"
+              : "=d"(px), "=d"(py), "=d"(pz), "=d"(pj) : "l"(v.cpts + t));
+          const int64_t j = (int64_t)__double_as_longlong(pj);
+          if (j != lj) {
+            const double dx = q[0] - px, dy = q[1] - py, dz = q[2] - pz;
+            const double d2 = dx * dx + dy * dy + dz * dz;
+            if (d2 < lb2 || (d2 == lb2 && j < lj)) {
+              lsec = fmin(lsec, lb2);
+              lb2 = d2;
+              lj = j;
+            } else {
+              lsec = fmin(lsec, d2);
+            }
+          }
         }
       }
     }
