@@ -782,7 +782,7 @@ __device__ __forceinline__ double warm_d2(const GridView& v, const double* q, in
 // neighbouring cells: measured faster than compacting the queries that fail
 // the persistence test into per-level lists, which loses that coherence).
 #ifndef SGAD_NN_WARP_BELOW
-#define SGAD_NN_WARP_BELOW 150000  // warp-cooperative searches when fewer queries searched (the call before)
+#define SGAD_NN_WARP_BELOW 500000  // warp-cooperative searches when fewer queries searched (the call before)
 #endif
 #ifndef SGAD_NN_MINB
 #define SGAD_NN_MINB 10  // 48 registers: +11 % GN iterations/s over the unbounded 56 (816 k queries)
