@@ -607,10 +607,13 @@ __device__ bool grid_nearest(const LevelView& v, const double* pts, const double
 // lanes prune with their own (at least as good) best, the termination test
 // is the same.  Used when few queries search, so that a search's chain of
 // dependent slot and point loads is split over 32 lanes.
+template <int G>
 __device__ bool grid_nearest_warp(const LevelView& v, const double* q, int64_t& best_j,
                                   double& best_d2, double& second) {
+  static_assert(G >= 4 && G <= 32 && (G & (G - 1)) == 0, "group size");
   const Grid& g = v.g;
-  const int lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & (G - 1);
+  const unsigned gm = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << ((threadIdx.x & 31) & ~(G - 1)));
   int c0[3];
   for (int k = 0; k < 3; ++k) c0[k] = cell_coord(q[k], g.lo[k], g.h, g.dim[k]);
   // the query's cell and its first ring together (27 cells: one round for
@@ -622,7 +625,7 @@ __device__ bool grid_nearest_warp(const LevelView& v, const double* q, int64_t& 
     const int ny = y1 - y0 + 1, nz = z1 - z0 + 1, total = (x1 - x0 + 1) * ny * nz;
     double lb2 = best_d2, lsec = INFINITY;
     int64_t lj = best_j;
-    for (int cb = 0; cb < total; cb += 32) {  // (uniform trip count: shuffles below)
+    for (int cb = 0; cb < total; cb += G) {  // (uniform trip count: shuffles below)
       // each lane probes one cell of the round ...
       const int ci = cb + lane;
       uint32_t cstart = 0, ccount = 0;
@@ -646,21 +649,21 @@ __device__ bool grid_nearest_warp(const LevelView& v, const double* q, int64_t& 
       // ... then the round's points are dealt to the lanes (one load each)
       uint32_t incl = ccount;
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+      for (int o = 1; o < G; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(gm, incl, o, G);
         if (lane >= o) incl += y;
       }
-      const uint32_t excl = incl - ccount, npts = __shfl_sync(0xffffffffu, incl, 31);
-      for (uint32_t pb = 0; pb < npts; pb += 32) {
+      const uint32_t excl = incl - ccount, npts = __shfl_sync(gm, incl, G - 1, G);
+      for (uint32_t pb = 0; pb < npts; pb += G) {
         const uint32_t pi = pb + lane;
         int own = 0;  // the lane whose cell holds point pi: last lane with excl <= pi
 #pragma unroll
-        for (int bit = 16; bit > 0; bit >>= 1) {
-          const uint32_t e = __shfl_sync(0xffffffffu, excl, own | bit);
+        for (int bit = G / 2; bit > 0; bit >>= 1) {
+          const uint32_t e = __shfl_sync(gm, excl, own | bit, G);
           if (e <= pi) own |= bit;
         }
-        const uint32_t t = __shfl_sync(0xffffffffu, cstart, own) +
-                           (pi - __shfl_sync(0xffffffffu, excl, own));
+        const uint32_t t = __shfl_sync(gm, cstart, own, G) +
+                           (pi - __shfl_sync(gm, excl, own, G));
         if (pi < npts) {
           double px, py, pz, pj;
           asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];"
@@ -684,9 +687,9 @@ __device__ bool grid_nearest_warp(const LevelView& v, const double* q, int64_t& 
     double wb = lb2;
     int64_t wj = lj;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const double ob = __shfl_xor_sync(0xffffffffu, wb, o);
-      const int64_t oj = __shfl_xor_sync(0xffffffffu, wj, o);
+    for (int o = G / 2; o > 0; o >>= 1) {
+      const double ob = __shfl_xor_sync(gm, wb, o, G);
+      const int64_t oj = __shfl_xor_sync(gm, wj, o, G);
       if (ob < wb || (ob == wb && oj < wj)) {
         wb = ob;
         wj = oj;
@@ -694,7 +697,7 @@ __device__ bool grid_nearest_warp(const LevelView& v, const double* q, int64_t& 
     }
     double sc = (lj != wj) ? fmin(lsec, lb2) : lsec;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) sc = fmin(sc, __shfl_xor_sync(0xffffffffu, sc, o));
+    for (int o = G / 2; o > 0; o >>= 1) sc = fmin(sc, __shfl_xor_sync(gm, sc, o, G));
     second = fmin(second, sc);
     best_d2 = wb;
     best_j = wj;
@@ -781,8 +784,14 @@ __device__ __forceinline__ double warm_d2(const GridView& v, const double* q, in
 // One thread per query, in query order (neighbouring queries search
 // neighbouring cells: measured faster than compacting the queries that fail
 // the persistence test into per-level lists, which loses that coherence).
-#ifndef SGAD_NN_WARP_BELOW
-#define SGAD_NN_WARP_BELOW 500000  // warp-cooperative searches when fewer queries searched (the call before)
+#ifndef SGAD_NN_COOP_BELOW
+// cooperative searches when fewer than this fraction of the queries searched
+// the call before (816 k queries: 0.98 ~ thread mode for a registration's
+// first five iterations, measured best; 0: never)
+#define SGAD_NN_COOP_BELOW 0.98
+#endif
+#ifndef SGAD_NN_GROUP
+#define SGAD_NN_GROUP 16  // lanes per query in the cooperative mode (2 queries per warp)
 #endif
 #ifndef SGAD_NN_MINB
 #define SGAD_NN_MINB 10  // 48 registers: +11 % GN iterations/s over the unbounded 56 (816 k queries)
@@ -841,12 +850,13 @@ __global__ void __launch_bounds__(128, SGAD_NN_MINB) k_nearest(GridView v, NNArg
 }
 
 // Warp mode: one warp per listed query (grid-stride over the list).
+template <int G>
 __global__ void __launch_bounds__(128) k_nn_warp(GridView v, NNArgs a) {
   if ((a.skip && *a.skip) || *a.mode != 1u) return;
   const uint32_t n = *a.n_list;
-  const int lane = threadIdx.x & 31;
-  const uint32_t nw = gridDim.x * (blockDim.x >> 5);
-  for (uint32_t w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); w < n; w += nw) {
+  const int lane = threadIdx.x & (G - 1);
+  const uint32_t ng = gridDim.x * (blockDim.x / G);
+  for (uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) / G; w < n; w += ng) {
     const int64_t i = a.list[w];
     double q[3];
     query_point(a, i, q);
@@ -857,7 +867,7 @@ __global__ void __launch_bounds__(128) k_nn_warp(GridView v, NNArgs a) {
     while (l0 < NLEV - 1 && MAX_RINGS * v.lv[l0].g.h < reach) ++l0;
     double second = INFINITY;
     bool ok = false;
-    for (int l = l0; l < NLEV && !ok; ++l) ok = grid_nearest_warp(v.lv[l], q, j, d2, second);
+    for (int l = l0; l < NLEV && !ok; ++l) ok = grid_nearest_warp<G>(v.lv[l], q, j, d2, second);
     if (lane == 0) {
       if (ok) {
         nn_commit(a, i, j, d2, q, second);
@@ -879,7 +889,7 @@ __global__ void __launch_bounds__(256) k_nearest_brute(GridView v, NNArgs a) {
     // (a cold call counts in thread mode whatever the mode says: one of the
     // two counts is zero)
     const uint32_t searched = *a.n_list + *a.n_search;
-    *a.mode = searched < (uint32_t)SGAD_NN_WARP_BELOW ? 1u : 0u;
+    *a.mode = (double)searched < SGAD_NN_COOP_BELOW * (double)a.m ? 1u : 0u;
     *a.n_list = 0u;
     *a.n_search = 0u;
   }
@@ -1550,7 +1560,7 @@ static int run_nearest(sgad_geomset* g, const double* queries, int64_t m, const 
   a.d2 = d2;
   a.unresolved = g->unres.as<uint32_t>();
   a.n_unres = g->counter.as<uint32_t>();
-  a.mode = SGAD_NN_WARP_BELOW > 0 ? g->counter.as<uint32_t>() + 1 : nullptr;
+  a.mode = SGAD_NN_COOP_BELOW > 0 ? g->counter.as<uint32_t>() + 1 : nullptr;
   a.n_list = g->counter.as<uint32_t>() + 2;
   a.n_search = g->counter.as<uint32_t>() + 3;
   a.list = g->nn_list.as<uint32_t>();
@@ -1566,7 +1576,7 @@ static int run_nearest(sgad_geomset* g, const double* queries, int64_t m, const 
   k_nearest<<<nblk(m, 128), 128, 0, st>>>(v, a);
   SGAD_LAUNCH_CHECK();
   if (a.mode) {
-    k_nn_warp<<<148 * 16, 128, 0, st>>>(v, a);
+    k_nn_warp<SGAD_NN_GROUP><<<148 * 16, 128, 0, st>>>(v, a);
     SGAD_LAUNCH_CHECK();
   }
   k_nearest_brute<<<256, 256, 0, st>>>(v, a);
