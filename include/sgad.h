@@ -275,6 +275,17 @@ int sgad_track_correspondences(sgad_geomset* g, int64_t* idx, int64_t m, void* s
 int sgad_track_cost(sgad_geomset* g, const double* local_centers, int64_t m, const double* poses,
                     int32_t n_cand, double* out, void* stream);
 
+/* update_global_set's change of frame (tracker.py:233-238) on the device:
+ * centres R c + t and normals R n (numpy's BLAS order), rotations R rot
+ * (einsum order), and the packed covariances rot' diag(s^2) rot'^T of the
+ * result (GlobalGeomSet.covariances, :130-133) -> out_cov6 [n, 6].  All
+ * device fp64: centres/normals/scales [n, 3], rotations [n, 3, 3]; rot/trans
+ * host [9] / [3]. */
+int sgad_track_to_world(const double* centers, const double* rotations, const double* scales,
+                        const double* normals, int64_t n, const double* rot, const double* trans,
+                        double* out_centers, double* out_rotations, double* out_normals,
+                        double* out_cov6, void* stream);
+
 /* A whole gicp_align (tracker.py:265-346) enqueued at once and read back once:
  * per iteration the 6x6 solve (np.linalg.solve's partial-pivot LU), the step
  * and its 5 halvings (se3_exp(xi).compose(pose)), their frozen-weight costs,

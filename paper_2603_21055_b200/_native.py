@@ -84,6 +84,8 @@ _SIGNATURES = {
     "sgad_track_accepted": (_i32, [_vp, _vp, _i64, _vp]),
     "sgad_track_correspondences": (_i32, [_vp, _vp, _i64, _vp]),
     "sgad_track_cost": (_i32, [_vp, _vp, _i64, ctypes.POINTER(_f64), _i32, _vp, _vp]),
+    "sgad_track_to_world": (_i32, [_vp, _vp, _vp, _vp, _i64, ctypes.POINTER(_f64),
+                                   ctypes.POINTER(_f64), _vp, _vp, _vp, _vp, _vp]),
     "sgad_track_gicp": (_i32, [_vp, _vp, _vp, _i64, ctypes.POINTER(_f64), _i32, _f64, _i32, _f64,
                                _i32, _i32, _vp, _vp, _vp, _vp, _vp]),
 }

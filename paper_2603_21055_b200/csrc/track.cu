@@ -1300,6 +1300,51 @@ __global__ void k_gn_accept(GnState* __restrict__ s, double* __restrict__ pairs,
 
 }
 
+
+// ---------------------------------------------------------------- to world frame
+// update_global_set (tracker.py:233-238) and the members' covariances
+// (GlobalGeomSet.covariances, :130-133) in the reference's operation order:
+// centres and normals as numpy's BLAS product pts @ R.T (+ t) -- fma(a2,
+// R[j,2], fma(a1, R[j,1], a0 R[j,0])) -- rotations as einsum('ij,njk->nik')
+// and covariances as einsum('nij,nj,nkj->nik', rot, s**2, rot), unfused.
+__global__ void k_to_world(const double* __restrict__ c, const double* __restrict__ rot,
+                           const double* __restrict__ sc, const double* __restrict__ nrm,
+                           int64_t n, PoseArg P, double* __restrict__ oc,
+                           double* __restrict__ orot, double* __restrict__ onrm,
+                           double* __restrict__ ocov) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double a[3] = {c[3 * i], c[3 * i + 1], c[3 * i + 2]};
+  const double m[3] = {nrm[3 * i], nrm[3 * i + 1], nrm[3 * i + 2]};
+  double r[9], w[9];
+  for (int k = 0; k < 9; ++k) r[k] = rot[9 * i + k];
+#pragma unroll
+  for (int j = 0; j < 3; ++j) {
+    oc[3 * i + j] = SG_ADD(SG_FMA(a[2], P.r[3 * j + 2], SG_FMA(a[1], P.r[3 * j + 1], SG_MUL(a[0], P.r[3 * j]))),
+                           P.t[j]);
+    onrm[3 * i + j] = SG_FMA(m[2], P.r[3 * j + 2], SG_FMA(m[1], P.r[3 * j + 1], SG_MUL(m[0], P.r[3 * j])));
+  }
+#pragma unroll
+  for (int ii = 0; ii < 3; ++ii)
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+      w[3 * ii + k] = SG_ADD(SG_ADD(SG_MUL(P.r[3 * ii], r[k]), SG_MUL(P.r[3 * ii + 1], r[3 + k])),
+                             SG_MUL(P.r[3 * ii + 2], r[6 + k]));
+  for (int k = 0; k < 9; ++k) orot[9 * i + k] = w[k];
+  const double s2[3] = {SG_MUL(sc[3 * i], sc[3 * i]), SG_MUL(sc[3 * i + 1], sc[3 * i + 1]),
+                        SG_MUL(sc[3 * i + 2], sc[3 * i + 2])};
+  // packed (00, 01, 02, 11, 12, 22)
+  const int pi[6] = {0, 0, 0, 1, 1, 2}, pk[6] = {0, 1, 2, 1, 2, 2};
+#pragma unroll
+  for (int e = 0; e < 6; ++e) {
+    const int ii = pi[e], k = pk[e];
+    double acc = SG_MUL(SG_MUL(w[3 * ii], s2[0]), w[3 * k]);
+    acc = SG_ADD(acc, SG_MUL(SG_MUL(w[3 * ii + 1], s2[1]), w[3 * k + 1]));
+    acc = SG_ADD(acc, SG_MUL(SG_MUL(w[3 * ii + 2], s2[2]), w[3 * k + 2]));
+    ocov[6 * i + e] = acc;
+  }
+}
+
 }  // namespace sgad
 
 struct sgad_geomset {
@@ -1781,6 +1826,25 @@ int sgad_track_gicp(sgad_geomset* g, const double* local_centers, const double* 
   result[16] = h.failed;
   result[17] = h.singular_it;
   result[18] = h.n_systems;
+  return SGAD_OK;
+}
+
+int sgad_track_to_world(const double* centers, const double* rotations, const double* scales,
+                        const double* normals, int64_t n, const double* rot, const double* trans,
+                        double* out_centers, double* out_rotations, double* out_normals,
+                        double* out_cov6, void* stream) {
+  SGAD_REQUIRE(n >= 0 && rot && trans, "sgad_track_to_world: bad arguments");
+  if (n == 0) return SGAD_OK;
+  SGAD_REQUIRE(centers && rotations && scales && normals && out_centers && out_rotations &&
+                   out_normals && out_cov6,
+               "sgad_track_to_world: null buffer");
+  PoseArg P;
+  for (int k = 0; k < 9; ++k) P.r[k] = rot[k];
+  for (int k = 0; k < 3; ++k) P.t[k] = trans[k];
+  k_to_world<<<nblk(n, 256), 256, 0, (cudaStream_t)stream>>>(centers, rotations, scales, normals,
+                                                             n, P, out_centers, out_rotations,
+                                                             out_normals, out_cov6);
+  SGAD_LAUNCH_CHECK();
   return SGAD_OK;
 }
 

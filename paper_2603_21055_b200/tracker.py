@@ -225,9 +225,10 @@ class GlobalGeomSet:
             raise TrackerError(N.load().sgad_last_error().decode())
         return keep.bool()
 
-    def insert(self, centers, rotations, scales, normals) -> int:
+    def insert(self, centers, rotations, scales, normals, cov6=None) -> int:
         """tracker.py:105-122: rows whose voxel cell is free join the set (in
-        row order); returns the number added."""
+        row order); returns the number added.  ``cov6`` (optional): the rows'
+        packed covariances, if already computed."""
         c = _t(centers).reshape(-1, 3).contiguous()
         keep = self._gate(c)
         n = int(keep.sum())
@@ -237,7 +238,8 @@ class GlobalGeomSet:
             self.rotations = torch.cat([self.rotations, rot])
             self.scales = torch.cat([self.scales, sc])
             self.normals = torch.cat([self.normals, _t(normals)[keep]])
-            self.cov6 = torch.cat([self.cov6, cov_packed(_cov_from(rot, sc))])
+            cv = _t(cov6)[keep] if cov6 is not None else cov_packed(_cov_from(rot, sc))
+            self.cov6 = torch.cat([self.cov6, cv])
             N.call("sgad_geomset_set", self._h, self.centers.data_ptr(), self.cov6.data_ptr(),
                    self.normals.data_ptr(), len(self), N.stream_ptr())
         return n
@@ -273,13 +275,23 @@ class GlobalGeomSet:
 
 
 def update_global_set(global_set: GlobalGeomSet, local: LocalGeomSet, pose: Pose) -> int:
-    """tracker.py:233-238."""
-    R = _t(pose.rotation)
-    t = _t(pose.translation)
-    centers = local.centers @ R.T + t
-    rotations = torch.einsum("ij,njk->nik", R, local.rotations)
-    normals = local.normals @ R.T
-    return global_set.insert(centers, rotations, local.scales.clone(), normals)
+    """tracker.py:233-238: the local set in the world frame (one kernel:
+    centres, rotations, normals and the members' covariances in the
+    reference's operation order), then the voxel-gated insertion."""
+    m = len(local)
+    dev = local.centers.device
+    out = [torch.empty((m, 3), dtype=torch.float64, device=dev),
+           torch.empty((m, 3, 3), dtype=torch.float64, device=dev),
+           torch.empty((m, 3), dtype=torch.float64, device=dev),
+           torch.empty((m, 6), dtype=torch.float64, device=dev)]
+    rot = (ctypes.c_double * 9)(*np.asarray(pose.rotation, dtype=np.float64).reshape(9))
+    tr = (ctypes.c_double * 3)(*np.asarray(pose.translation, dtype=np.float64).reshape(3))
+    src = [local.centers.contiguous(), local.rotations.contiguous(), local.scales.contiguous(),
+           local.normals.contiguous()]
+    N.call("sgad_track_to_world", *[x.data_ptr() for x in src], m, rot, tr,
+           *[x.data_ptr() for x in out], N.stream_ptr())
+    centers, rotations, normals, cov6 = out
+    return global_set.insert(centers, rotations, local.scales.clone(), normals, cov6=cov6)
 
 
 @dataclass

@@ -162,4 +162,6 @@ def test_gpu_map_frame_deterministic(golden, tmp_path):
         outs.append((gmap.planes.cpu().numpy().tobytes(), path.read_bytes(), losses))
     assert outs[0][0] == outs[1][0]
     assert outs[0][1] == outs[1][1]
-    np.testing.assert_allclose(outs[0][2], outs[1][2], rtol=1e-14)
+    # (the reported losses add per-warp partial sums with fp64 atomics: an
+    # ulp apart run to run; they do not feed the update)
+    np.testing.assert_allclose(outs[0][2], outs[1][2], rtol=1e-12)
