@@ -270,3 +270,29 @@ def test_device_gn_loop_stops_like_host_loop(iters, eps):
     assert rot_err < 1e-9 and t_err < 1e-9
     if eps == 1e3:
         assert dd.converged and dd.iterations == 1
+
+
+def test_update_global_set_matches_reference_formulas():
+    """update_global_set on the device (sgad_track_to_world) against the
+    reference's numpy formulas (tracker.py:233-238, covariances :130-133):
+    centres pose.apply(c), rotations einsum('ij,njk->nik'), normals n @ R.T,
+    covariances einsum('nij,nj,nkj->nik', rot, s**2, rot)."""
+    from paper_2603_21055_b200 import tracker as T
+    from paper_2603_21055_b200.geometry import Pose, se3_exp
+    rng = np.random.default_rng(4)
+    m = 5000
+    c = rng.normal(0.0, 2.0, (m, 3))
+    q, _ = np.linalg.qr(rng.normal(size=(m, 3, 3)))
+    s = rng.uniform(0.01, 1.0, (m, 3))
+    nrm = rng.normal(size=(m, 3))
+    local = T.LocalGeomSet(c, q, s, nrm)
+    pose = se3_exp([0.1, -0.2, 0.3, 0.4, -0.5, 0.6])
+    g = T.GlobalGeomSet(1e-4)  # (cells below 2^20 per axis; every row its own cell)
+    assert T.update_global_set(g, local, pose) == m
+    R, t = pose.rotation, pose.translation
+    rot = np.einsum("ij,njk->nik", R, q)
+    np.testing.assert_allclose(g.centers.cpu().numpy(), pose.apply(c), rtol=0, atol=1e-14)
+    np.testing.assert_allclose(g.rotations.cpu().numpy(), rot, rtol=0, atol=1e-15)
+    np.testing.assert_allclose(g.normals.cpu().numpy(), nrm @ R.T, rtol=0, atol=1e-14)
+    cov = np.einsum("nij,nj,nkj->nik", rot, s ** 2, rot)
+    np.testing.assert_allclose(g.covariances(slice(None)).cpu().numpy(), cov, rtol=0, atol=1e-15)
