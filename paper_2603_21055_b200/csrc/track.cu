@@ -781,9 +781,17 @@ __device__ __forceinline__ double warm_d2(const GridView& v, const double* q, in
   return dx * dx + dy * dy + dz * dz;
 }
 
-// One thread per query, in query order (neighbouring queries search
-// neighbouring cells: measured faster than compacting the queries that fail
-// the persistence test into per-level lists, which loses that coherence).
+// Two modes, chosen on the device from the previous call's count of
+// searching queries (k_nearest_brute updates it):
+//  * thread mode (nearly every query searches: a cold call, a registration's
+//    first iterations): one thread per query, in query order -- neighbouring
+//    queries search neighbouring cells; throughput bound, and faster there
+//    than groups of lanes per query or compacted lists (which lose the
+//    coherence);
+//  * cooperative mode (fewer search): k_nearest only triages -- persistence
+//    test, the rest listed -- and k_nn_warp gives each listed query a group
+//    of SGAD_NN_GROUP lanes (grid_nearest_warp): a lone search is a chain
+//    of dependent slot and point loads, which the group splits.
 #ifndef SGAD_NN_COOP_BELOW
 // cooperative searches when fewer than this fraction of the queries searched
 // the call before (816 k queries: 0.98 ~ thread mode for a registration's
