@@ -401,10 +401,21 @@ struct Grid {
   double h;
   int dim[3];
   unsigned long long hmask;  // hash table size - 1
+  double inv_h;              // 1 / h (a query's starting cell only: see query_cell)
 };
 
 __device__ __forceinline__ int cell_coord(double x, double lo, double h, int dim) {
   double c = floor((x - lo) / h);
+  c = fmin(fmax(c, 0.0), (double)(dim - 1));
+  return (int)c;
+}
+
+// The cell a search starts from.  It need not be the cell the build put a
+// point at q in: every pruning and termination test uses the exact
+// geometry of the cells visited (box distances, the visited box's faces), so
+// a multiplication by 1 / h (no fp64 division) is enough.
+__device__ __forceinline__ int query_cell(double x, double lo, double inv_h, int dim) {
+  double c = floor((x - lo) * inv_h);
   c = fmin(fmax(c, 0.0), (double)(dim - 1));
   return (int)c;
 }
@@ -529,7 +540,7 @@ __device__ bool grid_nearest(const LevelView& v, const double* pts, const double
   const Grid& g = v.g;
   NN_COUNT(1, 1);
   int c0[3];
-  for (int k = 0; k < 3; ++k) c0[k] = cell_coord(q[k], g.lo[k], g.h, g.dim[k]);
+  for (int k = 0; k < 3; ++k) c0[k] = query_cell(q[k], g.lo[k], g.inv_h, g.dim[k]);
   for (int r = 0; r <= MAX_RINGS; ++r) {
     const int x0 = max(c0[0] - r, 0), x1 = min(c0[0] + r, g.dim[0] - 1);
     const int y0 = max(c0[1] - r, 0), y1 = min(c0[1] + r, g.dim[1] - 1);
@@ -615,7 +626,7 @@ __device__ bool grid_nearest_warp(const LevelView& v, const double* q, int64_t& 
   const int lane = threadIdx.x & (G - 1);
   const unsigned gm = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << ((threadIdx.x & 31) & ~(G - 1)));
   int c0[3];
-  for (int k = 0; k < 3; ++k) c0[k] = cell_coord(q[k], g.lo[k], g.h, g.dim[k]);
+  for (int k = 0; k < 3; ++k) c0[k] = query_cell(q[k], g.lo[k], g.inv_h, g.dim[k]);
   // the query's cell and its first ring together (27 cells: one round for
   // the warp; ring 0 alone almost never settles a query), then ring by ring
   for (int r = 1; r <= MAX_RINGS; ++r) {
@@ -623,6 +634,10 @@ __device__ bool grid_nearest_warp(const LevelView& v, const double* q, int64_t& 
     const int y0 = max(c0[1] - r, 0), y1 = min(c0[1] + r, g.dim[1] - 1);
     const int z0 = max(c0[2] - r, 0), z1 = min(c0[2] + r, g.dim[2] - 1);
     const int ny = y1 - y0 + 1, nz = z1 - z0 + 1, total = (x1 - x0 + 1) * ny * nz;
+    // ci / (ny nz) and rem / nz by multiply-shift: exact for ci < 128 and
+    // divisors <= 25 (the error ci (ceil(2^16 / d) - 2^16 / d) / 2^16 < 1 / d)
+    const uint32_t mul_yz = (65535u + (uint32_t)(ny * nz)) / (uint32_t)(ny * nz),
+                   mul_z = (65535u + (uint32_t)nz) / (uint32_t)nz;
     double lb2 = best_d2, lsec = INFINITY;
     int64_t lj = best_j;
     for (int cb = 0; cb < total; cb += G) {  // (uniform trip count: shuffles below)
@@ -630,8 +645,9 @@ __device__ bool grid_nearest_warp(const LevelView& v, const double* q, int64_t& 
       const int ci = cb + lane;
       uint32_t cstart = 0, ccount = 0;
       if (ci < total) {
-        const int x = x0 + ci / (ny * nz), rem = ci % (ny * nz), y = y0 + rem / nz,
-                  z = z0 + rem % nz;
+        const int qx = (int)(((uint32_t)ci * mul_yz) >> 16), rem = ci - qx * ny * nz,
+                  qy = (int)(((uint32_t)rem * mul_z) >> 16);
+        const int x = x0 + qx, y = y0 + qy, z = z0 + (rem - qy * nz);
         if (r == 1 || abs(x - c0[0]) == r || abs(y - c0[1]) == r || abs(z - c0[2]) == r) {
           const double bx0 = g.lo[0] + x * g.h, bx = fmax(fmax(bx0 - q[0], q[0] - (bx0 + g.h)), 0.0);
           const double by0 = g.lo[1] + y * g.h, by = fmax(fmax(by0 - q[1], q[1] - (by0 + g.h)), 0.0);
@@ -1476,6 +1492,7 @@ static int grid_sort(sgad_geomset* g, Grid& gr, cudaStream_t st, int64_t* n_cell
 
 static void grid_dims(Grid& gr, const double* ext, double h) {
   gr.h = h;
+  gr.inv_h = 1.0 / h;
   for (int k = 0; k < 3; ++k) gr.dim[k] = (int)fmin(floor(ext[k] / h) + 1.0, (double)(1 << 21) - 1.0);
 }
 
